@@ -1,0 +1,133 @@
+/*
+ * petals_b200.h — C-ABI of the B200-native block-span server hot path.
+ *
+ * Everything here takes plain pointers, sizes and a cudaStream_t (passed as
+ * void*); no torch types cross this boundary. Device pointers are marked d_,
+ * host pointers h_. Every entry point returns 0 on success or one of the
+ * reference's wire error codes (PB_ERR_*, mirroring
+ * /root/reference/pkg/src/swarmlm/errors.py:38-44); pb_last_error() returns a
+ * thread-local message for the last failure.
+ *
+ * Reference interfaces replaced (file:line under /root/reference/pkg/src/swarmlm):
+ *   pb_quantize_blockwise    <- quant.py:33-54   quantize_blockwise (wire codec, bit-exact)
+ *   pb_dequantize_blockwise  <- quant.py:57-66   dequantize_blockwise (bit-exact)
+ *   pb_gen_tensor            <- model.py:36-62   splitmix64_array/uniform_from_u64/tensor_stream
+ *   pb_span_* weights        <- quant.py:81-108,132-149 quantize_weights_int8 / QuantizedBlockWeights.from_block
+ *   pb_span_step             <- model.py:314-380 block_forward looped over a span as in server.py:383-385,
+ *                               batched over sessions; KV caches = server.py:69-77 _Session.caches
+ */
+#ifndef PETALS_B200_H
+#define PETALS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* errors.py:38-44 */
+#define PB_OK 0
+#define PB_ERR_GENERIC 1
+#define PB_ERR_BUSY 2
+#define PB_ERR_DESYNC 3
+#define PB_ERR_UNKNOWN_SESSION 4
+#define PB_ERR_UNKNOWN_TAPE 5
+#define PB_ERR_BAD_REQUEST 6
+#define PB_ERR_CAPACITY 7
+
+/* weight storage of a span */
+#define PB_WEIGHTS_INT8 1 /* quantize in {weights, both}: LLM.int8-style codes + f32 outlier rows */
+#define PB_WEIGHTS_F32 0  /* quantize in {none, activations}: f32 weights, reference fp32 math */
+
+const char* pb_last_error(void);
+int pb_version(void);
+
+/* ---- wire codec (transport/wire.py:98-105,125-137 -> quant.py:33-66) ---- */
+/* codes[n] int8, scales[ceil(n/block)] f32; bit-exact with the reference. */
+int pb_quantize_blockwise(const float* d_x, int64_t n, int32_t block, int8_t* d_codes, float* d_scales,
+                          void* stream);
+int pb_dequantize_blockwise(const int8_t* d_codes, const float* d_scales, int64_t n, int32_t block,
+                            float* d_out, void* stream);
+
+/* ---- deterministic weights (model.py:36-62) ----
+ * out[i] = f32(((splitmix64(key, first + i + 1) >> 11) * 2^-53 - 0.5) * 0.1),
+ * key = seed ^ fnv1a64(path) (computed by the caller). */
+int pb_gen_tensor(uint64_t key, int64_t first, int64_t n, float* d_out, void* stream);
+
+/* ---- block span ---- */
+typedef struct pb_span pb_span;
+
+typedef struct {
+    int32_t hidden;      /* d */
+    int32_t n_heads;     /* H */
+    int32_t mlp_ratio;   /* r (model.py:72) */
+    int32_t max_seq;     /* model.py:71 */
+    int32_t n_blocks;    /* blocks hosted by this span */
+    int32_t first_block; /* global index of the first hosted block (weight stream paths) */
+    int32_t weights;     /* PB_WEIGHTS_INT8 | PB_WEIGHTS_F32 */
+    int32_t page_tokens; /* KV page size in tokens */
+    int32_t n_pages;     /* KV pool pages (each page holds page_tokens positions for every hosted block) */
+    int32_t max_tokens;  /* max new tokens per pb_span_step / rows*t per pb_span_forward chunk */
+    int32_t max_seqs;    /* max sequences (sessions) per pb_span_step */
+    float outlier_threshold; /* quant.py:14 (6.0) */
+    int32_t device;
+} pb_span_config;
+
+int pb_span_create(const pb_span_config* cfg, pb_span** out);
+int pb_span_destroy(pb_span* span);
+/* bytes of device memory held by the span (weights + KV pool + workspace) */
+int64_t pb_span_device_bytes(const pb_span* span);
+
+/* Fill hosted block j (0-based within the span) with gen_checkpoint weights
+ * for global block first_block + j (model.py:176-209): matrices from the
+ * SplitMix64 streams `blocks.{i}.{wqkv,wo,wmlp_in,wmlp_out}`, gammas 1,
+ * betas/biases 0. key_* = seed ^ fnv1a64(path) computed by the caller.
+ * outlier_boost (>1 enables) multiplies the rows of every `boost_every`-th
+ * input feature by outlier_boost before quantization (bench outlier injection);
+ * pass 0 to disable. */
+int pb_span_gen_block(pb_span* span, int32_t j, uint64_t key_wqkv, uint64_t key_wo, uint64_t key_win,
+                      uint64_t key_wout, float outlier_boost, int32_t boost_every, void* stream);
+
+/* Load hosted block j from device f32 tensors in the reference layout
+ * (model.py:87-100: matrices [in, out] row-major). */
+int pb_span_load_block(pb_span* span, int32_t j, const float* d_ln1_g, const float* d_ln1_b,
+                       const float* d_wqkv, const float* d_bqkv, const float* d_wo, const float* d_bo,
+                       const float* d_ln2_g, const float* d_ln2_b, const float* d_win, const float* d_bin,
+                       const float* d_wout, const float* d_bout, void* stream);
+
+/* Outlier input features chosen by the quantizer for matrix m (0 wqkv, 1 wo,
+ * 2 wmlp_in, 3 wmlp_out) of block j. Writes up to cap indices, returns count
+ * in *n. Scales/codes can be read back with pb_span_read_codes. */
+int pb_span_outliers(const pb_span* span, int32_t j, int32_t m, int32_t* h_idx, int32_t cap, int32_t* n);
+/* Copy matrix m of block j back as reference-layout int8 codes [out, in] and
+ * f32 scales [in] (test/inspection path). */
+int pb_span_read_codes(const pb_span* span, int32_t j, int32_t m, int8_t* h_codes, float* h_scales);
+
+/* One batched inference step through every hosted block.
+ * n_tok new positions from n_seq sequences; token i belongs to sequence
+ * h_tok_seq[i] at absolute position h_tok_pos[i] (positions of one sequence
+ * are consecutive and its cache already holds [0, first position)).
+ * h_pages[s * max_pages + p] is the KV pool page of sequence s's logical page
+ * p (max_pages = ceil(max_seq / page_tokens)). Input/output hidden states
+ * [n_tok, hidden] f32 on the device; d_in may equal d_out. */
+int pb_span_step(pb_span* span, int32_t n_tok, int32_t n_seq, const int32_t* h_tok_seq,
+                 const int32_t* h_tok_pos, const int32_t* h_pages, const float* d_in, float* d_out,
+                 void* stream);
+
+/* Same as pb_span_step but the hidden states arrive / leave as wire-codec
+ * int8 (codes [n_tok*hidden], scales [n_tok*hidden/64]), block 64; the
+ * decode is fused into the first block's prologue input path and the encode
+ * runs on the last block's output. Either codec side may be NULL (f32 then). */
+int pb_span_step_int8(pb_span* span, int32_t n_tok, int32_t n_seq, const int32_t* h_tok_seq,
+                      const int32_t* h_tok_pos, const int32_t* h_pages, const int8_t* d_in_codes,
+                      const float* d_in_scales, const float* d_in_f32, int8_t* d_out_codes,
+                      float* d_out_scales, float* d_out_f32, void* stream);
+
+/* Last-launch statistics: number of kernels the last step/forward launched. */
+int32_t pb_span_last_launches(const pb_span* span);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

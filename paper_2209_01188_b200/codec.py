@@ -1,0 +1,168 @@
+"""Device-side codecs behind the reference's quant/wire API.
+
+quantize_blockwise / dequantize_blockwise mirror
+/root/reference/pkg/src/swarmlm/quant.py:33-66 (same names, argument meaning
+and errors) on CUDA tensors; encode_tensor / decode_tensor mirror
+transport/wire.py:87-138 byte for byte, running the int8 codec on the GPU.
+gen_tensor mirrors model.py:60-62 tensor_stream.
+"""
+
+from __future__ import annotations
+
+import math
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import InputError, ProtocolError
+from .model import stream_key
+
+DEFAULT_BLOCK_SIZE = 64
+ENC_F32 = 0
+ENC_INT8 = 1
+MAX_PAYLOAD = 64 * 1024 * 1024
+
+
+@dataclass
+class QuantizedBlockwise:
+    block_size: int
+    scales: object  # torch f32 [n_blocks] (device)
+    codes: object   # torch int8 [n] (device)
+    shape: tuple
+
+
+def _dev():
+    import torch
+
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def quantize_blockwise(x, block_size: int = DEFAULT_BLOCK_SIZE) -> QuantizedBlockwise:
+    import torch
+
+    if block_size < 1:
+        raise InputError("block_size must be >= 1")
+    x = torch.as_tensor(x)
+    if not x.is_cuda:
+        x = x.to(_dev())
+    x = x.to(torch.float32).contiguous()
+    if not bool(torch.isfinite(x).all()):
+        raise InputError("non-finite input tensor")
+    n = x.numel()
+    nb = max(1, math.ceil(n / block_size)) if n else 0
+    scales = torch.empty(nb, dtype=torch.float32, device=x.device)
+    codes = torch.empty(n, dtype=torch.int8, device=x.device)
+    _lib.check(_lib.lib().pb_quantize_blockwise(_lib.ptr(x), n, block_size, _lib.ptr(codes), _lib.ptr(scales),
+                                                _lib.stream_ptr(torch.cuda.current_stream(x.device))))
+    return QuantizedBlockwise(block_size, scales, codes, tuple(x.shape))
+
+
+def dequantize_blockwise(q: QuantizedBlockwise):
+    import torch
+
+    n = int(np.prod(q.shape)) if q.shape else 1
+    expected = max(1, math.ceil(n / q.block_size)) if n else 0
+    if q.codes.numel() != n or q.scales.numel() != expected:
+        raise InputError("corrupt quantized tensor: size/scale count mismatch")
+    out = torch.empty(n, dtype=torch.float32, device=q.codes.device)
+    _lib.check(_lib.lib().pb_dequantize_blockwise(_lib.ptr(q.codes.contiguous()), _lib.ptr(q.scales.contiguous()),
+                                                  n, q.block_size, _lib.ptr(out),
+                                                  _lib.stream_ptr(torch.cuda.current_stream(out.device))))
+    return out.reshape(q.shape)
+
+
+def gen_tensor(seed: int, path: str, n: int, first: int = 0):
+    """tensor_stream(seed, path, n) on the device (elements [first, first+n))."""
+    import torch
+
+    out = torch.empty(n, dtype=torch.float32, device=_dev())
+    _lib.check(_lib.lib().pb_gen_tensor(stream_key(seed, path), first, n, _lib.ptr(out),
+                                        _lib.stream_ptr(torch.cuda.current_stream(out.device))))
+    return out
+
+
+# ------------------------------------------------------------------ wire TensorMsg
+
+
+def encode_header(encoding: int, shape) -> bytes:
+    return struct.pack(">BB", encoding, len(shape)) + b"".join(struct.pack(">I", d) for d in shape)
+
+
+def encode_tensor(t, encoding: int = ENC_F32, block_size: int = 64) -> bytes:
+    """TensorMsg bytes (transport/wire.py:87-106). `t` may be a numpy array or a
+    CUDA tensor; int8 encoding runs on the GPU."""
+    import torch
+
+    if isinstance(t, np.ndarray):
+        arr = np.asarray(t, np.float32)
+        shape = arr.shape
+        if not np.all(np.isfinite(arr)):
+            raise InputError("non-finite tensor")
+    else:
+        arr = None
+        shape = tuple(t.shape)
+        if not bool(torch.isfinite(t).all()):
+            raise InputError("non-finite tensor")
+    if len(shape) > 255:
+        raise InputError("too many dimensions")
+    n = int(np.prod(shape)) if shape else 1
+    if n and n * 4 > MAX_PAYLOAD:
+        raise InputError("tensor exceeds frame cap")
+    head = encode_header(encoding, shape)
+    if encoding == ENC_F32:
+        if arr is None:
+            arr = t.detach().to(torch.float32).cpu().numpy()
+        return head + np.ascontiguousarray(arr, "<f4").tobytes()
+    if encoding == ENC_INT8:
+        src = torch.as_tensor(arr) if arr is not None else t
+        q = quantize_blockwise(src, block_size)
+        return (head + struct.pack(">I", block_size) + q.scales.cpu().numpy().astype("<f4").tobytes()
+                + q.codes.cpu().numpy().tobytes())
+    raise InputError(f"unknown tensor encoding {encoding}")
+
+
+def parse_tensor(data: bytes):
+    """Split TensorMsg bytes into (encoding, dims, block_size, scales np, codes np | f32 np)
+    without decoding (transport/wire.py:109-138 validation)."""
+    if len(data) < 2:
+        raise ProtocolError("truncated tensor header")
+    encoding, ndim = struct.unpack(">BB", data[:2])
+    off = 2
+    if len(data) < off + 4 * ndim:
+        raise ProtocolError("truncated tensor dims")
+    dims = struct.unpack(f">{ndim}I", data[off:off + 4 * ndim]) if ndim else ()
+    off += 4 * ndim
+    n = int(math.prod(dims)) if ndim else 1
+    if encoding == ENC_F32:
+        if len(data) != off + 4 * n:
+            raise ProtocolError("f32 tensor size mismatch")
+        return encoding, dims, 0, None, np.frombuffer(data, "<f4", count=n, offset=off)
+    if encoding == ENC_INT8:
+        if len(data) < off + 4:
+            raise ProtocolError("truncated int8 tensor")
+        (block_size,) = struct.unpack(">I", data[off:off + 4])
+        off += 4
+        if block_size < 1:
+            raise ProtocolError("bad block size")
+        nb = math.ceil(n / block_size) if n else 0
+        if len(data) != off + 4 * nb + n:
+            raise ProtocolError("int8 tensor size mismatch")
+        scales = np.frombuffer(data, "<f4", count=nb, offset=off)
+        codes = np.frombuffer(data, np.int8, count=n, offset=off + 4 * nb)
+        return encoding, dims, block_size, scales, codes
+    raise ProtocolError(f"unknown tensor encoding {encoding}")
+
+
+def decode_tensor(data: bytes, device=None):
+    """TensorMsg -> CUDA f32 tensor (int8 decoded on the GPU)."""
+    import torch
+
+    dev = device or _dev()
+    enc, dims, bs, scales, payload = parse_tensor(data)
+    if enc == ENC_F32:
+        return torch.from_numpy(payload.copy()).to(dev).reshape(dims)
+    q = QuantizedBlockwise(bs, torch.from_numpy(scales.copy()).to(dev), torch.from_numpy(payload.copy()).to(dev),
+                           tuple(dims))
+    return dequantize_blockwise(q)

@@ -1,0 +1,427 @@
+// Block-span runtime and C-ABI: weights of a contiguous block range, the
+// paged KV pool, workspaces, and the per-step launch sequence of
+// block_forward (model.py:314-380) looped over the span (server.py:383-385),
+// batched over sessions.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "pb_common.cuh"
+#include "pb_span.h"
+
+namespace pb {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+}  // namespace pb
+
+using namespace pb;
+
+struct pb_span {
+    pb_span_config cfg{};
+    int d = 0, H = 0, dh = 0, rd = 0, max_pages = 0;
+    std::vector<BlockW> blocks;
+    half* kv = nullptr;          // [n_blocks][n_pages][2][H][P][dh]
+    int64_t kv_block_elems = 0;  // elements per block
+    float* slopes = nullptr;
+    // workspaces
+    float *xa = nullptr, *mid = nullptr, *q = nullptr, *ctx = nullptr, *act = nullptr, *xo = nullptr, *y32 = nullptr;
+    uint4* frag = nullptr;
+    float* back = nullptr;
+    float* partials = nullptr;
+    int64_t partial_cap = 0;
+    int* counters = nullptr;
+    float* attn_part = nullptr;
+    int64_t attn_cap = 0;
+    int32_t *d_tok_seq = nullptr, *d_tok_pos = nullptr, *d_pages = nullptr;
+    int32_t* h_meta = nullptr;  // pinned staging: tok_seq | tok_pos | pages
+    int64_t meta_ints = 0;
+    int8_t* hop_codes = nullptr;
+    float* hop_scales = nullptr;
+    int64_t bytes = 0;
+    int32_t last_launches = 0;
+    std::mutex mu;  // one step at a time per span (the stream is shared)
+};
+
+namespace {
+
+template <class T>
+int dalloc(pb_span* s, T** p, int64_t count) {
+    const size_t b = sizeof(T) * (size_t)std::max<int64_t>(count, 1);
+    PB_CHECK_CUDA(cudaMalloc((void**)p, b));
+    s->bytes += (int64_t)b;
+    return PB_OK;
+}
+
+int alloc_mat(pb_span* s, Mat& m, int K, int M, bool int8) {
+    m.K = K;
+    m.M = M;
+    m.Kp = (int)round_up(K, 32);
+    m.Mp = (int)round_up(M, 16);
+    m.int8 = int8;
+    if (int8) {
+        if (int rc = dalloc(s, &m.codes, (int64_t)m.Mp * m.Kp)) return rc;
+        if (int rc = dalloc(s, &m.scales, m.Kp)) return rc;
+        PB_CHECK_CUDA(cudaMemset(m.scales, 0, sizeof(float) * m.Kp));
+    } else {
+        if (int rc = dalloc(s, &m.w32, (int64_t)K * M)) return rc;
+    }
+    return PB_OK;
+}
+
+void free_span(pb_span* s) {
+    for (auto& b : s->blocks) {
+        for (auto& m : b.mat) {
+            cudaFree(m.codes);
+            cudaFree(m.scales);
+            cudaFree(m.w32);
+            m.free_outliers();
+        }
+        cudaFree(b.ln1_g);
+        cudaFree(b.ln1_b);
+        cudaFree(b.ln2_g);
+        cudaFree(b.ln2_b);
+        for (auto* p : b.bias) cudaFree(p);
+    }
+    void* ptrs[] = {s->kv, s->slopes, s->xa, s->mid, s->q, s->ctx, s->act, s->xo, s->y32, s->frag, s->back,
+                    s->partials, s->counters, s->attn_part, s->d_tok_seq, s->d_tok_pos, s->d_pages,
+                    s->hop_codes, s->hop_scales};
+    for (void* p : ptrs) cudaFree(p);
+    if (s->h_meta) cudaFreeHost(s->h_meta);
+}
+
+__global__ void k_fill(float* p, int64_t n, float v) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) p[i] = v;
+}
+
+int fill(float* p, int64_t n, float v, cudaStream_t st) {
+    k_fill<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 1024), 256, 0, st>>>(p, n, v);
+    return launch_check("fill");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pb_last_error(void) { return pb::g_err.c_str(); }
+int pb_version(void) { return 1; }
+
+int pb_span_create(const pb_span_config* cfg, pb_span** out) {
+    PB_REQUIRE(cfg && out, PB_ERR_BAD_REQUEST, "null argument");
+    PB_REQUIRE(cfg->hidden > 0 && cfg->n_heads > 0 && cfg->hidden % cfg->n_heads == 0, PB_ERR_BAD_REQUEST,
+               "hidden must be a positive multiple of n_heads");
+    PB_REQUIRE(cfg->n_blocks > 0 && cfg->mlp_ratio > 0 && cfg->max_seq > 0, PB_ERR_BAD_REQUEST, "bad span shape");
+    PB_REQUIRE(cfg->page_tokens > 0 && cfg->n_pages > 0 && cfg->max_tokens > 0 && cfg->max_seqs > 0,
+               PB_ERR_BAD_REQUEST, "bad pool/workspace sizes");
+    PB_CHECK_CUDA(cudaSetDevice(cfg->device));
+    auto* s = new pb_span();
+    s->cfg = *cfg;
+    s->d = cfg->hidden;
+    s->H = cfg->n_heads;
+    s->dh = cfg->hidden / cfg->n_heads;
+    s->rd = cfg->hidden * cfg->mlp_ratio;
+    s->max_pages = (int)ceil_div(cfg->max_seq, cfg->page_tokens);
+    const bool int8 = cfg->weights == PB_WEIGHTS_INT8;
+    const int d = s->d, rd = s->rd;
+    s->blocks.resize(cfg->n_blocks);
+    int rc = PB_OK;
+    for (auto& b : s->blocks) {
+        if ((rc = alloc_mat(s, b.mat[0], d, 3 * d, int8))) break;
+        if ((rc = alloc_mat(s, b.mat[1], d, d, int8))) break;
+        if ((rc = alloc_mat(s, b.mat[2], d, rd, int8))) break;
+        if ((rc = alloc_mat(s, b.mat[3], rd, d, int8))) break;
+        if ((rc = dalloc(s, &b.ln1_g, d)) || (rc = dalloc(s, &b.ln1_b, d)) || (rc = dalloc(s, &b.ln2_g, d)) ||
+            (rc = dalloc(s, &b.ln2_b, d)))
+            break;
+        if ((rc = dalloc(s, &b.bias[0], 3 * d)) || (rc = dalloc(s, &b.bias[1], d)) || (rc = dalloc(s, &b.bias[2], rd)) ||
+            (rc = dalloc(s, &b.bias[3], d)))
+            break;
+    }
+    const int NT = cfg->max_tokens;
+    s->kv_block_elems = (int64_t)cfg->n_pages * 2 * s->H * cfg->page_tokens * s->dh;
+    if (!rc) rc = dalloc(s, &s->kv, s->kv_block_elems * cfg->n_blocks);
+    if (!rc) rc = dalloc(s, &s->slopes, s->H);
+    if (!rc) rc = dalloc(s, &s->xa, (int64_t)NT * d);
+    if (!rc) rc = dalloc(s, &s->mid, (int64_t)NT * d);
+    if (!rc) rc = dalloc(s, &s->q, (int64_t)NT * d);
+    if (!rc) rc = dalloc(s, &s->ctx, (int64_t)NT * d);
+    if (!rc) rc = dalloc(s, &s->act, (int64_t)NT * rd);
+    if (!rc && int8) rc = dalloc(s, &s->xo, (int64_t)NT * rd);
+    if (!rc && !int8) rc = dalloc(s, &s->y32, (int64_t)NT * rd);
+    const int64_t kp_max = round_up(rd, 32);
+    if (!rc && int8) rc = dalloc(s, &s->frag, (int64_t)(NT + 31) * kp_max * 4 / 16 + 64);
+    if (!rc) rc = dalloc(s, &s->back, NT);
+    s->partial_cap = (int64_t)8 << 20;
+    if (!rc && int8) rc = dalloc(s, &s->partials, s->partial_cap);
+    if (!rc) rc = dalloc(s, &s->counters, 1 << 20);
+    s->attn_cap = attention_part_floats(NT, s->H, s->dh, cfg->max_seq);
+    if (!rc) rc = dalloc(s, &s->attn_part, s->attn_cap);
+    s->meta_ints = 2 * (int64_t)NT + (int64_t)cfg->max_seqs * s->max_pages;
+    if (!rc) rc = dalloc(s, &s->d_tok_seq, NT);
+    if (!rc) rc = dalloc(s, &s->d_tok_pos, NT);
+    if (!rc) rc = dalloc(s, &s->d_pages, (int64_t)cfg->max_seqs * s->max_pages);
+    if (!rc) rc = dalloc(s, &s->hop_codes, (int64_t)NT * d);
+    if (!rc) rc = dalloc(s, &s->hop_scales, ceil_div((int64_t)NT * d, 64));
+    if (!rc && cudaMallocHost((void**)&s->h_meta, sizeof(int32_t) * s->meta_ints) != cudaSuccess) {
+        set_error("pinned staging allocation failed");
+        rc = PB_ERR_GENERIC;
+    }
+    if (!rc && cudaMemset(s->counters, 0, sizeof(int) << 20) != cudaSuccess) rc = PB_ERR_GENERIC;
+    if (!rc) {
+        std::vector<float> sl(s->H);
+        for (int h = 1; h <= s->H; ++h) sl[h - 1] = (float)std::pow(2.0, -8.0 * h / s->H);  // model.py:301-302
+        if (cudaMemcpy(s->slopes, sl.data(), sizeof(float) * s->H, cudaMemcpyHostToDevice) != cudaSuccess)
+            rc = PB_ERR_GENERIC;
+    }
+    if (rc) {
+        if (pb::g_err.empty() || pb::g_err.find("out of memory") != std::string::npos)
+            set_error("span allocation failed: " + pb::g_err);
+        free_span(s);
+        delete s;
+        return rc == PB_ERR_GENERIC ? PB_ERR_CAPACITY : rc;
+    }
+    *out = s;
+    return PB_OK;
+}
+
+int pb_span_destroy(pb_span* span) {
+    if (!span) return PB_OK;
+    cudaSetDevice(span->cfg.device);
+    cudaDeviceSynchronize();
+    free_span(span);
+    delete span;
+    return PB_OK;
+}
+
+int64_t pb_span_device_bytes(const pb_span* span) { return span ? span->bytes : 0; }
+
+static int init_block_vectors(pb_span* s, BlockW& b, cudaStream_t st) {
+    const int d = s->d;
+    if (int rc = fill(b.ln1_g, d, 1.f, st)) return rc;
+    if (int rc = fill(b.ln2_g, d, 1.f, st)) return rc;
+    PB_CHECK_CUDA(cudaMemsetAsync(b.ln1_b, 0, sizeof(float) * d, st));
+    PB_CHECK_CUDA(cudaMemsetAsync(b.ln2_b, 0, sizeof(float) * d, st));
+    PB_CHECK_CUDA(cudaMemsetAsync(b.bias[0], 0, sizeof(float) * 3 * d, st));
+    PB_CHECK_CUDA(cudaMemsetAsync(b.bias[1], 0, sizeof(float) * d, st));
+    PB_CHECK_CUDA(cudaMemsetAsync(b.bias[2], 0, sizeof(float) * s->rd, st));
+    PB_CHECK_CUDA(cudaMemsetAsync(b.bias[3], 0, sizeof(float) * d, st));
+    return PB_OK;
+}
+
+int pb_span_gen_block(pb_span* span, int32_t j, uint64_t key_wqkv, uint64_t key_wo, uint64_t key_win,
+                      uint64_t key_wout, float outlier_boost, int32_t boost_every, void* stream) {
+    PB_REQUIRE(span && j >= 0 && j < span->cfg.n_blocks, PB_ERR_BAD_REQUEST, "block index out of range");
+    std::lock_guard<std::mutex> lk(span->mu);
+    PB_CHECK_CUDA(cudaSetDevice(span->cfg.device));
+    auto st = (cudaStream_t)stream;
+    BlockW& b = span->blocks[j];
+    if (int rc = init_block_vectors(span, b, st)) return rc;
+    const uint64_t keys[4] = {key_wqkv, key_wo, key_win, key_wout};
+    const int every = outlier_boost > 0.f ? boost_every : 0;
+    for (int m = 0; m < 4; ++m)
+        if (int rc = fill_matrix_gen(b.mat[m], keys[m], span->cfg.outlier_threshold, outlier_boost, every, st))
+            return rc;
+    PB_CHECK_CUDA(cudaStreamSynchronize(st));
+    return PB_OK;
+}
+
+int pb_span_load_block(pb_span* span, int32_t j, const float* d_ln1_g, const float* d_ln1_b, const float* d_wqkv,
+                       const float* d_bqkv, const float* d_wo, const float* d_bo, const float* d_ln2_g,
+                       const float* d_ln2_b, const float* d_win, const float* d_bin, const float* d_wout,
+                       const float* d_bout, void* stream) {
+    PB_REQUIRE(span && j >= 0 && j < span->cfg.n_blocks, PB_ERR_BAD_REQUEST, "block index out of range");
+    std::lock_guard<std::mutex> lk(span->mu);
+    PB_CHECK_CUDA(cudaSetDevice(span->cfg.device));
+    auto st = (cudaStream_t)stream;
+    BlockW& b = span->blocks[j];
+    const int d = span->d, rd = span->rd;
+    auto cp = [&](float* dst, const float* src, int64_t n) {
+        return cudaMemcpyAsync(dst, src, sizeof(float) * n, cudaMemcpyDeviceToDevice, st);
+    };
+    PB_CHECK_CUDA(cp(b.ln1_g, d_ln1_g, d));
+    PB_CHECK_CUDA(cp(b.ln1_b, d_ln1_b, d));
+    PB_CHECK_CUDA(cp(b.ln2_g, d_ln2_g, d));
+    PB_CHECK_CUDA(cp(b.ln2_b, d_ln2_b, d));
+    PB_CHECK_CUDA(cp(b.bias[0], d_bqkv, 3 * d));
+    PB_CHECK_CUDA(cp(b.bias[1], d_bo, d));
+    PB_CHECK_CUDA(cp(b.bias[2], d_bin, rd));
+    PB_CHECK_CUDA(cp(b.bias[3], d_bout, d));
+    const float* ws[4] = {d_wqkv, d_wo, d_win, d_wout};
+    for (int m = 0; m < 4; ++m)
+        if (int rc = fill_matrix_f32(b.mat[m], ws[m], span->cfg.outlier_threshold, st)) return rc;
+    PB_CHECK_CUDA(cudaStreamSynchronize(st));
+    return PB_OK;
+}
+
+int pb_span_outliers(const pb_span* span, int32_t j, int32_t m, int32_t* h_idx, int32_t cap, int32_t* n) {
+    PB_REQUIRE(span && j >= 0 && j < span->cfg.n_blocks && m >= 0 && m < 4, PB_ERR_BAD_REQUEST, "bad index");
+    const Mat& mat = span->blocks[j].mat[m];
+    *n = mat.n_outl;
+    for (int i = 0; i < std::min(cap, mat.n_outl); ++i) h_idx[i] = mat.h_outl_idx[i];
+    return PB_OK;
+}
+
+int pb_span_read_codes(const pb_span* span, int32_t j, int32_t m, int8_t* h_codes, float* h_scales) {
+    PB_REQUIRE(span && j >= 0 && j < span->cfg.n_blocks && m >= 0 && m < 4, PB_ERR_BAD_REQUEST, "bad index");
+    const Mat& mat = span->blocks[j].mat[m];
+    PB_REQUIRE(mat.int8, PB_ERR_BAD_REQUEST, "span holds f32 weights");
+    PB_CHECK_CUDA(cudaSetDevice(span->cfg.device));
+    int8_t* tmp = nullptr;
+    PB_CHECK_CUDA(cudaMalloc(&tmp, (size_t)mat.M * mat.K));
+    int rc = untile_codes(mat, tmp, 0);
+    if (!rc && cudaMemcpy(h_codes, tmp, (size_t)mat.M * mat.K, cudaMemcpyDeviceToHost) != cudaSuccess)
+        rc = PB_ERR_GENERIC;
+    if (!rc && cudaMemcpy(h_scales, mat.scales, sizeof(float) * mat.K, cudaMemcpyDeviceToHost) != cudaSuccess)
+        rc = PB_ERR_GENERIC;
+    cudaFree(tmp);
+    return rc;
+}
+
+int32_t pb_span_last_launches(const pb_span* span) { return span ? span->last_launches : 0; }
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ step
+
+static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float* out, cudaStream_t st) {
+    const int d = s->d, rd = s->rd;
+    const bool int8 = s->cfg.weights == PB_WEIGHTS_INT8;
+    const int tc = choose_tc(n_tok);
+    int launches = 0;
+    for (int j = 0; j < s->cfg.n_blocks; ++j) {
+        BlockW& b = s->blocks[j];
+        const float* x_in = j == 0 ? in : s->xa;
+        float* x_out = j == s->cfg.n_blocks - 1 ? out : s->xa;
+        half* kvb = s->kv + s->kv_block_elems * j;
+        Epi base{};
+        base.n_outl = 0;
+        base.kv = kvb;
+        base.tok_seq = s->d_tok_seq;
+        base.tok_pos = s->d_tok_pos;
+        base.pages = s->d_pages;
+        base.max_pages = s->max_pages;
+        base.H = s->H;
+        base.dh = s->dh;
+        base.P = s->cfg.page_tokens;
+        base.d = d;
+        auto matmul = [&](int mi, int mode, const float* x, int K, const float* g, const float* be, Epi e) -> int {
+            const Mat& m = b.mat[mi];
+            e.M = m.M;
+            e.bias = b.bias[mi];
+            if (int8) {
+                e.n_outl = m.n_outl;
+                e.outl_idx = m.outl_idx;
+                e.outl_rows = m.outl_rows;
+                e.xo = s->xo;
+                if (int rc = launch_prologue(mode, x, n_tok, K, m.Kp, g, be, m, tc, s->frag, s->back, s->xo, nullptr, st))
+                    return rc;
+                Act a{s->frag, s->back, n_tok, tc};
+                launches += 2;
+                return launch_gemv(m, a, e, s->partials, s->counters, s->partial_cap, st);
+            }
+            if (int rc = launch_prologue(mode, x, n_tok, K, K, g, be, m, tc, nullptr, s->back, nullptr, s->y32, st))
+                return rc;
+            launches += 2;
+            return launch_gemm_f32(m, s->y32, n_tok, e, st);
+        };
+        Epi e = base;
+        e.kind = EPI_QKV;
+        e.out = s->q;
+        if (int rc = matmul(0, PRO_LN, x_in, d, b.ln1_g, b.ln1_b, e)) return rc;
+        AttnArgs aa{s->q, kvb, s->d_tok_seq, s->d_tok_pos, s->d_pages, s->slopes, s->ctx, s->attn_part,
+                    n_tok, s->max_pages, s->H, s->dh, s->cfg.page_tokens, d, max_pos};
+        if (int rc = launch_attention(aa, s->attn_cap, st)) return rc;
+        launches += 2;
+        e = base;
+        e.kind = EPI_RESID;
+        e.resid = x_in;
+        e.out = s->mid;
+        if (int rc = matmul(1, PRO_SCALE, s->ctx, d, nullptr, nullptr, e)) return rc;
+        e = base;
+        e.kind = EPI_GELU;
+        e.out = s->act;
+        if (int rc = matmul(2, PRO_LN, s->mid, d, b.ln2_g, b.ln2_b, e)) return rc;
+        e = base;
+        e.kind = EPI_RESID;
+        e.resid = s->mid;
+        e.out = x_out;
+        if (int rc = matmul(3, PRO_SCALE, s->act, rd, nullptr, nullptr, e)) return rc;
+    }
+    s->last_launches = launches;
+    return PB_OK;
+}
+
+static int stage_meta(pb_span* s, int n_tok, int n_seq, const int32_t* tok_seq, const int32_t* tok_pos,
+                      const int32_t* pages, int* max_pos, cudaStream_t st) {
+    PB_REQUIRE(n_tok > 0 && n_tok <= s->cfg.max_tokens, PB_ERR_CAPACITY, "too many tokens for this span's workspace");
+    PB_REQUIRE(n_seq > 0 && n_seq <= s->cfg.max_seqs, PB_ERR_CAPACITY, "too many sequences in one step");
+    int mp = 0;
+    for (int i = 0; i < n_tok; ++i) {
+        PB_REQUIRE(tok_seq[i] >= 0 && tok_seq[i] < n_seq, PB_ERR_BAD_REQUEST, "token sequence index out of range");
+        PB_REQUIRE(tok_pos[i] >= 0 && tok_pos[i] < s->cfg.max_seq, PB_ERR_CAPACITY, "position exceeds max_seq");
+        mp = std::max(mp, tok_pos[i] + 1);
+        const int32_t pg = pages[(int64_t)tok_seq[i] * s->max_pages + tok_pos[i] / s->cfg.page_tokens];
+        PB_REQUIRE(pg >= 0 && pg < s->cfg.n_pages, PB_ERR_BAD_REQUEST, "KV page out of range");
+    }
+    *max_pos = mp;
+    // pinned staging: the previous step's copies must have completed before we overwrite it
+    PB_CHECK_CUDA(cudaStreamSynchronize(st));
+    int32_t* hm = s->h_meta;
+    std::memcpy(hm, tok_seq, sizeof(int32_t) * n_tok);
+    std::memcpy(hm + n_tok, tok_pos, sizeof(int32_t) * n_tok);
+    std::memcpy(hm + 2 * n_tok, pages, sizeof(int32_t) * (size_t)n_seq * s->max_pages);
+    PB_CHECK_CUDA(cudaMemcpyAsync(s->d_tok_seq, hm, sizeof(int32_t) * n_tok, cudaMemcpyHostToDevice, st));
+    PB_CHECK_CUDA(cudaMemcpyAsync(s->d_tok_pos, hm + n_tok, sizeof(int32_t) * n_tok, cudaMemcpyHostToDevice, st));
+    PB_CHECK_CUDA(cudaMemcpyAsync(s->d_pages, hm + 2 * n_tok, sizeof(int32_t) * (size_t)n_seq * s->max_pages,
+                                  cudaMemcpyHostToDevice, st));
+    return PB_OK;
+}
+
+extern "C" int pb_span_step(pb_span* span, int32_t n_tok, int32_t n_seq, const int32_t* h_tok_seq,
+                            const int32_t* h_tok_pos, const int32_t* h_pages, const float* d_in, float* d_out,
+                            void* stream) {
+    PB_REQUIRE(span, PB_ERR_BAD_REQUEST, "null span");
+    std::lock_guard<std::mutex> lk(span->mu);
+    PB_CHECK_CUDA(cudaSetDevice(span->cfg.device));
+    auto st = (cudaStream_t)stream;
+    int max_pos = 0;
+    if (int rc = stage_meta(span, n_tok, n_seq, h_tok_seq, h_tok_pos, h_pages, &max_pos, st)) return rc;
+    return run_blocks(span, n_tok, max_pos, d_in, d_out, st);
+}
+
+extern "C" int pb_span_step_int8(pb_span* span, int32_t n_tok, int32_t n_seq, const int32_t* h_tok_seq,
+                                 const int32_t* h_tok_pos, const int32_t* h_pages, const int8_t* d_in_codes,
+                                 const float* d_in_scales, const float* d_in_f32, int8_t* d_out_codes,
+                                 float* d_out_scales, float* d_out_f32, void* stream) {
+    PB_REQUIRE(span, PB_ERR_BAD_REQUEST, "null span");
+    PB_REQUIRE(d_in_codes || d_in_f32, PB_ERR_BAD_REQUEST, "no input");
+    PB_REQUIRE(d_out_codes || d_out_f32, PB_ERR_BAD_REQUEST, "no output");
+    std::lock_guard<std::mutex> lk(span->mu);
+    PB_CHECK_CUDA(cudaSetDevice(span->cfg.device));
+    auto st = (cudaStream_t)stream;
+    int max_pos = 0;
+    if (int rc = stage_meta(span, n_tok, n_seq, h_tok_seq, h_tok_pos, h_pages, &max_pos, st)) return rc;
+    const int64_t n = (int64_t)n_tok * span->d;
+    int extra = 0;
+    const float* in = d_in_f32;
+    if (d_in_codes) {
+        // xa is the inter-block buffer: block 0 reads its input for the last
+        // time (wo residual) before its final GEMV overwrites xa.
+        if (int rc = dequantize_blockwise(d_in_codes, d_in_scales, n, 64, span->xa, st)) return rc;
+        in = span->xa;
+        ++extra;
+    }
+    float* out = d_out_f32 ? d_out_f32 : span->xa;
+    if (int rc = run_blocks(span, n_tok, max_pos, in, out, st)) return rc;
+    if (d_out_codes) {
+        if (int rc = quantize_blockwise(out, n, 64, d_out_codes, d_out_scales, st)) return rc;
+        ++extra;
+    }
+    span->last_launches += extra;
+    return PB_OK;
+}

@@ -1,0 +1,114 @@
+// Internal structures of a block span (not part of the C-ABI).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+namespace pb {
+
+// One weight matrix of a block, reference shape W = [K = in, M = out].
+struct Mat {
+    int M = 0, K = 0, Mp = 0, Kp = 0;  // padded: Mp % 16 == 0, Kp % 32 == 0
+    bool int8 = true;
+    int8_t* codes = nullptr;   // fragment-tiled [Mp/16][Kp/32][512 B] (int8 mode)
+    float* scales = nullptr;   // [Kp] per input feature, 0 on outliers / padding
+    float* w32 = nullptr;      // [K][M] reference layout (f32 mode)
+    int n_outl = 0;
+    int32_t* outl_idx = nullptr;   // [n_outl] input features kept in f32
+    float* outl_rows = nullptr;    // [n_outl][M] = W[idx_j, :]
+    std::vector<int32_t> h_outl_idx;
+
+    void free_outliers() {
+        if (outl_idx) cudaFree(outl_idx);
+        if (outl_rows) cudaFree(outl_rows);
+        outl_idx = nullptr;
+        outl_rows = nullptr;
+        n_outl = 0;
+        h_outl_idx.clear();
+    }
+    int64_t bytes() const {
+        int64_t b = (int64_t)Kp * 4;
+        if (int8) b += (int64_t)Mp * Kp;
+        else b += (int64_t)K * M * 4;
+        return b + (int64_t)n_outl * (M * 4 + 4);
+    }
+};
+
+struct BlockW {
+    Mat mat[4];  // 0 wqkv [d,3d], 1 wo [d,d], 2 wmlp_in [d,rd], 3 wmlp_out [rd,d]
+    float* ln1_g = nullptr;
+    float* ln1_b = nullptr;
+    float* ln2_g = nullptr;
+    float* ln2_b = nullptr;
+    float* bias[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_GELU = 2 };
+
+// Epilogue parameters shared by every GEMV/GEMM flavour.
+struct Epi {
+    int kind;
+    int M;                   // output features
+    const float* bias;       // [M]
+    int n_outl;
+    const int32_t* outl_idx;
+    const float* outl_rows;  // [n_outl][M]
+    const float* xo;         // [n_tok][n_outl] unscaled activations at outlier features
+    const float* resid;      // EPI_RESID: [n_tok][M]
+    float* out;              // EPI_RESID/EPI_GELU: [n_tok][M]; EPI_QKV: q [n_tok][d]
+    // EPI_QKV: append k, v to the paged cache
+    half* kv;                // this block's pool base: [n_pages][2][H][P][dh]
+    const int32_t* tok_seq;
+    const int32_t* tok_pos;
+    const int32_t* pages;    // [n_seq][max_pages]
+    int max_pages, H, dh, P, d;
+};
+
+// B-operand (activation) layout parameters for one GEMV launch.
+struct Act {
+    const uint4* frag;      // hi/lo f16 fragments, see pb_gemv.cu
+    const float* back;      // [n_tok] 2^-shift per token
+    int n_tok;
+    int tc;                 // tokens per column chunk (4, 8, 16, 32)
+};
+
+// prologue modes
+enum ProMode { PRO_LN = 0, PRO_SCALE = 1 };
+
+int fill_matrix_gen(Mat& m, uint64_t key, float threshold, float boost, int every, cudaStream_t st);
+int fill_matrix_f32(Mat& m, const float* w, float threshold, cudaStream_t st);
+int untile_codes(const Mat& m, int8_t* d_out, cudaStream_t st);
+
+int quantize_blockwise(const float* x, int64_t n, int block, int8_t* codes, float* scales, cudaStream_t st);
+int dequantize_blockwise(const int8_t* codes, const float* scales, int64_t n, int block, float* out,
+                         cudaStream_t st);
+
+// prologue: y = LN(x) (PRO_LN) or x (PRO_SCALE); writes hi/lo fragments of
+// y * scales, the per-token 2^-shift, outlier activations xo, and (f32 mode) y.
+int launch_prologue(int mode, const float* x, int n_tok, int K, int Kp, const float* gamma, const float* beta,
+                    const Mat& m, int tc, uint4* frag, float* back, float* xo, float* y32, cudaStream_t st);
+int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
+                int64_t partial_cap, cudaStream_t st);
+int launch_gemm_f32(const Mat& m, const float* y, int n_tok, const Epi& epi, cudaStream_t st);
+int choose_tc(int n_tok);
+
+// attention over the paged cache
+struct AttnArgs {
+    const float* q;          // [n_tok][d]
+    const half* kv;          // block pool base
+    const int32_t* tok_seq;
+    const int32_t* tok_pos;
+    const int32_t* pages;
+    const float* slopes;     // [H]
+    float* ctx;              // [n_tok][d]
+    float* part;             // split workspace
+    int n_tok, max_pages, H, dh, P, d;
+    int max_pos;             // max over tokens of (pos + 1)
+};
+int launch_attention(const AttnArgs& a, int64_t part_cap, cudaStream_t st);
+int64_t attention_part_floats(int n_tok, int H, int dh, int max_seq);
+
+}  // namespace pb
