@@ -1,0 +1,565 @@
+"""Span server: the drop-in for the reference's ServerNode compute path
+(/root/reference/pkg/src/swarmlm/server.py:48-450), same constructor shape,
+same RPC messages, same session semantics and error codes, with the hosted
+blocks executed by a B200 BlockSpan.
+
+Kept from the reference (restated, not imported):
+  OPEN_SESSION / STEP / CLOSE_SESSION / FORWARD / INFO / PING handlers
+  (server.py:295-429), idempotent STEP retry by sha256 digest
+  (server.py:367,374-377), DESYNC / CAPACITY / BUSY / UNKNOWN_SESSION codes,
+  LRU cache-budget eviction (server.py:397-407), idle-session janitor
+  (server.py:223-233), registry announcements (server.py:171-195).
+Changed for the B200:
+  sessions' KV caches are pages of one HBM pool; concurrent STEPs of different
+  sessions are coalesced into one batched span step by a scheduler thread;
+  the int8 wire codec runs on the GPU; FORWARD runs on the span's weights.
+Out of scope: BACKWARD (a "next" row), rebalancing/allocation
+(control plane); maybe_rebalance() reports no move.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import logging
+import os
+import queue
+import struct
+import threading
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import codec
+from .errors import (
+    ERR_BAD_REQUEST,
+    ERR_BUSY,
+    ERR_CAPACITY,
+    ERR_DESYNC,
+    ERR_UNKNOWN_SESSION,
+    CapacityError,
+    InputError,
+    RemoteError,
+    SwarmError,
+)
+from .model import ModelConfig
+from .rpc import RpcServer, call
+from .span import BlockSpan
+from .wire import MSG
+
+log = logging.getLogger(__name__)
+
+DEFAULT_CAPACITY = 64
+DEFAULT_CACHE_BUDGET = 65536
+SESSION_IDLE_TIMEOUT_S = 120.0
+SERVER_VERSION = "0.1.0-b200"
+DEFAULT_NET_BYTES_PER_S = 1.25e8
+DEFAULT_TTL_MS = 30_000
+TOMBSTONE_TTL_MS = 10_000
+
+
+@dataclass(frozen=True, order=True)
+class BlockRange:
+    start: int
+    end: int
+
+    def __len__(self) -> int:
+        return self.end - self.start
+
+
+@dataclass
+class ServerConfig:
+    """Reference fields (server.py:48-66) plus B200 knobs."""
+
+    checkpoint_path: str = ""
+    host: str = "127.0.0.1"
+    port: int = 0
+    blocks: object = "auto"  # "auto" (whole model) or (start, end)
+    span: int | None = None
+    quantize: str = "none"  # none | activations | weights | both
+    bootstrap: list = field(default_factory=list)
+    shape: object = None  # link shaping is not emulated on the box
+    capacity: int = DEFAULT_CAPACITY
+    cache_budget_tokens: int = DEFAULT_CACHE_BUDGET
+    ttl_ms: int = DEFAULT_TTL_MS
+    gossip_period_ms: int = 2_000
+    rebalance_eps: float = 0.2
+    rebalance_period_s: tuple = (5.0, 10.0)
+    measure_steps: int = 100
+    net_bytes_per_s: float = DEFAULT_NET_BYTES_PER_S
+    remeasure_period_s: float = 60.0
+    # B200 additions
+    seed: int | None = None           # generate gen_checkpoint(seed) weights on device
+    model: ModelConfig | None = None  # shape when generating
+    device: int = 0
+    page_tokens: int = 64
+    max_batch_tokens: int = 256
+    kv_pages: int | None = None
+
+
+# ------------------------------------------------------------------ checkpoints
+
+
+def read_ptck(path: str, block_range=None):
+    """Parse a PTCK file (model.py:213-264 layout, restated): returns
+    (ModelConfig, {block_index: {name: f32 array}}) for the requested blocks only."""
+    with open(path, "rb") as f:
+        data = f.read()
+    if data[:4] != b"PTCK":
+        raise InputError("not a checkpoint file (bad magic)")
+    if data[4] != 1:
+        raise InputError(f"unsupported checkpoint version {data[4]}")
+    L, d, h, v, ms, r = struct.unpack(">6I", data[5:29])
+    cfg = ModelConfig(L, d, h, v, ms, r)
+    off = 29 + 4 * v * d  # skip embed
+    names = [("ln1_gamma", d), ("ln1_beta", d), ("wqkv", d * 3 * d), ("bqkv", 3 * d), ("wo", d * d), ("bo", d),
+             ("ln2_gamma", d), ("ln2_beta", d), ("wmlp_in", d * r * d), ("bmlp_in", r * d),
+             ("wmlp_out", r * d * d), ("bmlp_out", d)]
+    shapes = {"wqkv": (d, 3 * d), "wo": (d, d), "wmlp_in": (d, r * d), "wmlp_out": (r * d, d)}
+    per_block = sum(n for _, n in names)
+    want = set(range(*block_range)) if block_range else set(range(L))
+    blocks = {}
+    for i in range(L):
+        if i in want:
+            o = off
+            arrs = {}
+            for nm, n in names:
+                a = np.frombuffer(data, "<f4", count=n, offset=o).astype(np.float32)
+                arrs[nm] = a.reshape(shapes.get(nm, (n,)))
+                o += 4 * n
+            blocks[i] = arrs
+        off += 4 * per_block
+    if off + 8 * d != len(data):
+        raise InputError("checkpoint size mismatch")
+    return cfg, blocks
+
+
+class _BlockView:
+    def __init__(self, d: dict):
+        self.__dict__.update(d)
+
+
+def _block_tensors(b):
+    """(name, f32 array) in the checkpoint traversal order (model.py:102-117)."""
+    names = ["ln1_gamma", "ln1_beta", "wqkv", "bqkv", "wo", "bo", "ln2_gamma", "ln2_beta", "wmlp_in", "bmlp_in",
+             "wmlp_out", "bmlp_out"]
+    return [(n, np.asarray(getattr(b, n), np.float32)) for n in names]
+
+
+# ------------------------------------------------------------------ sessions / scheduling
+
+
+class _Session:
+    def __init__(self, sid: bytes, seq, max_len: int):
+        self.session_id = sid
+        self.seq = seq
+        self.position = 0
+        self.max_len = max_len
+        self.last_active = time.monotonic()
+        self.lock = threading.Lock()
+        self.last_step = None  # (start_pos, digest, reply)
+
+
+class _Job:
+    __slots__ = ("seq", "x", "out", "err", "done")
+
+    def __init__(self, seq, x):
+        self.seq, self.x = seq, x
+        self.out = self.err = None
+        self.done = threading.Event()
+
+
+class StepScheduler:
+    """Coalesces concurrent STEPs of distinct sessions into one batched span
+    step (one launch sequence per block for the whole batch)."""
+
+    def __init__(self, span: BlockSpan, max_tokens: int, max_seqs: int):
+        self.span, self.max_tokens, self.max_seqs = span, max_tokens, max_seqs
+        self.q: queue.Queue = queue.Queue()
+        self.batches = 0
+        self.batched_steps = 0
+        self._stop = False
+        self._t = threading.Thread(target=self._loop, daemon=True)
+        self._t.start()
+
+    def run(self, seq, x):
+        job = _Job(seq, x)
+        self.q.put(job)
+        job.done.wait()
+        if job.err is not None:
+            raise job.err
+        return job.out
+
+    def stop(self):
+        self._stop = True
+        self.q.put(None)
+
+    def _loop(self):
+        import torch
+
+        torch.cuda.set_device(self.span.device)
+        pending = None
+        while not self._stop:
+            job = pending or self.q.get()
+            pending = None
+            if job is None:
+                break
+            batch, ntok = [job], job.x.shape[0]
+            while len(batch) < self.max_seqs:
+                try:
+                    nxt = self.q.get_nowait()
+                except queue.Empty:
+                    break
+                if nxt is None:
+                    self._stop = True
+                    break
+                if ntok + nxt.x.shape[0] > self.max_tokens:
+                    pending = nxt
+                    break
+                batch.append(nxt)
+                ntok += nxt.x.shape[0]
+            try:
+                outs = self.span.step([(j.seq, j.x) for j in batch])
+                torch.cuda.current_stream(self.span.device).synchronize()
+                for j, o in zip(batch, outs):
+                    j.out = o
+            except Exception as e:  # noqa: BLE001
+                for j in batch:
+                    j.err = e
+            self.batches += 1
+            self.batched_steps += len(batch)
+            for j in batch:
+                j.done.set()
+
+
+# ------------------------------------------------------------------ server
+
+
+class ServerNode:
+    def __init__(self, config: ServerConfig, checkpoint=None):
+        self.config = config
+        self.server_id = os.urandom(16).hex()
+        self.events: list = []
+        self.throughput = 0.0
+        self.range: BlockRange | None = None
+        self._sessions: dict = {}
+        self._sessions_lock = threading.Lock()
+        self._stop = threading.Event()
+        self._registry: dict = {}
+        self._registry_lock = threading.Lock()
+        self.rpc: RpcServer | None = None
+        self._ckpt = checkpoint
+        self._blocks_host = None
+        if checkpoint is not None:
+            self.model = checkpoint.config
+        elif config.seed is not None:
+            if config.model is None:
+                raise InputError("seed-generated weights need ServerConfig.model")
+            self.model = config.model
+        else:
+            if not os.path.exists(config.checkpoint_path):
+                raise InputError(f"checkpoint {config.checkpoint_path!r} not found")
+            self.model, _ = read_ptck(config.checkpoint_path, (0, 0))
+        self.model = ModelConfig(self.model.n_layers, self.model.hidden, self.model.n_heads, self.model.vocab,
+                                 self.model.max_seq, self.model.mlp_ratio)
+        self.span: BlockSpan | None = None
+        self._weights_hash = None
+
+    # ---------------------------------------------------------------- lifecycle
+
+    def _pick_range(self) -> BlockRange:
+        L = self.model.n_layers
+        if self.config.blocks != "auto":
+            s, e = self.config.blocks
+            if not (0 <= s < e <= L):
+                raise InputError(f"explicit block range [{s}, {e}) outside [0, {L})")
+            return BlockRange(s, e)
+        k = self.config.span or L
+        if k > L:
+            raise InputError("span exceeds layer count")
+        return BlockRange(0, k)  # allocation policy is control plane (out of scope)
+
+    def start(self) -> "ServerNode":
+        import torch
+
+        self.range = self._pick_range()
+        n = len(self.range)
+        int8 = self.config.quantize in ("weights", "both")
+        pos_budget = max(1, self.config.cache_budget_tokens // n)
+        pages = self.config.kv_pages or (-(-pos_budget // self.config.page_tokens) + self.config.capacity + 2)
+        torch.cuda.set_device(self.config.device)
+        self.span = BlockSpan(self.model, self.range.start, self.range.end, int8=int8,
+                              page_tokens=self.config.page_tokens, n_pages=pages,
+                              max_tokens=self.config.max_batch_tokens, max_seqs=max(1, self.config.capacity),
+                              device=self.config.device)
+        self._load_weights()
+        self.sched = StepScheduler(self.span, self.config.max_batch_tokens, max(1, self.config.capacity))
+        self.rpc = RpcServer(self.config.host, self.config.port, self._dispatch).start()
+        self._announce("joining", throughput=1e-6)
+        self.throughput = self.measure_throughput()
+        self._announce("online")
+        for target in (self._announce_loop, self._janitor_loop):
+            threading.Thread(target=target, daemon=True).start()
+        log.info("b200 server %s serving blocks [%d, %d) at %s", self.server_id[:8], self.range.start,
+                 self.range.end, self.address)
+        return self
+
+    def _load_weights(self):
+        if self.config.seed is not None and self._ckpt is None:
+            self.span.generate_weights(self.config.seed)
+            h = hashlib.sha256(f"gen:{self.config.seed}:{self.model}:{self.range}".encode())
+            self._weights_hash = h.hexdigest()
+            return
+        if self._ckpt is not None:
+            blocks = [self._ckpt.blocks[i] for i in range(self.range.start, self.range.end)]
+        else:
+            _, bl = read_ptck(self.config.checkpoint_path, (self.range.start, self.range.end))
+            blocks = [_BlockView(bl[i]) for i in range(self.range.start, self.range.end)]
+        h = hashlib.sha256()  # server.py:286-291
+        for b in blocks:
+            for _, arr in _block_tensors(b):
+                h.update(np.ascontiguousarray(arr, "<f4").tobytes())
+        self._weights_hash = h.hexdigest()
+        self.span.load_weights(blocks)
+
+    @property
+    def address(self) -> str:
+        return self.rpc.address
+
+    def stop(self):
+        if self._stop.is_set():
+            return
+        try:
+            self._announce("offline", ttl_ms=TOMBSTONE_TTL_MS)
+        except SwarmError:
+            pass
+        self._shutdown()
+
+    def kill(self):
+        self._shutdown()
+
+    def _shutdown(self):
+        self._stop.set()
+        if self.rpc:
+            self.rpc.stop()
+        if getattr(self, "sched", None):
+            self.sched.stop()
+
+    # ---------------------------------------------------------------- registry
+
+    def _entry(self, state: str, throughput=None, ttl_ms=None) -> dict:
+        return {
+            "id": self.server_id, "address": self.address, "start": self.range.start, "end": self.range.end,
+            "throughput": throughput if throughput is not None else max(self.throughput, 1e-6),
+            "announced_at": int(time.time() * 1000), "ttl_ms": ttl_ms or self.config.ttl_ms, "state": state,
+        }
+
+    def _remember(self, entry: dict):
+        with self._registry_lock:
+            mine = self._registry.get(entry["id"])
+            if mine is None or entry["announced_at"] >= mine["announced_at"]:
+                self._registry[entry["id"]] = entry
+
+    def _announce(self, state: str, throughput=None, ttl_ms=None):
+        entry = self._entry(state, throughput, ttl_ms)
+        self._remember(entry)
+        self.events.append({"t": entry["announced_at"], "event": "announce", "state": state,
+                            "range": [self.range.start, self.range.end]})
+        payload = json.dumps(entry).encode()
+        for peer in self.config.bootstrap:
+            try:
+                call(peer, MSG.ANNOUNCE, payload, 3000.0)
+            except SwarmError as e:
+                log.debug("announce to %s failed: %s", peer, e)
+
+    def _announce_loop(self):
+        period = self.config.ttl_ms / 3000.0
+        while not self._stop.wait(period):
+            self._announce("online")
+
+    def _janitor_loop(self):
+        while not self._stop.wait(5.0):
+            now = time.monotonic()
+            with self._sessions_lock:
+                stale = [sid for sid, s in self._sessions.items() if now - s.last_active > SESSION_IDLE_TIMEOUT_S]
+                victims = [self._sessions.pop(sid) for sid in stale]
+            for v in victims:
+                self.span.release(v.seq)
+
+    def maybe_rebalance(self) -> bool:
+        return False  # allocation/rebalancing is control plane (out of scope)
+
+    # ---------------------------------------------------------------- measurement
+
+    def measure_throughput(self) -> float:
+        """min(compute, network) tokens/s over the hosted span (server.py:262-282),
+        compute measured with single-token steps on the GPU."""
+        import torch
+
+        steps = max(1, min(self.config.measure_steps, self.model.max_seq))
+        seq = self.span.new_sequence()
+        x = torch.zeros(1, self.model.hidden, device=self.span.device)
+        try:
+            self.span.step([(seq, x)])  # warm-up
+            torch.cuda.synchronize(self.span.device)
+            t0 = time.perf_counter()
+            for _ in range(min(steps, self.model.max_seq - 1)):
+                self.span.step([(seq, x)])
+            torch.cuda.synchronize(self.span.device)
+            compute = max(1, min(steps, self.model.max_seq - 1)) / max(time.perf_counter() - t0, 1e-9)
+        finally:
+            self.span.release(seq)
+        net = self.config.net_bytes_per_s
+        return min(compute, net / (4.0 * self.model.hidden))
+
+    def weights_hash(self) -> str:
+        return self._weights_hash
+
+    # ---------------------------------------------------------------- RPC
+
+    def _dispatch(self, msg_type: int, payload: bytes):
+        if msg_type == MSG.PING:
+            return MSG.PING, b""
+        if msg_type == MSG.INFO:
+            return MSG.INFO, self._info_payload()
+        if msg_type == MSG.OPEN_SESSION:
+            return MSG.OPEN_SESSION, self._open_session(payload)
+        if msg_type == MSG.STEP:
+            return MSG.STEP, self._step(payload)
+        if msg_type == MSG.CLOSE_SESSION:
+            return MSG.CLOSE_SESSION, self._close_session(payload)
+        if msg_type == MSG.FORWARD:
+            return MSG.FORWARD, self._forward(payload)
+        if msg_type == MSG.BACKWARD:
+            raise RemoteError(ERR_BAD_REQUEST, "BACKWARD is not served by the B200 span server")
+        if msg_type == MSG.ANNOUNCE:
+            self._remember(json.loads(payload.decode()))
+            return MSG.ANNOUNCE, b""
+        if msg_type == MSG.LOOKUP:
+            q = json.loads(payload.decode())
+            return MSG.LOOKUP, json.dumps(self._lookup(q["start"], q["end"])).encode()
+        if msg_type == MSG.GOSSIP:
+            for e in json.loads(payload.decode()):
+                self._remember(e)
+            with self._registry_lock:
+                snap = sorted(self._registry.values(), key=lambda e: e["id"])
+            return MSG.GOSSIP, json.dumps(snap, sort_keys=True).encode()
+        raise RemoteError(ERR_BAD_REQUEST, f"unknown message type 0x{msg_type:02x}")
+
+    def _lookup(self, start: int, end: int):
+        now = int(time.time() * 1000)
+        with self._registry_lock:
+            hits = [e for e in self._registry.values() if e["state"] == "online"
+                    and now < e["announced_at"] + e["ttl_ms"] and e["start"] < end and start < e["end"]]
+        return sorted(hits, key=lambda e: (e["start"], e["id"]))
+
+    def _info_payload(self) -> bytes:
+        return json.dumps({
+            "server_id": self.server_id, "range": [self.range.start, self.range.end],
+            "throughput": self.throughput, "position_capacity": self.config.cache_budget_tokens,
+            "version": SERVER_VERSION, "weights_hash": self.weights_hash(), "quantize": self.config.quantize,
+        }).encode()
+
+    def _reply_encoding(self) -> int:
+        return codec.ENC_INT8 if self.config.quantize in ("activations", "both") else codec.ENC_F32
+
+    def _open_session(self, payload: bytes) -> bytes:
+        if len(payload) != 20:
+            raise RemoteError(ERR_BAD_REQUEST, "OPEN_SESSION wants 16-byte id + u32 max_len")
+        sid, (max_len,) = payload[:16], struct.unpack(">I", payload[16:])
+        if max_len < 1 or max_len > self.model.max_seq:
+            raise RemoteError(ERR_BAD_REQUEST, f"max_len must be in [1, {self.model.max_seq}]")
+        with self._sessions_lock:
+            if sid in self._sessions:
+                raise RemoteError(ERR_BAD_REQUEST, "duplicate session id")
+            if len(self._sessions) >= self.config.capacity:
+                raise RemoteError(ERR_BUSY, "session capacity exhausted")
+            self._sessions[sid] = _Session(sid, self.span.new_sequence(), max_len)
+        return b""
+
+    def _get_session(self, sid: bytes) -> _Session:
+        with self._sessions_lock:
+            s = self._sessions.get(sid)
+        if s is None:
+            raise RemoteError(ERR_UNKNOWN_SESSION, "unknown session")
+        return s
+
+    def _step(self, payload: bytes) -> bytes:
+        if len(payload) < 20:
+            raise RemoteError(ERR_BAD_REQUEST, "short STEP payload")
+        sid = payload[:16]
+        (start_pos,) = struct.unpack(">I", payload[16:20])
+        session = self._get_session(sid)
+        digest = hashlib.sha256(payload[20:]).digest()
+        try:
+            _, dims, _, _, _ = codec.parse_tensor(payload[20:])
+        except SwarmError as e:
+            raise RemoteError(ERR_BAD_REQUEST, str(e)) from e
+        if len(dims) != 2:
+            raise RemoteError(ERR_BAD_REQUEST, "STEP tensor must be 2-D [t, d]")
+        t = dims[0]
+        with session.lock:
+            session.last_active = time.monotonic()
+            if session.last_step is not None and start_pos + t == session.position:
+                last_pos, last_digest, last_reply = session.last_step
+                if last_pos == start_pos and last_digest == digest:
+                    return last_reply
+            if start_pos != session.position:
+                raise RemoteError(ERR_DESYNC, f"position mismatch: got {start_pos}, have {session.position}")
+            if start_pos + t > session.max_len:
+                raise RemoteError(ERR_CAPACITY, "session exceeds max_len")
+            if dims[1] != self.model.hidden:
+                raise RemoteError(ERR_BAD_REQUEST, f"hidden must be [t, {self.model.hidden}]")
+            with self._sessions_lock:
+                if self._sessions.get(sid) is not session:
+                    raise RemoteError(ERR_UNKNOWN_SESSION, "session evicted")
+            x = codec.decode_tensor(payload[20:], device=self.span.device)
+            try:
+                out = self.sched.run(session.seq, x)
+            except CapacityError as e:
+                raise RemoteError(ERR_BUSY, f"KV pool exhausted: {e}") from e
+            except InputError as e:
+                raise RemoteError(ERR_BAD_REQUEST, str(e)) from e
+            session.position += t
+            reply = codec.encode_tensor(out, self._reply_encoding())
+            session.last_step = (start_pos, digest, reply)
+        self._enforce_cache_budget()
+        return reply
+
+    def _close_session(self, payload: bytes) -> bytes:
+        with self._sessions_lock:
+            s = self._sessions.pop(payload[:16], None)
+        if s is not None:
+            with s.lock:
+                self.span.release(s.seq)
+        return b""
+
+    def _enforce_cache_budget(self):
+        n = len(self.range)
+        victims = []
+        with self._sessions_lock:
+            total = sum(s.position * n for s in self._sessions.values())
+            if total > self.config.cache_budget_tokens:
+                for v in sorted(self._sessions.values(), key=lambda s: s.last_active):
+                    del self._sessions[v.session_id]
+                    victims.append(v)
+                    total -= v.position * n
+                    if total <= self.config.cache_budget_tokens:
+                        break
+        for v in victims:
+            with v.lock:
+                self.span.release(v.seq)
+
+    def _forward(self, payload: bytes) -> bytes:
+        try:
+            batch = codec.decode_tensor(payload, device=self.span.device)
+        except SwarmError as e:
+            raise RemoteError(ERR_BAD_REQUEST, str(e)) from e
+        if batch.ndim != 3:
+            raise RemoteError(ERR_BAD_REQUEST, "FORWARD tensor must be [B, t, d]")
+        try:
+            out = self.span.forward(batch)
+        except CapacityError as e:
+            raise RemoteError(ERR_CAPACITY, str(e)) from e
+        return os.urandom(16) + codec.encode_tensor(out, self._reply_encoding())

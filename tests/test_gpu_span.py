@@ -86,9 +86,14 @@ def test_loaded_outlier_weights_bit_exact():
             assert np.array_equal(codes, want.codes)
             assert np.array_equal(scales.view(np.uint32), want.scales.view(np.uint32))
             assert np.array_equal(span.outliers(j, m), want.outlier_idx)
-    # forward with outliers vs the oracle int8 path
+    # forward with outliers vs the oracle int8 path. The x200 outlier features
+    # make q.k scores O(10^3), where the fp16 KV cache itself moves the softmax;
+    # compare against the oracle with the same fp16 rounding of K/V.
     x = rng.normal(size=(7, shape.hidden)).astype(np.float32)
-    want = O.forward_span(blocks, x, shape, quantized=True)
+    f16 = lambda a: a.astype(np.float16).astype(np.float32)  # noqa: E731
+    want = x
+    for b in blocks:
+        want = O.block_step(b, want, O.KV(shape), 0, shape, O.QuantBlock(b), kv_round=f16)
     got = span.forward(torch.from_numpy(x).cuda()[None])[0].cpu().numpy()
     assert rel_err(got, want) <= TOL
     span.close()
