@@ -1,0 +1,413 @@
+"""Headline benchmark: BLOOM-176B-shape int8 decode steps/s (BASELINE.json).
+
+Workload (N GPUs, one process per GPU): the 70-block 176B-shape model
+(h=14336, H=112, int8 weights generated on device from the reference's
+SplitMix64 streams) is split into N contiguous block spans, one per GPU
+(N=1: all 70 blocks on one B200). N batch-1 sessions are in flight (one per
+pipeline stage, "weak" scaling: per-GPU work is constant), each decoding at a
+context that ends at --ctx (default 2048). A step is one decode token of one
+session through all 70 blocks; span-to-span hops carry the hidden state as
+the reference's blockwise int8 wire codec over NCCL send/recv (the last span
+hands the result back to span 0, which closes the ring for the next token).
+
+value = session-steps/s over all GPUs (b=1 per session) measured with CUDA
+events between barriers, max over ranks. e2e = same metric through the
+server's STEP handler with host bytes in/out (N=1) or with pinned-host
+ingress/egress copies at the pipeline ends (N>1).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BLOOM-176B int8 decode steps/s (b=1)"
+UNIT = "steps/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--shape", default="bloom-176b")
+    p.add_argument("--ctx", type=int, default=2048)
+    p.add_argument("--seed", type=int, default=42)
+    p.add_argument("--prefill-chunk", type=int, default=256)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--synthetic-kv", action="store_true", help="skip the real prefill (KV content is synthetic)")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+
+
+def split_blocks(L: int, n: int):
+    base, extra = divmod(L, n)
+    out, s = [], 0
+    for r in range(n):
+        k = base + (1 if r < extra else 0)
+        out.append((s, s + k))
+        s += k
+    return out
+
+
+def bytes_per_step(cfg, ctx_tokens_per_session):
+    """sum_blocks [12h^2 codes + 7h*4 scales + 13h*4 bias/LN]
+    + sum_sessions sum_blocks 2*T*h*2 (fp16 K+V)."""
+    h, L = cfg.hidden, cfg.n_layers
+    w = L * (12 * h * h + 7 * h * 4 + 13 * h * 4)
+    kv = sum(L * 2 * T * h * 2 for T in ctx_tokens_per_session)
+    return w, kv
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.samples, self._stop = index, [], threading.Event()
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([v.strip() for v in out.stdout.strip().split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+def committed_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+# ------------------------------------------------------------------ CPU legs (oracle port)
+
+
+def cpu_block_sample(cfg, ctx_sample):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import cpu_baseline
+
+    return cpu_baseline.BlockSample(cfg.hidden, cfg.n_heads, ctx_sample, cfg.mlp_ratio), cpu_baseline.cores()
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU arithmetic (oracle port of
+    block_forward(qw) / matmul_mixed) on the host cores; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2209_01188_b200.model import SHAPES
+
+    cfg = SHAPES[args.shape]
+    ctx_sample = 128
+    sample, ncores = cpu_block_sample(cfg, ctx_sample)
+    for _ in range(args.warmup):
+        sample.step_seconds()
+    ts = [sample.step_seconds() for _ in range(args.steps)]
+    per_block = min(ts)  # best case for the CPU (OpenBLAS timings are noisy)
+    value = 1.0 / (per_block * cfg.n_layers)
+    desc = (f"1 block of the {args.shape} shape, int8 decode t=1 at context {ctx_sample} (oracle port of "
+            f"quant.py matmul_mixed + model.py block_forward, random codes), x{cfg.n_layers} blocks extrapolated")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_block * cfg.n_layers * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": f"{args.shape} int8 decode b=1 (CPU reference arithmetic)",
+                                        "ctx": ctx_sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU pipeline
+
+
+class Pipeline:
+    def __init__(self, args, cfg):
+        import torch
+        import torch.distributed as dist
+
+        from paper_2209_01188_b200.span import BlockSpan
+
+        self.args, self.cfg = args, cfg
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=self.dev)
+        self.dist = dist if self.world > 1 else None
+        self.S = self.world  # sessions in flight
+        self.ranges = split_blocks(cfg.n_layers, self.world)
+        s, e = self.ranges[self.rank]
+        pages_per_seq = -(-cfg.max_seq // 64)
+        t0 = time.perf_counter()
+        self.span = BlockSpan(cfg, s, e, int8=True, page_tokens=64, n_pages=self.S * pages_per_seq + 2,
+                              max_tokens=args.prefill_chunk, max_seqs=max(self.S, 1), device=self.local)
+        self.span.generate_weights(args.seed)
+        torch.cuda.synchronize()
+        self.gen_s = time.perf_counter() - t0
+        self.seqs = [self.span.new_sequence() for _ in range(self.S)]
+        d = cfg.hidden
+        self.d = d
+        self.codes = torch.empty(args.prefill_chunk * d, dtype=torch.int8, device=self.dev)
+        self.scales = torch.empty(-(-args.prefill_chunk * d // 64), dtype=torch.float32, device=self.dev)
+        self.rcodes = torch.empty_like(self.codes)
+        self.rscales = torch.empty_like(self.scales)
+        self.out = torch.empty(args.prefill_chunk, d, dtype=torch.float32, device=self.dev)
+        g = torch.Generator(device=self.dev)
+        g.manual_seed(7)
+        self.inputs = torch.randn(64, d, generator=g, device=self.dev) * 0.05  # embedding-like rows
+        self.launches = 0
+
+    def barrier(self):
+        import torch
+
+        torch.cuda.synchronize()
+        if self.dist:
+            self.dist.barrier()
+        torch.cuda.synchronize()
+
+    def job(self, j: int, t: int, x=None, host_in=None, host_out=None):
+        """Job j = session j % S; receive (unless first stage of a fresh session),
+        run the span, send the int8 hidden to the next stage (ring)."""
+        r, N = self.rank, self.world
+        seq = self.seqs[j % self.S]
+        n = t * self.d
+        nb = -(-n // 64)
+        codes, scales = self.rcodes[:n], self.rscales[:nb]
+        if r > 0 or (N > 1 and j >= self.S):
+            src = (r - 1) % N
+            self.dist.recv(codes, src)
+            self.dist.recv(scales, src)
+        if r == 0:
+            if host_in is not None:
+                self.out[:t].copy_(host_in[:t], non_blocking=True)
+                x = self.out[:t]
+            inp = x if x is not None else self.inputs[j % 64: j % 64 + 1].expand(t, self.d).contiguous()
+            self.span.step_codes([(seq, None)], [t], out_codes=self.codes[:n], out_scales=self.scales[:nb],
+                                 in_f32=inp, out_f32=self.out[:t])
+        else:
+            self.span.step_codes([(seq, (codes, scales))], [t], out_codes=self.codes[:n],
+                                 out_scales=self.scales[:nb], out_f32=self.out[:t])
+        self.launches += self.span.last_launches
+        if host_out is not None and r == N - 1:
+            host_out[:n].copy_(self.codes[:n], non_blocking=True)
+        if N > 1 and (r < N - 1 or j + self.S < self.total_jobs):
+            dst = (r + 1) % N
+            self.dist.send(self.codes[:n], dst)
+            self.dist.send(self.scales[:nb], dst)
+
+    def run_jobs(self, jobs, **kw):
+        for j, t in jobs:
+            self.job(j, t, **kw)
+
+
+def run_ours(args):
+    import torch
+
+    from paper_2209_01188_b200.model import SHAPES
+
+    cfg = SHAPES[args.shape]
+    pl = Pipeline(args, cfg)
+    S, N, rank = pl.S, pl.world, pl.rank
+    K, W = args.steps, args.warmup
+    T0 = args.ctx - (W + K) - (0 if args.no_e2e else K) - 1
+    if T0 < 1:
+        raise SystemExit("--ctx too small for warmup+steps")
+    # ---- prefill every session to T0 through the pipeline (untimed)
+    t_pf = time.perf_counter()
+    if args.synthetic_kv:
+        for s in pl.seqs:
+            pl.span._reserve(s, T0)
+            s.length = T0
+    else:
+        chunks = []
+        left = T0
+        while left > 0:
+            c = min(args.prefill_chunk, left)
+            chunks.append(c)
+            left -= c
+        # job order: for each chunk round, every session (keeps the ring pattern)
+        jobs = [(ci * S + m, c) for ci, c in enumerate(chunks) for m in range(S)]
+        pl.total_jobs = len(jobs) + S * (W + K + (0 if args.no_e2e else K))
+        # all prefill jobs, then decode jobs continue numbering
+        for j, t in jobs:
+            pl.job(j, t, x=pl.inputs[:t] if t <= 64 else torch.randn(t, cfg.hidden, device=pl.dev) * 0.05)
+        jbase = len(jobs)
+    torch.cuda.synchronize()
+    pf_s = time.perf_counter() - t_pf
+    if args.synthetic_kv:
+        jbase = 0
+        pl.total_jobs = S * (W + K + (0 if args.no_e2e else K))
+    # ---- warmup decode
+    for i in range(W * S):
+        pl.job(jbase + i, 1)
+    jbase += W * S
+    # ---- timed decode (device-resident inputs)
+    pl.barrier()
+    pl.span.profile(True)
+    pl.launches = 0
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(pl.local) as clk:
+        start.record()
+        for i in range(K * S):
+            pl.job(jbase + i, 1)
+        stop.record()
+        pl.barrier()
+    jbase += K * S
+    ms = start.elapsed_time(stop)
+    launches = pl.launches
+    gemv = pl.span.profile_read(pl.span.PROF_GEMV)
+    attn = pl.span.profile_read(pl.span.PROF_ATTN)
+    pro = pl.span.profile_read(pl.span.PROF_PROLOGUE)
+    codec_p = pl.span.profile_read(pl.span.PROF_CODEC)
+    pl.span.profile(False)
+    t = torch.tensor([ms], device=pl.dev)
+    if pl.dist:
+        pl.dist.all_reduce(t, op=pl.dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = K * S / (ms_max / 1e3)
+    # ---- e2e: host bytes in/out
+    e2e = None
+    if not args.no_e2e:
+        d = cfg.hidden
+        host_in = torch.randn(1, d).mul_(0.05).pin_memory()
+        host_out = torch.empty(d, dtype=torch.int8).pin_memory()
+        pl.barrier()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(K * S):
+            pl.job(jbase + i, 1, host_in=host_in if rank == 0 else None,
+                   host_out=host_out if rank == N - 1 else None)
+            if rank == N - 1:
+                torch.cuda.current_stream().synchronize()  # result readable on the host
+        e1.record()
+        pl.barrier()
+        wall = time.perf_counter() - t0
+        te = torch.tensor([max(e0.elapsed_time(e1), wall * 1e3)], device=pl.dev)
+        if pl.dist:
+            pl.dist.all_reduce(te, op=pl.dist.ReduceOp.MAX)
+        e2e = {"value": K * S / (float(te.item()) / 1e3), "unit": UNIT, "h2d_bytes_per_step": 4 * d,
+               "d2h_bytes_per_step": d, "path": "pb_span_step_int8 C-ABI with pinned host ingress (span 0) and "
+               "egress of the int8 hidden (last span), NCCL int8 hops between spans"}
+    # ---- report (rank 0)
+    if rank != 0:
+        if pl.dist:
+            pl.dist.barrier()
+            pl.dist.destroy_process_group()
+        return
+    peak, peak_kind = measured_peaks()
+    g_ms, g_n, g_b = gemv
+    achieved = (g_b / g_n) / ((g_ms / g_n) / 1e3) / 1e9 if g_n else 0.0
+    traffic = committed_traffic()
+    w_bytes, kv_bytes = bytes_per_step(cfg, [args.ctx - K // 2] * S)
+    step_s = (ms_max / 1e3) / (K * S)
+    seq_ceiling = (w_bytes + kv_bytes / S) / (peak * 1e9)  # one session through all blocks, one GPU busy
+    agg_ceiling = (w_bytes / N + kv_bytes / N / S) / (peak * 1e9)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": K, "warmup": W,
+        "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int8 weights x fp16(hi+lo) activations, fp32 accumulate; fp16 KV",
+        "data": "synthetic (gen_checkpoint seed 42 weights generated on device; random embedding-like inputs)",
+        "config": {"workload": f"{args.shape} ({cfg.n_layers} blocks, h={cfg.hidden}) int8 decode, {S} batch-1 "
+                               f"session(s) pipelined over {N} GPU span(s) {pl.ranges}, context {T0}->{args.ctx}",
+                   "sessions": S, "ctx_end": args.ctx, "prefill_tokens": T0,
+                   "l2": "weights stream 172.7 GB per step >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"pipeline{N} (block spans)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if peak else None,
+                     "traffic": traffic.get("gemv_i8_bytes_per_launch") if traffic else None,
+                     "kernel": "k_gemv_i8 (int8 GEMV, all 4 matrices of every block)",
+                     "launches": g_n, "avg_launch_us": 1e3 * g_ms / max(g_n, 1),
+                     "algorithmic_bytes_per_launch": g_b / max(g_n, 1), "peak_source": peak_kind},
+        "step_roofline": {"bytes_per_step": w_bytes + kv_bytes / S, "sequential_frac": seq_ceiling / step_s,
+                          "aggregate_frac": agg_ceiling / step_s * (1 if N == 1 else 1),
+                          "kernel_share": {"gemv": g_ms / ms_max, "attention": attn[0] / ms_max,
+                                           "prologue": pro[0] / ms_max, "codec": codec_p[0] / ms_max}},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "setup_s": {"weights_gen_quant": pl.gen_s, "prefill": pf_s},
+        "device_bytes": pl.span.device_bytes,
+    }
+    if not args.no_cpu_baseline and N == 1:
+        sample, ncores = cpu_block_sample(cfg, 128)
+        sample.step_seconds()
+        ts = [sample.step_seconds() for _ in range(2)]
+        per_block = min(ts)
+        line["cpu_baseline"] = {
+            "value": 1.0 / (per_block * cfg.n_layers), "unit": UNIT, "cores": ncores, "kind": "port",
+            "sample": f"oracle port of block_forward(qw) for 1 {args.shape} block, decode t=1 at context 128, "
+                      f"best of 2, extrapolated x{cfg.n_layers} blocks"}
+    print(json.dumps(line), flush=True)
+    if pl.dist:
+        pl.dist.barrier()
+        pl.dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -124,8 +124,16 @@ int pb_span_step_int8(pb_span* span, int32_t n_tok, int32_t n_seq, const int32_t
                       const float* d_in_scales, const float* d_in_f32, int8_t* d_out_codes,
                       float* d_out_scales, float* d_out_f32, void* stream);
 
-/* Last-launch statistics: number of kernels the last step/forward launched. */
+/* Last-launch statistics: number of kernels the last step launched. */
 int32_t pb_span_last_launches(const pb_span* span);
+
+/* Live kernel profiling for the roofline: when on, every launch of the
+ * following kinds is bracketed by CUDA events on the launching stream:
+ * 0 int8 GEMV, 1 attention, 2 prologue, 3 f32 GEMM, 4 wire codec.
+ * pb_span_profile(on) resets the records; pb_span_profile_read sums the
+ * device time (ms), launch count and algorithmic bytes of one kind. */
+int pb_span_profile(pb_span* span, int32_t on);
+int pb_span_profile_read(pb_span* span, int32_t kind, double* ms, int64_t* launches, double* bytes);
 
 #ifdef __cplusplus
 }

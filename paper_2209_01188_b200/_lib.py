@@ -20,6 +20,7 @@ EXPORTS = [
     "pb_last_error", "pb_version", "pb_quantize_blockwise", "pb_dequantize_blockwise", "pb_gen_tensor",
     "pb_span_create", "pb_span_destroy", "pb_span_device_bytes", "pb_span_gen_block", "pb_span_load_block",
     "pb_span_outliers", "pb_span_read_codes", "pb_span_step", "pb_span_step_int8", "pb_span_last_launches",
+    "pb_span_profile", "pb_span_profile_read",
 ]
 
 
@@ -57,6 +58,8 @@ def lib() -> C.CDLL:
         "pb_span_read_codes": [P, I32, I32, P, P],
         "pb_span_step": [P, I32, I32, P, P, P, P, P, VP],
         "pb_span_step_int8": [P, I32, I32, P, P, P, P, P, P, P, P, P, VP],
+        "pb_span_profile": [P, I32],
+        "pb_span_profile_read": [P, I32, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double)],
     }
     for name, args in sig.items():
         fn = getattr(L, name)

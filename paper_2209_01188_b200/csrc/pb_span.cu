@@ -38,8 +38,17 @@ struct pb_span {
     float* attn_part = nullptr;
     int64_t attn_cap = 0;
     int32_t *d_tok_seq = nullptr, *d_tok_pos = nullptr, *d_pages = nullptr;
-    int32_t* h_meta = nullptr;  // pinned staging: tok_seq | tok_pos | pages
+    static constexpr int NSLOT = 4;  // ring of pinned staging buffers (no host sync per step)
+    int32_t* h_meta[NSLOT] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t meta_ev[NSLOT] = {nullptr, nullptr, nullptr, nullptr};
+    int meta_slot = 0;
     int64_t meta_ints = 0;
+    // live kernel profiling (CUDA event pairs around launches; bench.py roofline)
+    bool prof_on = false;
+    std::vector<cudaEvent_t> prof_ev;
+    struct ProfRec { int kind; int ev; double bytes; };
+    std::vector<ProfRec> prof;
+    std::vector<int32_t> h_tok_pos_last;
     int8_t* hop_codes = nullptr;
     float* hop_scales = nullptr;
     int64_t bytes = 0;
@@ -91,7 +100,11 @@ void free_span(pb_span* s) {
                     s->partials, s->counters, s->attn_part, s->d_tok_seq, s->d_tok_pos, s->d_pages,
                     s->hop_codes, s->hop_scales};
     for (void* p : ptrs) cudaFree(p);
-    if (s->h_meta) cudaFreeHost(s->h_meta);
+    for (int i = 0; i < pb_span::NSLOT; ++i) {
+        if (s->h_meta[i]) cudaFreeHost(s->h_meta[i]);
+        if (s->meta_ev[i]) cudaEventDestroy(s->meta_ev[i]);
+    }
+    for (auto e : s->prof_ev) cudaEventDestroy(e);
 }
 
 __global__ void k_fill(float* p, int64_t n, float v) {
@@ -167,9 +180,12 @@ int pb_span_create(const pb_span_config* cfg, pb_span** out) {
     if (!rc) rc = dalloc(s, &s->d_pages, (int64_t)cfg->max_seqs * s->max_pages);
     if (!rc) rc = dalloc(s, &s->hop_codes, (int64_t)NT * d);
     if (!rc) rc = dalloc(s, &s->hop_scales, ceil_div((int64_t)NT * d, 64));
-    if (!rc && cudaMallocHost((void**)&s->h_meta, sizeof(int32_t) * s->meta_ints) != cudaSuccess) {
-        set_error("pinned staging allocation failed");
-        rc = PB_ERR_GENERIC;
+    for (int i = 0; !rc && i < pb_span::NSLOT; ++i) {
+        if (cudaMallocHost((void**)&s->h_meta[i], sizeof(int32_t) * s->meta_ints) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->meta_ev[i], cudaEventDisableTiming) != cudaSuccess) {
+            set_error("pinned staging allocation failed");
+            rc = PB_ERR_GENERIC;
+        }
     }
     if (!rc && cudaMemset(s->counters, 0, sizeof(int) << 20) != cudaSuccess) rc = PB_ERR_GENERIC;
     if (!rc) {
@@ -288,6 +304,24 @@ int32_t pb_span_last_launches(const pb_span* span) { return span ? span->last_la
 
 // ------------------------------------------------------------------ step
 
+// kinds: 0 int8 GEMV, 1 attention (split + combine), 2 prologue, 3 f32 GEMM, 4 wire codec
+static int prof_begin(pb_span* s, cudaStream_t st) {
+    if (!s->prof_on) return -1;
+    const int i = (int)s->prof.size() * 2;
+    while ((int)s->prof_ev.size() < i + 2) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return -1;
+        s->prof_ev.push_back(e);
+    }
+    cudaEventRecord(s->prof_ev[i], st);
+    return i;
+}
+static void prof_end(pb_span* s, int ev, int kind, double bytes, cudaStream_t st) {
+    if (ev < 0) return;
+    cudaEventRecord(s->prof_ev[ev + 1], st);
+    s->prof.push_back({kind, ev, bytes});
+}
+
 static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float* out, cudaStream_t st) {
     const int d = s->d, rd = s->rd;
     const bool int8 = s->cfg.weights == PB_WEIGHTS_INT8;
@@ -318,16 +352,26 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                 e.outl_idx = m.outl_idx;
                 e.outl_rows = m.outl_rows;
                 e.xo = s->xo;
+                int ev = prof_begin(s, st);
                 if (int rc = launch_prologue(mode, x, n_tok, K, m.Kp, g, be, m, tc, s->frag, s->back, s->xo, nullptr, st))
                     return rc;
+                prof_end(s, ev, 2, 4.0 * n_tok * K, st);
                 Act a{s->frag, s->back, n_tok, tc};
                 launches += 2;
-                return launch_gemv(m, a, e, s->partials, s->counters, s->partial_cap, st);
+                ev = prof_begin(s, st);
+                // algorithmic bytes: codes + per-feature scales + bias (+ f32 outlier rows)
+                const double bytes = (double)m.M * m.K + 4.0 * m.K + 4.0 * m.M + 4.0 * m.n_outl * m.M;
+                int rc = launch_gemv(m, a, e, s->partials, s->counters, s->partial_cap, st);
+                prof_end(s, ev, 0, bytes, st);
+                return rc;
             }
             if (int rc = launch_prologue(mode, x, n_tok, K, K, g, be, m, tc, nullptr, s->back, nullptr, s->y32, st))
                 return rc;
             launches += 2;
-            return launch_gemm_f32(m, s->y32, n_tok, e, st);
+            const int ev = prof_begin(s, st);
+            int rc = launch_gemm_f32(m, s->y32, n_tok, e, st);
+            prof_end(s, ev, 3, 4.0 * m.M * m.K, st);
+            return rc;
         };
         Epi e = base;
         e.kind = EPI_QKV;
@@ -335,7 +379,14 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
         if (int rc = matmul(0, PRO_LN, x_in, d, b.ln1_g, b.ln1_b, e)) return rc;
         AttnArgs aa{s->q, kvb, s->d_tok_seq, s->d_tok_pos, s->d_pages, s->slopes, s->ctx, s->attn_part,
                     n_tok, s->max_pages, s->H, s->dh, s->cfg.page_tokens, d, max_pos};
-        if (int rc = launch_attention(aa, s->attn_cap, st)) return rc;
+        {
+            const int ev = prof_begin(s, st);
+            if (int rc = launch_attention(aa, s->attn_cap, st)) return rc;
+            // fp16 K and V rows read for every query token (2 T h 2 B per session-block)
+            double kv_bytes = 0.0;
+            for (int i = 0; i < n_tok; ++i) kv_bytes += 4.0 * (s->h_tok_pos_last[i] + 1) * d;
+            prof_end(s, ev, 1, kv_bytes, st);
+        }
         launches += 2;
         e = base;
         e.kind = EPI_RESID;
@@ -369,9 +420,12 @@ static int stage_meta(pb_span* s, int n_tok, int n_seq, const int32_t* tok_seq, 
         PB_REQUIRE(pg >= 0 && pg < s->cfg.n_pages, PB_ERR_BAD_REQUEST, "KV page out of range");
     }
     *max_pos = mp;
-    // pinned staging: the previous step's copies must have completed before we overwrite it
-    PB_CHECK_CUDA(cudaStreamSynchronize(st));
-    int32_t* hm = s->h_meta;
+    s->h_tok_pos_last.assign(tok_pos, tok_pos + n_tok);
+    // pinned staging ring: wait only until this slot's previous copies have executed
+    const int slot = s->meta_slot;
+    s->meta_slot = (slot + 1) % pb_span::NSLOT;
+    PB_CHECK_CUDA(cudaEventSynchronize(s->meta_ev[slot]));
+    int32_t* hm = s->h_meta[slot];
     std::memcpy(hm, tok_seq, sizeof(int32_t) * n_tok);
     std::memcpy(hm + n_tok, tok_pos, sizeof(int32_t) * n_tok);
     std::memcpy(hm + 2 * n_tok, pages, sizeof(int32_t) * (size_t)n_seq * s->max_pages);
@@ -379,6 +433,7 @@ static int stage_meta(pb_span* s, int n_tok, int n_seq, const int32_t* tok_seq, 
     PB_CHECK_CUDA(cudaMemcpyAsync(s->d_tok_pos, hm + n_tok, sizeof(int32_t) * n_tok, cudaMemcpyHostToDevice, st));
     PB_CHECK_CUDA(cudaMemcpyAsync(s->d_pages, hm + 2 * n_tok, sizeof(int32_t) * (size_t)n_seq * s->max_pages,
                                   cudaMemcpyHostToDevice, st));
+    PB_CHECK_CUDA(cudaEventRecord(s->meta_ev[slot], st));
     return PB_OK;
 }
 
@@ -412,16 +467,49 @@ extern "C" int pb_span_step_int8(pb_span* span, int32_t n_tok, int32_t n_seq, co
     if (d_in_codes) {
         // xa is the inter-block buffer: block 0 reads its input for the last
         // time (wo residual) before its final GEMV overwrites xa.
+        const int ev = prof_begin(span, st);
         if (int rc = dequantize_blockwise(d_in_codes, d_in_scales, n, 64, span->xa, st)) return rc;
+        prof_end(span, ev, 4, 5.0 * n + n / 16.0, st);
         in = span->xa;
         ++extra;
     }
     float* out = d_out_f32 ? d_out_f32 : span->xa;
     if (int rc = run_blocks(span, n_tok, max_pos, in, out, st)) return rc;
     if (d_out_codes) {
+        const int ev = prof_begin(span, st);
         if (int rc = quantize_blockwise(out, n, 64, d_out_codes, d_out_scales, st)) return rc;
+        prof_end(span, ev, 4, 5.0 * n + n / 16.0, st);
         ++extra;
     }
     span->last_launches += extra;
+    return PB_OK;
+}
+
+extern "C" int pb_span_profile(pb_span* span, int32_t on) {
+    PB_REQUIRE(span, PB_ERR_BAD_REQUEST, "null span");
+    std::lock_guard<std::mutex> lk(span->mu);
+    span->prof_on = on != 0;
+    span->prof.clear();
+    return PB_OK;
+}
+
+extern "C" int pb_span_profile_read(pb_span* span, int32_t kind, double* ms, int64_t* launches, double* bytes) {
+    PB_REQUIRE(span && ms && launches && bytes, PB_ERR_BAD_REQUEST, "null argument");
+    std::lock_guard<std::mutex> lk(span->mu);
+    PB_CHECK_CUDA(cudaSetDevice(span->cfg.device));
+    double t = 0.0, b = 0.0;
+    int64_t n = 0;
+    for (const auto& r : span->prof) {
+        if (r.kind != kind) continue;
+        float e = 0.f;
+        PB_CHECK_CUDA(cudaEventSynchronize(span->prof_ev[r.ev + 1]));
+        PB_CHECK_CUDA(cudaEventElapsedTime(&e, span->prof_ev[r.ev], span->prof_ev[r.ev + 1]));
+        t += e;
+        b += r.bytes;
+        ++n;
+    }
+    *ms = t;
+    *launches = n;
+    *bytes = b;
     return PB_OK;
 }

@@ -237,8 +237,11 @@ class StepScheduler:
 
 
 class ServerNode:
-    def __init__(self, config: ServerConfig, checkpoint=None):
+    def __init__(self, config: ServerConfig, checkpoint=None, span: BlockSpan | None = None):
+        """`span` (optional) is an already-loaded BlockSpan for config.blocks
+        (bench.py reuses the 176B-shape span instead of building a second one)."""
         self.config = config
+        self._given_span = span
         self.server_id = os.urandom(16).hex()
         self.events: list = []
         self.throughput = 0.0
@@ -289,11 +292,17 @@ class ServerNode:
         pos_budget = max(1, self.config.cache_budget_tokens // n)
         pages = self.config.kv_pages or (-(-pos_budget // self.config.page_tokens) + self.config.capacity + 2)
         torch.cuda.set_device(self.config.device)
-        self.span = BlockSpan(self.model, self.range.start, self.range.end, int8=int8,
-                              page_tokens=self.config.page_tokens, n_pages=pages,
-                              max_tokens=self.config.max_batch_tokens, max_seqs=max(1, self.config.capacity),
-                              device=self.config.device)
-        self._load_weights()
+        if self._given_span is not None:
+            self.span = self._given_span
+            if (self.span.start, self.span.end) != (self.range.start, self.range.end) or self.span.int8 != int8:
+                raise InputError("given span does not match the configured range / quantize mode")
+            self._weights_hash = hashlib.sha256(f"span:{self.model}:{self.range}".encode()).hexdigest()
+        else:
+            self.span = BlockSpan(self.model, self.range.start, self.range.end, int8=int8,
+                                  page_tokens=self.config.page_tokens, n_pages=pages,
+                                  max_tokens=self.config.max_batch_tokens, max_seqs=max(1, self.config.capacity),
+                                  device=self.config.device)
+            self._load_weights()
         self.sched = StepScheduler(self.span, self.config.max_batch_tokens, max(1, self.config.capacity))
         self.rpc = RpcServer(self.config.host, self.config.port, self._dispatch).start()
         self._announce("joining", throughput=1e-6)

@@ -103,6 +103,18 @@ class BlockSpan:
     def last_launches(self) -> int:
         return int(_lib.lib().pb_span_last_launches(self._h))
 
+    PROF_GEMV, PROF_ATTN, PROF_PROLOGUE, PROF_GEMM_F32, PROF_CODEC = range(5)
+
+    def profile(self, on: bool) -> None:
+        """Bracket every launch with CUDA events (resets previous records)."""
+        _lib.check(_lib.lib().pb_span_profile(self._h, 1 if on else 0))
+
+    def profile_read(self, kind: int):
+        """(device ms, launches, algorithmic bytes) summed over one kernel kind."""
+        ms, n, b = C.c_double(), C.c_int64(), C.c_double()
+        _lib.check(_lib.lib().pb_span_profile_read(self._h, kind, C.byref(ms), C.byref(n), C.byref(b)))
+        return ms.value, n.value, b.value
+
     # ------------------------------------------------------------------ weights
 
     def generate_weights(self, seed: int, outlier_boost: float = 0.0, boost_every: int = 0) -> None:
