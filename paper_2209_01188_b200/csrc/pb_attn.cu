@@ -20,7 +20,8 @@
 
 namespace pb {
 
-constexpr int ATT_KCH = 256;  // keys per CTA
+constexpr int ATT_KCH = 128;  // keys per CTA
+constexpr int ATT_U = 4;      // key rows in flight per lane
 constexpr int ATT_WARPS = 4;
 
 template <int DH>
@@ -87,22 +88,30 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) k_attn_split(AttnArgs a, int n
     const int64_t head_off = (int64_t)h * a.P * DH;
     const int64_t kv_stride = (int64_t)a.H * a.P * DH;  // K -> V within a page
 
-    // scores
-    for (int base = j0 + warp * C::KPW; base < j1; base += ATT_WARPS * C::KPW) {
-        const int j = base + slot;
-        float dot = 0.f;
-        if (j < j1) {
-            const int page = pt[j / a.P];
-            const half* kp = a.kv + (int64_t)page * 2 * kv_stride + head_off + (int64_t)(j % a.P) * DH + d0;
-            float kf[C::DPL];
-            load_h<C::DPL>(kp, kf);
+    // scores: ATT_U key vectors in flight per lane before any dot product
+    for (int base = j0 + warp * C::KPW * ATT_U; base < j1; base += ATT_WARPS * C::KPW * ATT_U) {
+        float kf[ATT_U][C::DPL];
 #pragma unroll
-            for (int i = 0; i < C::DPL; ++i) dot = fmaf(qv[i], kf[i], dot);
+        for (int u = 0; u < ATT_U; ++u) {
+            const int j = base + u * C::KPW + slot;
+            if (j < j1) {
+                const int page = pt[j / a.P];
+                load_h<C::DPL>(a.kv + (int64_t)page * 2 * kv_stride + head_off + (int64_t)(j % a.P) * DH + d0, kf[u]);
+            }
         }
 #pragma unroll
-        for (int o = C::LPK / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        if (j < j1 && sub == 0)
-            sc[j - j0] = __fadd_rn(__fdiv_rn(dot, sq), __fmul_rn(slope, (float)(j - pos)));
+        for (int u = 0; u < ATT_U; ++u) {
+            const int j = base + u * C::KPW + slot;
+            float dot = 0.f;
+            if (j < j1) {
+#pragma unroll
+                for (int i = 0; i < C::DPL; ++i) dot = fmaf(qv[i], kf[u][i], dot);
+            }
+#pragma unroll
+            for (int o = C::LPK / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+            if (j < j1 && sub == 0)
+                sc[j - j0] = __fadd_rn(__fdiv_rn(dot, sq), __fmul_rn(slope, (float)(j - pos)));
+        }
     }
     __syncthreads();
     const int nk = j1 - j0;
@@ -132,17 +141,25 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) k_attn_split(AttnArgs a, int n
     float ov[C::DPL];
 #pragma unroll
     for (int i = 0; i < C::DPL; ++i) ov[i] = 0.f;
-    for (int base = j0 + warp * C::KPW; base < j1; base += ATT_WARPS * C::KPW) {
-        const int j = base + slot;
-        if (j < j1) {
-            const int page = pt[j / a.P];
-            const half* vp =
-                a.kv + (int64_t)page * 2 * kv_stride + kv_stride + head_off + (int64_t)(j % a.P) * DH + d0;
-            float vf[C::DPL];
-            load_h<C::DPL>(vp, vf);
-            const float p = sc[j - j0];
+    for (int base = j0 + warp * C::KPW * ATT_U; base < j1; base += ATT_WARPS * C::KPW * ATT_U) {
+        float vf[ATT_U][C::DPL];
 #pragma unroll
-            for (int i = 0; i < C::DPL; ++i) ov[i] = fmaf(p, vf[i], ov[i]);
+        for (int u = 0; u < ATT_U; ++u) {
+            const int j = base + u * C::KPW + slot;
+            if (j < j1) {
+                const int page = pt[j / a.P];
+                load_h<C::DPL>(a.kv + (int64_t)page * 2 * kv_stride + kv_stride + head_off + (int64_t)(j % a.P) * DH + d0,
+                               vf[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < ATT_U; ++u) {
+            const int j = base + u * C::KPW + slot;
+            if (j < j1) {
+                const float p = sc[j - j0];
+#pragma unroll
+                for (int i = 0; i < C::DPL; ++i) ov[i] = fmaf(p, vf[u][i], ov[i]);
+            }
         }
     }
 #pragma unroll

@@ -96,85 +96,143 @@ struct ProArgs {
     const int32_t* outl_idx;
     int tc;
     uint4* frag;
-    float* back;
+    float* back;   // [n_tok] 2^-shift (epilogue rescale)
+    float4* stats; // [n_tok] {mu, inv, 2^shift, -}
     float* xo;
     float* y32;
 };
 
-// one CTA per token (model.py:271-276 LayerNorm, population variance, eps 1e-5)
-__global__ void __launch_bounds__(256) k_prologue(ProArgs a) {
+__device__ __forceinline__ float pro_y(const ProArgs& a, const float* x, int k, float mu, float inv) {
+    if (a.mode == PRO_LN) return fmaf(a.gamma[k], (x[k] - mu) * inv, a.beta[k]);  // model.py:271-276
+    return x[k];
+}
+
+// Row statistics, one CTA per token: LayerNorm mean / inverse std (population
+// variance, eps 1e-5; accumulated in f64) and the power-of-two shift that maps
+// max |y * s| into [2^13, 2^14) for the hi/lo fp16 split.
+constexpr int STATS_THREADS = 1024;
+
+__global__ void __launch_bounds__(STATS_THREADS) k_rowstats(ProArgs a) {
     __shared__ double redd[32];
     __shared__ float redf[32];
     const int tok = blockIdx.x;
     const float* x = a.x + (int64_t)tok * a.K;
+    const bool vec = (a.K & 3) == 0 && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
     float mu = 0.f, inv = 1.f;
     if (a.mode == PRO_LN) {
         double s = 0.0;
-        for (int k = threadIdx.x; k < a.K; k += blockDim.x) s += (double)x[k];
-        const double mean = block_sum_d(s, redd) / a.K;
-        double v = 0.0;
-        for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
-            const double dv = (double)x[k] - mean;
-            v += dv * dv;
+        if (vec) {
+            for (int k = threadIdx.x * 4; k < a.K; k += STATS_THREADS * 4) {
+                const float4 v = *reinterpret_cast<const float4*>(x + k);
+                s += (double)v.x + (double)v.y + (double)v.z + (double)v.w;
+            }
+        } else {
+            for (int k = threadIdx.x; k < a.K; k += STATS_THREADS) s += (double)x[k];
         }
-        const float var = (float)(block_sum_d(v, redd) / a.K);
+        const double mean = block_sum_d(s, redd) / a.K;
+        double v2 = 0.0;
+        if (vec) {
+            for (int k = threadIdx.x * 4; k < a.K; k += STATS_THREADS * 4) {
+                const float4 v = *reinterpret_cast<const float4*>(x + k);
+                const double d0 = v.x - mean, d1 = v.y - mean, d2 = v.z - mean, d3 = v.w - mean;
+                v2 += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+            }
+        } else {
+            for (int k = threadIdx.x; k < a.K; k += STATS_THREADS) {
+                const double d0 = (double)x[k] - mean;
+                v2 += d0 * d0;
+            }
+        }
+        const float var = (float)(block_sum_d(v2, redd) / a.K);
         mu = (float)mean;
         inv = 1.0f / sqrtf(var + 1e-5f);
     }
-    auto yval = [&](int k) -> float {
-        if (a.mode == PRO_LN) return fmaf(a.gamma[k], (x[k] - mu) * inv, a.beta[k]);
-        return x[k];
-    };
-    if (a.y32) {  // f32-weights mode: plain activations
-        for (int k = threadIdx.x; k < a.K; k += blockDim.x) a.y32[(int64_t)tok * a.K + k] = yval(k);
-        return;
-    }
-    for (int j = threadIdx.x; j < a.n_outl; j += blockDim.x) a.xo[(int64_t)tok * a.n_outl + j] = yval(a.outl_idx[j]);
     float m = 0.f;
-    for (int k = threadIdx.x; k < a.K; k += blockDim.x) m = fmaxf(m, fabsf(yval(k) * a.scales[k]));
-    m = block_max(m, redf);
+    if (a.scales) {
+        for (int k = threadIdx.x; k < a.K; k += STATS_THREADS) m = fmaxf(m, fabsf(pro_y(a, x, k, mu, inv) * a.scales[k]));
+        m = block_max(m, redf);
+    }
     int shift = 0;
     if (m > 0.f && isfinite(m)) {
         int e;
         frexpf(m, &e);  // m in [2^(e-1), 2^e)
         shift = 14 - e;
     }
-    if (threadIdx.x == 0) a.back[tok] = ldexpf(1.f, -shift);
+    if (threadIdx.x == 0) {
+        a.back[tok] = ldexpf(1.f, -shift);
+        a.stats[tok] = make_float4(mu, inv, ldexpf(1.f, shift), 0.f);
+    }
+}
+
+// hi/lo fp16 B fragments of x~ = y * s * 2^shift (layout in the header comment);
+// one thread per (token, 32-wide k chunk, lane quad q).
+__global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
+    const int tok = blockIdx.y;
+    const float* x = a.x + (int64_t)tok * a.K;
+    const float4 st = a.stats[tok];
     const int KC = a.Kp / 32;
+    const int it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (blockIdx.x == 0 && a.xo) {
+        for (int j = threadIdx.x; j < a.n_outl; j += blockDim.x)
+            a.xo[(int64_t)tok * a.n_outl + j] = pro_y(a, x, a.outl_idx[j], st.x, st.y);
+    }
+    if (it >= KC * 4) return;
+    const int kc = it >> 2, q = it & 3;
     const int NT = a.tc / 4;
     const int c = tok / a.tc, col = tok % a.tc;
     const int nt_hi = col >> 3, g_hi = col & 7;
     const int nt_lo = (a.tc + col) >> 3, g_lo = (a.tc + col) & 7;
-    for (int it = threadIdx.x; it < KC * 4; it += blockDim.x) {
-        const int kc = it >> 2, q = it & 3;
-        uint32_t hw[4], lw[4];
+    uint32_t hw[4], lw[4];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-            const int kt = w >> 1, upper = w & 1;
-            const int k0 = kc * 32 + kt * 16 + 2 * q + 8 * upper;
-            float v[2];
+    for (int w = 0; w < 4; ++w) {
+        const int kt = w >> 1, upper = w & 1;
+        const int k0 = kc * 32 + kt * 16 + 2 * q + 8 * upper;
+        float v[2];
 #pragma unroll
-            for (int e2 = 0; e2 < 2; ++e2) {
-                const int k = k0 + e2;
-                v[e2] = k < a.K ? ldexpf(yval(k) * a.scales[k], shift) : 0.f;
-            }
-            const half h0 = __float2half_rn(v[0]), h1 = __float2half_rn(v[1]);
-            const half l0 = __float2half_rn(v[0] - __half2float(h0));
-            const half l1 = __float2half_rn(v[1] - __half2float(h1));
-            hw[w] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-            lw[w] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+        for (int e2 = 0; e2 < 2; ++e2) {
+            const int k = k0 + e2;
+            v[e2] = k < a.K ? (pro_y(a, x, k, st.x, st.y) * a.scales[k]) * st.z : 0.f;
         }
-        const int64_t base = ((int64_t)c * KC + kc) * NT;
-        a.frag[(base + nt_hi) * 32 + 4 * g_hi + q] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        a.frag[(base + nt_lo) * 32 + 4 * g_lo + q] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        const half h0 = __float2half_rn(v[0]), h1 = __float2half_rn(v[1]);
+        const half l0 = __float2half_rn(v[0] - __half2float(h0));
+        const half l1 = __float2half_rn(v[1] - __half2float(h1));
+        hw[w] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+        lw[w] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
     }
+    const int64_t base = ((int64_t)c * KC + kc) * NT;
+    a.frag[(base + nt_hi) * 32 + 4 * g_hi + q] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    a.frag[(base + nt_lo) * 32 + 4 * g_lo + q] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+}
+
+// f32-weights mode: plain y = LN(x) (or x) rows for the CUDA-core GEMM
+__global__ void __launch_bounds__(256) k_rows_f32(ProArgs a) {
+    const int tok = blockIdx.y;
+    const float* x = a.x + (int64_t)tok * a.K;
+    const float4 st = a.stats[tok];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < a.K; k += gridDim.x * blockDim.x)
+        a.y32[(int64_t)tok * a.K + k] = pro_y(a, x, k, st.x, st.y);
 }
 
 int launch_prologue(int mode, const float* x, int n_tok, int K, int Kp, const float* gamma, const float* beta,
-                    const Mat& m, int tc, uint4* frag, float* back, float* xo, float* y32, cudaStream_t st) {
-    ProArgs a{mode, x, K, Kp, gamma, beta, m.scales, m.n_outl, m.outl_idx, tc, frag, back, xo, y32};
-    k_prologue<<<n_tok, 256, 0, st>>>(a);
-    return launch_check("prologue");
+                    const Mat& m, int tc, uint4* frag, float* back, float4* stats, float* xo, float* y32,
+                    cudaStream_t st) {
+    ProArgs a{mode, x, K, Kp, gamma, beta, y32 ? nullptr : m.scales, m.n_outl, m.outl_idx, tc, frag, back, stats,
+              xo, y32};
+    if (mode == PRO_LN || !y32) {
+        k_rowstats<<<n_tok, STATS_THREADS, 0, st>>>(a);
+        if (int rc = launch_check("rowstats")) return rc;
+    }
+    if (y32) {
+        if (mode != PRO_LN) {  // plain copy semantics: stats unused, mu=0 inv=1 not needed
+            PB_CHECK_CUDA(cudaMemcpyAsync(y32, x, sizeof(float) * (size_t)n_tok * K, cudaMemcpyDeviceToDevice, st));
+            return PB_OK;
+        }
+        k_rows_f32<<<dim3((unsigned)ceil_div(K, 256), n_tok), 256, 0, st>>>(a);
+        return launch_check("rows_f32");
+    }
+    const int items = (Kp / 32) * 4;
+    k_fragwrite<<<dim3((unsigned)ceil_div(items, 256), n_tok), 256, 0, st>>>(a);
+    return launch_check("fragwrite");
 }
 
 // ------------------------------------------------------------------ epilogue

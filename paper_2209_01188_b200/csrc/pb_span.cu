@@ -32,6 +32,7 @@ struct pb_span {
     float *xa = nullptr, *mid = nullptr, *q = nullptr, *ctx = nullptr, *act = nullptr, *xo = nullptr, *y32 = nullptr;
     uint4* frag = nullptr;
     float* back = nullptr;
+    float4* stats = nullptr;
     float* partials = nullptr;
     int64_t partial_cap = 0;
     int* counters = nullptr;
@@ -96,7 +97,7 @@ void free_span(pb_span* s) {
         cudaFree(b.ln2_b);
         for (auto* p : b.bias) cudaFree(p);
     }
-    void* ptrs[] = {s->kv, s->slopes, s->xa, s->mid, s->q, s->ctx, s->act, s->xo, s->y32, s->frag, s->back,
+    void* ptrs[] = {s->kv, s->slopes, s->xa, s->mid, s->q, s->ctx, s->act, s->xo, s->y32, s->frag, s->back, s->stats,
                     s->partials, s->counters, s->attn_part, s->d_tok_seq, s->d_tok_pos, s->d_pages,
                     s->hop_codes, s->hop_scales};
     for (void* p : ptrs) cudaFree(p);
@@ -169,6 +170,7 @@ int pb_span_create(const pb_span_config* cfg, pb_span** out) {
     const int64_t kp_max = round_up(rd, 32);
     if (!rc && int8) rc = dalloc(s, &s->frag, (int64_t)(NT + 31) * kp_max * 4 / 16 + 64);
     if (!rc) rc = dalloc(s, &s->back, NT);
+    if (!rc) rc = dalloc(s, &s->stats, NT);
     s->partial_cap = (int64_t)8 << 20;
     if (!rc && int8) rc = dalloc(s, &s->partials, s->partial_cap);
     if (!rc) rc = dalloc(s, &s->counters, 1 << 20);
@@ -353,7 +355,7 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                 e.outl_rows = m.outl_rows;
                 e.xo = s->xo;
                 int ev = prof_begin(s, st);
-                if (int rc = launch_prologue(mode, x, n_tok, K, m.Kp, g, be, m, tc, s->frag, s->back, s->xo, nullptr, st))
+                if (int rc = launch_prologue(mode, x, n_tok, K, m.Kp, g, be, m, tc, s->frag, s->back, s->stats, s->xo, nullptr, st))
                     return rc;
                 prof_end(s, ev, 2, 4.0 * n_tok * K, st);
                 Act a{s->frag, s->back, n_tok, tc};
@@ -365,7 +367,7 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                 prof_end(s, ev, 0, bytes, st);
                 return rc;
             }
-            if (int rc = launch_prologue(mode, x, n_tok, K, K, g, be, m, tc, nullptr, s->back, nullptr, s->y32, st))
+            if (int rc = launch_prologue(mode, x, n_tok, K, K, g, be, m, tc, nullptr, s->back, s->stats, nullptr, s->y32, st))
                 return rc;
             launches += 2;
             const int ev = prof_begin(s, st);

@@ -89,7 +89,8 @@ int dequantize_blockwise(const int8_t* codes, const float* scales, int64_t n, in
 // prologue: y = LN(x) (PRO_LN) or x (PRO_SCALE); writes hi/lo fragments of
 // y * scales, the per-token 2^-shift, outlier activations xo, and (f32 mode) y.
 int launch_prologue(int mode, const float* x, int n_tok, int K, int Kp, const float* gamma, const float* beta,
-                    const Mat& m, int tc, uint4* frag, float* back, float* xo, float* y32, cudaStream_t st);
+                    const Mat& m, int tc, uint4* frag, float* back, float4* stats, float* xo, float* y32,
+                    cudaStream_t st);
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
                 int64_t partial_cap, cudaStream_t st);
 int launch_gemm_f32(const Mat& m, const float* y, int n_tok, const Epi& epi, cudaStream_t st);
