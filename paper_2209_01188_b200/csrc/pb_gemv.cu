@@ -25,10 +25,6 @@
 
 namespace pb {
 
-constexpr int GEMV_WARPS = 4;
-constexpr int GEMV_MW = 2;                              // m-tiles per warp
-constexpr int GEMV_ROWS = GEMV_WARPS * GEMV_MW * 16;    // 128 rows per CTA
-constexpr int GEMV_UNROLL = 4;
 
 int choose_tc(int n_tok) {
     if (n_tok <= 4) return 4;
@@ -289,157 +285,296 @@ __device__ __forceinline__ void i8x4_to_f16x2(uint32_t w, uint32_t& lo, uint32_t
     hi = *reinterpret_cast<uint32_t*>(&r1);
 }
 
+// ---- TMA-bulk pipelined stream-K GEMV ----------------------------------------
+// CTA = 1 producer warp + 4 consumer warps. The CTA owns a contiguous range of
+// the linearized work space u = mg * KC + kc (mg = 128-row group, kc = 32-wide
+// K tile), so every CTA streams the same number of weight bytes (no wave
+// tail). The producer's elected lane streams stages of SK_KCS k-tiles
+// (4 KB of codes each: the 128-row group's tiles are contiguous in HBM) plus
+// the matching B fragments into shared memory with cp.async.bulk
+// (UBLKCP, mbarrier complete_tx); consumers read them with LDS.128, convert
+// int8 -> fp16 in registers and issue mma.sync. An m-group that lies entirely
+// in one CTA's range goes straight to the fused epilogue; a split m-group
+// (range boundary) is finished by its last-arriving contributor, which sums
+// the contributors' partial tiles in CTA order (deterministic).
+constexpr int SK_CONS = 4;                       // consumer warps (2 m-tiles each)
+constexpr int SK_THREADS = (SK_CONS + 1) * 32;   // + producer warp
+constexpr int SK_KCS = 2;                        // k-tiles per stage
+constexpr int SK_STAGES = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void cons_sync() {  // the 4 consumer warps only
+    asm volatile("bar.sync 1, %0;" ::"n"(SK_CONS * 32) : "memory");
+}
+
+struct SkArgs {
+    const int8_t* codes;
+    int MG, KC;       // 128-row groups, 32-wide k tiles
+    int64_t total;    // MG * KC work units
+    int G;            // CTAs per column chunk
+    Act act;
+    Epi epi;
+    float* partials;  // [chunk][G][2][128 * 2tc]
+    int* counters;    // [chunk][MG]
+};
+
+__device__ __forceinline__ int sk_owner(int64_t u, int G, int64_t total) {
+    return (int)(((u + 1) * G - 1) / total);
+}
+
 template <int NT>
-__global__ void __launch_bounds__(GEMV_WARPS * 32) k_gemv_i8(const int8_t* __restrict__ codes, int MT, int KC,
-                                                             int kc_per_split, Act act, Epi epi,
-                                                             float* __restrict__ partials, int* __restrict__ counters) {
+__global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
     constexpr int TC = NT * 4;
-    constexpr int SST = 2 * TC + 1;
-    __shared__ float S[GEMV_ROWS * SST];
-    __shared__ int s_last;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane >> 2, q = lane & 3;
-    const int chunk = blockIdx.y, split = blockIdx.z, nsplit = gridDim.z;
-    const int mt0 = blockIdx.x * (GEMV_WARPS * GEMV_MW) + warp * GEMV_MW;
-    const int kc_begin = split * kc_per_split;
-    const int kc_end = min(KC, kc_begin + kc_per_split);
+    constexpr int COLS = 2 * TC;
+    constexpr int SST = COLS + 1;
+    constexpr int A_STAGE = SK_KCS * 4096;
+    constexpr int B_STAGE = SK_KCS * NT * 512;
+    constexpr int PER = 128 * COLS;  // floats per partial tile
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t* sa = smem;                                        // [STAGES][A_STAGE]
+    uint8_t* sb = sa + SK_STAGES * A_STAGE;                    // [STAGES][B_STAGE]
+    float* S = reinterpret_cast<float*>(sb + SK_STAGES * B_STAGE);  // [128][SST]
+    uint64_t* full = reinterpret_cast<uint64_t*>(S + 128 * SST + 3);  // 8-byte aligned below
+    full = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(full) + 7) & ~uintptr_t(7));
+    uint64_t* empty = full + SK_STAGES;
+    int* s_flag = reinterpret_cast<int*>(empty + SK_STAGES);
 
-    float acc[GEMV_MW][NT][4];
-#pragma unroll
-    for (int i = 0; i < GEMV_MW; ++i)
-#pragma unroll
-        for (int j = 0; j < NT; ++j)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.f;
-
-    const uint4* bf = act.frag + (int64_t)chunk * KC * NT * 32 + lane;
-    bool mvalid[GEMV_MW];
-    const int8_t* ap[GEMV_MW];
-#pragma unroll
-    for (int i = 0; i < GEMV_MW; ++i) {
-        mvalid[i] = (mt0 + i) < MT;
-        ap[i] = codes + ((int64_t)(mvalid[i] ? mt0 + i : 0) * KC) * 512 + lane * 16;
-    }
-
-    for (int kc0 = kc_begin; kc0 < kc_end; kc0 += GEMV_UNROLL) {
-        int4 av[GEMV_UNROLL][GEMV_MW];
-        uint4 bv[GEMV_UNROLL][NT];
-#pragma unroll
-        for (int u = 0; u < GEMV_UNROLL; ++u) {
-            const int kc = kc0 + u;
-            const bool kv = kc < kc_end;
-#pragma unroll
-            for (int i = 0; i < GEMV_MW; ++i)
-                av[u][i] = (kv && mvalid[i]) ? ld_stream_v4(ap[i] + (int64_t)kc * 512) : make_int4(0, 0, 0, 0);
-#pragma unroll
-            for (int j = 0; j < NT; ++j) bv[u][j] = kv ? bf[((int64_t)kc * NT + j) * 32] : make_uint4(0, 0, 0, 0);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int chunk = blockIdx.y;
+    const int c = blockIdx.x;
+    const int64_t u0 = (int64_t)c * a.total / a.G, u1 = (int64_t)(c + 1) * a.total / a.G;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < SK_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], SK_CONS);
         }
-#pragma unroll
-        for (int u = 0; u < GEMV_UNROLL; ++u) {
-#pragma unroll
-            for (int i = 0; i < GEMV_MW; ++i) {
-                uint32_t a[8];
-                i8x4_to_f16x2((uint32_t)av[u][i].x, a[0], a[1]);
-                i8x4_to_f16x2((uint32_t)av[u][i].y, a[2], a[3]);
-                i8x4_to_f16x2((uint32_t)av[u][i].z, a[4], a[5]);
-                i8x4_to_f16x2((uint32_t)av[u][i].w, a[6], a[7]);
-#pragma unroll
-                for (int j = 0; j < NT; ++j) {
-                    mma16816(acc[i][j], a[0], a[1], a[2], a[3], bv[u][j].x, bv[u][j].y);
-                    mma16816(acc[i][j], a[4], a[5], a[6], a[7], bv[u][j].z, bv[u][j].w);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (u0 >= u1) return;
+
+    if (warp == 0) {
+        // ---------------- producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            const uint8_t* bsrc = reinterpret_cast<const uint8_t*>(a.act.frag) + (int64_t)chunk * a.KC * NT * 512;
+            for (int64_t u = u0; u < u1;) {
+                const int mg = (int)(u / a.KC);
+                const int ka = (int)(u % a.KC);
+                const int kb = (int)((int64_t)a.KC < ka + (u1 - u) ? (int64_t)a.KC : ka + (u1 - u));
+                for (int kc = ka; kc < kb; kc += SK_KCS) {
+                    const int n = min(SK_KCS, kb - kc);
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], n * (4096 + NT * 512));
+                    bulk_g2s(sa + stage * A_STAGE, a.codes + ((int64_t)mg * a.KC + kc) * 4096, n * 4096, &full[stage]);
+                    bulk_g2s(sb + stage * B_STAGE, bsrc + (int64_t)kc * NT * 512, n * NT * 512, &full[stage]);
+                    if (++stage == SK_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
                 }
+                u += kb - ka;
             }
         }
+        return;
     }
 
-    if (nsplit > 1) {
-        // deterministic split-K: stash, count, last CTA reduces in split order
-        constexpr int PER_CTA = GEMV_WARPS * GEMV_MW * NT * 32 * 4;
-        const int64_t tile_id = (int64_t)chunk * gridDim.x + blockIdx.x;
-        float* mine = partials + (tile_id * nsplit + split) * PER_CTA;
+    // ---------------- consumers
+    const int cw = warp - 1;  // consumer warp: m-tiles 2cw, 2cw+1 of the group
+    const int g = lane >> 2, q = lane & 3;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t u = u0; u < u1;) {
+        const int mg = (int)(u / a.KC);
+        const int ka = (int)(u % a.KC);
+        const int kb = (int)((int64_t)a.KC < ka + (u1 - u) ? (int64_t)a.KC : ka + (u1 - u));
+        float acc[2][NT][4];
 #pragma unroll
-        for (int i = 0; i < GEMV_MW; ++i)
-#pragma unroll
-            for (int j = 0; j < NT; ++j)
-                *reinterpret_cast<float4*>(mine + (((warp * GEMV_MW + i) * NT + j) * 32 + lane) * 4) =
-                    make_float4(acc[i][j][0], acc[i][j][1], acc[i][j][2], acc[i][j][3]);
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const int prev = atomicAdd(counters + tile_id, 1);
-            s_last = prev == nsplit - 1;
-        }
-        __syncthreads();
-        if (!s_last) return;
-        __threadfence();
-        if (threadIdx.x == 0) counters[tile_id] = 0;  // ready for the next launch
-#pragma unroll
-        for (int i = 0; i < GEMV_MW; ++i)
+        for (int i = 0; i < 2; ++i)
 #pragma unroll
             for (int j = 0; j < NT; ++j)
 #pragma unroll
                 for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.f;
-        for (int s = 0; s < nsplit; ++s) {
-            const float* p = partials + (tile_id * nsplit + s) * PER_CTA;
+        for (int kc = ka; kc < kb; kc += SK_KCS) {
+            const int n = min(SK_KCS, kb - kc);
+            mbar_wait(&full[stage], phase);
+            const uint8_t* As = sa + stage * A_STAGE;
+            const uint8_t* Bs = sb + stage * B_STAGE;
 #pragma unroll
-            for (int i = 0; i < GEMV_MW; ++i)
+            for (int kk = 0; kk < SK_KCS; ++kk) {
+                if (kk < n) {
+                    uint4 bv[NT];
 #pragma unroll
-                for (int j = 0; j < NT; ++j) {
-                    const float4 v = __ldcg(reinterpret_cast<const float4*>(p + (((warp * GEMV_MW + i) * NT + j) * 32 + lane) * 4));
-                    acc[i][j][0] += v.x;
-                    acc[i][j][1] += v.y;
-                    acc[i][j][2] += v.z;
-                    acc[i][j][3] += v.w;
+                    for (int j = 0; j < NT; ++j)
+                        bv[j] = *reinterpret_cast<const uint4*>(Bs + (kk * NT + j) * 512 + lane * 16);
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) {
+                        const uint4 av = *reinterpret_cast<const uint4*>(As + kk * 4096 + (cw * 2 + i) * 512 + lane * 16);
+                        uint32_t f[8];
+                        i8x4_to_f16x2(av.x, f[0], f[1]);
+                        i8x4_to_f16x2(av.y, f[2], f[3]);
+                        i8x4_to_f16x2(av.z, f[4], f[5]);
+                        i8x4_to_f16x2(av.w, f[6], f[7]);
+#pragma unroll
+                        for (int j = 0; j < NT; ++j) {
+                            mma16816(acc[i][j], f[0], f[1], f[2], f[3], bv[j].x, bv[j].y);
+                            mma16816(acc[i][j], f[4], f[5], f[6], f[7], bv[j].z, bv[j].w);
+                        }
+                    }
                 }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == SK_STAGES) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+        u += kb - ka;
+
+        // ---- segment finished: complete group or a piece of a split group
+        const int64_t g0 = (int64_t)mg * a.KC, g1 = g0 + a.KC;
+        const int c_first = sk_owner(g0, a.G, a.total), c_last = sk_owner(g1 - 1, a.G, a.total);
+        if (c_first != c_last) {
+            const int slot = (u0 < g0) ? 1 : 0;  // not this CTA's first segment -> slot 1
+            float* mine = a.partials + (((int64_t)chunk * a.G + c) * 2 + slot) * PER;
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j)
+                    *reinterpret_cast<float4*>(mine + (((cw * 2 + i) * NT + j) * 32 + lane) * 4) =
+                        make_float4(acc[i][j][0], acc[i][j][1], acc[i][j][2], acc[i][j][3]);
+            __threadfence();
+            cons_sync();
+            if (threadIdx.x == 32) {
+                int* ctr = a.counters + (int64_t)chunk * a.MG + mg;
+                const int prev = atomicAdd(ctr, 1);
+                const int last = prev == c_last - c_first;
+                if (last) *ctr = 0;
+                *s_flag = last;
+            }
+            cons_sync();
+            if (!*s_flag) continue;
+            __threadfence();
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.f;
+            for (int cc = c_first; cc <= c_last; ++cc) {
+                const int64_t cu0 = (int64_t)cc * a.total / a.G;
+                const float* p = a.partials + (((int64_t)chunk * a.G + cc) * 2 + (cu0 < g0 ? 1 : 0)) * PER;
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) {
+                        const float4 v =
+                            __ldcg(reinterpret_cast<const float4*>(p + (((cw * 2 + i) * NT + j) * 32 + lane) * 4));
+                        acc[i][j][0] += v.x;
+                        acc[i][j][1] += v.y;
+                        acc[i][j][2] += v.z;
+                        acc[i][j][3] += v.w;
+                    }
+            }
+        }
+        // ---- fused epilogue of the 128-row group
+        cons_sync();  // S is free (previous epilogue done)
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int row = (cw * 2 + i) * 16 + g + 8 * (r >> 1);
+                    const int col = j * 8 + 2 * q + (r & 1);
+                    S[row * SST + col] = acc[i][j][r];
+                }
+        cons_sync();
+        const int row_base = mg * 128;
+        for (int t = threadIdx.x - 32; t < 128 * TC; t += SK_CONS * 32) {
+            const int r = t % 128, j = t / 128;
+            const int o = row_base + r;
+            const int tok = chunk * TC + j;
+            if (o >= a.epi.M || tok >= a.act.n_tok) continue;
+            const float v = (S[r * SST + j] + S[r * SST + TC + j]) * a.act.back[tok];
+            epi_store(a.epi, tok, o, v);
         }
     }
+}
 
-    // C fragments -> smem [row][col]
-#pragma unroll
-    for (int i = 0; i < GEMV_MW; ++i)
-#pragma unroll
-        for (int j = 0; j < NT; ++j)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int row = (warp * GEMV_MW + i) * 16 + g + 8 * (r >> 1);
-                const int col = j * 8 + 2 * q + (r & 1);
-                S[row * SST + col] = acc[i][j][r];
-            }
-    __syncthreads();
-    const int row_base = blockIdx.x * GEMV_ROWS;
-    for (int t = threadIdx.x; t < GEMV_ROWS * TC; t += blockDim.x) {
-        const int r = t % GEMV_ROWS, j = t / GEMV_ROWS;
-        const int o = row_base + r;
-        const int tok = chunk * TC + j;
-        if (o >= epi.M || tok >= act.n_tok) continue;
-        const float v = (S[r * SST + j] + S[r * SST + TC + j]) * act.back[tok];
-        epi_store(epi, tok, o, v);
+template <int NT>
+static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
+                     int64_t partial_cap, cudaStream_t st) {
+    constexpr int TC = NT * 4;
+    const size_t smem = (size_t)SK_STAGES * (SK_KCS * 4096 + SK_KCS * NT * 512) + 128 * (2 * TC + 1) * 4 + 16 +
+                        2 * SK_STAGES * 8 + 16;
+    static int blocks_per_sm = 0, sms = 0;
+    if (!blocks_per_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_gemv_i8<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_gemv_i8<NT>, SK_THREADS, smem);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
+    SkArgs a;
+    a.codes = m.codes;
+    a.MG = m.Mp / 128;
+    a.KC = m.Kp / 32;
+    a.total = (int64_t)a.MG * a.KC;
+    const int chunks = (int)ceil_div(act.n_tok, act.tc);
+    int64_t G = std::max<int64_t>(1, (int64_t)sms * blocks_per_sm / chunks);
+    G = std::min<int64_t>(G, a.total);
+    const int64_t per_tile = 128 * 2 * TC;
+    while (G > 1 && (int64_t)chunks * G * 2 * per_tile > partial_cap) G /= 2;
+    a.G = (int)G;
+    a.act = act;
+    a.epi = epi;
+    a.partials = partials;
+    a.counters = counters;
+    k_gemv_i8<NT><<<dim3((unsigned)G, chunks), SK_THREADS, smem, st>>>(a);
+    return launch_check("gemv_i8");
 }
 
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters, int64_t partial_cap,
                 cudaStream_t st) {
-    const int MT = m.Mp / 16, KC = m.Kp / 32;
-    const int gx = (int)ceil_div(MT, GEMV_WARPS * GEMV_MW);
-    const int chunks = (int)ceil_div(act.n_tok, act.tc);
-    const int NT = act.tc / 4;
-    // split K so the grid covers the machine a few times over; >= 4 k-chunks per split
-    int splits = (int)ceil_div(148 * 8, (int64_t)gx * chunks);
-    splits = std::max(1, std::min(splits, KC / 4));
-    const int64_t per_cta = (int64_t)GEMV_WARPS * GEMV_MW * NT * 32 * 4;
-    while (splits > 1 && (int64_t)gx * chunks * splits * per_cta > partial_cap) --splits;
-    int kc_per = (int)ceil_div(KC, splits);
-    kc_per = (int)round_up(kc_per, GEMV_UNROLL);
-    splits = (int)ceil_div(KC, kc_per);
-    dim3 grid(gx, chunks, splits);
-    switch (NT) {
-        case 1: k_gemv_i8<1><<<grid, GEMV_WARPS * 32, 0, st>>>(m.codes, MT, KC, kc_per, act, epi, partials, counters); break;
-        case 2: k_gemv_i8<2><<<grid, GEMV_WARPS * 32, 0, st>>>(m.codes, MT, KC, kc_per, act, epi, partials, counters); break;
-        case 4: k_gemv_i8<4><<<grid, GEMV_WARPS * 32, 0, st>>>(m.codes, MT, KC, kc_per, act, epi, partials, counters); break;
-        case 8: k_gemv_i8<8><<<grid, GEMV_WARPS * 32, 0, st>>>(m.codes, MT, KC, kc_per, act, epi, partials, counters); break;
+    switch (act.tc / 4) {
+        case 1: return sk_launch<1>(m, act, epi, partials, counters, partial_cap, st);
+        case 2: return sk_launch<2>(m, act, epi, partials, counters, partial_cap, st);
+        case 4: return sk_launch<4>(m, act, epi, partials, counters, partial_cap, st);
+        case 8: return sk_launch<8>(m, act, epi, partials, counters, partial_cap, st);
         default: set_error("bad column tile"); return PB_ERR_GENERIC;
     }
-    return launch_check("gemv_i8");
 }
 
 // ------------------------------------------------------------------ f32-weights path

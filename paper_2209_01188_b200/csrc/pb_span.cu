@@ -71,7 +71,7 @@ int alloc_mat(pb_span* s, Mat& m, int K, int M, bool int8) {
     m.K = K;
     m.M = M;
     m.Kp = (int)round_up(K, 32);
-    m.Mp = (int)round_up(M, 16);
+    m.Mp = (int)round_up(M, 128);  // 128-row groups (pb_gemv.cu)
     m.int8 = int8;
     if (int8) {
         if (int rc = dalloc(s, &m.codes, (int64_t)m.Mp * m.Kp)) return rc;

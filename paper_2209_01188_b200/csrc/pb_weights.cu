@@ -6,7 +6,9 @@
 // feature as an outlier when max_o |W[k, o]| > threshold. Codes are stored in a
 // fragment-tiled [out, in] layout consumed by the mma GEMV (pb_gemv.cu):
 //   tile (mt, kc) = rows [16 mt, 16 mt + 16) x inputs [32 kc, 32 kc + 32),
-//   512 B at ((mt * KC + kc) * 512); lane l = 4g + q owns bytes [16 l, 16 l + 16):
+//   512 B at (((mt / 8) * KC + kc) * 8 + mt % 8) * 512, i.e. the eight m-tiles of
+//   a 128-row group are adjacent for each kc (one 4 KB bulk copy per k tile);
+//   lane l = 4g + q owns bytes [16 l, 16 l + 16):
 //   byte 8 kt + i holds A[row(i), 16 kt + col(i)] with the m16n8k16 A-fragment
 //   map row(i) = g + 8((i >> 1) & 1), col(i) = 2q + (i & 1) + 8(i >> 2).
 // Weights are generated on the fly from the counter-form SplitMix64 stream, so
@@ -92,7 +94,8 @@ __global__ void __launch_bounds__(256) k_quant_tiles(Src src, int64_t K, int64_t
             }
             words[b >> 2] |= (uint32_t)(uint8_t)(int8_t)code << (8 * (b & 3));
         }
-        *reinterpret_cast<uint4*>(codes + t * 16) = make_uint4(words[0], words[1], words[2], words[3]);
+        const int64_t off = ((((mt >> 3) * KC + kc) * 8 + (mt & 7)) * 32 + lane) * 16;
+        *reinterpret_cast<uint4*>(codes + off) = make_uint4(words[0], words[1], words[2], words[3]);
     }
 }
 
@@ -129,7 +132,7 @@ __global__ void k_untile(const int8_t* __restrict__ tiles, int64_t K, int64_t M,
         const int q = cc >> 1, lo = cc & 1;
         const int i = lo + 2 * hi_r + 4 * hi_c;
         const int lane = 4 * g + q;
-        out[t] = tiles[((mt * KC + kc) * 32 + lane) * 16 + kt * 8 + i];
+        out[t] = tiles[((((mt >> 3) * KC + kc) * 8 + (mt & 7)) * 32 + lane) * 16 + kt * 8 + i];
     }
 }
 
