@@ -20,6 +20,7 @@
 // B (activation) fragment layout, chunk c of tc tokens (columns: tc hi then tc lo):
 //   uint4 at ((c * KC + kc) * NT + nt) * 32 + lane, NT = 2 tc / 8,
 //   words {kt0: B[2q..2q+1][g], B[2q+8..2q+9][g]; kt1: same +16}, column = 8 nt + g.
+#include "pb_async.cuh"
 #include "pb_common.cuh"
 #include "pb_span.h"
 
@@ -302,35 +303,6 @@ constexpr int SK_THREADS = (SK_CONS + 1) * 32;   // + producer warp
 constexpr int SK_KCS = 2;                        // k-tiles per stage
 constexpr int SK_STAGES = 4;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
 __device__ __forceinline__ void cons_sync() {  // the 4 consumer warps only
     asm volatile("bar.sync 1, %0;" ::"n"(SK_CONS * 32) : "memory");
 }
@@ -376,7 +348,7 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], SK_CONS);
         }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_fence_init();
     }
     __syncthreads();
     if (u0 >= u1) return;

@@ -359,7 +359,7 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                     return rc;
                 prof_end(s, ev, 2, 4.0 * n_tok * K, st);
                 Act a{s->frag, s->back, n_tok, tc};
-                launches += 2;
+                launches += 3;  // rowstats + fragwrite + gemv
                 ev = prof_begin(s, st);
                 // algorithmic bytes: codes + per-feature scales + bias (+ f32 outlier rows)
                 const double bytes = (double)m.M * m.K + 4.0 * m.K + 4.0 * m.M + 4.0 * m.n_outl * m.M;
@@ -369,7 +369,7 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
             }
             if (int rc = launch_prologue(mode, x, n_tok, K, K, g, be, m, tc, nullptr, s->back, s->stats, nullptr, s->y32, st))
                 return rc;
-            launches += 2;
+            launches += mode == PRO_LN ? 3 : 1;  // (rowstats + rows) + gemm
             const int ev = prof_begin(s, st);
             int rc = launch_gemm_f32(m, s->y32, n_tok, e, st);
             prof_end(s, ev, 3, 4.0 * m.M * m.K, st);
@@ -380,7 +380,7 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
         e.out = s->q;
         if (int rc = matmul(0, PRO_LN, x_in, d, b.ln1_g, b.ln1_b, e)) return rc;
         AttnArgs aa{s->q, kvb, s->d_tok_seq, s->d_tok_pos, s->d_pages, s->slopes, s->ctx, s->attn_part,
-                    n_tok, s->max_pages, s->H, s->dh, s->cfg.page_tokens, d, max_pos};
+                    s->counters + (1 << 19), n_tok, s->max_pages, s->H, s->dh, s->cfg.page_tokens, d, max_pos};
         {
             const int ev = prof_begin(s, st);
             if (int rc = launch_attention(aa, s->attn_cap, st)) return rc;
@@ -389,7 +389,7 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
             for (int i = 0; i < n_tok; ++i) kv_bytes += 4.0 * (s->h_tok_pos_last[i] + 1) * d;
             prof_end(s, ev, 1, kv_bytes, st);
         }
-        launches += 2;
+        launches += 1;
         e = base;
         e.kind = EPI_RESID;
         e.resid = x_in;

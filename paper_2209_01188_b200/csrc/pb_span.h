@@ -106,6 +106,7 @@ struct AttnArgs {
     const float* slopes;     // [H]
     float* ctx;              // [n_tok][d]
     float* part;             // split workspace
+    int* counters;           // [n_tok][H] last-CTA merge counters (zeroed, self-resetting)
     int n_tok, max_pages, H, dh, P, d;
     int max_pos;             // max over tokens of (pos + 1)
 };
