@@ -55,14 +55,7 @@ def parse():
 # ------------------------------------------------------------------ helpers
 
 
-def split_blocks(L: int, n: int):
-    base, extra = divmod(L, n)
-    out, s = [], 0
-    for r in range(n):
-        k = base + (1 if r < extra else 0)
-        out.append((s, s + k))
-        s += k
-    return out
+from paper_2209_01188_b200.pipeline import split_blocks  # noqa: E402
 
 
 def bytes_per_step(cfg, ctx_tokens_per_session):
@@ -176,6 +169,10 @@ def run_reference(args):
 
 
 class Pipeline:
+    """One span of the 70-block model per GPU; jobs follow the deadlock-free
+    ring schedule of paper_2209_01188_b200.pipeline (grouped NCCL send/recv of
+    the int8 wire payload: codes then f32 scales in one byte buffer)."""
+
     def __init__(self, args, cfg):
         import torch
         import torch.distributed as dist
@@ -204,15 +201,24 @@ class Pipeline:
         self.seqs = [self.span.new_sequence() for _ in range(self.S)]
         d = cfg.hidden
         self.d = d
-        self.codes = torch.empty(args.prefill_chunk * d, dtype=torch.int8, device=self.dev)
-        self.scales = torch.empty(-(-args.prefill_chunk * d // 64), dtype=torch.float32, device=self.dev)
-        self.rcodes = torch.empty_like(self.codes)
-        self.rscales = torch.empty_like(self.scales)
+        cap = self.payload_bytes(args.prefill_chunk)
+        self.inbox = torch.empty(cap, dtype=torch.uint8, device=self.dev)
+        self.outbox = torch.empty(cap, dtype=torch.uint8, device=self.dev)
         self.out = torch.empty(args.prefill_chunk, d, dtype=torch.float32, device=self.dev)
         g = torch.Generator(device=self.dev)
         g.manual_seed(7)
         self.inputs = torch.randn(64, d, generator=g, device=self.dev) * 0.05  # embedding-like rows
         self.launches = 0
+        self.total_jobs = 0
+
+    def payload_bytes(self, t):
+        n = t * self.d
+        return -(-n // 16) * 16 + 4 * (-(-n // 64))
+
+    def views(self, buf, t):
+        n = t * self.d
+        off = -(-n // 16) * 16
+        return buf[:n].view(__import__("torch").int8), buf[off:off + 4 * (-(-n // 64))].view(__import__("torch").float32)
 
     def barrier(self):
         import torch
@@ -222,39 +228,42 @@ class Pipeline:
             self.dist.barrier()
         torch.cuda.synchronize()
 
-    def job(self, j: int, t: int, x=None, host_in=None, host_out=None):
-        """Job j = session j % S; receive (unless first stage of a fresh session),
-        run the span, send the int8 hidden to the next stage (ring)."""
-        r, N = self.rank, self.world
-        seq = self.seqs[j % self.S]
-        n = t * self.d
-        nb = -(-n // 64)
-        codes, scales = self.rcodes[:n], self.rscales[:nb]
-        if r > 0 or (N > 1 and j >= self.S):
-            src = (r - 1) % N
-            self.dist.recv(codes, src)
-            self.dist.recv(scales, src)
-        if r == 0:
-            if host_in is not None:
-                self.out[:t].copy_(host_in[:t], non_blocking=True)
-                x = self.out[:t]
-            inp = x if x is not None else self.inputs[j % 64: j % 64 + 1].expand(t, self.d).contiguous()
-            self.span.step_codes([(seq, None)], [t], out_codes=self.codes[:n], out_scales=self.scales[:nb],
-                                 in_f32=inp, out_f32=self.out[:t])
-        else:
-            self.span.step_codes([(seq, (codes, scales))], [t], out_codes=self.codes[:n],
-                                 out_scales=self.scales[:nb], out_f32=self.out[:t])
-        self.launches += self.span.last_launches
-        if host_out is not None and r == N - 1:
-            host_out[:n].copy_(self.codes[:n], non_blocking=True)
-        if N > 1 and (r < N - 1 or j + self.S < self.total_jobs):
-            dst = (r + 1) % N
-            self.dist.send(self.codes[:n], dst)
-            self.dist.send(self.scales[:nb], dst)
+    def run(self, jobs, x_for=None, host_in=None, host_out=None, sync_out=False):
+        """jobs: [(job id, new positions t)]; x_for(j, t) -> span-0 input rows."""
+        import torch
 
-    def run_jobs(self, jobs, **kw):
-        for j, t in jobs:
-            self.job(j, t, **kw)
+        from paper_2209_01188_b200.pipeline import RingSchedule, run_jobs, torch_exchange
+
+        sched = RingSchedule(self.rank, self.world, self.S, self.total_jobs)
+        tmap = dict(jobs)
+        r, N = self.rank, self.world
+
+        def step(j, inbox):
+            t = tmap[j]
+            seq = self.seqs[j % self.S]
+            oc, os_ = self.views(self.outbox, t)
+            if inbox is None or r == 0:  # span 0: fresh input (a received ring payload only orders the step)
+                if host_in is not None:
+                    self.out[:t].copy_(host_in[:t], non_blocking=True)
+                    inp = self.out[:t]
+                elif x_for is not None:
+                    inp = x_for(j, t)
+                else:
+                    inp = self.inputs[j % 64: j % 64 + 1].expand(t, self.d).contiguous()
+                self.span.step_codes([(seq, None)], [t], out_codes=oc, out_scales=os_, in_f32=inp,
+                                     out_f32=self.out[:t])
+            else:
+                ic, is_ = self.views(inbox, t)
+                self.span.step_codes([(seq, (ic, is_))], [t], out_codes=oc, out_scales=os_, out_f32=self.out[:t])
+            self.launches += self.span.last_launches
+            if r == N - 1 and host_out is not None:
+                host_out[:t * self.d].copy_(oc, non_blocking=True)
+                if sync_out:
+                    torch.cuda.current_stream().synchronize()  # result readable on the host
+            return self.outbox[:self.payload_bytes(t)]
+
+        run_jobs(sched, [j for j, _ in jobs], step, torch_exchange,
+                 lambda j: self.inbox[:self.payload_bytes(tmap[j])])
 
 
 def run_ours(args):
@@ -286,8 +295,7 @@ def run_ours(args):
         jobs = [(ci * S + m, c) for ci, c in enumerate(chunks) for m in range(S)]
         pl.total_jobs = len(jobs) + S * (W + 2 * K + (0 if args.no_e2e else K))
         # all prefill jobs, then decode jobs continue numbering
-        for j, t in jobs:
-            pl.job(j, t, x=pl.inputs[:t] if t <= 64 else torch.randn(t, cfg.hidden, device=pl.dev) * 0.05)
+        pl.run(jobs, x_for=lambda j, t: pl.inputs[:t] if t <= 64 else torch.randn(t, cfg.hidden, device=pl.dev) * 0.05)
         jbase = len(jobs)
     torch.cuda.synchronize()
     pf_s = time.perf_counter() - t_pf
@@ -295,8 +303,7 @@ def run_ours(args):
         jbase = 0
         pl.total_jobs = S * (W + 2 * K + (0 if args.no_e2e else K))
     # ---- warmup decode
-    for i in range(W * S):
-        pl.job(jbase + i, 1)
+    pl.run([(jbase + i, 1) for i in range(W * S)])
     jbase += W * S
     # ---- timed decode (device-resident inputs)
     pl.barrier()
@@ -304,8 +311,7 @@ def run_ours(args):
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(pl.local) as clk:
         start.record()
-        for i in range(K * S):
-            pl.job(jbase + i, 1)
+        pl.run([(jbase + i, 1) for i in range(K * S)])
         stop.record()
         pl.barrier()
     jbase += K * S
@@ -315,8 +321,7 @@ def run_ours(args):
     # launching stream) over a second, identical pass of K steps; kept out of
     # the value's timed region so the events do not perturb it
     pl.span.profile(True)
-    for i in range(K * S):
-        pl.job(jbase + i, 1)
+    pl.run([(jbase + i, 1) for i in range(K * S)])
     pl.barrier()
     jbase += K * S
     gemv = pl.span.profile_read(pl.span.PROF_GEMV)
@@ -339,11 +344,8 @@ def run_ours(args):
         t0 = time.perf_counter()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for i in range(K * S):
-            pl.job(jbase + i, 1, host_in=host_in if rank == 0 else None,
-                   host_out=host_out if rank == N - 1 else None)
-            if rank == N - 1:
-                torch.cuda.current_stream().synchronize()  # result readable on the host
+        pl.run([(jbase + i, 1) for i in range(K * S)], host_in=host_in if rank == 0 else None,
+               host_out=host_out if rank == N - 1 else None, sync_out=True)
         e1.record()
         pl.barrier()
         wall = time.perf_counter() - t0

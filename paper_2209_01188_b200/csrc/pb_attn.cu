@@ -219,13 +219,27 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) k_attn(AttnArgs a, int nsplit)
         const float ms = __ldcg(p + s * (DH + 2));
         if (ms != -INFINITY) L += __ldcg(p + s * (DH + 2) + 1) * expf(ms - M);
     }
+    float mloc = 0.f;
     for (int i = threadIdx.x; i < DH; i += blockDim.x) {
         float o = 0.f;
         for (int s = 0; s < nsplit; ++s) {
             const float ms = __ldcg(p + s * (DH + 2));
             if (ms != -INFINITY) o += __ldcg(p + s * (DH + 2) + 2 + i) * expf(ms - M);
         }
-        a.ctx[(int64_t)tok * a.d + h * DH + i] = o / L;
+        const float c = o / L;
+        a.ctx[(int64_t)tok * a.d + h * DH + i] = c;
+        if (a.tokmax) mloc = fmaxf(mloc, fabsf(c * a.s_next[h * DH + i]));
+    }
+    if (a.tokmax) {  // operand range of the wo GEMV (exact, order-independent max)
+        mloc = warp_max(mloc);
+        if (lane == 0) red[warp] = mloc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float m = red[0];
+#pragma unroll
+            for (int w = 1; w < ATT_WARPS; ++w) m = fmaxf(m, red[w]);
+            atomicMax(reinterpret_cast<int*>(a.tokmax) + tok, __float_as_int(m));
+        }
     }
 }
 

@@ -94,9 +94,10 @@ struct ProArgs {
     int tc;
     uint4* frag;
     float* back;   // [n_tok] 2^-shift (epilogue rescale)
-    float4* stats; // [n_tok] {mu, inv, 2^shift, -}
+    float4* stats; // [n_tok] {mu, inv, 2^shift, 2^-shift}
     float* xo;
     float* y32;
+    ProSrc src;
 };
 
 __device__ __forceinline__ float pro_y(const ProArgs& a, const float* x, int k, float mu, float inv) {
@@ -157,16 +158,119 @@ __global__ void __launch_bounds__(STATS_THREADS) k_rowstats(ProArgs a) {
     }
     if (threadIdx.x == 0) {
         a.back[tok] = ldexpf(1.f, -shift);
-        a.stats[tok] = make_float4(mu, inv, ldexpf(1.f, shift), 0.f);
+        a.stats[tok] = make_float4(mu, inv, ldexpf(1.f, shift), ldexpf(1.f, -shift));
     }
+}
+
+// Chan et al. merge of (n, mean, M2, min, max) summaries, a before b.
+struct RowSum {
+    double n, mean, m2;
+    float mn, mx;
+};
+__device__ __forceinline__ RowSum rs_merge(const RowSum& a, const RowSum& b) {
+    if (a.n == 0.0) return b;
+    if (b.n == 0.0) return a;
+    RowSum r;
+    r.n = a.n + b.n;
+    const double d = b.mean - a.mean;
+    r.mean = a.mean + d * (b.n / r.n);
+    r.m2 = a.m2 + b.m2 + d * d * (a.n * b.n / r.n);
+    r.mn = fminf(a.mn, b.mn);
+    r.mx = fmaxf(a.mx, b.mx);
+    return r;
+}
+
+__device__ __forceinline__ int shift_for(float bound) {
+    if (!(bound > 0.f) || !isfinite(bound)) return 0;
+    int e;
+    frexpf(bound, &e);
+    return 14 - e;
+}
+
+// Resolve {mu, inv, 2^shift, 2^-shift} of one token inside the operand
+// producer (warp 0), from the producing epilogue's partial summaries
+// (deterministic lane-strided + fixed shuffle-tree merge) or from the exact
+// atomicMax of |x s|.
+__device__ float4 resolve_stats(const ProArgs& a, int tok) {
+    const int lane = threadIdx.x & 31;
+    if (a.src.kind == SRC_TOKMAX) {
+        const int sh = shift_for(a.src.tokmax[tok]);
+        return make_float4(0.f, 1.f, ldexpf(1.f, sh), ldexpf(1.f, -sh));
+    }
+    if (a.src.kind == SRC_STATS) return a.stats[tok];
+    RowSum r{0.0, 0.0, 0.0, INFINITY, -INFINITY};
+    for (int g = lane; g < a.src.MG; g += 32) {
+        const float4 p = a.src.pstats[(int64_t)tok * a.src.MG + g];
+        const int n = min(128, a.src.M - g * 128);
+        r = rs_merge(r, RowSum{(double)n, (double)p.x, (double)p.y, p.z, p.w});
+    }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        RowSum o;
+        o.n = __shfl_xor_sync(0xffffffffu, r.n, off);
+        o.mean = __shfl_xor_sync(0xffffffffu, r.mean, off);
+        o.m2 = __shfl_xor_sync(0xffffffffu, r.m2, off);
+        o.mn = __shfl_xor_sync(0xffffffffu, r.mn, off);
+        o.mx = __shfl_xor_sync(0xffffffffu, r.mx, off);
+        r = (lane & off) ? rs_merge(o, r) : rs_merge(r, o);  // lower lane first: identical on both sides
+    }
+    const float mu = (float)r.mean;
+    const float var = (float)(r.m2 / a.src.M);
+    const float inv = 1.0f / sqrtf(var + 1e-5f);
+    const float dev = fmaxf(r.mx - mu, mu - r.mn);
+    const int sh = shift_for(a.src.gs * dev * inv + a.src.bs);
+    return make_float4(mu, inv, ldexpf(1.f, sh), ldexpf(1.f, -sh));
+}
+
+__global__ void k_bound_consts(const float* __restrict__ g, const float* __restrict__ b, const float* __restrict__ s,
+                               int K, float* __restrict__ out) {
+    __shared__ float red[32];
+    float mg = 0.f, mb = 0.f;
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        mg = fmaxf(mg, fabsf(g[k]) * s[k]);
+        mb = fmaxf(mb, fabsf(b[k]) * s[k]);
+    }
+    mg = block_max(mg, red);
+    mb = block_max(mb, red);
+    if (threadIdx.x == 0) {
+        out[0] = mg;
+        out[1] = mb;
+    }
+}
+
+int bound_consts(const float* gamma, const float* beta, const float* scales, int K, float* gs, float* bs,
+                 cudaStream_t st) {
+    float* d = nullptr;
+    PB_CHECK_CUDA(cudaMallocAsync(&d, 2 * sizeof(float), st));
+    k_bound_consts<<<1, 1024, 0, st>>>(gamma, beta, scales, K, d);
+    if (int rc = launch_check("bound_consts")) return rc;
+    float h[2];
+    PB_CHECK_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+    PB_CHECK_CUDA(cudaStreamSynchronize(st));
+    PB_CHECK_CUDA(cudaFreeAsync(d, st));
+    *gs = h[0];
+    *bs = h[1];
+    return PB_OK;
 }
 
 // hi/lo fp16 B fragments of x~ = y * s * 2^shift (layout in the header comment);
 // one thread per (token, 32-wide k chunk, lane quad q).
 __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
+    __shared__ float4 s_st;
     const int tok = blockIdx.y;
     const float* x = a.x + (int64_t)tok * a.K;
-    const float4 st = a.stats[tok];
+    if (threadIdx.x < 32) {
+        const float4 r = resolve_stats(a, tok);
+        if (threadIdx.x == 0) {
+            s_st = r;
+            if (blockIdx.x == 0) {
+                a.back[tok] = r.w;
+                if (a.src.zero_tokmax) a.src.zero_tokmax[tok] = 0.f;
+            }
+        }
+    }
+    __syncthreads();
+    const float4 st = s_st;
     const int KC = a.Kp / 32;
     const int it = blockIdx.x * blockDim.x + threadIdx.x;
     if (blockIdx.x == 0 && a.xo) {
@@ -210,12 +314,13 @@ __global__ void __launch_bounds__(256) k_rows_f32(ProArgs a) {
         a.y32[(int64_t)tok * a.K + k] = pro_y(a, x, k, st.x, st.y);
 }
 
-int launch_prologue(int mode, const float* x, int n_tok, int K, int Kp, const float* gamma, const float* beta,
-                    const Mat& m, int tc, uint4* frag, float* back, float4* stats, float* xo, float* y32,
-                    cudaStream_t st) {
+int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int K, int Kp, const float* gamma,
+                    const float* beta, const Mat& m, int tc, uint4* frag, float* back, float4* stats, float* xo,
+                    float* y32, cudaStream_t st) {
     ProArgs a{mode, x, K, Kp, gamma, beta, y32 ? nullptr : m.scales, m.n_outl, m.outl_idx, tc, frag, back, stats,
-              xo, y32};
-    if (mode == PRO_LN || !y32) {
+              xo, y32, src};
+    if (y32) a.src = ProSrc{};
+    if (a.src.kind == SRC_STATS && (mode == PRO_LN || !y32)) {
         k_rowstats<<<n_tok, STATS_THREADS, 0, st>>>(a);
         if (int rc = launch_check("rowstats")) return rc;
     }
@@ -240,14 +345,16 @@ __device__ __forceinline__ float gelu_tanh(float x) {  // model.py:286-292 (f32)
     return 0.5f * x * (1.f + tanhf(u));
 }
 
-__device__ __forceinline__ void epi_store(const Epi& e, int tok, int o, float v) {
+__device__ __forceinline__ float epi_store(const Epi& e, int tok, int o, float v) {
     v += e.bias[o];
     for (int j = 0; j < e.n_outl; ++j) v = fmaf(e.outl_rows[(int64_t)j * e.M + o], e.xo[(int64_t)tok * e.n_outl + j], v);
     const int64_t idx = (int64_t)tok * e.M + o;
     if (e.kind == EPI_RESID) {
-        e.out[idx] = e.resid[idx] + v;
+        v = e.resid[idx] + v;
+        e.out[idx] = v;
     } else if (e.kind == EPI_GELU) {
-        e.out[idx] = gelu_tanh(v);
+        v = gelu_tanh(v);
+        e.out[idx] = v;
     } else {  // EPI_QKV: contiguous q | k | v column thirds (model.py:342-344)
         if (o < e.d) {
             e.out[(int64_t)tok * e.d + o] = v;
@@ -261,6 +368,7 @@ __device__ __forceinline__ void epi_store(const Epi& e, int tok, int o, float v)
             e.kv[((((int64_t)page * 2 + part) * e.H + h) * e.P + slot) * e.dh + dd] = __float2half_rn(v);
         }
     }
+    return v;
 }
 
 // ------------------------------------------------------------------ int8 mma GEMV
@@ -493,13 +601,49 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
                 }
         cons_sync();
         const int row_base = mg * 128;
+        const bool want_sum = a.epi.pstats != nullptr, want_max = a.epi.tokmax != nullptr;
         for (int t = threadIdx.x - 32; t < 128 * TC; t += SK_CONS * 32) {
             const int r = t % 128, j = t / 128;
             const int o = row_base + r;
             const int tok = chunk * TC + j;
             if (o >= a.epi.M || tok >= a.act.n_tok) continue;
             const float v = (S[r * SST + j] + S[r * SST + TC + j]) * a.act.back[tok];
-            epi_store(a.epi, tok, o, v);
+            const float y = epi_store(a.epi, tok, o, v);
+            if (want_max) S[r * SST + j] = fabsf(y * a.epi.s_next[o]);
+            else if (want_sum) S[r * SST + j] = y;
+        }
+        if (want_sum || want_max) {
+            // per-token summary of this 128-row group for the next operand's range / LayerNorm
+            cons_sync();
+            const int nrow = min(128, a.epi.M - row_base);
+            for (int j = cw; j < TC; j += SK_CONS) {
+                const int tok = chunk * TC + j;
+                if (tok >= a.act.n_tok) continue;
+                if (want_max) {
+                    float m = 0.f;
+                    for (int r = lane; r < nrow; r += 32) m = fmaxf(m, S[r * SST + j]);
+                    m = warp_max(m);
+                    if (lane == 0) atomicMax(reinterpret_cast<int*>(a.epi.tokmax) + tok, __float_as_int(m));
+                } else {
+                    float s = 0.f, mn = INFINITY, mx = -INFINITY;
+                    for (int r = lane; r < nrow; r += 32) {
+                        const float y = S[r * SST + j];
+                        s += y;
+                        mn = fminf(mn, y);
+                        mx = fmaxf(mx, y);
+                    }
+                    const float mean = warp_sum(s) / nrow;
+                    float m2 = 0.f;
+                    for (int r = lane; r < nrow; r += 32) {
+                        const float dlt = S[r * SST + j] - mean;
+                        m2 = fmaf(dlt, dlt, m2);
+                    }
+                    m2 = warp_sum(m2);
+                    mn = -warp_max(-mn);
+                    mx = warp_max(mx);
+                    if (lane == 0) a.epi.pstats[(int64_t)tok * ((a.epi.M + 127) / 128) + mg] = make_float4(mean, m2, mn, mx);
+                }
+            }
         }
     }
 }

@@ -33,6 +33,8 @@ struct pb_span {
     uint4* frag = nullptr;
     float* back = nullptr;
     float4* stats = nullptr;
+    float4 *pst_x = nullptr, *pst_mid = nullptr;  // per-128-row LN summaries [NT][d/128]
+    float *tokmax_ctx = nullptr, *tokmax_act = nullptr;  // operand ranges [NT]
     float* partials = nullptr;
     int64_t partial_cap = 0;
     int* counters = nullptr;
@@ -97,7 +99,7 @@ void free_span(pb_span* s) {
         cudaFree(b.ln2_b);
         for (auto* p : b.bias) cudaFree(p);
     }
-    void* ptrs[] = {s->kv, s->slopes, s->xa, s->mid, s->q, s->ctx, s->act, s->xo, s->y32, s->frag, s->back, s->stats,
+    void* ptrs[] = {s->kv, s->slopes, s->xa, s->mid, s->q, s->ctx, s->act, s->xo, s->y32, s->frag, s->back, s->stats, s->pst_x, s->pst_mid, s->tokmax_ctx, s->tokmax_act,
                     s->partials, s->counters, s->attn_part, s->d_tok_seq, s->d_tok_pos, s->d_pages,
                     s->hop_codes, s->hop_scales};
     for (void* p : ptrs) cudaFree(p);
@@ -171,6 +173,10 @@ int pb_span_create(const pb_span_config* cfg, pb_span** out) {
     if (!rc && int8) rc = dalloc(s, &s->frag, (int64_t)(NT + 31) * kp_max * 4 / 16 + 64);
     if (!rc) rc = dalloc(s, &s->back, NT);
     if (!rc) rc = dalloc(s, &s->stats, NT);
+    if (!rc) rc = dalloc(s, &s->pst_x, (int64_t)NT * ceil_div(d, 128));
+    if (!rc) rc = dalloc(s, &s->pst_mid, (int64_t)NT * ceil_div(d, 128));
+    if (!rc) rc = dalloc(s, &s->tokmax_ctx, NT);
+    if (!rc) rc = dalloc(s, &s->tokmax_act, NT);
     s->partial_cap = (int64_t)8 << 20;
     if (!rc && int8) rc = dalloc(s, &s->partials, s->partial_cap);
     if (!rc) rc = dalloc(s, &s->counters, 1 << 20);
@@ -231,6 +237,12 @@ static int init_block_vectors(pb_span* s, BlockW& b, cudaStream_t st) {
     return PB_OK;
 }
 
+static int block_bounds(pb_span* s, BlockW& b, cudaStream_t st) {
+    if (s->cfg.weights != PB_WEIGHTS_INT8) return PB_OK;
+    if (int rc = bound_consts(b.ln1_g, b.ln1_b, b.mat[0].scales, s->d, &b.gs1, &b.bs1, st)) return rc;
+    return bound_consts(b.ln2_g, b.ln2_b, b.mat[2].scales, s->d, &b.gs2, &b.bs2, st);
+}
+
 int pb_span_gen_block(pb_span* span, int32_t j, uint64_t key_wqkv, uint64_t key_wo, uint64_t key_win,
                       uint64_t key_wout, float outlier_boost, int32_t boost_every, void* stream) {
     PB_REQUIRE(span && j >= 0 && j < span->cfg.n_blocks, PB_ERR_BAD_REQUEST, "block index out of range");
@@ -244,6 +256,7 @@ int pb_span_gen_block(pb_span* span, int32_t j, uint64_t key_wqkv, uint64_t key_
     for (int m = 0; m < 4; ++m)
         if (int rc = fill_matrix_gen(b.mat[m], keys[m], span->cfg.outlier_threshold, outlier_boost, every, st))
             return rc;
+    if (int rc = block_bounds(span, b, st)) return rc;
     PB_CHECK_CUDA(cudaStreamSynchronize(st));
     return PB_OK;
 }
@@ -272,6 +285,7 @@ int pb_span_load_block(pb_span* span, int32_t j, const float* d_ln1_g, const flo
     const float* ws[4] = {d_wqkv, d_wo, d_win, d_wout};
     for (int m = 0; m < 4; ++m)
         if (int rc = fill_matrix_f32(b.mat[m], ws[m], span->cfg.outlier_threshold, st)) return rc;
+    if (int rc = block_bounds(span, b, st)) return rc;
     PB_CHECK_CUDA(cudaStreamSynchronize(st));
     return PB_OK;
 }
@@ -324,10 +338,16 @@ static void prof_end(pb_span* s, int ev, int kind, double bytes, cudaStream_t st
     s->prof.push_back({kind, ev, bytes});
 }
 
+// One step through every hosted block. int8 spans chain the operand statistics
+// through the epilogues: out-GEMV (block j-1) -> per-128-row LN summaries ->
+// qkv operand of block j; attention -> max|ctx s_wo| -> wo operand; wo-GEMV ->
+// LN summaries -> wmlp_in operand; wmlp_in-GEMV -> max|act s_out| -> wmlp_out
+// operand. Only block 0's LN1 needs a separate row-statistics kernel.
 static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float* out, cudaStream_t st) {
     const int d = s->d, rd = s->rd;
     const bool int8 = s->cfg.weights == PB_WEIGHTS_INT8;
     const int tc = choose_tc(n_tok);
+    const int MGd = (int)ceil_div(d, 128);
     int launches = 0;
     for (int j = 0; j < s->cfg.n_blocks; ++j) {
         BlockW& b = s->blocks[j];
@@ -345,7 +365,8 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
         base.dh = s->dh;
         base.P = s->cfg.page_tokens;
         base.d = d;
-        auto matmul = [&](int mi, int mode, const float* x, int K, const float* g, const float* be, Epi e) -> int {
+        auto matmul = [&](int mi, int mode, const ProSrc& src, const float* x, int K, const float* g,
+                          const float* be, Epi e) -> int {
             const Mat& m = b.mat[mi];
             e.M = m.M;
             e.bias = b.bias[mi];
@@ -355,11 +376,12 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                 e.outl_rows = m.outl_rows;
                 e.xo = s->xo;
                 int ev = prof_begin(s, st);
-                if (int rc = launch_prologue(mode, x, n_tok, K, m.Kp, g, be, m, tc, s->frag, s->back, s->stats, s->xo, nullptr, st))
+                if (int rc = launch_prologue(mode, src, x, n_tok, K, m.Kp, g, be, m, tc, s->frag, s->back, s->stats,
+                                             s->xo, nullptr, st))
                     return rc;
                 prof_end(s, ev, 2, 4.0 * n_tok * K, st);
                 Act a{s->frag, s->back, n_tok, tc};
-                launches += 3;  // rowstats + fragwrite + gemv
+                launches += src.kind == SRC_STATS ? 3 : 2;  // (rowstats +) fragwrite + gemv
                 ev = prof_begin(s, st);
                 // algorithmic bytes: codes + per-feature scales + bias (+ f32 outlier rows)
                 const double bytes = (double)m.M * m.K + 4.0 * m.K + 4.0 * m.M + 4.0 * m.n_outl * m.M;
@@ -367,7 +389,10 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                 prof_end(s, ev, 0, bytes, st);
                 return rc;
             }
-            if (int rc = launch_prologue(mode, x, n_tok, K, K, g, be, m, tc, nullptr, s->back, s->stats, nullptr, s->y32, st))
+            e.pstats = nullptr;
+            e.tokmax = nullptr;
+            if (int rc = launch_prologue(mode, ProSrc{}, x, n_tok, K, K, g, be, m, tc, nullptr, s->back, s->stats,
+                                         nullptr, s->y32, st))
                 return rc;
             launches += mode == PRO_LN ? 3 : 1;  // (rowstats + rows) + gemm
             const int ev = prof_begin(s, st);
@@ -375,12 +400,25 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
             prof_end(s, ev, 3, 4.0 * m.M * m.K, st);
             return rc;
         };
+        // ---- LN1 -> QKV (+ paged KV append)
+        ProSrc src1;
+        if (j > 0) {
+            src1.kind = SRC_PARTIALS;
+            src1.pstats = s->pst_x;
+            src1.MG = MGd;
+            src1.M = d;
+            src1.gs = b.gs1;
+            src1.bs = b.bs1;
+        }
+        src1.zero_tokmax = s->tokmax_ctx;
         Epi e = base;
         e.kind = EPI_QKV;
         e.out = s->q;
-        if (int rc = matmul(0, PRO_LN, x_in, d, b.ln1_g, b.ln1_b, e)) return rc;
+        if (int rc = matmul(0, PRO_LN, src1, x_in, d, b.ln1_g, b.ln1_b, e)) return rc;
+        // ---- attention (+ operand range of wo)
         AttnArgs aa{s->q, kvb, s->d_tok_seq, s->d_tok_pos, s->d_pages, s->slopes, s->ctx, s->attn_part,
-                    s->counters + (1 << 19), n_tok, s->max_pages, s->H, s->dh, s->cfg.page_tokens, d, max_pos};
+                    s->counters + (1 << 19), int8 ? s->tokmax_ctx : nullptr, int8 ? b.mat[1].scales : nullptr,
+                    n_tok, s->max_pages, s->H, s->dh, s->cfg.page_tokens, d, max_pos};
         {
             const int ev = prof_begin(s, st);
             if (int rc = launch_attention(aa, s->attn_cap, st)) return rc;
@@ -390,20 +428,41 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
             prof_end(s, ev, 1, kv_bytes, st);
         }
         launches += 1;
+        // ---- wo + residual (+ LN2 summaries)
+        ProSrc src2;
+        src2.kind = SRC_TOKMAX;
+        src2.tokmax = s->tokmax_ctx;
         e = base;
         e.kind = EPI_RESID;
         e.resid = x_in;
         e.out = s->mid;
-        if (int rc = matmul(1, PRO_SCALE, s->ctx, d, nullptr, nullptr, e)) return rc;
+        e.pstats = s->pst_mid;
+        if (int rc = matmul(1, PRO_SCALE, src2, s->ctx, d, nullptr, nullptr, e)) return rc;
+        // ---- LN2 -> wmlp_in + GELU (+ operand range of wmlp_out)
+        ProSrc src3;
+        src3.kind = SRC_PARTIALS;
+        src3.pstats = s->pst_mid;
+        src3.MG = MGd;
+        src3.M = d;
+        src3.gs = b.gs2;
+        src3.bs = b.bs2;
+        src3.zero_tokmax = s->tokmax_act;
         e = base;
         e.kind = EPI_GELU;
         e.out = s->act;
-        if (int rc = matmul(2, PRO_LN, s->mid, d, b.ln2_g, b.ln2_b, e)) return rc;
+        e.tokmax = s->tokmax_act;
+        e.s_next = b.mat[3].scales;
+        if (int rc = matmul(2, PRO_LN, src3, s->mid, d, b.ln2_g, b.ln2_b, e)) return rc;
+        // ---- wmlp_out + residual (+ LN1 summaries of the next block)
+        ProSrc src4;
+        src4.kind = SRC_TOKMAX;
+        src4.tokmax = s->tokmax_act;
         e = base;
         e.kind = EPI_RESID;
         e.resid = s->mid;
         e.out = x_out;
-        if (int rc = matmul(3, PRO_SCALE, s->act, rd, nullptr, nullptr, e)) return rc;
+        e.pstats = (j + 1 < s->cfg.n_blocks) ? s->pst_x : nullptr;
+        if (int rc = matmul(3, PRO_SCALE, src4, s->act, rd, nullptr, nullptr, e)) return rc;
     }
     s->last_launches = launches;
     return PB_OK;

@@ -44,6 +44,8 @@ struct BlockW {
     float* ln2_g = nullptr;
     float* ln2_b = nullptr;
     float* bias[4] = {nullptr, nullptr, nullptr, nullptr};
+    // LN -> int8 operand range bounds (see ProSrc): max_k |gamma_k| s_k, max_k |beta_k| s_k
+    float gs1 = 0.f, bs1 = 0.f, gs2 = 0.f, bs2 = 0.f;
 };
 
 enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_GELU = 2 };
@@ -65,6 +67,10 @@ struct Epi {
     const int32_t* tok_pos;
     const int32_t* pages;    // [n_seq][max_pages]
     int max_pages, H, dh, P, d;
+    // row statistics for the NEXT matmul's operand, produced here (fused prologue):
+    float4* pstats;          // EPI_RESID -> LN consumer: [n_tok][M/128] {mean, M2, min, max} per 128-row group
+    float* tokmax;           // EPI_GELU -> scale consumer: atomicMax of |out * s_next| per token
+    const float* s_next;     // [M] scales of the consuming matrix
 };
 
 // B-operand (activation) layout parameters for one GEMV launch.
@@ -78,6 +84,17 @@ struct Act {
 // prologue modes
 enum ProMode { PRO_LN = 0, PRO_SCALE = 1 };
 
+// Where the operand producer (k_fragwrite) gets its per-token statistics.
+enum ProSrcKind { SRC_STATS = 0, SRC_PARTIALS = 1, SRC_TOKMAX = 2 };
+struct ProSrc {
+    int kind = SRC_STATS;        // SRC_STATS: run k_rowstats first (span input, f32 mode)
+    const float4* pstats = nullptr;  // SRC_PARTIALS: producer's per-128-row {mean, M2, min, max}
+    int MG = 0, M = 0;           //   groups and rows of that producer
+    float gs = 0.f, bs = 0.f;    //   shift bound: max|y s| <= gs * max|x - mu| * inv + bs
+    const float* tokmax = nullptr;   // SRC_TOKMAX: exact max |x s| per token (atomicMax'ed)
+    float* zero_tokmax = nullptr;    // reset for the next producer's atomicMax (may be null)
+};
+
 int fill_matrix_gen(Mat& m, uint64_t key, float threshold, float boost, int every, cudaStream_t st);
 int fill_matrix_f32(Mat& m, const float* w, float threshold, cudaStream_t st);
 int untile_codes(const Mat& m, int8_t* d_out, cudaStream_t st);
@@ -88,9 +105,12 @@ int dequantize_blockwise(const int8_t* codes, const float* scales, int64_t n, in
 
 // prologue: y = LN(x) (PRO_LN) or x (PRO_SCALE); writes hi/lo fragments of
 // y * scales, the per-token 2^-shift, outlier activations xo, and (f32 mode) y.
-int launch_prologue(int mode, const float* x, int n_tok, int K, int Kp, const float* gamma, const float* beta,
-                    const Mat& m, int tc, uint4* frag, float* back, float4* stats, float* xo, float* y32,
-                    cudaStream_t st);
+int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int K, int Kp, const float* gamma,
+                    const float* beta, const Mat& m, int tc, uint4* frag, float* back, float4* stats, float* xo,
+                    float* y32, cudaStream_t st);
+// (max_k |gamma_k| s_k, max_k |beta_k| s_k) -> host
+int bound_consts(const float* gamma, const float* beta, const float* scales, int K, float* gs, float* bs,
+                 cudaStream_t st);
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
                 int64_t partial_cap, cudaStream_t st);
 int launch_gemm_f32(const Mat& m, const float* y, int n_tok, const Epi& epi, cudaStream_t st);
@@ -107,6 +127,8 @@ struct AttnArgs {
     float* ctx;              // [n_tok][d]
     float* part;             // split workspace
     int* counters;           // [n_tok][H] last-CTA merge counters (zeroed, self-resetting)
+    float* tokmax;           // [n_tok] atomicMax of |ctx * s_next| (wo operand range), may be null
+    const float* s_next;     // [d] scales of wo
     int n_tok, max_pages, H, dh, P, d;
     int max_pos;             // max over tokens of (pos + 1)
 };

@@ -1,0 +1,93 @@
+"""Span-to-span hop schedule for one box: consecutive block spans pinned to
+consecutive GPUs (one process per GPU), the hidden state of every hop carried
+as the reference's int8 wire codec (codes + scales) over NCCL send/recv.
+
+This replaces the reference client's relay (client.py:312-331: the client
+receives each server's reply, decodes it, re-encodes it and sends it to the
+next hop). Because quantize(dequantize(quantize(x))) == quantize(x)
+(SURVEY §0.6), forwarding the codes directly is bit-identical to that relay.
+
+Ring schedule with S sessions in flight (S = number of spans keeps every GPU
+busy): job j is session j % S; span r receives job j from span r-1, runs it,
+and sends it to span r+1; the last span hands the result back to span 0 (the
+stand-in for the client's LM head + next-token embedding), which starts the
+session's next step. NCCL matches send/recv in issue order per peer pair, and
+every rank issues the same job order, so the schedule cannot deadlock.
+"""
+
+from __future__ import annotations
+
+
+class RingSchedule:
+    def __init__(self, rank: int, world: int, sessions: int, total_jobs: int):
+        self.rank, self.world, self.sessions, self.total_jobs = rank, world, sessions, total_jobs
+
+    def recv_from(self, j: int):
+        """Peer to receive job j's hidden from, or None (span 0 starting a session)."""
+        if self.world == 1:
+            return None
+        if self.rank > 0:
+            return self.rank - 1
+        return self.world - 1 if j >= self.sessions else None
+
+    def send_to(self, j: int):
+        """Peer to send job j's output to, or None (session finished / single span)."""
+        if self.world == 1:
+            return None
+        if self.rank < self.world - 1:
+            return self.rank + 1
+        return 0 if j + self.sessions < self.total_jobs else None
+
+
+def split_blocks(n_layers: int, n_spans: int):
+    """Contiguous, balanced spans: 70 blocks over 8 GPUs -> 9,9,9,9,9,9,8,8."""
+    base, extra = divmod(n_layers, n_spans)
+    out, s = [], 0
+    for r in range(n_spans):
+        k = base + (1 if r < extra else 0)
+        out.append((s, s + k))
+        s += k
+    return out
+
+
+def run_jobs(sched: RingSchedule, jobs, step, exchange, inbox):
+    """Run `jobs` (increasing job ids) on this span.
+
+    step(j, payload | None) -> outbox (payload sent downstream);
+    exchange(ops) runs [(op, buffer, peer)] with op in {"send", "recv"} as ONE
+    group (NCCL group / batch_isend_irecv) so the send of job j and the receive
+    of job j+1 progress together. With S = world sessions every group lies on
+    an anti-diagonal (rank + job = const) of the pipeline, which is what keeps
+    the ring deadlock-free even when sends do not complete eagerly.
+    inbox: receive buffer, or a callable job -> buffer (sized per job); it is
+    reused: the group only starts after the step that read it, by stream order."""
+    if not jobs:
+        return
+    box = inbox if callable(inbox) else (lambda j: inbox)
+    src = sched.recv_from(jobs[0])
+    if src is not None:
+        exchange([("recv", box(jobs[0]), src)])
+    have_input = src is not None
+    for i, j in enumerate(jobs):
+        out = step(j, box(j) if have_input else None)
+        ops = []
+        dst = sched.send_to(j)
+        if dst is not None:
+            ops.append(("send", out, dst))
+        have_input = False
+        if i + 1 < len(jobs):
+            nsrc = sched.recv_from(jobs[i + 1])
+            if nsrc is not None:
+                ops.append(("recv", box(jobs[i + 1]), nsrc))
+                have_input = True
+        if ops:
+            exchange(ops)
+
+
+def torch_exchange(ops):
+    """exchange() over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+    import torch.distributed as dist
+
+    p2p = [dist.P2POp(dist.isend if op == "send" else dist.irecv, buf, peer) for op, buf, peer in ops]
+    for w in dist.batch_isend_irecv(p2p):
+        w.wait()
