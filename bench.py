@@ -186,7 +186,9 @@ class Pipeline:
         torch.cuda.set_device(self.local)
         self.dev = torch.device("cuda", self.local)
         if self.world > 1:
-            dist.init_process_group("nccl", device_id=self.dev)
+            import datetime
+
+            dist.init_process_group("nccl", device_id=self.dev, timeout=datetime.timedelta(seconds=180))
         self.dist = dist if self.world > 1 else None
         self.S = self.world  # sessions in flight
         self.ranges = split_blocks(cfg.n_layers, self.world)
