@@ -22,6 +22,7 @@
 //   words {kt0: B[2q..2q+1][g], B[2q+8..2q+9][g]; kt1: same +16}, column = 8 nt + g.
 #include "pb_async.cuh"
 #include "pb_common.cuh"
+#include "pb_epi.cuh"
 #include "pb_span.h"
 
 namespace pb {
@@ -305,6 +306,60 @@ __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
     a.frag[(base + nt_lo) * 32 + 4 * g_lo + q] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
 }
 
+// Same operand, written for the tcgen05 GEMM (pb_gemm_tc.cu): UMMA canonical
+// K-major no-swizzle layout, per (128-token tile, 32-wide k tile) a 16 KB block
+// of 256 columns (hi of the 128 tokens, then lo); column c, k: byte
+// (c/8)*512 + (k/8)*128 + (c%8)*16 + (k%8)*2. One thread per (token, k tile,
+// 8-wide chunk) -> two 16-byte stores. Padding tokens are written as zeros.
+__global__ void __launch_bounds__(256) k_canonwrite(ProArgs a, uint8_t* __restrict__ bcanon, int n_tok) {
+    __shared__ float4 s_st;
+    const int tok = blockIdx.y;
+    const float* x = a.x + (int64_t)tok * a.K;
+    const bool real = tok < n_tok;
+    if (real && threadIdx.x < 32) {
+        const float4 r = resolve_stats(a, tok);
+        if (threadIdx.x == 0) {
+            s_st = r;
+            if (blockIdx.x == 0) {
+                a.back[tok] = r.w;
+                if (a.src.zero_tokmax) a.src.zero_tokmax[tok] = 0.f;
+            }
+        }
+    }
+    __syncthreads();
+    const int KC = a.Kp / 32;
+    const int it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (real && blockIdx.x == 0 && a.xo) {
+        for (int j = threadIdx.x; j < a.n_outl; j += blockDim.x)
+            a.xo[(int64_t)tok * a.n_outl + j] = pro_y(a, x, a.outl_idx[j], s_st.x, s_st.y);
+    }
+    if (it >= KC * 4) return;
+    const int kc = it >> 2, ch = it & 3;
+    uint32_t hw[4] = {0u, 0u, 0u, 0u}, lw[4] = {0u, 0u, 0u, 0u};
+    if (real) {
+        const float4 st = s_st;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            float v[2];
+#pragma unroll
+            for (int e2 = 0; e2 < 2; ++e2) {
+                const int k = kc * 32 + ch * 8 + 2 * p + e2;
+                v[e2] = k < a.K ? (pro_y(a, x, k, st.x, st.y) * a.scales[k]) * st.z : 0.f;
+            }
+            const half h0 = __float2half_rn(v[0]), h1 = __float2half_rn(v[1]);
+            const half l0 = __float2half_rn(v[0] - __half2float(h0));
+            const half l1 = __float2half_rn(v[1] - __half2float(h1));
+            hw[p] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+            lw[p] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+        }
+    }
+    const int nt = tok >> 7, c = tok & 127;
+    uint8_t* blk = bcanon + ((int64_t)nt * KC + kc) * 16384 + ch * 128;
+    *reinterpret_cast<uint4*>(blk + (c >> 3) * 512 + (c & 7) * 16) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    const int cl = c + 128;
+    *reinterpret_cast<uint4*>(blk + (cl >> 3) * 512 + (cl & 7) * 16) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+}
+
 // f32-weights mode: plain y = LN(x) (or x) rows for the CUDA-core GEMM
 __global__ void __launch_bounds__(256) k_rows_f32(ProArgs a) {
     const int tok = blockIdx.y;
@@ -316,7 +371,7 @@ __global__ void __launch_bounds__(256) k_rows_f32(ProArgs a) {
 
 int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int K, int Kp, const float* gamma,
                     const float* beta, const Mat& m, int tc, uint4* frag, float* back, float4* stats, float* xo,
-                    float* y32, cudaStream_t st) {
+                    float* y32, cudaStream_t st, uint8_t* bcanon) {
     ProArgs a{mode, x, K, Kp, gamma, beta, y32 ? nullptr : m.scales, m.n_outl, m.outl_idx, tc, frag, back, stats,
               xo, y32, src};
     if (y32) a.src = ProSrc{};
@@ -333,43 +388,16 @@ int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int 
         return launch_check("rows_f32");
     }
     const int items = (Kp / 32) * 4;
+    if (bcanon) {
+        k_canonwrite<<<dim3((unsigned)ceil_div(items, 256), (unsigned)round_up(n_tok, 128)), 256, 0, st>>>(a, bcanon,
+                                                                                                      n_tok);
+        return launch_check("canonwrite");
+    }
     k_fragwrite<<<dim3((unsigned)ceil_div(items, 256), n_tok), 256, 0, st>>>(a);
     return launch_check("fragwrite");
 }
 
 // ------------------------------------------------------------------ epilogue
-
-__device__ __forceinline__ float gelu_tanh(float x) {  // model.py:286-292 (f32)
-    const float c = 0.7978845608028654f;
-    const float u = c * (x + 0.044715f * x * x * x);
-    return 0.5f * x * (1.f + tanhf(u));
-}
-
-__device__ __forceinline__ float epi_store(const Epi& e, int tok, int o, float v) {
-    v += e.bias[o];
-    for (int j = 0; j < e.n_outl; ++j) v = fmaf(e.outl_rows[(int64_t)j * e.M + o], e.xo[(int64_t)tok * e.n_outl + j], v);
-    const int64_t idx = (int64_t)tok * e.M + o;
-    if (e.kind == EPI_RESID) {
-        v = e.resid[idx] + v;
-        e.out[idx] = v;
-    } else if (e.kind == EPI_GELU) {
-        v = gelu_tanh(v);
-        e.out[idx] = v;
-    } else {  // EPI_QKV: contiguous q | k | v column thirds (model.py:342-344)
-        if (o < e.d) {
-            e.out[(int64_t)tok * e.d + o] = v;
-        } else {
-            const int part = o < 2 * e.d ? 0 : 1;
-            const int oo = o - e.d * (1 + part);
-            const int h = oo / e.dh, dd = oo - h * e.dh;
-            const int seq = e.tok_seq[tok], pos = e.tok_pos[tok];
-            const int page = e.pages[(int64_t)seq * e.max_pages + pos / e.P];
-            const int slot = pos % e.P;
-            e.kv[((((int64_t)page * 2 + part) * e.H + h) * e.P + slot) * e.dh + dd] = __float2half_rn(v);
-        }
-    }
-    return v;
-}
 
 // ------------------------------------------------------------------ int8 mma GEMV
 

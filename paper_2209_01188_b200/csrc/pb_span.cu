@@ -4,6 +4,7 @@
 // batched over sessions.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -31,6 +32,8 @@ struct pb_span {
     // workspaces
     float *xa = nullptr, *mid = nullptr, *q = nullptr, *ctx = nullptr, *act = nullptr, *xo = nullptr, *y32 = nullptr;
     uint4* frag = nullptr;
+    uint8_t* bcanon = nullptr;  // tcgen05 B operand [ceil(NT/128)][KC][16 KB]
+    int tc_min = TC_MIN_TOKENS_DEFAULT;
     float* back = nullptr;
     float4* stats = nullptr;
     float4 *pst_x = nullptr, *pst_mid = nullptr;  // per-128-row LN summaries [NT][d/128]
@@ -99,7 +102,7 @@ void free_span(pb_span* s) {
         cudaFree(b.ln2_b);
         for (auto* p : b.bias) cudaFree(p);
     }
-    void* ptrs[] = {s->kv, s->slopes, s->xa, s->mid, s->q, s->ctx, s->act, s->xo, s->y32, s->frag, s->back, s->stats, s->pst_x, s->pst_mid, s->tokmax_ctx, s->tokmax_act,
+    void* ptrs[] = {s->kv, s->slopes, s->xa, s->mid, s->q, s->ctx, s->act, s->xo, s->y32, s->frag, s->bcanon, s->back, s->stats, s->pst_x, s->pst_mid, s->tokmax_ctx, s->tokmax_act,
                     s->partials, s->counters, s->attn_part, s->d_tok_seq, s->d_tok_pos, s->d_pages,
                     s->hop_codes, s->hop_scales};
     for (void* p : ptrs) cudaFree(p);
@@ -171,6 +174,8 @@ int pb_span_create(const pb_span_config* cfg, pb_span** out) {
     if (!rc && !int8) rc = dalloc(s, &s->y32, (int64_t)NT * rd);
     const int64_t kp_max = round_up(rd, 32);
     if (!rc && int8) rc = dalloc(s, &s->frag, (int64_t)(NT + 31) * kp_max * 4 / 16 + 64);
+    if (const char* e = getenv("PB_TC_MIN")) s->tc_min = atoi(e);
+    if (!rc && int8 && NT >= s->tc_min) rc = dalloc(s, &s->bcanon, ceil_div(NT, 128) * (kp_max / 32) * 16384);
     if (!rc) rc = dalloc(s, &s->back, NT);
     if (!rc) rc = dalloc(s, &s->stats, NT);
     if (!rc) rc = dalloc(s, &s->pst_x, (int64_t)NT * ceil_div(d, 128));
@@ -347,6 +352,7 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
     const int d = s->d, rd = s->rd;
     const bool int8 = s->cfg.weights == PB_WEIGHTS_INT8;
     const int tc = choose_tc(n_tok);
+    const bool use_tc = int8 && s->bcanon && n_tok >= s->tc_min;
     const int MGd = (int)ceil_div(d, 128);
     int launches = 0;
     for (int j = 0; j < s->cfg.n_blocks; ++j) {
@@ -370,6 +376,32 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
             const Mat& m = b.mat[mi];
             e.M = m.M;
             e.bias = b.bias[mi];
+            if (use_tc) {
+                // prefill / large batches: tcgen05 GEMM. LN operands take exact
+                // row statistics (k_rowstats); scale operands keep the atomicMax range.
+                e.n_outl = m.n_outl;
+                e.outl_idx = m.outl_idx;
+                e.outl_rows = m.outl_rows;
+                e.xo = s->xo;
+                e.pstats = nullptr;
+                ProSrc srct = src;
+                if (mode == PRO_LN) {
+                    srct.kind = SRC_STATS;
+                    srct.pstats = nullptr;
+                }
+                int ev = prof_begin(s, st);
+                if (int rc = launch_prologue(mode, srct, x, n_tok, K, m.Kp, g, be, m, tc, nullptr, s->back, s->stats,
+                                             s->xo, nullptr, st, s->bcanon))
+                    return rc;
+                prof_end(s, ev, 2, 4.0 * n_tok * K, st);
+                launches += srct.kind == SRC_STATS ? 3 : 2;
+                Act a{nullptr, s->back, n_tok, 0};
+                ev = prof_begin(s, st);
+                int rc = launch_gemm_tc(m, s->bcanon, a, e, st);
+                // tensor roofline: 2 * M * K * (2 columns per token: hi + lo) flops
+                prof_end(s, ev, 5, 2.0 * m.M * m.K * 2.0 * n_tok, st);
+                return rc;
+            }
             if (int8) {
                 e.n_outl = m.n_outl;
                 e.outl_idx = m.outl_idx;

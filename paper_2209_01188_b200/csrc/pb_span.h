@@ -107,7 +107,10 @@ int dequantize_blockwise(const int8_t* codes, const float* scales, int64_t n, in
 // y * scales, the per-token 2^-shift, outlier activations xo, and (f32 mode) y.
 int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int K, int Kp, const float* gamma,
                     const float* beta, const Mat& m, int tc, uint4* frag, float* back, float4* stats, float* xo,
-                    float* y32, cudaStream_t st);
+                    float* y32, cudaStream_t st, uint8_t* bcanon = nullptr);
+// tcgen05 GEMM over a canonical-layout B operand (pb_gemm_tc.cu)
+int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Epi& epi, cudaStream_t st);
+constexpr int TC_MIN_TOKENS_DEFAULT = 64;
 // (max_k |gamma_k| s_k, max_k |beta_k| s_k) -> host
 int bound_consts(const float* gamma, const float* beta, const float* scales, int K, float* gs, float* bs,
                  cudaStream_t st);

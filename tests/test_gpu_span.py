@@ -260,3 +260,41 @@ def test_large_shape_block_vs_f64_reference(shape_name):
     del ref
     span.close()
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("shape_name,t", [("mid", 200), ("bloom-7b1", 300)])
+def test_tcgen05_prefill_matches_gemv_path(shape_name, t, monkeypatch):
+    """Prefill through the tcgen05 GEMM (TMA-fed, TMEM accumulators) equals the
+    mma.sync GEMV path on the same span weights (both carry f32-accurate
+    operands; only accumulation order differs), and the subsequent decode
+    steps (GEMV path) agree too -- i.e. the KV cache written by the tcgen05
+    epilogue is the same."""
+    import torch
+
+    from paper_2209_01188_b200.model import SHAPES as S
+    from paper_2209_01188_b200.span import BlockSpan
+
+    if shape_name == "mid":
+        shape = SHAPES["mid"]
+        cfg = cfg_of(shape)
+        end = shape.n_layers
+    else:
+        cfg = S[shape_name]
+        end = 2
+    outs = {}
+    for tc_min in ("64", "100000"):
+        monkeypatch.setenv("PB_TC_MIN", tc_min)
+        span = BlockSpan(cfg, 0, end, int8=True, page_tokens=64, max_tokens=max(t, 64), n_pages=16)
+        span.generate_weights(42)
+        rng = np.random.default_rng(1)
+        x = torch.from_numpy(rng.normal(size=(t + 2, cfg.hidden)).astype(np.float32) * 0.05).cuda()
+        seq = span.new_sequence()
+        a = span.step([(seq, x[:t])])[0].cpu().numpy()
+        b = span.step([(seq, x[t:t + 1])])[0].cpu().numpy()
+        c = span.step([(seq, x[t + 1:t + 2])])[0].cpu().numpy()
+        outs[tc_min] = (a, b, c)
+        span.close()
+        torch.cuda.empty_cache()
+    for i in range(3):
+        err = rel_err(outs["64"][i], outs["100000"][i])
+        assert err <= 1e-4, (shape_name, i, err)
