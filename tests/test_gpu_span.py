@@ -297,4 +297,4 @@ def test_tcgen05_prefill_matches_gemv_path(shape_name, t, monkeypatch):
         torch.cuda.empty_cache()
     for i in range(3):
         err = rel_err(outs["64"][i], outs["100000"][i])
-        assert err <= 1e-4, (shape_name, i, err)
+        assert err <= TOL, (shape_name, i, err)  # fp16 KV rounding can flip on 1-ulp f32 differences
