@@ -21,7 +21,8 @@
 
 namespace pb {
 
-constexpr int ATT_KCH = 128;  // keys per CTA
+constexpr int ATT_SK = 64;    // keys per pipeline stage (one 64-token KV page)
+constexpr int ATT_ST = 2;     // stages in flight (TMA ring)
 constexpr int ATT_WARPS = 4;
 
 template <int DH>
@@ -61,54 +62,60 @@ __device__ __forceinline__ void load_h(const half* p, float* out) {
 
 template <int DH>
 constexpr size_t attn_smem() {
-    return (size_t)2 * ATT_KCH * DH * 2 + ATT_KCH * 4 + ATT_WARPS * DH * 4 + 64;
+    return (size_t)ATT_ST * 2 * ATT_SK * DH * 2 + ATT_SK * 4 + ATT_WARPS * DH * 4 + 64 + 64;
+}
+
+// stage i of this CTA's key range: keys [j0 + i*SK, min(j1, j0 + (i+1)*SK)), K and V
+// rows copied page piece by page piece into buffer i % ST
+template <int DH>
+__device__ __forceinline__ void attn_issue(const AttnArgs& a, const int32_t* pt, int64_t head_off, int64_t kv_stride,
+                                           int j0, int j1, int i, half* Ks, half* Vs, uint64_t* full) {
+    const int k0 = j0 + i * ATT_SK;
+    if (k0 >= j1) return;
+    const int k1 = min(j1, k0 + ATT_SK);
+    const int b = i % ATT_ST;
+    uint64_t* bar = &full[b];
+    mbar_expect_tx(bar, (uint32_t)(k1 - k0) * DH * 2 * 2);
+    for (int j = k0; j < k1;) {
+        const int page = pt[j / a.P];
+        const int jn = min(k1, (j / a.P + 1) * a.P);
+        const half* kp = a.kv + (int64_t)page * 2 * kv_stride + head_off + (int64_t)(j % a.P) * DH;
+        const uint32_t bytes = (uint32_t)(jn - j) * DH * 2;
+        bulk_g2s(Ks + ((int64_t)b * ATT_SK + (j - k0)) * DH, kp, bytes, bar);
+        bulk_g2s(Vs + ((int64_t)b * ATT_SK + (j - k0)) * DH, kp + kv_stride, bytes, bar);
+        j = jn;
+    }
 }
 
 template <int DH>
-__global__ void __launch_bounds__(ATT_WARPS * 32) k_attn(AttnArgs a, int nsplit) {
+__global__ void __launch_bounds__(ATT_WARPS * 32) k_attn(AttnArgs a, int nsplit, int kps) {
     using C = AttnCfg<DH>;
     extern __shared__ __align__(128) uint8_t smem[];
-    half* Ks = reinterpret_cast<half*>(smem);                     // [KCH][DH]
-    half* Vs = Ks + ATT_KCH * DH;                                 // [KCH][DH]
-    float* sc = reinterpret_cast<float*>(Vs + ATT_KCH * DH);      // [KCH]
-    float* osum = sc + ATT_KCH;                                   // [WARPS][DH]
-    float* red = osum + ATT_WARPS * DH;                           // [WARPS]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(red + 8);
-    int* s_flag = reinterpret_cast<int*>(bar + 1);
+    half* Ks = reinterpret_cast<half*>(smem);                       // [ST][SK][DH]
+    half* Vs = Ks + ATT_ST * ATT_SK * DH;                           // [ST][SK][DH]
+    float* sc = reinterpret_cast<float*>(Vs + ATT_ST * ATT_SK * DH);  // [SK]
+    float* osum = sc + ATT_SK;                                      // [WARPS][DH]
+    float* red = osum + ATT_WARPS * DH;                             // [WARPS]
+    uint64_t* full = reinterpret_cast<uint64_t*>(red + 8);          // [ST]
+    int* s_flag = reinterpret_cast<int*>(full + ATT_ST);
 
     const int h = blockIdx.x, tok = blockIdx.y, split = blockIdx.z;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int pos = a.tok_pos[tok], seq = a.tok_seq[tok];
-    const int j0 = split * ATT_KCH;
-    const int j1 = min(j0 + ATT_KCH, pos + 1);
+    const int j0 = split * kps;
+    const int j1 = min(j0 + kps, pos + 1);
     float* out = a.part + (((int64_t)tok * a.H + h) * nsplit + split) * (DH + 2);
     const int32_t* pt = a.pages + (int64_t)seq * a.max_pages;
     const int64_t head_off = (int64_t)h * a.P * DH;
     const int64_t kv_stride = (int64_t)a.H * a.P * DH;  // K -> V within a page
 
     if (j0 < j1) {
-        // ---- stage the chunk's K and V rows in shared memory
+        const int nst = (j1 - j0 + ATT_SK - 1) / ATT_SK;
         if constexpr (C::BULK) {
             if (threadIdx.x == 0) {
-                mbar_init(bar, 1);
+                for (int b = 0; b < ATT_ST; ++b) mbar_init(&full[b], 1);
                 mbar_fence_init();
-                mbar_expect_tx(bar, (uint32_t)(j1 - j0) * DH * 2 * 2);
-                for (int j = j0; j < j1;) {
-                    const int page = pt[j / a.P];
-                    const int jn = min(j1, (j / a.P + 1) * a.P);
-                    const half* kp = a.kv + (int64_t)page * 2 * kv_stride + head_off + (int64_t)(j % a.P) * DH;
-                    const uint32_t bytes = (uint32_t)(jn - j) * DH * 2;
-                    bulk_g2s(Ks + (j - j0) * DH, kp, bytes, bar);
-                    bulk_g2s(Vs + (j - j0) * DH, kp + kv_stride, bytes, bar);
-                    j = jn;
-                }
-            }
-        } else {
-            for (int i = threadIdx.x; i < (j1 - j0) * DH; i += blockDim.x) {
-                const int j = j0 + i / DH, dd = i % DH;
-                const half* kp = a.kv + (int64_t)pt[j / a.P] * 2 * kv_stride + head_off + (int64_t)(j % a.P) * DH + dd;
-                Ks[i] = kp[0];
-                Vs[i] = kp[kv_stride];
+                for (int i = 0; i < ATT_ST && i < nst; ++i) attn_issue<DH>(a, pt, head_off, kv_stride, j0, j1, i, Ks, Vs, full);
             }
         }
         const int sub = lane % C::LPK, slot = lane / C::LPK;
@@ -118,82 +125,95 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) k_attn(AttnArgs a, int nsplit)
         for (int i = 0; i < C::DPL; ++i) qv[i] = a.q[(int64_t)tok * a.d + h * DH + d0 + i];
         const float sq = (float)sqrt((double)DH);
         const float slope = a.slopes[h];
-        __syncthreads();
-        if constexpr (C::BULK) mbar_wait(bar, 0);
-
-        // ---- scores
-        for (int base = j0 + warp * C::KPW; base < j1; base += ATT_WARPS * C::KPW) {
-            const int j = base + slot;
-            float dot = 0.f;
-            if (j < j1) {
-                float kf[C::DPL];
-                load_h<C::DPL>(Ks + (j - j0) * DH + d0, kf);
-#pragma unroll
-                for (int i = 0; i < C::DPL; ++i) dot = fmaf(qv[i], kf[i], dot);
-            }
-#pragma unroll
-            for (int o = C::LPK / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-            if (j < j1 && sub == 0) sc[j - j0] = __fadd_rn(__fdiv_rn(dot, sq), __fmul_rn(slope, (float)(j - pos)));
-        }
-        __syncthreads();
-        const int nk = j1 - j0;
-        float m = -INFINITY;
-        for (int i = threadIdx.x; i < nk; i += blockDim.x) m = fmaxf(m, sc[i]);
-        m = warp_max(m);
-        if (lane == 0) red[warp] = m;
-        __syncthreads();
-        m = red[0];
-#pragma unroll
-        for (int w = 1; w < ATT_WARPS; ++w) m = fmaxf(m, red[w]);
-        __syncthreads();
-        float l = 0.f;
-        for (int i = threadIdx.x; i < nk; i += blockDim.x) {
-            const float p = expf(__fsub_rn(sc[i], m));
-            sc[i] = p;
-            l += p;
-        }
-        l = warp_sum(l);
-        if (lane == 0) red[warp] = l;
-        __syncthreads();
-        l = 0.f;
-#pragma unroll
-        for (int w = 0; w < ATT_WARPS; ++w) l += red[w];
-
-        // ---- P V
+        float m_run = -INFINITY, l_run = 0.f;
         float ov[C::DPL];
 #pragma unroll
         for (int i = 0; i < C::DPL; ++i) ov[i] = 0.f;
-        for (int base = j0 + warp * C::KPW; base < j1; base += ATT_WARPS * C::KPW) {
-            const int j = base + slot;
-            if (j < j1) {
-                float vf[C::DPL];
-                load_h<C::DPL>(Vs + (j - j0) * DH + d0, vf);
-                const float p = sc[j - j0];
+        __syncthreads();
+        for (int i = 0; i < nst; ++i) {
+            const int b = i % ATT_ST;
+            const int k0 = j0 + i * ATT_SK, nk = min(ATT_SK, j1 - k0);
+            const half* Kb = Ks + (int64_t)b * ATT_SK * DH;
+            const half* Vb = Vs + (int64_t)b * ATT_SK * DH;
+            if constexpr (C::BULK) {
+                mbar_wait(&full[b], (i / ATT_ST) & 1);
+            } else {
+                half* Kw = Ks + (int64_t)b * ATT_SK * DH;
+                half* Vw = Vs + (int64_t)b * ATT_SK * DH;
+                for (int e = threadIdx.x; e < nk * DH; e += blockDim.x) {
+                    const int j = k0 + e / DH, dd = e % DH;
+                    const half* kp = a.kv + (int64_t)pt[j / a.P] * 2 * kv_stride + head_off + (int64_t)(j % a.P) * DH + dd;
+                    Kw[e] = kp[0];
+                    Vw[e] = kp[kv_stride];
+                }
+                __syncthreads();
+            }
+            // scores of this stage
+            for (int base = warp * C::KPW; base < nk; base += ATT_WARPS * C::KPW) {
+                const int jj = base + slot;
+                float dot = 0.f;
+                if (jj < nk) {
+                    float kf[C::DPL];
+                    load_h<C::DPL>(Kb + jj * DH + d0, kf);
 #pragma unroll
-                for (int i = 0; i < C::DPL; ++i) ov[i] = fmaf(p, vf[i], ov[i]);
+                    for (int e = 0; e < C::DPL; ++e) dot = fmaf(qv[e], kf[e], dot);
+                }
+#pragma unroll
+                for (int o = C::LPK / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+                if (jj < nk && sub == 0)
+                    sc[jj] = __fadd_rn(__fdiv_rn(dot, sq), __fmul_rn(slope, (float)(k0 + jj - pos)));
+            }
+            __syncthreads();
+            // online softmax: every warp reduces the stage redundantly (no extra barrier)
+            float smax = -INFINITY;
+            for (int jj = lane; jj < nk; jj += 32) smax = fmaxf(smax, sc[jj]);
+            smax = warp_max(smax);
+            const float m_new = fmaxf(m_run, smax);
+            const float alpha = m_run == -INFINITY ? 0.f : expf(__fsub_rn(m_run, m_new));
+            float ls = 0.f;
+            for (int jj = lane; jj < nk; jj += 32) ls += expf(__fsub_rn(sc[jj], m_new));
+            ls = warp_sum(ls);
+            l_run = l_run * alpha + ls;
+            m_run = m_new;
+#pragma unroll
+            for (int e = 0; e < C::DPL; ++e) ov[e] *= alpha;
+            for (int base = warp * C::KPW; base < nk; base += ATT_WARPS * C::KPW) {
+                const int jj = base + slot;
+                if (jj < nk) {
+                    float vf[C::DPL];
+                    load_h<C::DPL>(Vb + jj * DH + d0, vf);
+                    const float p = expf(__fsub_rn(sc[jj], m_new));
+#pragma unroll
+                    for (int e = 0; e < C::DPL; ++e) ov[e] = fmaf(p, vf[e], ov[e]);
+                }
+            }
+            __syncthreads();  // buffer b and sc free
+            if constexpr (C::BULK) {
+                if (threadIdx.x == 0 && i + ATT_ST < nst)
+                    attn_issue<DH>(a, pt, head_off, kv_stride, j0, j1, i + ATT_ST, Ks, Vs, full);
             }
         }
 #pragma unroll
-        for (int i = 0; i < C::DPL; ++i) {
+        for (int e = 0; e < C::DPL; ++e) {
 #pragma unroll
-            for (int o = 16; o >= C::LPK; o >>= 1) ov[i] += __shfl_xor_sync(0xffffffffu, ov[i], o);
+            for (int o = 16; o >= C::LPK; o >>= 1) ov[e] += __shfl_xor_sync(0xffffffffu, ov[e], o);
         }
         if (slot == 0) {
 #pragma unroll
-            for (int i = 0; i < C::DPL; ++i) osum[warp * DH + d0 + i] = ov[i];
+            for (int e = 0; e < C::DPL; ++e) osum[warp * DH + d0 + e] = ov[e];
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < DH; i += blockDim.x) {
+        for (int e = threadIdx.x; e < DH; e += blockDim.x) {
             float s = 0.f;
 #pragma unroll
-            for (int w = 0; w < ATT_WARPS; ++w) s += osum[w * DH + i];
-            out[2 + i] = s;
+            for (int w = 0; w < ATT_WARPS; ++w) s += osum[w * DH + e];
+            out[2 + e] = s;
         }
         if (threadIdx.x == 0) {
-            out[0] = m;
-            out[1] = l;
+            out[0] = m_run;
+            out[1] = l_run;
         }
-    } else if (threadIdx.x == 0) {  // chunk entirely in the causal future
+    } else if (threadIdx.x == 0) {  // range entirely in the causal future
         out[0] = -INFINITY;
         out[1] = 0.f;
     }
@@ -243,13 +263,23 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) k_attn(AttnArgs a, int nsplit)
     }
 }
 
+constexpr int ATT_MAX_SPLIT = 16;
+
 int64_t attention_part_floats(int n_tok, int H, int dh, int max_seq) {
-    return (int64_t)n_tok * H * ceil_div(max_seq, ATT_KCH) * (dh + 2);
+    return (int64_t)n_tok * H * ATT_MAX_SPLIT * (dh + 2);
 }
 
 template <int DH>
 static int run_attn(const AttnArgs& a, int64_t cap, cudaStream_t st) {
-    const int nsplit = (int)ceil_div(a.max_pos, ATT_KCH);
+    // split the key range only as far as needed to cover the machine (~2 CTAs
+    // per SM); each split streams >= 4 stages
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int nsplit = (int)ceil_div(2 * sms, (int64_t)a.n_tok * a.H);
+    nsplit = std::max(1, std::min<int>(nsplit, std::min<int>(ATT_MAX_SPLIT, (int)ceil_div(a.max_pos, 4 * ATT_SK))));
+    const int kps = (int)round_up(ceil_div(a.max_pos, nsplit), ATT_SK);
+    nsplit = (int)ceil_div(a.max_pos, kps);
     if ((int64_t)a.n_tok * a.H * nsplit * (DH + 2) > cap) {
         set_error("attention workspace too small");
         return PB_ERR_CAPACITY;
@@ -260,7 +290,7 @@ static int run_attn(const AttnArgs& a, int64_t cap, cudaStream_t st) {
         cudaFuncSetAttribute(k_attn<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    k_attn<DH><<<dim3(a.H, a.n_tok, nsplit), ATT_WARPS * 32, smem, st>>>(a, nsplit);
+    k_attn<DH><<<dim3(a.H, a.n_tok, nsplit), ATT_WARPS * 32, smem, st>>>(a, nsplit, kps);
     return launch_check("attention");
 }
 

@@ -199,26 +199,33 @@ __device__ float4 resolve_stats(const ProArgs& a, int tok) {
         return make_float4(0.f, 1.f, ldexpf(1.f, sh), ldexpf(1.f, -sh));
     }
     if (a.src.kind == SRC_STATS) return a.stats[tok];
-    RowSum r{0.0, 0.0, 0.0, INFINITY, -INFINITY};
+    // parallel two-pass combination of the 128-row group summaries:
+    // mean = sum n_g mean_g / N ; M2 = sum M2_g + n_g (mean_g - mean)^2 (f64;
+    // butterfly sums are commutative, so every lane gets the same bits)
+    const float4* ps = a.src.pstats + (int64_t)tok * a.src.MG;
+    double s1 = 0.0;
+    float mn = INFINITY, mx = -INFINITY;
     for (int g = lane; g < a.src.MG; g += 32) {
-        const float4 p = a.src.pstats[(int64_t)tok * a.src.MG + g];
-        const int n = min(128, a.src.M - g * 128);
-        r = rs_merge(r, RowSum{(double)n, (double)p.x, (double)p.y, p.z, p.w});
+        const float4 p = ps[g];
+        s1 += (double)min(128, a.src.M - g * 128) * (double)p.x;
+        mn = fminf(mn, p.z);
+        mx = fmaxf(mx, p.w);
     }
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        RowSum o;
-        o.n = __shfl_xor_sync(0xffffffffu, r.n, off);
-        o.mean = __shfl_xor_sync(0xffffffffu, r.mean, off);
-        o.m2 = __shfl_xor_sync(0xffffffffu, r.m2, off);
-        o.mn = __shfl_xor_sync(0xffffffffu, r.mn, off);
-        o.mx = __shfl_xor_sync(0xffffffffu, r.mx, off);
-        r = (lane & off) ? rs_merge(o, r) : rs_merge(r, o);  // lower lane first: identical on both sides
+    s1 = warp_sum_d(s1);
+    mn = -warp_max(-mn);
+    mx = warp_max(mx);
+    const double mean = s1 / a.src.M;
+    double s2 = 0.0;
+    for (int g = lane; g < a.src.MG; g += 32) {
+        const float4 p = ps[g];
+        const double dm = (double)p.x - mean;
+        s2 += (double)p.y + (double)min(128, a.src.M - g * 128) * dm * dm;
     }
-    const float mu = (float)r.mean;
-    const float var = (float)(r.m2 / a.src.M);
+    s2 = warp_sum_d(s2);
+    const float mu = (float)mean;
+    const float var = (float)(s2 / a.src.M);
     const float inv = 1.0f / sqrtf(var + 1e-5f);
-    const float dev = fmaxf(r.mx - mu, mu - r.mn);
+    const float dev = fmaxf(mx - mu, mu - mn);
     const int sh = shift_for(a.src.gs * dev * inv + a.src.bs);
     return make_float4(mu, inv, ldexpf(1.f, sh), ldexpf(1.f, -sh));
 }
