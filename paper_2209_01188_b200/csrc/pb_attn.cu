@@ -276,8 +276,13 @@ static int run_attn(const AttnArgs& a, int64_t cap, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int nsplit = (int)ceil_div(2 * sms, (int64_t)a.n_tok * a.H);
-    nsplit = std::max(1, std::min<int>(nsplit, std::min<int>(ATT_MAX_SPLIT, (int)ceil_div(a.max_pos, 4 * ATT_SK))));
+    static int ctas_per_sm = 0;
+    if (!ctas_per_sm) {
+        const char* e = getenv("PB_ATT_CTAS_PER_SM");  // tuning knob
+        ctas_per_sm = e ? atoi(e) : 2;
+    }
+    int nsplit = (int)ceil_div((int64_t)ctas_per_sm * sms, (int64_t)a.n_tok * a.H);
+    nsplit = std::max(1, std::min<int>(nsplit, std::min<int>(ATT_MAX_SPLIT, (int)ceil_div(a.max_pos, 2 * ATT_SK))));
     const int kps = (int)round_up(ceil_div(a.max_pos, nsplit), ATT_SK);
     nsplit = (int)ceil_div(a.max_pos, kps);
     if ((int64_t)a.n_tok * a.H * nsplit * (DH + 2) > cap) {
