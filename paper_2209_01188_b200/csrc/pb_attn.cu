@@ -21,8 +21,8 @@
 
 namespace pb {
 
-constexpr int ATT_SK = 64;    // keys per pipeline stage (one 64-token KV page)
-constexpr int ATT_ST = 2;     // stages in flight (TMA ring)
+constexpr int ATT_SK = 32;    // keys per pipeline stage
+constexpr int ATT_ST = 4;     // stages in flight (TMA ring)
 constexpr int ATT_WARPS = 4;
 
 template <int DH>
@@ -62,42 +62,59 @@ __device__ __forceinline__ void load_h(const half* p, float* out) {
 
 template <int DH>
 constexpr size_t attn_smem() {
-    return (size_t)ATT_ST * 2 * ATT_SK * DH * 2 + ATT_SK * 4 + ATT_WARPS * DH * 4 + 64 + 64;
+    // K, V ring + per-warp (m, l, o) + reduction scratch + barriers
+    return (size_t)ATT_ST * 2 * ATT_SK * DH * 2 + (size_t)ATT_WARPS * (DH + 2) * 4 + 8 * 4 + 2 * ATT_ST * 8 + 64;
 }
 
-// stage i of this CTA's key range: keys [j0 + i*SK, min(j1, j0 + (i+1)*SK)), K and V
-// rows copied page piece by page piece into buffer i % ST
-template <int DH>
-__device__ __forceinline__ void attn_issue(const AttnArgs& a, const int32_t* pt, int64_t head_off, int64_t kv_stride,
-                                           int j0, int j1, int i, half* Ks, half* Vs, uint64_t* full) {
-    const int k0 = j0 + i * ATT_SK;
-    if (k0 >= j1) return;
-    const int k1 = min(j1, k0 + ATT_SK);
-    const int b = i % ATT_ST;
-    uint64_t* bar = &full[b];
-    mbar_expect_tx(bar, (uint32_t)(k1 - k0) * DH * 2 * 2);
-    for (int j = k0; j < k1;) {
-        const int page = pt[j / a.P];
-        const int jn = min(k1, (j / a.P + 1) * a.P);
-        const half* kp = a.kv + (int64_t)page * 2 * kv_stride + head_off + (int64_t)(j % a.P) * DH;
-        const uint32_t bytes = (uint32_t)(jn - j) * DH * 2;
-        bulk_g2s(Ks + ((int64_t)b * ATT_SK + (j - k0)) * DH, kp, bytes, bar);
-        bulk_g2s(Vs + ((int64_t)b * ATT_SK + (j - k0)) * DH, kp + kv_stride, bytes, bar);
-        j = jn;
+// Producer side of stage i: keys [k0, k1) of this CTA's range into ring slot i % ST.
+template <int DH, bool BULK>
+__device__ __forceinline__ void attn_fill(const AttnArgs& a, const int32_t* pt, int64_t head_off, int64_t kv_stride,
+                                          int k0, int k1, half* Kb, half* Vb, uint64_t* bar, int lane) {
+    if constexpr (BULK) {
+        if (lane == 0) {
+            mbar_expect_tx(bar, (uint32_t)(k1 - k0) * DH * 2 * 2);
+            for (int j = k0; j < k1;) {
+                const int page = pt[j / a.P];
+                const int jn = min(k1, (j / a.P + 1) * a.P);
+                const half* kp = a.kv + (int64_t)page * 2 * kv_stride + head_off + (int64_t)(j % a.P) * DH;
+                const uint32_t bytes = (uint32_t)(jn - j) * DH * 2;
+                bulk_g2s(Kb + (j - k0) * DH, kp, bytes, bar);
+                bulk_g2s(Vb + (j - k0) * DH, kp + kv_stride, bytes, bar);
+                j = jn;
+            }
+        }
+    } else {
+        for (int e = lane; e < (k1 - k0) * DH; e += 32) {
+            const int j = k0 + e / DH, dd = e % DH;
+            const half* kp = a.kv + (int64_t)pt[j / a.P] * 2 * kv_stride + head_off + (int64_t)(j % a.P) * DH + dd;
+            Kb[e] = kp[0];
+            Vb[e] = kp[kv_stride];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar);
     }
 }
 
+// Split-T decode/prefill attention. CTA = (head, query token, key split);
+// warp 4 streams the split's K/V rows page piece by page piece into a 4-stage
+// smem ring (cp.async.bulk, mbarrier complete_tx); warps 0-3 each own a
+// quarter of every stage and keep their own online-softmax state (no CTA-wide
+// barrier per stage), releasing the slot with an mbarrier arrive. The four
+// warp states are merged at the end, then the last CTA of (token, head)
+// merges the splits in split order.
 template <int DH>
-__global__ void __launch_bounds__(ATT_WARPS * 32) k_attn(AttnArgs a, int nsplit, int kps) {
+__global__ void __launch_bounds__((ATT_WARPS + 1) * 32) k_attn(AttnArgs a, int nsplit, int kps) {
     using C = AttnCfg<DH>;
+    constexpr int KW = ATT_SK / ATT_WARPS;  // keys per warp per stage
+    constexpr int IT = (KW + C::KPW - 1) / C::KPW;
     extern __shared__ __align__(128) uint8_t smem[];
-    half* Ks = reinterpret_cast<half*>(smem);                       // [ST][SK][DH]
-    half* Vs = Ks + ATT_ST * ATT_SK * DH;                           // [ST][SK][DH]
-    float* sc = reinterpret_cast<float*>(Vs + ATT_ST * ATT_SK * DH);  // [SK]
-    float* osum = sc + ATT_SK;                                      // [WARPS][DH]
-    float* red = osum + ATT_WARPS * DH;                             // [WARPS]
-    uint64_t* full = reinterpret_cast<uint64_t*>(red + 8);          // [ST]
-    int* s_flag = reinterpret_cast<int*>(full + ATT_ST);
+    half* Ks = reinterpret_cast<half*>(smem);                                // [ST][SK][DH]
+    half* Vs = Ks + ATT_ST * ATT_SK * DH;                                    // [ST][SK][DH]
+    float* wst = reinterpret_cast<float*>(Vs + ATT_ST * ATT_SK * DH);        // [WARPS][DH + 2]
+    float* red = wst + ATT_WARPS * (DH + 2);                                 // [8]
+    uint64_t* full = reinterpret_cast<uint64_t*>(red + 8);                   // [ST]
+    uint64_t* empty = full + ATT_ST;                                         // [ST]
+    int* s_flag = reinterpret_cast<int*>(empty + ATT_ST);
 
     const int h = blockIdx.x, tok = blockIdx.y, split = blockIdx.z;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -108,51 +125,54 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) k_attn(AttnArgs a, int nsplit,
     const int32_t* pt = a.pages + (int64_t)seq * a.max_pages;
     const int64_t head_off = (int64_t)h * a.P * DH;
     const int64_t kv_stride = (int64_t)a.H * a.P * DH;  // K -> V within a page
+    const int nst = j0 < j1 ? (j1 - j0 + ATT_SK - 1) / ATT_SK : 0;
 
-    if (j0 < j1) {
-        const int nst = (j1 - j0 + ATT_SK - 1) / ATT_SK;
-        if constexpr (C::BULK) {
-            if (threadIdx.x == 0) {
-                for (int b = 0; b < ATT_ST; ++b) mbar_init(&full[b], 1);
-                mbar_fence_init();
-                for (int i = 0; i < ATT_ST && i < nst; ++i) attn_issue<DH>(a, pt, head_off, kv_stride, j0, j1, i, Ks, Vs, full);
-            }
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < ATT_ST; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&empty[b], ATT_WARPS);
         }
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    if (warp == ATT_WARPS) {
+        // ---------------- producer warp
+        for (int i = 0; i < nst; ++i) {
+            const int b = i % ATT_ST;
+            mbar_wait(&empty[b], ((i / ATT_ST) & 1) ^ 1);
+            const int k0 = j0 + i * ATT_SK;
+            attn_fill<DH, C::BULK>(a, pt, head_off, kv_stride, k0, min(j1, k0 + ATT_SK), Ks + b * ATT_SK * DH,
+                                   Vs + b * ATT_SK * DH, &full[b], lane);
+        }
+    } else {
+        // ---------------- compute warps
         const int sub = lane % C::LPK, slot = lane / C::LPK;
         const int d0 = sub * C::DPL;
         float qv[C::DPL];
 #pragma unroll
-        for (int i = 0; i < C::DPL; ++i) qv[i] = a.q[(int64_t)tok * a.d + h * DH + d0 + i];
+        for (int e = 0; e < C::DPL; ++e) qv[e] = a.q[(int64_t)tok * a.d + h * DH + d0 + e];
         const float sq = (float)sqrt((double)DH);
         const float slope = a.slopes[h];
         float m_run = -INFINITY, l_run = 0.f;
         float ov[C::DPL];
 #pragma unroll
-        for (int i = 0; i < C::DPL; ++i) ov[i] = 0.f;
-        __syncthreads();
+        for (int e = 0; e < C::DPL; ++e) ov[e] = 0.f;
         for (int i = 0; i < nst; ++i) {
             const int b = i % ATT_ST;
-            const int k0 = j0 + i * ATT_SK, nk = min(ATT_SK, j1 - k0);
-            const half* Kb = Ks + (int64_t)b * ATT_SK * DH;
-            const half* Vb = Vs + (int64_t)b * ATT_SK * DH;
-            if constexpr (C::BULK) {
-                mbar_wait(&full[b], (i / ATT_ST) & 1);
-            } else {
-                half* Kw = Ks + (int64_t)b * ATT_SK * DH;
-                half* Vw = Vs + (int64_t)b * ATT_SK * DH;
-                for (int e = threadIdx.x; e < nk * DH; e += blockDim.x) {
-                    const int j = k0 + e / DH, dd = e % DH;
-                    const half* kp = a.kv + (int64_t)pt[j / a.P] * 2 * kv_stride + head_off + (int64_t)(j % a.P) * DH + dd;
-                    Kw[e] = kp[0];
-                    Vw[e] = kp[kv_stride];
-                }
-                __syncthreads();
-            }
-            // scores of this stage
-            for (int base = warp * C::KPW; base < nk; base += ATT_WARPS * C::KPW) {
-                const int jj = base + slot;
+            const int k0 = j0 + i * ATT_SK;
+            const int nk = min(ATT_SK, j1 - k0);
+            mbar_wait(&full[b], (i / ATT_ST) & 1);
+            const half* Kb = Ks + b * ATT_SK * DH;
+            const half* Vb = Vs + b * ATT_SK * DH;
+            float s[IT];
+            float smax = -INFINITY;
+#pragma unroll
+            for (int it = 0; it < IT; ++it) {
+                const int jj = warp * KW + it * C::KPW + slot;
+                const bool ok = jj < nk && (it * C::KPW + slot) < KW;
                 float dot = 0.f;
-                if (jj < nk) {
+                if (ok) {
                     float kf[C::DPL];
                     load_h<C::DPL>(Kb + jj * DH + d0, kf);
 #pragma unroll
@@ -160,62 +180,76 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) k_attn(AttnArgs a, int nsplit,
                 }
 #pragma unroll
                 for (int o = C::LPK / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-                if (jj < nk && sub == 0)
-                    sc[jj] = __fadd_rn(__fdiv_rn(dot, sq), __fmul_rn(slope, (float)(k0 + jj - pos)));
+                s[it] = ok ? __fadd_rn(__fdiv_rn(dot, sq), __fmul_rn(slope, (float)(k0 + jj - pos))) : -INFINITY;
+                smax = fmaxf(smax, s[it]);
             }
-            __syncthreads();
-            // online softmax: every warp reduces the stage redundantly (no extra barrier)
-            float smax = -INFINITY;
-            for (int jj = lane; jj < nk; jj += 32) smax = fmaxf(smax, sc[jj]);
-            smax = warp_max(smax);
+#pragma unroll
+            for (int o = 16; o >= C::LPK; o >>= 1) smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, o));
             const float m_new = fmaxf(m_run, smax);
-            const float alpha = m_run == -INFINITY ? 0.f : expf(__fsub_rn(m_run, m_new));
-            float ls = 0.f;
-            for (int jj = lane; jj < nk; jj += 32) ls += expf(__fsub_rn(sc[jj], m_new));
-            ls = warp_sum(ls);
-            l_run = l_run * alpha + ls;
-            m_run = m_new;
+            if (m_new != -INFINITY) {
+                const float alpha = m_run == -INFINITY ? 0.f : expf(__fsub_rn(m_run, m_new));
+                float ls = 0.f;
 #pragma unroll
-            for (int e = 0; e < C::DPL; ++e) ov[e] *= alpha;
-            for (int base = warp * C::KPW; base < nk; base += ATT_WARPS * C::KPW) {
-                const int jj = base + slot;
-                if (jj < nk) {
-                    float vf[C::DPL];
-                    load_h<C::DPL>(Vb + jj * DH + d0, vf);
-                    const float p = expf(__fsub_rn(sc[jj], m_new));
+                for (int e = 0; e < C::DPL; ++e) ov[e] *= alpha;
 #pragma unroll
-                    for (int e = 0; e < C::DPL; ++e) ov[e] = fmaf(p, vf[e], ov[e]);
+                for (int it = 0; it < IT; ++it) {
+                    const int jj = warp * KW + it * C::KPW + slot;
+                    if (s[it] != -INFINITY) {
+                        const float p = expf(__fsub_rn(s[it], m_new));
+                        ls += p;
+                        float vf[C::DPL];
+                        load_h<C::DPL>(Vb + jj * DH + d0, vf);
+#pragma unroll
+                        for (int e = 0; e < C::DPL; ++e) ov[e] = fmaf(p, vf[e], ov[e]);
+                    }
                 }
+#pragma unroll
+                for (int o = 16; o >= C::LPK; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
+                l_run = l_run * alpha + ls;
+                m_run = m_new;
             }
-            __syncthreads();  // buffer b and sc free
-            if constexpr (C::BULK) {
-                if (threadIdx.x == 0 && i + ATT_ST < nst)
-                    attn_issue<DH>(a, pt, head_off, kv_stride, j0, j1, i + ATT_ST, Ks, Vs, full);
-            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[b]);
         }
+        // per-warp state -> smem (dims reduced over the key slots)
 #pragma unroll
         for (int e = 0; e < C::DPL; ++e) {
 #pragma unroll
             for (int o = 16; o >= C::LPK; o >>= 1) ov[e] += __shfl_xor_sync(0xffffffffu, ov[e], o);
         }
+        float* w = wst + warp * (DH + 2);
         if (slot == 0) {
 #pragma unroll
-            for (int e = 0; e < C::DPL; ++e) osum[warp * DH + d0 + e] = ov[e];
+            for (int e = 0; e < C::DPL; ++e) w[2 + d0 + e] = ov[e];
         }
-        __syncthreads();
-        for (int e = threadIdx.x; e < DH; e += blockDim.x) {
-            float s = 0.f;
+        if (lane == 0) {
+            w[0] = m_run;
+            w[1] = l_run;
+        }
+    }
+    __syncthreads();
+    {  // merge the 4 warp states of this split (fixed order)
+    float M = -INFINITY;
 #pragma unroll
-            for (int w = 0; w < ATT_WARPS; ++w) s += osum[w * DH + e];
-            out[2 + e] = s;
-        }
-        if (threadIdx.x == 0) {
-            out[0] = m_run;
-            out[1] = l_run;
-        }
-    } else if (threadIdx.x == 0) {  // range entirely in the causal future
-        out[0] = -INFINITY;
-        out[1] = 0.f;
+    for (int w = 0; w < ATT_WARPS; ++w) M = fmaxf(M, wst[w * (DH + 2)]);
+    float L = 0.f;
+    float sc[ATT_WARPS];
+#pragma unroll
+    for (int w = 0; w < ATT_WARPS; ++w) {
+        const float mw = wst[w * (DH + 2)];
+        sc[w] = mw == -INFINITY ? 0.f : expf(mw - M);
+        L += wst[w * (DH + 2) + 1] * sc[w];
+    }
+    for (int e = threadIdx.x; e < DH; e += blockDim.x) {
+        float o = 0.f;
+#pragma unroll
+        for (int w = 0; w < ATT_WARPS; ++w) o += wst[w * (DH + 2) + 2 + e] * sc[w];
+        out[2 + e] = o;
+    }
+    if (threadIdx.x == 0) {
+        out[0] = M;
+        out[1] = L;
+    }
     }
 
     // ---- last CTA of (token, head) merges the chunks in chunk order
@@ -257,7 +291,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) k_attn(AttnArgs a, int nsplit,
         if (threadIdx.x == 0) {
             float m = red[0];
 #pragma unroll
-            for (int w = 1; w < ATT_WARPS; ++w) m = fmaxf(m, red[w]);
+            for (int w = 1; w <= ATT_WARPS; ++w) m = fmaxf(m, red[w]);
             atomicMax(reinterpret_cast<int*>(a.tokmax) + tok, __float_as_int(m));
         }
     }
@@ -282,7 +316,7 @@ static int run_attn(const AttnArgs& a, int64_t cap, cudaStream_t st) {
         ctas_per_sm = e ? atoi(e) : 2;
     }
     int nsplit = (int)ceil_div((int64_t)ctas_per_sm * sms, (int64_t)a.n_tok * a.H);
-    nsplit = std::max(1, std::min<int>(nsplit, std::min<int>(ATT_MAX_SPLIT, (int)ceil_div(a.max_pos, 2 * ATT_SK))));
+    nsplit = std::max(1, std::min<int>(nsplit, std::min<int>(ATT_MAX_SPLIT, (int)ceil_div(a.max_pos, 4 * ATT_SK))));
     const int kps = (int)round_up(ceil_div(a.max_pos, nsplit), ATT_SK);
     nsplit = (int)ceil_div(a.max_pos, kps);
     if ((int64_t)a.n_tok * a.H * nsplit * (DH + 2) > cap) {
@@ -295,7 +329,7 @@ static int run_attn(const AttnArgs& a, int64_t cap, cudaStream_t st) {
         cudaFuncSetAttribute(k_attn<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    k_attn<DH><<<dim3(a.H, a.n_tok, nsplit), ATT_WARPS * 32, smem, st>>>(a, nsplit, kps);
+    k_attn<DH><<<dim3(a.H, a.n_tok, nsplit), (ATT_WARPS + 1) * 32, smem, st>>>(a, nsplit, kps);
     return launch_check("attention");
 }
 
