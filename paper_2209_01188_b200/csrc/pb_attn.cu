@@ -136,17 +136,30 @@ __global__ void __launch_bounds__((ATT_WARPS + 1) * 32) k_attn(AttnArgs a, int n
     }
     __syncthreads();
 
+    pdl_trigger();
     if (warp == ATT_WARPS) {
         // ---------------- producer warp
+        // In a pure decode step the keys before each query's own position were
+        // written by earlier steps: stream them while the QKV GEMV (PDL
+        // predecessor) is still finishing; wait before the newest key.
+        const int safe_end = a.decode_only ? pos : j0;
+        bool waited = false;
         for (int i = 0; i < nst; ++i) {
             const int b = i % ATT_ST;
             mbar_wait(&empty[b], ((i / ATT_ST) & 1) ^ 1);
             const int k0 = j0 + i * ATT_SK;
-            attn_fill<DH, C::BULK>(a, pt, head_off, kv_stride, k0, min(j1, k0 + ATT_SK), Ks + b * ATT_SK * DH,
-                                   Vs + b * ATT_SK * DH, &full[b], lane);
+            const int k1 = min(j1, k0 + ATT_SK);
+            if (!waited && k1 > safe_end) {
+                pdl_wait();
+                waited = true;
+            }
+            attn_fill<DH, C::BULK>(a, pt, head_off, kv_stride, k0, k1, Ks + b * ATT_SK * DH, Vs + b * ATT_SK * DH,
+                                   &full[b], lane);
         }
+        if (!waited) pdl_wait();
     } else {
         // ---------------- compute warps
+        pdl_wait();
         const int sub = lane % C::LPK, slot = lane / C::LPK;
         const int d0 = sub * C::DPL;
         float qv[C::DPL];
@@ -329,8 +342,7 @@ static int run_attn(const AttnArgs& a, int64_t cap, cudaStream_t st) {
         cudaFuncSetAttribute(k_attn<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    k_attn<DH><<<dim3(a.H, a.n_tok, nsplit), (ATT_WARPS + 1) * 32, smem, st>>>(a, nsplit, kps);
-    return launch_check("attention");
+    return launch_pdl(k_attn<DH>, dim3(a.H, a.n_tok, nsplit), dim3((ATT_WARPS + 1) * 32), smem, st, a, nsplit, kps);
 }
 
 int launch_attention(const AttnArgs& a, int64_t cap, cudaStream_t st) {

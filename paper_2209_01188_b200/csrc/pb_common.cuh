@@ -108,6 +108,35 @@ __device__ __forceinline__ int8_t wire_code(float x, float s, float amax) {
     return (int8_t)(x < 0.f ? -m : m);
 }
 
+// Programmatic dependent launch (PDL): kernels of the decode chain are launched
+// with cudaLaunchAttributeProgrammaticStreamSerialization, may start while the
+// previous kernel drains, and must execute pdl_wait() before touching anything
+// the previous kernels wrote (every such kernel calls it, so the chain stays
+// transitively ordered). pdl_trigger() lets the next kernel launch early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+template <typename... KArgs, typename... Args>
+inline int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+    if (e != cudaSuccess) {
+        set_error(std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
+        return PB_ERR_GENERIC;
+    }
+    return PB_OK;
+}
+
 // SplitMix64 word i of the stream keyed by `key` (model.py:36-44: state =
 // key + i*gamma, i >= 1) mapped to f32 in [-0.05, 0.05) (model.py:54-57).
 __device__ __forceinline__ float gen_weight(uint64_t key, uint64_t i1) {

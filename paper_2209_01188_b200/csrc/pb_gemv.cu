@@ -265,6 +265,8 @@ int bound_consts(const float* gamma, const float* beta, const float* scales, int
 // one thread per (token, 32-wide k chunk, lane quad q).
 __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
     __shared__ float4 s_st;
+    pdl_trigger();  // the GEMV that consumes this operand may start streaming its weights
+    pdl_wait();
     const int tok = blockIdx.y;
     const float* x = a.x + (int64_t)tok * a.K;
     if (threadIdx.x < 32) {
@@ -400,8 +402,7 @@ int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int 
                                                                                                       n_tok);
         return launch_check("canonwrite");
     }
-    k_fragwrite<<<dim3((unsigned)ceil_div(items, 256), n_tok), 256, 0, st>>>(a);
-    return launch_check("fragwrite");
+    return launch_pdl(k_fragwrite, dim3((unsigned)ceil_div(items, 256), n_tok), dim3(256), 0, st, a);
 }
 
 // ------------------------------------------------------------------ epilogue
@@ -494,14 +495,21 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
         mbar_fence_init();
     }
     __syncthreads();
-    if (u0 >= u1) return;
+    pdl_trigger();
+    if (u0 >= u1) {
+        pdl_wait();
+        return;
+    }
 
     if (warp == 0) {
         // ---------------- producer
         if (lane == 0) {
-            int stage = 0;
+            int stage = 0, issued = 0;
             uint32_t phase = 0;
+            int pk[SK_STAGES];  // k tiles of the stages prefetched before the dependency wait
+            int pn[SK_STAGES];
             const uint8_t* bsrc = reinterpret_cast<const uint8_t*>(a.act.frag) + (int64_t)chunk * a.KC * NT * 512;
+            bool waited = false;
             for (int64_t u = u0; u < u1;) {
                 const int mg = (int)(u / a.KC);
                 const int ka = (int)(u % a.KC);
@@ -510,8 +518,22 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
                     const int n = min(SK_KCS, kb - kc);
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], n * (4096 + NT * 512));
+                    // weights never depend on the previous kernels: start streaming them
+                    // while the operand producer (PDL predecessor) is still running
                     bulk_g2s(sa + stage * A_STAGE, a.codes + ((int64_t)mg * a.KC + kc) * 4096, n * 4096, &full[stage]);
-                    bulk_g2s(sb + stage * B_STAGE, bsrc + (int64_t)kc * NT * 512, n * NT * 512, &full[stage]);
+                    if (!waited && issued < SK_STAGES) {
+                        pk[issued] = kc;
+                        pn[issued] = n;
+                    } else {
+                        bulk_g2s(sb + stage * B_STAGE, bsrc + (int64_t)kc * NT * 512, n * NT * 512, &full[stage]);
+                    }
+                    ++issued;
+                    if (!waited && issued == SK_STAGES) {
+                        pdl_wait();
+                        waited = true;
+                        for (int i = 0; i < SK_STAGES; ++i)
+                            bulk_g2s(sb + i * B_STAGE, bsrc + (int64_t)pk[i] * NT * 512, pn[i] * NT * 512, &full[i]);
+                    }
                     if (++stage == SK_STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -519,11 +541,19 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
                 }
                 u += kb - ka;
             }
+            if (!waited) {  // fewer stages than the ring depth
+                pdl_wait();
+                for (int i = 0; i < issued; ++i)
+                    bulk_g2s(sb + i * B_STAGE, bsrc + (int64_t)pk[i] * NT * 512, pn[i] * NT * 512, &full[i]);
+            }
+        } else {
+            pdl_wait();
         }
         return;
     }
 
     // ---------------- consumers
+    pdl_wait();
     const int cw = warp - 1;  // consumer warp: m-tiles 2cw, 2cw+1 of the group
     const int g = lane >> 2, q = lane & 3;
     int stage = 0;
@@ -713,8 +743,7 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
     a.epi = epi;
     a.partials = partials;
     a.counters = counters;
-    k_gemv_i8<NT><<<dim3((unsigned)G, chunks), SK_THREADS, smem, st>>>(a);
-    return launch_check("gemv_i8");
+    return launch_pdl(k_gemv_i8<NT>, dim3((unsigned)G, chunks), dim3(SK_THREADS), smem, st, a);
 }
 
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters, int64_t partial_cap,

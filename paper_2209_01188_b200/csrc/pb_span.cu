@@ -59,6 +59,7 @@ struct pb_span {
     float* hop_scales = nullptr;
     int64_t bytes = 0;
     int32_t last_launches = 0;
+    int last_n_seq = 0;
     std::mutex mu;  // one step at a time per span (the stream is shared)
 };
 
@@ -450,7 +451,7 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
         // ---- attention (+ operand range of wo)
         AttnArgs aa{s->q, kvb, s->d_tok_seq, s->d_tok_pos, s->d_pages, s->slopes, s->ctx, s->attn_part,
                     s->counters + (1 << 19), int8 ? s->tokmax_ctx : nullptr, int8 ? b.mat[1].scales : nullptr,
-                    n_tok, s->max_pages, s->H, s->dh, s->cfg.page_tokens, d, max_pos};
+                    n_tok, s->max_pages, s->H, s->dh, s->cfg.page_tokens, d, max_pos, s->last_n_seq == n_tok ? 1 : 0};
         {
             const int ev = prof_begin(s, st);
             if (int rc = launch_attention(aa, s->attn_cap, st)) return rc;
@@ -514,6 +515,7 @@ static int stage_meta(pb_span* s, int n_tok, int n_seq, const int32_t* tok_seq, 
     }
     *max_pos = mp;
     s->h_tok_pos_last.assign(tok_pos, tok_pos + n_tok);
+    s->last_n_seq = n_seq;
     // pinned staging ring: wait only until this slot's previous copies have executed
     const int slot = s->meta_slot;
     s->meta_slot = (slot + 1) % pb_span::NSLOT;

@@ -134,6 +134,7 @@ struct AttnArgs {
     const float* s_next;     // [d] scales of wo
     int n_tok, max_pages, H, dh, P, d;
     int max_pos;             // max over tokens of (pos + 1)
+    int decode_only;         // every sequence adds one position (older keys are safe to prefetch early)
 };
 int launch_attention(const AttnArgs& a, int64_t part_cap, cudaStream_t st);
 int64_t attention_part_floats(int n_tok, int H, int dh, int max_seq);
