@@ -136,7 +136,6 @@ __global__ void __launch_bounds__((ATT_WARPS + 1) * 32) k_attn(AttnArgs a, int n
     }
     __syncthreads();
 
-    pdl_trigger();
     if (warp == ATT_WARPS) {
         // ---------------- producer warp
         // In a pure decode step the keys before each query's own position were
@@ -151,15 +150,20 @@ __global__ void __launch_bounds__((ATT_WARPS + 1) * 32) k_attn(AttnArgs a, int n
             const int k1 = min(j1, k0 + ATT_SK);
             if (!waited && k1 > safe_end) {
                 pdl_wait();
+                pdl_trigger();
                 waited = true;
             }
             attn_fill<DH, C::BULK>(a, pt, head_off, kv_stride, k0, k1, Ks + b * ATT_SK * DH, Vs + b * ATT_SK * DH,
                                    &full[b], lane);
         }
-        if (!waited) pdl_wait();
+        if (!waited) {
+            pdl_wait();
+            pdl_trigger();
+        }
     } else {
         // ---------------- compute warps
         pdl_wait();
+        pdl_trigger();
         const int sub = lane % C::LPK, slot = lane / C::LPK;
         const int d0 = sub * C::DPL;
         float qv[C::DPL];

@@ -6,6 +6,8 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <utility>
 #include <string>
 
 #include "../../include/petals_b200.h"
@@ -127,8 +129,12 @@ inline int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    static const int pdl_on = [] {
+        const char* e = getenv("PB_NO_PDL");
+        return (e && *e == '1') ? 0 : 1;
+    }();
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_on;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
     if (e != cudaSuccess) {
         set_error(std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));

@@ -265,8 +265,8 @@ int bound_consts(const float* gamma, const float* beta, const float* scales, int
 // one thread per (token, 32-wide k chunk, lane quad q).
 __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
     __shared__ float4 s_st;
-    pdl_trigger();  // the GEMV that consumes this operand may start streaming its weights
     pdl_wait();
+    pdl_trigger();  // the GEMV that consumes this operand may launch and start streaming its weights
     const int tok = blockIdx.y;
     const float* x = a.x + (int64_t)tok * a.K;
     if (threadIdx.x < 32) {
@@ -495,9 +495,9 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
         mbar_fence_init();
     }
     __syncthreads();
-    pdl_trigger();
     if (u0 >= u1) {
         pdl_wait();
+        pdl_trigger();
         return;
     }
 
@@ -530,6 +530,7 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
                     ++issued;
                     if (!waited && issued == SK_STAGES) {
                         pdl_wait();
+                        pdl_trigger();
                         waited = true;
                         for (int i = 0; i < SK_STAGES; ++i)
                             bulk_g2s(sb + i * B_STAGE, bsrc + (int64_t)pk[i] * NT * 512, pn[i] * NT * 512, &full[i]);
@@ -543,17 +544,20 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
             }
             if (!waited) {  // fewer stages than the ring depth
                 pdl_wait();
+                pdl_trigger();
                 for (int i = 0; i < issued; ++i)
                     bulk_g2s(sb + i * B_STAGE, bsrc + (int64_t)pk[i] * NT * 512, pn[i] * NT * 512, &full[i]);
             }
         } else {
             pdl_wait();
+            pdl_trigger();
         }
         return;
     }
 
     // ---------------- consumers
     pdl_wait();
+    pdl_trigger();
     const int cw = warp - 1;  // consumer warp: m-tiles 2cw, 2cw+1 of the group
     const int g = lane >> 2, q = lane & 3;
     int stage = 0;
