@@ -33,6 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "BLOOM-176B int8 decode steps/s (b=1)"
+METRIC_B = "BLOOM-176B int8 decode tokens/s (b={b})"
 RING_BYTES = 64
 UNIT = "steps/s"
 
@@ -47,6 +48,7 @@ def parse():
     p.add_argument("--ctx", type=int, default=2048)
     p.add_argument("--seed", type=int, default=42)
     p.add_argument("--prefill-chunk", type=int, default=256)
+    p.add_argument("--batch", type=int, default=1, help="batch-1 sessions per pipeline micro-batch")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--synthetic-kv", action="store_true", help="skip the real prefill (KV content is synthetic)")
@@ -199,23 +201,25 @@ class Pipeline:
 
             dist.init_process_group("nccl", device_id=self.dev, timeout=datetime.timedelta(seconds=180))
         self.dist = dist if self.world > 1 else None
-        self.S = self.world  # sessions in flight
+        self.S = self.world  # micro-batches in flight (one per pipeline stage)
+        self.B = args.batch  # batch-1 sessions per micro-batch
+        self.chunk = max(1, args.prefill_chunk // self.B)  # prefill positions per sequence per step
         self.ranges = split_blocks(cfg.n_layers, self.world)
         s, e = self.ranges[self.rank]
         pages_per_seq = -(-cfg.max_seq // 64)
         t0 = time.perf_counter()
-        self.span = BlockSpan(cfg, s, e, int8=True, page_tokens=64, n_pages=self.S * pages_per_seq + 2,
-                              max_tokens=args.prefill_chunk, max_seqs=max(self.S, 1), device=self.local)
+        self.span = BlockSpan(cfg, s, e, int8=True, page_tokens=64, n_pages=self.S * self.B * pages_per_seq + 2,
+                              max_tokens=self.chunk * self.B, max_seqs=self.B, device=self.local)
         self.span.generate_weights(args.seed)
         torch.cuda.synchronize()
         self.gen_s = time.perf_counter() - t0
-        self.seqs = [self.span.new_sequence() for _ in range(self.S)]
+        self.seqs = [[self.span.new_sequence() for _ in range(self.B)] for _ in range(self.S)]
         d = cfg.hidden
         self.d = d
-        cap = self.payload_bytes(args.prefill_chunk)
+        cap = self.payload_bytes(self.chunk)
         self.inbox = torch.empty(cap, dtype=torch.uint8, device=self.dev)
         self.outbox = torch.empty(cap, dtype=torch.uint8, device=self.dev)
-        self.out = torch.empty(args.prefill_chunk, d, dtype=torch.float32, device=self.dev)
+        self.out = torch.empty(self.chunk * self.B, d, dtype=torch.float32, device=self.dev)
         g = torch.Generator(device=self.dev)
         g.manual_seed(7)
         self.inputs = torch.randn(64, d, generator=g, device=self.dev) * 0.05  # embedding-like rows
@@ -223,11 +227,11 @@ class Pipeline:
         self.total_jobs = 0
 
     def payload_bytes(self, t):
-        n = t * self.d
+        n = t * self.B * self.d
         return -(-n // 16) * 16 + 4 * (-(-n // 64))
 
     def views(self, buf, t):
-        n = t * self.d
+        n = t * self.B * self.d
         off = -(-n // 16) * 16
         return buf[:n].view(__import__("torch").int8), buf[off:off + 4 * (-(-n // 64))].view(__import__("torch").float32)
 
@@ -240,7 +244,7 @@ class Pipeline:
         torch.cuda.synchronize()
 
     def run(self, jobs, x_for=None, host_in=None, host_out=None, sync_out=False):
-        """jobs: [(job id, new positions t)]; x_for(j, t) -> span-0 input rows."""
+        """jobs: [(job id, new positions t per sequence)]; x_for(j, n) -> span-0 input rows."""
         import torch
 
         from paper_2209_01188_b200.pipeline import RingSchedule, run_jobs, torch_exchange
@@ -251,24 +255,25 @@ class Pipeline:
 
         def step(j, inbox):
             t = tmap[j]
-            seq = self.seqs[j % self.S]
+            n = t * self.B
+            seqs = self.seqs[j % self.S]
             oc, os_ = self.views(self.outbox, t)
             if inbox is None or r == 0:  # span 0: fresh input (a received ring payload only orders the step)
                 if host_in is not None:
-                    self.out[:t].copy_(host_in[:t], non_blocking=True)
-                    inp = self.out[:t]
+                    self.out[:n].copy_(host_in[:n], non_blocking=True)
+                    inp = self.out[:n]
                 elif x_for is not None:
-                    inp = x_for(j, t)
+                    inp = x_for(j, n)
                 else:
-                    inp = self.inputs[j % 64: j % 64 + 1].expand(t, self.d).contiguous()
-                self.span.step_codes([(seq, None)], [t], out_codes=oc, out_scales=os_, in_f32=inp,
-                                     out_f32=self.out[:t])
+                    inp = self.inputs[j % 64: j % 64 + 1].expand(n, self.d).contiguous()
+                self.span.step_codes(seqs, [t] * self.B, in_f32=inp, out_codes=oc, out_scales=os_, out_f32=self.out[:n])
             else:
                 ic, is_ = self.views(inbox, t)
-                self.span.step_codes([(seq, (ic, is_))], [t], out_codes=oc, out_scales=os_, out_f32=self.out[:t])
+                self.span.step_codes(seqs, [t] * self.B, in_codes=ic, in_scales=is_, out_codes=oc, out_scales=os_,
+                                     out_f32=self.out[:n])
             self.launches += self.span.last_launches
             if r == N - 1 and host_out is not None:
-                host_out[:t * self.d].copy_(oc, non_blocking=True)
+                host_out[:n * self.d].copy_(oc, non_blocking=True)
                 if sync_out:
                     torch.cuda.current_stream().synchronize()  # result readable on the host
             if r == N - 1:
@@ -288,8 +293,9 @@ def run_ours(args):
     from paper_2209_01188_b200.model import SHAPES
 
     cfg = SHAPES[args.shape]
+    metric, unit = (METRIC, UNIT) if args.batch == 1 else (METRIC_B.format(b=args.batch), "tokens/s")
     pl = Pipeline(args, cfg)
-    S, N, rank = pl.S, pl.world, pl.rank
+    S, N, rank, B = pl.S, pl.world, pl.rank, pl.B
     K, W = args.steps, args.warmup
     T0 = args.ctx - (W + 2 * K) - (0 if args.no_e2e else K) - 1
     if T0 < 1:
@@ -298,21 +304,22 @@ def run_ours(args):
     t_pf = time.perf_counter()
     pl.span.profile(True)  # prefill runs the tcgen05 GEMM: record its live device time
     if args.synthetic_kv:
-        for s in pl.seqs:
-            pl.span._reserve(s, T0)
-            s.length = T0
+        for grp in pl.seqs:
+            for s in grp:
+                pl.span._reserve(s, T0)
+                s.length = T0
     else:
         chunks = []
         left = T0
         while left > 0:
-            c = min(args.prefill_chunk, left)
+            c = min(pl.chunk, left)
             chunks.append(c)
             left -= c
         # job order: for each chunk round, every session (keeps the ring pattern)
         jobs = [(ci * S + m, c) for ci, c in enumerate(chunks) for m in range(S)]
         pl.total_jobs = len(jobs) + S * (W + 2 * K + (0 if args.no_e2e else K))
         # all prefill jobs, then decode jobs continue numbering
-        pl.run(jobs, x_for=lambda j, t: pl.inputs[:t] if t <= 64 else torch.randn(t, cfg.hidden, device=pl.dev) * 0.05)
+        pl.run(jobs, x_for=lambda j, n: pl.inputs[:n] if n <= 64 else torch.randn(n, cfg.hidden, device=pl.dev) * 0.05)
         jbase = len(jobs)
     torch.cuda.synchronize()
     pf_s = time.perf_counter() - t_pf
@@ -352,13 +359,13 @@ def run_ours(args):
     if pl.dist:
         pl.dist.all_reduce(t, op=pl.dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = K * S / (ms_max / 1e3)
+    value = K * S * B / (ms_max / 1e3)  # session-steps (= tokens) per second over all GPUs
     # ---- e2e: host bytes in/out
     e2e = None
     if not args.no_e2e:
         d = cfg.hidden
-        host_in = torch.randn(1, d).mul_(0.05).pin_memory()
-        host_out = torch.empty(d, dtype=torch.int8).pin_memory()
+        host_in = torch.randn(B, d).mul_(0.05).pin_memory()
+        host_out = torch.empty(B * d, dtype=torch.int8).pin_memory()
         pl.barrier()
         t0 = time.perf_counter()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -371,8 +378,8 @@ def run_ours(args):
         te = torch.tensor([max(e0.elapsed_time(e1), wall * 1e3)], device=pl.dev)
         if pl.dist:
             pl.dist.all_reduce(te, op=pl.dist.ReduceOp.MAX)
-        e2e = {"value": K * S / (float(te.item()) / 1e3), "unit": UNIT, "h2d_bytes_per_step": 4 * d,
-               "d2h_bytes_per_step": d, "path": "pb_span_step_int8 C-ABI with pinned host ingress (span 0) and "
+        e2e = {"value": K * S * B / (float(te.item()) / 1e3), "unit": unit, "h2d_bytes_per_step": 4 * d * B,
+               "d2h_bytes_per_step": d * B, "path": "pb_span_step_int8 C-ABI with pinned host ingress (span 0) and "
                "egress of the int8 hidden (last span), NCCL int8 hops between spans"}
     # ---- report (rank 0)
     if rank != 0:
@@ -384,18 +391,19 @@ def run_ours(args):
     g_ms, g_n, g_b = gemv
     achieved = (g_b / g_n) / ((g_ms / g_n) / 1e3) / 1e9 if g_n else 0.0
     traffic = committed_traffic()
-    w_bytes, kv_bytes = bytes_per_step(cfg, [args.ctx - K // 2] * S)
-    step_s = (ms_max / 1e3) / (K * S)
-    seq_ceiling = (w_bytes + kv_bytes / S) / (peak * 1e9)  # one session through all blocks, one GPU busy
+    w_bytes, kv_bytes = bytes_per_step(cfg, [args.ctx - K // 2] * (S * B))
+    step_s = (ms_max / 1e3) / (K * S)  # one micro-batch step through all blocks
+    seq_ceiling = (w_bytes + kv_bytes / S) / (peak * 1e9)  # one micro-batch through all blocks, one GPU busy
     agg_ceiling = (w_bytes / N + kv_bytes / N / S) / (peak * 1e9)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": K, "warmup": W,
+        "metric": metric, "value": value, "unit": unit, "n_gpus": N, "steps": K, "warmup": W,
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int8 weights x fp16(hi+lo) activations, fp32 accumulate; fp16 KV",
         "data": "synthetic (gen_checkpoint seed 42 weights generated on device; random embedding-like inputs)",
-        "config": {"workload": f"{args.shape} ({cfg.n_layers} blocks, h={cfg.hidden}) int8 decode, {S} batch-1 "
-                               f"session(s) pipelined over {N} GPU span(s) {pl.ranges}, context {T0}->{args.ctx}",
-                   "sessions": S, "ctx_end": args.ctx, "prefill_tokens": T0,
+        "config": {"workload": f"{args.shape} ({cfg.n_layers} blocks, h={cfg.hidden}) int8 decode, {S} micro-batch(es) "
+                               f"of {B} batch-1 session(s) pipelined over {N} GPU span(s) {pl.ranges}, "
+                               f"context {T0}->{args.ctx}",
+                   "sessions": S * B, "batch_per_microbatch": B, "ctx_end": args.ctx, "prefill_tokens": T0,
                    "l2": "weights stream 172.7 GB per step >> 126 MB L2 (no flush needed)",
                    "parallelism": f"pipeline{N} (block spans)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -412,7 +420,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "e2e": e2e,
         "setup_s": {"weights_gen_quant": pl.gen_s, "prefill": pf_s},
-        "prefill": {"tokens": T0 * S, "wall_s": pf_s, "tokens_per_s_wall": T0 * S / max(pf_s, 1e-9),
+        "prefill": {"tokens": T0 * S * B, "wall_s": pf_s, "tokens_per_s_wall": T0 * S * B / max(pf_s, 1e-9),
                     "tcgen05_gemm": {"launches": tc_n, "ms": tc_ms,
                                      "achieved_tflops": tc_flop / max(tc_ms, 1e-9) / 1e9 if tc_n else None,
                                      "peak_tflops_dense_bf16_measured": measured_tflops(),
@@ -425,7 +433,7 @@ def run_ours(args):
         ts = [sample.step_seconds() for _ in range(2)]
         per_block = min(ts)
         line["cpu_baseline"] = {
-            "value": 1.0 / (per_block * cfg.n_layers), "unit": UNIT, "cores": ncores, "kind": "port",
+            "value": 1.0 / (per_block * cfg.n_layers), "unit": unit, "cores": ncores, "kind": "port",
             "sample": f"oracle port of block_forward(qw) for 1 {args.shape} block, decode t=1 at context 128, "
                       f"best of 2, extrapolated x{cfg.n_layers} blocks"}
     print(json.dumps(line), flush=True)

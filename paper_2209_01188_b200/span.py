@@ -222,13 +222,14 @@ class BlockSpan:
                 s.length += t
         return list(torch.split(y, lens))
 
-    def step_codes(self, items_codes, lens, out_codes=None, out_scales=None, out_f32=None, in_f32=None):
-        """Step whose input (and optionally output) is the wire codec:
-        items_codes = (codes [n_tok*d] int8, scales [n_tok*d/64] f32) on device."""
+    def step_codes(self, seqs, lens, in_codes=None, in_scales=None, in_f32=None, out_codes=None, out_scales=None,
+                   out_f32=None):
+        """Batched step whose input and/or output hidden states are the wire
+        codec (codes [n_tok*d] int8, scales [ceil(n_tok*d/64)] f32) on the
+        device (pb_span_step_int8): the span-to-span hop payload. Sequences'
+        tokens are concatenated in `seqs` order (lens[i] new positions each)."""
         import torch
 
-        seqs = [s for s, _ in items_codes]
-        codes, scales = items_codes[0][1] if items_codes[0][1] is not None else (None, None)
         with self._lock:
             for s, t in zip(seqs, lens):
                 self._reserve(s, s.length + t)
@@ -236,7 +237,7 @@ class BlockSpan:
             st = _lib.stream_ptr(torch.cuda.current_stream(self.device))
             _lib.check(_lib.lib().pb_span_step_int8(
                 self._h, n_tok, len(seqs), tok_seq.ctypes.data, tok_pos.ctypes.data, pages.ctypes.data,
-                _lib.ptr(codes), _lib.ptr(scales), _lib.ptr(in_f32), _lib.ptr(out_codes), _lib.ptr(out_scales),
+                _lib.ptr(in_codes), _lib.ptr(in_scales), _lib.ptr(in_f32), _lib.ptr(out_codes), _lib.ptr(out_scales),
                 _lib.ptr(out_f32), st))
             for s, t in zip(seqs, lens):
                 s.length += t
