@@ -444,8 +444,7 @@ __device__ __forceinline__ void i8x4_to_f16x2(uint32_t w, uint32_t& lo, uint32_t
 // the contributors' partial tiles in CTA order (deterministic).
 constexpr int SK_CONS = 4;                       // consumer warps (2 m-tiles each)
 constexpr int SK_THREADS = (SK_CONS + 1) * 32;   // + producer warp
-constexpr int SK_KCS = 2;                        // k-tiles per stage
-constexpr int SK_STAGES = 4;
+// (k-tiles per stage, stages) are template parameters; sk_launch picks them
 
 __device__ __forceinline__ void cons_sync() {  // the 4 consumer warps only
     asm volatile("bar.sync 1, %0;" ::"n"(SK_CONS * 32) : "memory");
@@ -466,7 +465,7 @@ __device__ __forceinline__ int sk_owner(int64_t u, int G, int64_t total) {
     return (int)(((u + 1) * G - 1) / total);
 }
 
-template <int NT>
+template <int NT, int SK_KCS, int SK_STAGES>
 __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
     constexpr int TC = NT * 4;
     constexpr int COLS = 2 * TC;
@@ -717,7 +716,7 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
     }
 }
 
-template <int NT>
+template <int NT, int SK_KCS, int SK_STAGES>
 static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
                      int64_t partial_cap, cudaStream_t st) {
     constexpr int TC = NT * 4;
@@ -728,8 +727,8 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_gemv_i8<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_gemv_i8<NT>, SK_THREADS, smem);
+        cudaFuncSetAttribute(k_gemv_i8<NT, SK_KCS, SK_STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_gemv_i8<NT, SK_KCS, SK_STAGES>, SK_THREADS, smem);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
     SkArgs a;
@@ -747,16 +746,27 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
     a.epi = epi;
     a.partials = partials;
     a.counters = counters;
-    return launch_pdl(k_gemv_i8<NT>, dim3((unsigned)G, chunks), dim3(SK_THREADS), smem, st, a);
+    return launch_pdl(k_gemv_i8<NT, SK_KCS, SK_STAGES>, dim3((unsigned)G, chunks), dim3(SK_THREADS), smem, st, a);
 }
 
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters, int64_t partial_cap,
                 cudaStream_t st) {
+    static int cfg = -1;
+    if (cfg < 0) {
+        const char* e = getenv("PB_GEMV_CFG");  // tuning knob: 0 = 2x4, 1 = 4x4, 2 = 2x8, 3 = 4x6
+        cfg = e ? atoi(e) : 0;
+    }
     switch (act.tc / 4) {
-        case 1: return sk_launch<1>(m, act, epi, partials, counters, partial_cap, st);
-        case 2: return sk_launch<2>(m, act, epi, partials, counters, partial_cap, st);
-        case 4: return sk_launch<4>(m, act, epi, partials, counters, partial_cap, st);
-        case 8: return sk_launch<8>(m, act, epi, partials, counters, partial_cap, st);
+        case 1:
+            switch (cfg) {
+                case 1: return sk_launch<1, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
+                case 2: return sk_launch<1, 2, 8>(m, act, epi, partials, counters, partial_cap, st);
+                case 3: return sk_launch<1, 4, 6>(m, act, epi, partials, counters, partial_cap, st);
+                default: return sk_launch<1, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
+            }
+        case 2: return sk_launch<2, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
+        case 4: return sk_launch<4, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
+        case 8: return sk_launch<8, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
         default: set_error("bad column tile"); return PB_ERR_GENERIC;
     }
 }
