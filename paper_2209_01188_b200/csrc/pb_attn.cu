@@ -350,6 +350,8 @@ static int run_attn(const AttnArgs& a, int64_t cap, cudaStream_t st) {
 }
 
 int launch_attention(const AttnArgs& a, int64_t cap, cudaStream_t st) {
+    if (a.dh == 64) return run_attn_mma<64>(a, a.n_groups, cap, st);
+    if (a.dh == 128) return run_attn_mma<128>(a, a.n_groups, cap, st);
     switch (a.dh) {
         case 4: return run_attn<4>(a, cap, st);
         case 8: return run_attn<8>(a, cap, st);

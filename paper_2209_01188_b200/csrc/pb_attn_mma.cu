@@ -1,0 +1,372 @@
+// Tensor-core ALiBi attention over the paged fp16 KV cache (model.py:345-361)
+// for head_dim 64 / 128: decode (one query per session) and prefill (up to 8
+// consecutive queries of one sequence per CTA, so K/V are read once per group).
+//
+// CTA = (head, query group, key split); warp 4 streams the split's K/V rows
+// (page pieces, cp.async.bulk on an mbarrier ring of 64-key stages); each of
+// warps 0-3 owns 16 keys of every stage and keeps its own online softmax:
+//   S = [Q_hi; Q_lo] K^T   mma.m16n8k16: rows g = query g hi, g+8 = query g lo
+//                          (fp32-accurate scores: q split hi/lo, K exact fp16),
+//                          K fragments via ldmatrix (B operand = K row-major);
+//   P = exp(S - m)         in registers; the S accumulator layout IS the A
+//                          fragment layout of P (FlashAttention-2 register
+//                          reuse), split again into hi (rows g) / lo (rows g+8);
+//   O += [P_hi; P_lo] V    V fragments via ldmatrix.trans.
+// The KV cache rows are stored with their 16-byte chunks XOR-swizzled by
+// (slot & 7) (written that way by the QKV epilogue), so the ldmatrix row
+// gathers are bank-conflict free after a linear bulk copy.
+// Splits are merged in split order by the last CTA of (group, head).
+#include "pb_async.cuh"
+#include "pb_common.cuh"
+#include "pb_span.h"
+
+namespace pb {
+
+constexpr int AM_SK = 64;    // keys per stage
+constexpr int AM_ST = 3;     // stages in flight
+constexpr int AM_WARPS = 4;  // compute warps, 16 keys each per stage
+constexpr int AM_G = 8;      // queries per group
+
+__device__ __forceinline__ int kv_chunk_swz(int chunk, int slot) { return chunk ^ (slot & 7); }
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void mma_f16(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+    return (uint32_t)__half_as_ushort(__float2half_rn(lo)) | ((uint32_t)__half_as_ushort(__float2half_rn(hi)) << 16);
+}
+// hi/lo split of two floats into two f16x2 words
+__device__ __forceinline__ void split_h2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+    const half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
+    hi = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+    lo = pack_h2(x0 - __half2float(h0), x1 - __half2float(h1));
+}
+
+template <int DH>
+constexpr size_t attn_mma_smem() {
+    return (size_t)AM_ST * 2 * AM_SK * DH * 2 + (size_t)AM_WARPS * AM_G * (DH + 2) * 4 + 2 * AM_ST * 8 + 64;
+}
+
+template <int DH>
+__global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, int nsplit, int kps) {
+    constexpr int NKT = DH / 16;  // k-steps of S
+    constexpr int NNT = DH / 8;   // n-tiles of O
+    constexpr int ROWB = DH * 2;  // bytes per K/V row
+    extern __shared__ __align__(128) uint8_t smem[];
+    half* Ks = reinterpret_cast<half*>(smem);                         // [ST][SK][DH]
+    half* Vs = Ks + AM_ST * AM_SK * DH;                               // [ST][SK][DH]
+    float* wst = reinterpret_cast<float*>(Vs + AM_ST * AM_SK * DH);   // [WARPS][G][DH + 2]
+    uint64_t* full = reinterpret_cast<uint64_t*>(wst + AM_WARPS * AM_G * (DH + 2));
+    uint64_t* empty = full + AM_ST;
+    int* s_flag = reinterpret_cast<int*>(empty + AM_ST);
+
+    const int h = blockIdx.x, grp = blockIdx.y, split = blockIdx.z;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t0 = a.grp_first[grp], nq = a.grp_count[grp];
+    const int seq = a.tok_seq[t0], pos0 = a.tok_pos[t0];
+    const int posL = pos0 + nq - 1;
+    const int j0 = split * kps;
+    const int j1 = min(j0 + kps, posL + 1);
+    const int32_t* pt = a.pages + (int64_t)seq * a.max_pages;
+    const int64_t head_off = (int64_t)h * a.P * DH;
+    const int64_t kv_stride = (int64_t)a.H * a.P * DH;
+    const int nst = j0 < j1 ? (j1 - j0 + AM_SK - 1) / AM_SK : 0;
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < AM_ST; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&empty[b], AM_WARPS);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    if (warp == AM_WARPS) {
+        // ---------------- producer warp (older keys may be streamed before the QKV GEMV completes)
+        const int safe_end = a.decode_only ? pos0 : j0;
+        bool waited = false;
+        for (int i = 0; i < nst; ++i) {
+            const int b = i % AM_ST;
+            mbar_wait(&empty[b], ((i / AM_ST) & 1) ^ 1);
+            const int k0 = j0 + i * AM_SK;
+            const int k1 = min(j1, k0 + AM_SK);
+            if (!waited && k1 > safe_end) {
+                pdl_wait();
+                pdl_trigger();
+                waited = true;
+            }
+            if (lane == 0) {
+                mbar_expect_tx(&full[b], (uint32_t)(k1 - k0) * ROWB * 2);
+                for (int j = k0; j < k1;) {
+                    const int page = pt[j / a.P];
+                    const int jn = min(k1, (j / a.P + 1) * a.P);
+                    const half* kp = a.kv + (int64_t)page * 2 * kv_stride + head_off + (int64_t)(j % a.P) * DH;
+                    const uint32_t bytes = (uint32_t)(jn - j) * ROWB;
+                    bulk_g2s(Ks + ((int64_t)b * AM_SK + (j - k0)) * DH, kp, bytes, &full[b]);
+                    bulk_g2s(Vs + ((int64_t)b * AM_SK + (j - k0)) * DH, kp + kv_stride, bytes, &full[b]);
+                    j = jn;
+                }
+            }
+        }
+        if (!waited) {
+            pdl_wait();
+            pdl_trigger();
+        }
+    } else {
+        // ---------------- compute warps
+        pdl_wait();
+        pdl_trigger();
+        const int g = lane >> 2, qd = lane & 3;
+        const bool qv = g < nq;
+        const int my_pos = pos0 + g;
+        // Q fragments (A operand): rows g (hi) / g+8 (lo) of query g, scaled by 1/sqrt(dh)
+        uint32_t qa[NKT][4];
+        {
+            const float isq = 1.0f / sqrtf((float)DH);
+            const float* q = a.q + (int64_t)(t0 + (qv ? g : 0)) * a.d + h * DH;
+#pragma unroll
+            for (int ks = 0; ks < NKT; ++ks) {
+                float x0 = 0.f, x1 = 0.f, x2 = 0.f, x3 = 0.f;
+                if (qv) {
+                    x0 = q[ks * 16 + 2 * qd] * isq;
+                    x1 = q[ks * 16 + 2 * qd + 1] * isq;
+                    x2 = q[ks * 16 + 2 * qd + 8] * isq;
+                    x3 = q[ks * 16 + 2 * qd + 9] * isq;
+                }
+                split_h2(x0, x1, qa[ks][0], qa[ks][1]);  // a0a1 (row g) hi, a2a3 (row g+8) lo
+                split_h2(x2, x3, qa[ks][2], qa[ks][3]);  // a4a5 hi, a6a7 lo
+            }
+        }
+        const float slope = a.slopes[h];
+        float m_row = -INFINITY, l_row = 0.f;
+        float o[NNT][4];
+#pragma unroll
+        for (int n = 0; n < NNT; ++n)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) o[n][r] = 0.f;
+        const uint32_t ks_base = smem_u32(Ks), vs_base = smem_u32(Vs);
+        // ldmatrix lane roles: matrix mi = lane / 8, row ri = lane % 8
+        const int mi = lane >> 3, ri = lane & 7;
+        for (int i = 0; i < nst; ++i) {
+            const int b = i % AM_ST;
+            const int k0 = j0 + i * AM_SK;
+            mbar_wait(&full[b], (i / AM_ST) & 1);
+            const int kb = warp * 16;  // this warp's 16 keys of the stage
+            if (k0 + kb + 16 > j1) {
+                // partial last stage: rows past the range hold stale smem; P is 0
+                // there but 0 * NaN would poison O, so clear this warp's V rows
+                for (int idx = lane; idx < 16 * (DH / 8); idx += 32) {
+                    const int r = idx / (DH / 8), c = idx % (DH / 8);
+                    if (k0 + kb + r >= j1)
+                        *reinterpret_cast<uint4*>(Vs + ((int64_t)(b * AM_SK + kb + r)) * DH + c * 8) =
+                            make_uint4(0u, 0u, 0u, 0u);
+                }
+                __syncwarp();
+            }
+            // ---- S = Q K^T over 16 keys (2 n-tiles)
+            float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+            {
+                const int key = kb + ((mi & 2) ? 8 : 0) + ri;  // row of the K tile
+                const uint32_t rowaddr = ks_base + (uint32_t)((b * AM_SK + key) * ROWB);
+#pragma unroll
+                for (int ks = 0; ks < NKT; ++ks) {
+                    const int chunk = ks * 2 + (mi & 1);
+                    uint32_t r0, r1, r2, r3;
+                    ldsm_x4(rowaddr + (uint32_t)(kv_chunk_swz(chunk, key) * 16), r0, r1, r2, r3);
+                    mma_f16(s0, qa[ks], r0, r1);
+                    mma_f16(s1, qa[ks], r2, r3);
+                }
+            }
+            // ---- scores of query g: keys kb + 2qd + {0,1} (s0), kb + 8 + 2qd + {0,1} (s1)
+            float sc[4];
+            float mx = -INFINITY;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int jrel = kb + (e >> 1) * 8 + 2 * qd + (e & 1);
+                const int j = k0 + jrel;
+                const float dot = (e < 2) ? (s0[e] + s0[2 + e]) : (s1[e - 2] + s1[e]);
+                const bool ok = qv && j < j1 && j <= my_pos;
+                sc[e] = ok ? dot + slope * (float)(j - my_pos) : -INFINITY;
+                mx = fmaxf(mx, sc[e]);
+            }
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            const float m_new = fmaxf(m_row, mx);
+            float p[4];
+            float ls = 0.f;
+            float alpha = 1.f;
+            if (m_new != -INFINITY) {
+                alpha = m_row == -INFINITY ? 0.f : expf(m_row - m_new);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    p[e] = sc[e] == -INFINITY ? 0.f : expf(sc[e] - m_new);
+                    ls += p[e];
+                }
+                m_row = m_new;
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) p[e] = 0.f;
+            }
+            ls += __shfl_xor_sync(0xffffffffu, ls, 1);
+            ls += __shfl_xor_sync(0xffffffffu, ls, 2);
+            l_row = l_row * alpha + ls;
+            if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+                for (int n = 0; n < NNT; ++n)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) o[n][r] *= alpha;
+            }
+            // ---- P as the A operand: rows g hi / g+8 lo
+            uint32_t pa[4];
+            split_h2(p[0], p[1], pa[0], pa[1]);
+            split_h2(p[2], p[3], pa[2], pa[3]);
+            // ---- O += P V  (V fragments via ldmatrix.trans, 2 n-tiles per load)
+            {
+                const int key = kb + ((mi & 1) ? 8 : 0) + ri;
+                const uint32_t rowaddr = vs_base + (uint32_t)((b * AM_SK + key) * ROWB);
+#pragma unroll
+                for (int n2 = 0; n2 < NNT / 2; ++n2) {
+                    const int chunk = n2 * 2 + ((mi & 2) ? 1 : 0);
+                    uint32_t r0, r1, r2, r3;
+                    ldsm_x4_t(rowaddr + (uint32_t)(kv_chunk_swz(chunk, key) * 16), r0, r1, r2, r3);
+                    mma_f16(o[2 * n2], pa, r0, r1);
+                    mma_f16(o[2 * n2 + 1], pa, r2, r3);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[b]);
+        }
+        // per-warp state for query g: m, l, O[dims] = hi rows + lo rows
+        if (qv) {
+            float* w = wst + (warp * AM_G + g) * (DH + 2);
+            if (qd == 0) {
+                w[0] = m_row;
+                w[1] = l_row;
+            }
+#pragma unroll
+            for (int n = 0; n < NNT; ++n) {
+                w[2 + n * 8 + 2 * qd] = o[n][0] + o[n][2];
+                w[2 + n * 8 + 2 * qd + 1] = o[n][1] + o[n][3];
+            }
+        }
+    }
+    __syncthreads();
+    // ---- merge the 4 warps per query (fixed order) -> split partials
+    for (int g = 0; g < nq; ++g) {
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < AM_WARPS; ++w) M = fmaxf(M, wst[(w * AM_G + g) * (DH + 2)]);
+        float sw[AM_WARPS];
+        float L = 0.f;
+#pragma unroll
+        for (int w = 0; w < AM_WARPS; ++w) {
+            const float mw = wst[(w * AM_G + g) * (DH + 2)];
+            sw[w] = mw == -INFINITY ? 0.f : expf(mw - M);
+            L += wst[(w * AM_G + g) * (DH + 2) + 1] * sw[w];
+        }
+        float* out = a.part + (((int64_t)(t0 + g) * a.H + h) * nsplit + split) * (DH + 2);
+        for (int e = threadIdx.x; e < DH; e += blockDim.x) {
+            float acc = 0.f;
+#pragma unroll
+            for (int w = 0; w < AM_WARPS; ++w) acc += wst[(w * AM_G + g) * (DH + 2) + 2 + e] * sw[w];
+            out[2 + e] = acc;
+        }
+        if (threadIdx.x == 0) {
+            out[0] = M;
+            out[1] = L;
+        }
+    }
+    // ---- last CTA of (group, head) merges the splits in split order
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int* ctr = a.counters + (int64_t)t0 * a.H + h;
+        const int prev = atomicAdd(ctr, 1);
+        const int last = prev == nsplit - 1;
+        if (last) *ctr = 0;
+        *s_flag = last;
+    }
+    __syncthreads();
+    if (!*s_flag) return;
+    __threadfence();
+    float mloc[AM_G];
+    for (int g = 0; g < nq; ++g) {
+        const int tok = t0 + g;
+        const float* pp = a.part + ((int64_t)tok * a.H + h) * nsplit * (DH + 2);
+        float M = -INFINITY;
+        for (int s = 0; s < nsplit; ++s) M = fmaxf(M, __ldcg(pp + s * (DH + 2)));
+        float L = 0.f;
+        for (int s = 0; s < nsplit; ++s) {
+            const float ms = __ldcg(pp + s * (DH + 2));
+            if (ms != -INFINITY) L += __ldcg(pp + s * (DH + 2) + 1) * expf(ms - M);
+        }
+        float ml = 0.f;
+        for (int e = threadIdx.x; e < DH; e += blockDim.x) {
+            float acc = 0.f;
+            for (int s = 0; s < nsplit; ++s) {
+                const float ms = __ldcg(pp + s * (DH + 2));
+                if (ms != -INFINITY) acc += __ldcg(pp + s * (DH + 2) + 2 + e) * expf(ms - M);
+            }
+            const float c = acc / L;
+            a.ctx[(int64_t)tok * a.d + h * DH + e] = c;
+            if (a.tokmax) ml = fmaxf(ml, fabsf(c * a.s_next[h * DH + e]));
+        }
+        mloc[g] = ml;
+    }
+    if (a.tokmax) {
+        float* red = wst;  // reuse (all warps are past the merge)
+        __syncthreads();
+        for (int g = 0; g < nq; ++g) {
+            float v = warp_max(mloc[g]);
+            if (lane == 0) red[g * 8 + warp] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < nq) {
+            float v = 0.f;
+            for (int w = 0; w <= AM_WARPS; ++w) v = fmaxf(v, red[threadIdx.x * 8 + w]);
+            atomicMax(reinterpret_cast<int*>(a.tokmax) + t0 + threadIdx.x, __float_as_int(v));
+        }
+    }
+}
+
+template <int DH>
+int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int nsplit = (int)ceil_div(2 * sms, (int64_t)n_groups * a.H);
+    nsplit = std::max(1, std::min<int>(nsplit, std::min<int>(16, (int)ceil_div(a.max_pos, 2 * AM_SK))));
+    const int kps = (int)round_up(ceil_div(a.max_pos, nsplit), AM_SK);
+    nsplit = (int)ceil_div(a.max_pos, kps);
+    if ((int64_t)a.n_tok * a.H * nsplit * (DH + 2) > cap) {
+        set_error("attention workspace too small");
+        return PB_ERR_CAPACITY;
+    }
+    constexpr size_t smem = attn_mma_smem<DH>();
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_attn_mma<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    return launch_pdl(k_attn_mma<DH>, dim3(a.H, n_groups, nsplit), dim3((AM_WARPS + 1) * 32), smem, st, a, nsplit,
+                      kps);
+}
+
+template int run_attn_mma<64>(const AttnArgs&, int, int64_t, cudaStream_t);
+template int run_attn_mma<128>(const AttnArgs&, int, int64_t, cudaStream_t);
+
+}  // namespace pb

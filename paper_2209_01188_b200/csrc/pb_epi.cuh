@@ -34,7 +34,8 @@ __device__ __forceinline__ float epi_store(const Epi& e, int tok, int o, float v
             const int seq = e.tok_seq[tok], pos = e.tok_pos[tok];
             const int page = e.pages[(int64_t)seq * e.max_pages + pos / e.P];
             const int slot = pos % e.P;
-            e.kv[((((int64_t)page * 2 + part) * e.H + h) * e.P + slot) * e.dh + dd] = __float2half_rn(v);
+            const int ddp = kv_swizzled(e.dh) ? ((((dd >> 3) ^ (slot & 7)) << 3) | (dd & 7)) : dd;
+            e.kv[((((int64_t)page * 2 + part) * e.H + h) * e.P + slot) * e.dh + ddp] = __float2half_rn(v);
         }
     }
     return v;

@@ -753,18 +753,23 @@ int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, i
                 cudaStream_t st) {
     static int cfg = -1;
     if (cfg < 0) {
-        const char* e = getenv("PB_GEMV_CFG");  // tuning knob: 0 = 2x4, 1 = 4x4, 2 = 2x8, 3 = 4x6
-        cfg = e ? atoi(e) : 0;
+        // tuning knob (k tiles per stage x stages): 0 = 2x4, 1 = 4x4 (default), 2 = 2x8, 3 = 4x6,
+        // 4 = 8x3, 5 = 4x3, 6 = 8x2
+        const char* e = getenv("PB_GEMV_CFG");
+        cfg = e ? atoi(e) : 1;
     }
     switch (act.tc / 4) {
         case 1:
             switch (cfg) {
-                case 1: return sk_launch<1, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
+                case 0: return sk_launch<1, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
                 case 2: return sk_launch<1, 2, 8>(m, act, epi, partials, counters, partial_cap, st);
                 case 3: return sk_launch<1, 4, 6>(m, act, epi, partials, counters, partial_cap, st);
-                default: return sk_launch<1, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
+                case 4: return sk_launch<1, 8, 3>(m, act, epi, partials, counters, partial_cap, st);
+                case 5: return sk_launch<1, 4, 3>(m, act, epi, partials, counters, partial_cap, st);
+                case 6: return sk_launch<1, 8, 2>(m, act, epi, partials, counters, partial_cap, st);
+                default: return sk_launch<1, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
             }
-        case 2: return sk_launch<2, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
+        case 2: return sk_launch<2, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
         case 4: return sk_launch<4, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
         case 8: return sk_launch<8, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
         default: set_error("bad column tile"); return PB_ERR_GENERIC;

@@ -44,6 +44,8 @@ struct pb_span {
     float* attn_part = nullptr;
     int64_t attn_cap = 0;
     int32_t *d_tok_seq = nullptr, *d_tok_pos = nullptr, *d_pages = nullptr;
+    int32_t *d_grp_first = nullptr, *d_grp_count = nullptr;
+    int n_groups = 0;
     static constexpr int NSLOT = 4;  // ring of pinned staging buffers (no host sync per step)
     int32_t* h_meta[NSLOT] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t meta_ev[NSLOT] = {nullptr, nullptr, nullptr, nullptr};
@@ -104,7 +106,7 @@ void free_span(pb_span* s) {
         for (auto* p : b.bias) cudaFree(p);
     }
     void* ptrs[] = {s->kv, s->slopes, s->xa, s->mid, s->q, s->ctx, s->act, s->xo, s->y32, s->frag, s->bcanon, s->back, s->stats, s->pst_x, s->pst_mid, s->tokmax_ctx, s->tokmax_act,
-                    s->partials, s->counters, s->attn_part, s->d_tok_seq, s->d_tok_pos, s->d_pages,
+                    s->partials, s->counters, s->attn_part, s->d_tok_seq, s->d_tok_pos, s->d_pages, s->d_grp_first, s->d_grp_count,
                     s->hop_codes, s->hop_scales};
     for (void* p : ptrs) cudaFree(p);
     for (int i = 0; i < pb_span::NSLOT; ++i) {
@@ -188,10 +190,12 @@ int pb_span_create(const pb_span_config* cfg, pb_span** out) {
     if (!rc) rc = dalloc(s, &s->counters, 1 << 20);
     s->attn_cap = attention_part_floats(NT, s->H, s->dh, cfg->max_seq);
     if (!rc) rc = dalloc(s, &s->attn_part, s->attn_cap);
-    s->meta_ints = 2 * (int64_t)NT + (int64_t)cfg->max_seqs * s->max_pages;
+    s->meta_ints = 4 * (int64_t)NT + (int64_t)cfg->max_seqs * s->max_pages;
     if (!rc) rc = dalloc(s, &s->d_tok_seq, NT);
     if (!rc) rc = dalloc(s, &s->d_tok_pos, NT);
     if (!rc) rc = dalloc(s, &s->d_pages, (int64_t)cfg->max_seqs * s->max_pages);
+    if (!rc) rc = dalloc(s, &s->d_grp_first, NT);
+    if (!rc) rc = dalloc(s, &s->d_grp_count, NT);
     if (!rc) rc = dalloc(s, &s->hop_codes, (int64_t)NT * d);
     if (!rc) rc = dalloc(s, &s->hop_scales, ceil_div((int64_t)NT * d, 64));
     for (int i = 0; !rc && i < pb_span::NSLOT; ++i) {
@@ -451,7 +455,8 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
         // ---- attention (+ operand range of wo)
         AttnArgs aa{s->q, kvb, s->d_tok_seq, s->d_tok_pos, s->d_pages, s->slopes, s->ctx, s->attn_part,
                     s->counters + (1 << 19), int8 ? s->tokmax_ctx : nullptr, int8 ? b.mat[1].scales : nullptr,
-                    n_tok, s->max_pages, s->H, s->dh, s->cfg.page_tokens, d, max_pos, s->last_n_seq == n_tok ? 1 : 0};
+                    n_tok, s->max_pages, s->H, s->dh, s->cfg.page_tokens, d, max_pos, s->last_n_seq == n_tok ? 1 : 0,
+                    s->d_grp_first, s->d_grp_count, s->n_groups};
         {
             const int ev = prof_begin(s, st);
             if (int rc = launch_attention(aa, s->attn_cap, st)) return rc;
@@ -528,6 +533,22 @@ static int stage_meta(pb_span* s, int n_tok, int n_seq, const int32_t* tok_seq, 
     PB_CHECK_CUDA(cudaMemcpyAsync(s->d_tok_pos, hm + n_tok, sizeof(int32_t) * n_tok, cudaMemcpyHostToDevice, st));
     PB_CHECK_CUDA(cudaMemcpyAsync(s->d_pages, hm + 2 * n_tok, sizeof(int32_t) * (size_t)n_seq * s->max_pages,
                                   cudaMemcpyHostToDevice, st));
+    // attention query groups: up to 8 consecutive positions of one sequence
+    int32_t* gf = hm + 2 * n_tok + (size_t)n_seq * s->max_pages;
+    int32_t* gc = gf + n_tok;
+    int ng = 0;
+    for (int i = 0; i < n_tok; ++i) {
+        if (ng > 0 && tok_seq[i] == tok_seq[i - 1] && tok_pos[i] == tok_pos[i - 1] + 1 && gc[ng - 1] < 8) {
+            ++gc[ng - 1];
+        } else {
+            gf[ng] = i;
+            gc[ng] = 1;
+            ++ng;
+        }
+    }
+    s->n_groups = ng;
+    PB_CHECK_CUDA(cudaMemcpyAsync(s->d_grp_first, gf, sizeof(int32_t) * ng, cudaMemcpyHostToDevice, st));
+    PB_CHECK_CUDA(cudaMemcpyAsync(s->d_grp_count, gc, sizeof(int32_t) * ng, cudaMemcpyHostToDevice, st));
     PB_CHECK_CUDA(cudaEventRecord(s->meta_ev[slot], st));
     return PB_OK;
 }

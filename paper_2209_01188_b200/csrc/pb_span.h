@@ -135,8 +135,16 @@ struct AttnArgs {
     int n_tok, max_pages, H, dh, P, d;
     int max_pos;             // max over tokens of (pos + 1)
     int decode_only;         // every sequence adds one position (older keys are safe to prefetch early)
+    const int32_t* grp_first;  // query groups: up to 8 consecutive positions of one sequence
+    const int32_t* grp_count;
+    int n_groups;
 };
 int launch_attention(const AttnArgs& a, int64_t part_cap, cudaStream_t st);
+template <int DH>
+int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st);
+// the tensor-core attention (head_dim 64/128) reads KV rows whose 16-byte
+// chunks are XOR-swizzled by (slot & 7); the QKV epilogue writes them so
+__host__ __device__ inline bool kv_swizzled(int dh) { return dh == 64 || dh == 128; }
 int64_t attention_part_floats(int n_tok, int H, int dh, int max_seq);
 
 }  // namespace pb
