@@ -412,8 +412,11 @@ def run_ours(args):
                      "kernel": "k_gemv_i8 (int8 GEMV, all 4 matrices of every block)",
                      "launches": g_n, "avg_launch_us": 1e3 * g_ms / max(g_n, 1),
                      "algorithmic_bytes_per_launch": g_b / max(g_n, 1), "peak_source": peak_kind},
-        "step_roofline": {"bytes_per_step": w_bytes + kv_bytes / S, "sequential_frac": seq_ceiling / step_s,
-                          "aggregate_frac": agg_ceiling / step_s * (1 if N == 1 else 1),
+        # sequential: one session's step latency (each session stepped K times in the timed
+        # region) vs all of its bytes through one GPU; aggregate: job throughput vs every GPU
+        # streaming its own span's bytes for every micro-batch step
+        "step_roofline": {"bytes_per_step": w_bytes + kv_bytes / S, "sequential_frac": seq_ceiling / (ms_max / 1e3 / K),
+                          "aggregate_frac": agg_ceiling / step_s,
                           "kernel_share": {"gemv": g_ms / ms_max, "attention": attn[0] / ms_max,
                                            "prologue": pro[0] / ms_max, "codec": codec_p[0] / ms_max}},
         "gpu_launches": launches,

@@ -15,6 +15,8 @@
  *   pb_span_* weights        <- quant.py:81-108,132-149 quantize_weights_int8 / QuantizedBlockWeights.from_block
  *   pb_span_step             <- model.py:314-380 block_forward looped over a span as in server.py:383-385,
  *                               batched over sessions; KV caches = server.py:69-77 _Session.caches
+ *   pb_head_*                <- model.py:421-446 embed / lm_head / sample_next("greedy"), the client side of
+ *                               client.py:247-250
  */
 #ifndef PETALS_B200_H
 #define PETALS_B200_H
@@ -134,6 +136,32 @@ int32_t pb_span_last_launches(const pb_span* span);
  * device time (ms), launch count and algorithmic bytes of one kind. */
 int pb_span_profile(pb_span* span, int32_t on);
 int pb_span_profile_read(pb_span* span, int32_t kind, double* ms, int64_t* launches, double* bytes);
+
+/* ---- client head: embedding, final LayerNorm + tied LM head, greedy ---- */
+typedef struct pb_head pb_head;
+
+/* vocab x hidden embedding (f32, kept for lookups and exact rescoring) plus an
+ * int8 copy of its transpose for the approximate-logit pass; max_tokens <= 32
+ * hidden rows per call. */
+int pb_head_create(int32_t vocab, int32_t hidden, int32_t max_tokens, int32_t device, pb_head** out);
+int pb_head_destroy(pb_head* head);
+int64_t pb_head_device_bytes(const pb_head* head);
+/* gen_checkpoint embed (model.py:190, stream key = seed ^ fnv1a64("embed")), final LN gamma 1 / beta 0 */
+int pb_head_gen(pb_head* head, uint64_t key_embed, void* stream);
+/* embed [vocab, hidden] f32, final_ln gamma/beta [hidden] f32 (device pointers) */
+int pb_head_load(pb_head* head, const float* d_embed, const float* d_gamma, const float* d_beta, void* stream);
+/* model.py:421-425: out[i] = embed[tokens[i]]; host token ids, range-checked (PB_ERR_BAD_REQUEST) */
+int pb_head_embed(pb_head* head, const int32_t* h_tokens, int32_t n, float* d_out, void* stream);
+/* same with device token ids (already validated, e.g. from pb_head_greedy) */
+int pb_head_embed_device(pb_head* head, const int32_t* d_tokens, int32_t n, float* d_out, void* stream);
+/* model.py:428-433: logits [n, vocab] f32 = LN_f(hidden) @ embed^T (f64 accumulation, rounded to f32) */
+int pb_head_logits(pb_head* head, const float* d_hidden, int32_t n, float* d_logits, void* stream);
+/* model.py:445-446 greedy sample_next of every row: argmax of the exact logits, lowest index on ties,
+ * via int8 approximate logits + rigorous error bound + f64 rescoring of the candidates.
+ * d_tokens[i] = -1 marks non-finite logits (model.py:442-443 InputError). If d_next_embed is not
+ * NULL the chosen tokens' embedding rows are written there (the next step's input). */
+int pb_head_greedy(pb_head* head, const float* d_hidden, int32_t n, int32_t* d_tokens, float* d_next_embed,
+                   void* stream);
 
 #ifdef __cplusplus
 }

@@ -20,7 +20,8 @@ EXPORTS = [
     "pb_last_error", "pb_version", "pb_quantize_blockwise", "pb_dequantize_blockwise", "pb_gen_tensor",
     "pb_span_create", "pb_span_destroy", "pb_span_device_bytes", "pb_span_gen_block", "pb_span_load_block",
     "pb_span_outliers", "pb_span_read_codes", "pb_span_step", "pb_span_step_int8", "pb_span_last_launches",
-    "pb_span_profile", "pb_span_profile_read",
+    "pb_span_profile", "pb_span_profile_read", "pb_head_create", "pb_head_destroy", "pb_head_device_bytes",
+    "pb_head_gen", "pb_head_load", "pb_head_embed", "pb_head_embed_device", "pb_head_logits", "pb_head_greedy",
 ]
 
 
@@ -60,6 +61,14 @@ def lib() -> C.CDLL:
         "pb_span_step_int8": [P, I32, I32, P, P, P, P, P, P, P, P, P, VP],
         "pb_span_profile": [P, I32],
         "pb_span_profile_read": [P, I32, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double)],
+        "pb_head_create": [I32, I32, I32, I32, C.POINTER(C.c_void_p)],
+        "pb_head_destroy": [P],
+        "pb_head_gen": [P, U64, VP],
+        "pb_head_load": [P, P, P, P, VP],
+        "pb_head_embed": [P, P, I32, P, VP],
+        "pb_head_embed_device": [P, P, I32, P, VP],
+        "pb_head_logits": [P, P, I32, P, VP],
+        "pb_head_greedy": [P, P, I32, P, P, VP],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -67,6 +76,8 @@ def lib() -> C.CDLL:
         fn.restype = C.c_int
     L.pb_span_device_bytes.argtypes = [P]
     L.pb_span_device_bytes.restype = C.c_int64
+    L.pb_head_device_bytes.argtypes = [P]
+    L.pb_head_device_bytes.restype = C.c_int64
     L.pb_span_last_launches.argtypes = [P]
     L.pb_span_last_launches.restype = C.c_int32
     _lib = L

@@ -2,9 +2,10 @@
 // for head_dim 64 / 128: decode (one query per session) and prefill (up to 8
 // consecutive queries of one sequence per CTA, so K/V are read once per group).
 //
-// CTA = (head, query group, key split); warp 4 streams the split's K/V rows
-// (page pieces, cp.async.bulk on an mbarrier ring of 64-key stages); each of
-// warps 0-3 owns 16 keys of every stage and keeps its own online softmax:
+// Stream-K grid (see k_attn_mma): each CTA owns an equal run of (query group,
+// head, 64-key stage) units; warp 4 streams their K/V rows (page pieces,
+// cp.async.bulk on an mbarrier ring of 64-key stages); each of warps 0-3 owns
+// 16 keys of every stage and keeps its own online softmax:
 //   S = [Q_hi; Q_lo] K^T   mma.m16n8k16: rows g = query g hi, g+8 = query g lo
 //                          (fp32-accurate scores: q split hi/lo, K exact fp16),
 //                          K fragments via ldmatrix (B operand = K row-major);
@@ -15,7 +16,10 @@
 // The KV cache rows are stored with their 16-byte chunks XOR-swizzled by
 // (slot & 7) (written that way by the QKV epilogue), so the ldmatrix row
 // gathers are bank-conflict free after a linear bulk copy.
-// Splits are merged in split order by the last CTA of (group, head).
+// The pieces of a (group, head) split across CTAs are merged in CTA order by
+// the last contributor.
+#include <algorithm>
+
 #include "pb_async.cuh"
 #include "pb_common.cuh"
 #include "pb_span.h"
@@ -26,6 +30,7 @@ constexpr int AM_SK = 64;    // keys per stage
 constexpr int AM_ST = 3;     // stages in flight
 constexpr int AM_WARPS = 4;  // compute warps, 16 keys each per stage
 constexpr int AM_G = 8;      // queries per group
+constexpr int AM_MAXC = 16;  // max CTAs contributing to one (group, head): split workspace slots
 
 __device__ __forceinline__ int kv_chunk_swz(int chunk, int slot) { return chunk ^ (slot & 7); }
 
@@ -61,8 +66,53 @@ constexpr size_t attn_mma_smem() {
     return (size_t)AM_ST * 2 * AM_SK * DH * 2 + (size_t)AM_WARPS * AM_G * (DH + 2) * 4 + 2 * AM_ST * 8 + 64;
 }
 
+__device__ __forceinline__ void cons_bar() {  // the AM_WARPS compute warps only
+    asm volatile("bar.sync 1, %0;" ::"n"(AM_WARPS * 32) : "memory");
+}
+
+// Stream-K decomposition: the work units are (query group, head, 64-key
+// stage), numbered group-major (unit_base[g] = first unit of group g, every
+// head of group g has ns_g = (unit_base[g+1] - unit_base[g]) / H stages). CTA c
+// of G owns units [c U / G, (c+1) U / G), so every CTA streams the same number
+// of K/V bytes (no wave tail) whatever the head count and context length.
+struct AmSeg {
+    int g, h, i0, n;  // group, head, first stage, stages in this CTA
+    int ns;           // stages of (g, h)
+    int64_t a;        // first unit of (g, h)
+};
+
+__device__ __forceinline__ AmSeg am_seg(const AttnArgs& a, int64_t u, int64_t u1) {
+    int lo = 0, hi = a.n_groups - 1;  // largest g with unit_base[g] <= u
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a.unit_base[mid] <= u) lo = mid;
+        else hi = mid - 1;
+    }
+    AmSeg s;
+    s.g = lo;
+    const int64_t b0 = a.unit_base[lo];
+    s.ns = (int)((a.unit_base[lo + 1] - b0) / a.H);
+    const int64_t r = u - b0;
+    s.h = (int)(r / s.ns);
+    s.i0 = (int)(r % s.ns);
+    s.a = b0 + (int64_t)s.h * s.ns;
+    const int64_t left = u1 - u;
+    s.n = left < (int64_t)(s.ns - s.i0) ? (int)left : s.ns - s.i0;
+    return s;
+}
+
+__device__ __forceinline__ int am_owner(int64_t u, int G, int64_t U) { return (int)(((u + 1) * G - 1) / U); }
+
+// ctx of query t0 + g (head h) from merged state (M, L, O) + the wo operand range
 template <int DH>
-__global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, int nsplit, int kps) {
+__device__ __forceinline__ float am_final(const AttnArgs& a, int tok, int h, int e, float o, float L) {
+    const float c = o / L;
+    a.ctx[(int64_t)tok * a.d + h * DH + e] = c;
+    return a.tokmax ? fabsf(c * a.s_next[h * DH + e]) : 0.f;
+}
+
+template <int DH>
+__global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, int G, int64_t U) {
     constexpr int NKT = DH / 16;  // k-steps of S
     constexpr int NNT = DH / 8;   // n-tiles of O
     constexpr int ROWB = DH * 2;  // bytes per K/V row
@@ -74,17 +124,10 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
     uint64_t* empty = full + AM_ST;
     int* s_flag = reinterpret_cast<int*>(empty + AM_ST);
 
-    const int h = blockIdx.x, grp = blockIdx.y, split = blockIdx.z;
+    const int c = blockIdx.x;
+    const int64_t u0 = (int64_t)c * U / G, u1 = (int64_t)(c + 1) * U / G;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int t0 = a.grp_first[grp], nq = a.grp_count[grp];
-    const int seq = a.tok_seq[t0], pos0 = a.tok_pos[t0];
-    const int posL = pos0 + nq - 1;
-    const int j0 = split * kps;
-    const int j1 = min(j0 + kps, posL + 1);
-    const int32_t* pt = a.pages + (int64_t)seq * a.max_pages;
-    const int64_t head_off = (int64_t)h * a.P * DH;
     const int64_t kv_stride = (int64_t)a.H * a.P * DH;
-    const int nst = j0 < j1 ? (j1 - j0 + AM_SK - 1) / AM_SK : 0;
 
     if (threadIdx.x == 0) {
         for (int b = 0; b < AM_ST; ++b) {
@@ -96,56 +139,82 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
     __syncthreads();
 
     if (warp == AM_WARPS) {
-        // ---------------- producer warp (older keys may be streamed before the QKV GEMV completes)
-        const int safe_end = a.decode_only ? pos0 : j0;
+        // ---------------- producer warp: K/V page pieces of every stage of the range.
+        // In a pure decode step the keys before each query's own position were
+        // written by earlier steps: stream them while the QKV GEMV (PDL
+        // predecessor) is still finishing; wait before the newest key.
         bool waited = false;
-        for (int i = 0; i < nst; ++i) {
-            const int b = i % AM_ST;
-            mbar_wait(&empty[b], ((i / AM_ST) & 1) ^ 1);
-            const int k0 = j0 + i * AM_SK;
-            const int k1 = min(j1, k0 + AM_SK);
-            if (!waited && k1 > safe_end) {
-                pdl_wait();
-                pdl_trigger();
-                waited = true;
-            }
-            if (lane == 0) {
-                mbar_expect_tx(&full[b], (uint32_t)(k1 - k0) * ROWB * 2);
-                for (int j = k0; j < k1;) {
-                    const int page = pt[j / a.P];
-                    const int jn = min(k1, (j / a.P + 1) * a.P);
-                    const half* kp = a.kv + (int64_t)page * 2 * kv_stride + head_off + (int64_t)(j % a.P) * DH;
-                    const uint32_t bytes = (uint32_t)(jn - j) * ROWB;
-                    bulk_g2s(Ks + ((int64_t)b * AM_SK + (j - k0)) * DH, kp, bytes, &full[b]);
-                    bulk_g2s(Vs + ((int64_t)b * AM_SK + (j - k0)) * DH, kp + kv_stride, bytes, &full[b]);
-                    j = jn;
+        int it = 0;
+        for (int64_t u = u0; u < u1;) {
+            const AmSeg sg = am_seg(a, u, u1);
+            const int t0 = a.grp_first[sg.g], nq = a.grp_count[sg.g];
+            const int pos0 = a.tok_pos[t0];
+            const int jend = pos0 + nq;  // keys [0, jend)
+            const int safe_end = a.decode_only ? pos0 : 0;
+            const int32_t* pt = a.pages + (int64_t)a.tok_seq[t0] * a.max_pages;
+            const int64_t head_off = (int64_t)sg.h * a.P * DH;
+            for (int i = sg.i0; i < sg.i0 + sg.n; ++i, ++it) {
+                const int b = it % AM_ST;
+                mbar_wait(&empty[b], ((it / AM_ST) & 1) ^ 1);
+                const int k0 = i * AM_SK;
+                const int k1 = min(jend, k0 + AM_SK);
+                if (!waited && k1 > safe_end) {
+                    pdl_wait();
+                    pdl_trigger();
+                    waited = true;
+                }
+                if (lane == 0) {
+                    mbar_expect_tx(&full[b], (uint32_t)(k1 - k0) * ROWB * 2);
+                    for (int j = k0; j < k1;) {
+                        const int page = pt[j / a.P];
+                        const int jn = min(k1, (j / a.P + 1) * a.P);
+                        const half* kp = a.kv + (int64_t)page * 2 * kv_stride + head_off + (int64_t)(j % a.P) * DH;
+                        const uint32_t bytes = (uint32_t)(jn - j) * ROWB;
+                        bulk_g2s(Ks + ((int64_t)b * AM_SK + (j - k0)) * DH, kp, bytes, &full[b]);
+                        bulk_g2s(Vs + ((int64_t)b * AM_SK + (j - k0)) * DH, kp + kv_stride, bytes, &full[b]);
+                        j = jn;
+                    }
                 }
             }
+            u += sg.n;
         }
         if (!waited) {
             pdl_wait();
             pdl_trigger();
         }
-    } else {
-        // ---------------- compute warps
-        pdl_wait();
-        pdl_trigger();
-        const int g = lane >> 2, qd = lane & 3;
+        return;
+    }
+
+    // ---------------- compute warps
+    pdl_wait();
+    pdl_trigger();
+    const int g = lane >> 2, qd = lane & 3;
+    const uint32_t ks_base = smem_u32(Ks), vs_base = smem_u32(Vs);
+    const int mi = lane >> 3, ri = lane & 7;  // ldmatrix lane roles: matrix mi, row ri
+    const float isq = 1.0f / sqrtf((float)DH);
+    int it = 0;
+    for (int64_t u = u0; u < u1;) {
+        const AmSeg sg = am_seg(a, u, u1);
+        const int h = sg.h;
+        const int t0 = a.grp_first[sg.g], nq = a.grp_count[sg.g];
+        const int pos0 = a.tok_pos[t0];
+        const int j1 = pos0 + nq;
         const bool qv = g < nq;
         const int my_pos = pos0 + g;
         // Q fragments (A operand): rows g (hi) / g+8 (lo) of query g, scaled by 1/sqrt(dh)
         uint32_t qa[NKT][4];
         {
-            const float isq = 1.0f / sqrtf((float)DH);
             const float* q = a.q + (int64_t)(t0 + (qv ? g : 0)) * a.d + h * DH;
 #pragma unroll
             for (int ks = 0; ks < NKT; ++ks) {
                 float x0 = 0.f, x1 = 0.f, x2 = 0.f, x3 = 0.f;
                 if (qv) {
-                    x0 = q[ks * 16 + 2 * qd] * isq;
-                    x1 = q[ks * 16 + 2 * qd + 1] * isq;
-                    x2 = q[ks * 16 + 2 * qd + 8] * isq;
-                    x3 = q[ks * 16 + 2 * qd + 9] * isq;
+                    const float2 v01 = *reinterpret_cast<const float2*>(q + ks * 16 + 2 * qd);
+                    const float2 v23 = *reinterpret_cast<const float2*>(q + ks * 16 + 2 * qd + 8);
+                    x0 = v01.x * isq;
+                    x1 = v01.y * isq;
+                    x2 = v23.x * isq;
+                    x3 = v23.y * isq;
                 }
                 split_h2(x0, x1, qa[ks][0], qa[ks][1]);  // a0a1 (row g) hi, a2a3 (row g+8) lo
                 split_h2(x2, x3, qa[ks][2], qa[ks][3]);  // a4a5 hi, a6a7 lo
@@ -158,21 +227,18 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
         for (int n = 0; n < NNT; ++n)
 #pragma unroll
             for (int r = 0; r < 4; ++r) o[n][r] = 0.f;
-        const uint32_t ks_base = smem_u32(Ks), vs_base = smem_u32(Vs);
-        // ldmatrix lane roles: matrix mi = lane / 8, row ri = lane % 8
-        const int mi = lane >> 3, ri = lane & 7;
-        for (int i = 0; i < nst; ++i) {
-            const int b = i % AM_ST;
-            const int k0 = j0 + i * AM_SK;
-            mbar_wait(&full[b], (i / AM_ST) & 1);
+        for (int i = sg.i0; i < sg.i0 + sg.n; ++i, ++it) {
+            const int b = it % AM_ST;
+            const int k0 = i * AM_SK;
+            mbar_wait(&full[b], (it / AM_ST) & 1);
             const int kb = warp * 16;  // this warp's 16 keys of the stage
             if (k0 + kb + 16 > j1) {
                 // partial last stage: rows past the range hold stale smem; P is 0
                 // there but 0 * NaN would poison O, so clear this warp's V rows
                 for (int idx = lane; idx < 16 * (DH / 8); idx += 32) {
-                    const int r = idx / (DH / 8), c = idx % (DH / 8);
+                    const int r = idx / (DH / 8), cc = idx % (DH / 8);
                     if (k0 + kb + r >= j1)
-                        *reinterpret_cast<uint4*>(Vs + ((int64_t)(b * AM_SK + kb + r)) * DH + c * 8) =
+                        *reinterpret_cast<uint4*>(Vs + ((int64_t)(b * AM_SK + kb + r)) * DH + cc * 8) =
                             make_uint4(0u, 0u, 0u, 0u);
                 }
                 __syncwarp();
@@ -250,7 +316,7 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[b]);
         }
-        // per-warp state for query g: m, l, O[dims] = hi rows + lo rows
+        // ---- per-warp state for query g: m, l, O[dims] = hi rows + lo rows
         if (qv) {
             float* w = wst + (warp * AM_G + g) * (DH + 2);
             if (qd == 0) {
@@ -263,83 +329,91 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
                 w[2 + n * 8 + 2 * qd + 1] = o[n][1] + o[n][3];
             }
         }
-    }
-    __syncthreads();
-    // ---- merge the 4 warps per query (fixed order) -> split partials
-    for (int g = 0; g < nq; ++g) {
-        float M = -INFINITY;
+        cons_bar();
+        // ---- merge the 4 warps per query (fixed order); this CTA's piece of (g, h)
+        const int cf = am_owner(sg.a, G, U), cl = am_owner(sg.a + sg.ns - 1, G, U);
+        const int tid = threadIdx.x;  // 0 .. 127
+        float mloc[AM_G];
 #pragma unroll
-        for (int w = 0; w < AM_WARPS; ++w) M = fmaxf(M, wst[(w * AM_G + g) * (DH + 2)]);
-        float sw[AM_WARPS];
-        float L = 0.f;
+        for (int q = 0; q < AM_G; ++q) mloc[q] = 0.f;
+        for (int q = 0; q < nq; ++q) {
+            float M = -INFINITY;
 #pragma unroll
-        for (int w = 0; w < AM_WARPS; ++w) {
-            const float mw = wst[(w * AM_G + g) * (DH + 2)];
-            sw[w] = mw == -INFINITY ? 0.f : expf(mw - M);
-            L += wst[(w * AM_G + g) * (DH + 2) + 1] * sw[w];
-        }
-        float* out = a.part + (((int64_t)(t0 + g) * a.H + h) * nsplit + split) * (DH + 2);
-        for (int e = threadIdx.x; e < DH; e += blockDim.x) {
-            float acc = 0.f;
+            for (int w = 0; w < AM_WARPS; ++w) M = fmaxf(M, wst[(w * AM_G + q) * (DH + 2)]);
+            float sw[AM_WARPS];
+            float L = 0.f;
 #pragma unroll
-            for (int w = 0; w < AM_WARPS; ++w) acc += wst[(w * AM_G + g) * (DH + 2) + 2 + e] * sw[w];
-            out[2 + e] = acc;
-        }
-        if (threadIdx.x == 0) {
-            out[0] = M;
-            out[1] = L;
-        }
-    }
-    // ---- last CTA of (group, head) merges the splits in split order
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int* ctr = a.counters + (int64_t)t0 * a.H + h;
-        const int prev = atomicAdd(ctr, 1);
-        const int last = prev == nsplit - 1;
-        if (last) *ctr = 0;
-        *s_flag = last;
-    }
-    __syncthreads();
-    if (!*s_flag) return;
-    __threadfence();
-    float mloc[AM_G];
-    for (int g = 0; g < nq; ++g) {
-        const int tok = t0 + g;
-        const float* pp = a.part + ((int64_t)tok * a.H + h) * nsplit * (DH + 2);
-        float M = -INFINITY;
-        for (int s = 0; s < nsplit; ++s) M = fmaxf(M, __ldcg(pp + s * (DH + 2)));
-        float L = 0.f;
-        for (int s = 0; s < nsplit; ++s) {
-            const float ms = __ldcg(pp + s * (DH + 2));
-            if (ms != -INFINITY) L += __ldcg(pp + s * (DH + 2) + 1) * expf(ms - M);
-        }
-        float ml = 0.f;
-        for (int e = threadIdx.x; e < DH; e += blockDim.x) {
-            float acc = 0.f;
-            for (int s = 0; s < nsplit; ++s) {
-                const float ms = __ldcg(pp + s * (DH + 2));
-                if (ms != -INFINITY) acc += __ldcg(pp + s * (DH + 2) + 2 + e) * expf(ms - M);
+            for (int w = 0; w < AM_WARPS; ++w) {
+                const float mw = wst[(w * AM_G + q) * (DH + 2)];
+                sw[w] = mw == -INFINITY ? 0.f : expf(mw - M);
+                L += wst[(w * AM_G + q) * (DH + 2) + 1] * sw[w];
             }
-            const float c = acc / L;
-            a.ctx[(int64_t)tok * a.d + h * DH + e] = c;
-            if (a.tokmax) ml = fmaxf(ml, fabsf(c * a.s_next[h * DH + e]));
+            float* out = a.part + (((int64_t)(t0 + q) * a.H + h) * AM_MAXC + (c - cf)) * (DH + 2);
+            for (int e = tid; e < DH; e += AM_WARPS * 32) {
+                float acc = 0.f;
+#pragma unroll
+                for (int w = 0; w < AM_WARPS; ++w) acc += wst[(w * AM_G + q) * (DH + 2) + 2 + e] * sw[w];
+                if (cf == cl) mloc[q] = fmaxf(mloc[q], am_final<DH>(a, t0 + q, h, e, acc, L));
+                else out[2 + e] = acc;
+            }
+            if (cf != cl && tid == 0) {
+                out[0] = M;
+                out[1] = L;
+            }
         }
-        mloc[g] = ml;
-    }
-    if (a.tokmax) {
-        float* red = wst;  // reuse (all warps are past the merge)
-        __syncthreads();
-        for (int g = 0; g < nq; ++g) {
-            float v = warp_max(mloc[g]);
-            if (lane == 0) red[g * 8 + warp] = v;
+        bool finalize = cf == cl;
+        if (!finalize) {
+            // ---- last contributor of (g, h) merges the pieces in CTA order
+            __threadfence();
+            cons_bar();
+            if (tid == 0) {
+                int* ctr = a.counters + (int64_t)t0 * a.H + h;
+                const int prev = atomicAdd(ctr, 1);
+                const int last = prev == cl - cf;
+                if (last) *ctr = 0;
+                *s_flag = last;
+            }
+            cons_bar();
+            finalize = *s_flag != 0;
+            if (finalize) {
+                __threadfence();
+                const int np = cl - cf + 1;
+                for (int q = 0; q < nq; ++q) {
+                    const float* pp = a.part + ((int64_t)(t0 + q) * a.H + h) * AM_MAXC * (DH + 2);
+                    float M = -INFINITY;
+                    for (int s = 0; s < np; ++s) M = fmaxf(M, __ldcg(pp + s * (DH + 2)));
+                    float L = 0.f;
+                    for (int s = 0; s < np; ++s) {
+                        const float ms = __ldcg(pp + s * (DH + 2));
+                        if (ms != -INFINITY) L += __ldcg(pp + s * (DH + 2) + 1) * expf(ms - M);
+                    }
+                    for (int e = tid; e < DH; e += AM_WARPS * 32) {
+                        float acc = 0.f;
+                        for (int s = 0; s < np; ++s) {
+                            const float ms = __ldcg(pp + s * (DH + 2));
+                            if (ms != -INFINITY) acc += __ldcg(pp + s * (DH + 2) + 2 + e) * expf(ms - M);
+                        }
+                        mloc[q] = fmaxf(mloc[q], am_final<DH>(a, t0 + q, h, e, acc, L));
+                    }
+                }
+            }
         }
-        __syncthreads();
-        if (threadIdx.x < nq) {
-            float v = 0.f;
-            for (int w = 0; w <= AM_WARPS; ++w) v = fmaxf(v, red[threadIdx.x * 8 + w]);
-            atomicMax(reinterpret_cast<int*>(a.tokmax) + t0 + threadIdx.x, __float_as_int(v));
+        cons_bar();  // wst free; every warp past the merge
+        if (finalize && a.tokmax) {
+            // operand range of the wo GEMV: exact, order-independent max per token
+            for (int q = 0; q < nq; ++q) {
+                const float v = warp_max(mloc[q]);
+                if (lane == 0) wst[q * 8 + warp] = v;
+            }
+            cons_bar();
+            if (tid < nq) {
+                float v = 0.f;
+                for (int w = 0; w < AM_WARPS; ++w) v = fmaxf(v, wst[tid * 8 + w]);
+                atomicMax(reinterpret_cast<int*>(a.tokmax) + t0 + tid, __float_as_int(v));
+            }
+            cons_bar();
         }
+        u += sg.n;
     }
 }
 
@@ -348,11 +422,16 @@ int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st) 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int nsplit = (int)ceil_div(2 * sms, (int64_t)n_groups * a.H);
-    nsplit = std::max(1, std::min<int>(nsplit, std::min<int>(16, (int)ceil_div(a.max_pos, 2 * AM_SK))));
-    const int kps = (int)round_up(ceil_div(a.max_pos, nsplit), AM_SK);
-    nsplit = (int)ceil_div(a.max_pos, kps);
-    if ((int64_t)a.n_tok * a.H * nsplit * (DH + 2) > cap) {
+    static const int per_sm = [] {
+        const char* e = getenv("PB_ATTM_CTAS");  // tuning knob: CTAs per SM (smem allows 2)
+        return e ? atoi(e) : 2;
+    }();
+    const int64_t U = a.total_units;
+    if (U <= 0) return PB_OK;
+    // CTAs: fill the machine, but keep every (group, head) within AM_MAXC contributors
+    int64_t G = std::min<int64_t>(U, (int64_t)per_sm * sms);
+    while (G > 1 && ceil_div(a.max_stages, U / G) + 1 > AM_MAXC) --G;
+    if ((int64_t)a.n_tok * a.H * AM_MAXC * (DH + 2) > cap) {
         set_error("attention workspace too small");
         return PB_ERR_CAPACITY;
     }
@@ -362,8 +441,8 @@ int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st) 
         cudaFuncSetAttribute(k_attn_mma<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    return launch_pdl(k_attn_mma<DH>, dim3(a.H, n_groups, nsplit), dim3((AM_WARPS + 1) * 32), smem, st, a, nsplit,
-                      kps);
+    (void)n_groups;
+    return launch_pdl(k_attn_mma<DH>, dim3((unsigned)G), dim3((AM_WARPS + 1) * 32), smem, st, a, (int)G, U);
 }
 
 template int run_attn_mma<64>(const AttnArgs&, int, int64_t, cudaStream_t);

@@ -21,6 +21,8 @@ __device__ __forceinline__ float epi_store(const Epi& e, int tok, int o, float v
     if (e.kind == EPI_RESID) {
         v = e.resid[idx] + v;
         e.out[idx] = v;
+    } else if (e.kind == EPI_PLAIN) {
+        e.out[idx] = v;
     } else if (e.kind == EPI_GELU) {
         v = gelu_tanh(v);
         e.out[idx] = v;

@@ -99,6 +99,7 @@ struct ProArgs {
     float* xo;
     float* y32;
     ProSrc src;
+    int early;
 };
 
 __device__ __forceinline__ float pro_y(const ProArgs& a, const float* x, int k, float mu, float inv) {
@@ -265,8 +266,12 @@ int bound_consts(const float* gamma, const float* beta, const float* scales, int
 // one thread per (token, 32-wide k chunk, lane quad q).
 __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
     __shared__ float4 s_st;
+    // early trigger (default): the GEMV that consumes this operand launches while
+    // this kernel still waits for its producer and starts streaming weights
+    // (its own griddepcontrol.wait still orders it after this grid completes)
+    if (a.early) pdl_trigger();
     pdl_wait();
-    pdl_trigger();  // the GEMV that consumes this operand may launch and start streaming its weights
+    if (!a.early) pdl_trigger();
     const int tok = blockIdx.y;
     const float* x = a.x + (int64_t)tok * a.K;
     if (threadIdx.x < 32) {
@@ -381,8 +386,12 @@ __global__ void __launch_bounds__(256) k_rows_f32(ProArgs a) {
 int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int K, int Kp, const float* gamma,
                     const float* beta, const Mat& m, int tc, uint4* frag, float* back, float4* stats, float* xo,
                     float* y32, cudaStream_t st, uint8_t* bcanon) {
+    static const int early = [] {
+        const char* e = getenv("PB_FRAG_EARLY");
+        return e ? atoi(e) : 1;
+    }();
     ProArgs a{mode, x, K, Kp, gamma, beta, y32 ? nullptr : m.scales, m.n_outl, m.outl_idx, tc, frag, back, stats,
-              xo, y32, src};
+              xo, y32, src, early};
     if (y32) a.src = ProSrc{};
     if (a.src.kind == SRC_STATS && (mode == PRO_LN || !y32)) {
         k_rowstats<<<n_tok, STATS_THREADS, 0, st>>>(a);
@@ -730,6 +739,9 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
         cudaFuncSetAttribute(k_gemv_i8<NT, SK_KCS, SK_STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_gemv_i8<NT, SK_KCS, SK_STAGES>, SK_THREADS, smem);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
+        // tuning knob: fewer CTAs per SM than fit leaves a slot for the next
+        // kernel of the chain (PDL) to become resident and start streaming
+        if (const char* e = getenv("PB_GEMV_CTAS")) blocks_per_sm = std::max(1, std::min(blocks_per_sm, atoi(e)));
     }
     SkArgs a;
     a.codes = m.codes;

@@ -46,8 +46,12 @@ struct pb_span {
     int32_t *d_tok_seq = nullptr, *d_tok_pos = nullptr, *d_pages = nullptr;
     int32_t *d_grp_first = nullptr, *d_grp_count = nullptr;
     int n_groups = 0;
+    int64_t* d_unit_base = nullptr;  // stream-K attention units per query group
+    int64_t total_units = 0;
+    int max_stages = 0;
     static constexpr int NSLOT = 4;  // ring of pinned staging buffers (no host sync per step)
     int32_t* h_meta[NSLOT] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t* h_ub[NSLOT] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t meta_ev[NSLOT] = {nullptr, nullptr, nullptr, nullptr};
     int meta_slot = 0;
     int64_t meta_ints = 0;
@@ -107,10 +111,11 @@ void free_span(pb_span* s) {
     }
     void* ptrs[] = {s->kv, s->slopes, s->xa, s->mid, s->q, s->ctx, s->act, s->xo, s->y32, s->frag, s->bcanon, s->back, s->stats, s->pst_x, s->pst_mid, s->tokmax_ctx, s->tokmax_act,
                     s->partials, s->counters, s->attn_part, s->d_tok_seq, s->d_tok_pos, s->d_pages, s->d_grp_first, s->d_grp_count,
-                    s->hop_codes, s->hop_scales};
+                    s->hop_codes, s->hop_scales, s->d_unit_base};
     for (void* p : ptrs) cudaFree(p);
     for (int i = 0; i < pb_span::NSLOT; ++i) {
         if (s->h_meta[i]) cudaFreeHost(s->h_meta[i]);
+        if (s->h_ub[i]) cudaFreeHost(s->h_ub[i]);
         if (s->meta_ev[i]) cudaEventDestroy(s->meta_ev[i]);
     }
     for (auto e : s->prof_ev) cudaEventDestroy(e);
@@ -196,10 +201,12 @@ int pb_span_create(const pb_span_config* cfg, pb_span** out) {
     if (!rc) rc = dalloc(s, &s->d_pages, (int64_t)cfg->max_seqs * s->max_pages);
     if (!rc) rc = dalloc(s, &s->d_grp_first, NT);
     if (!rc) rc = dalloc(s, &s->d_grp_count, NT);
+    if (!rc) rc = dalloc(s, &s->d_unit_base, NT + 1);
     if (!rc) rc = dalloc(s, &s->hop_codes, (int64_t)NT * d);
     if (!rc) rc = dalloc(s, &s->hop_scales, ceil_div((int64_t)NT * d, 64));
     for (int i = 0; !rc && i < pb_span::NSLOT; ++i) {
         if (cudaMallocHost((void**)&s->h_meta[i], sizeof(int32_t) * s->meta_ints) != cudaSuccess ||
+            cudaMallocHost((void**)&s->h_ub[i], sizeof(int64_t) * (NT + 1)) != cudaSuccess ||
             cudaEventCreateWithFlags(&s->meta_ev[i], cudaEventDisableTiming) != cudaSuccess) {
             set_error("pinned staging allocation failed");
             rc = PB_ERR_GENERIC;
@@ -456,7 +463,7 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
         AttnArgs aa{s->q, kvb, s->d_tok_seq, s->d_tok_pos, s->d_pages, s->slopes, s->ctx, s->attn_part,
                     s->counters + (1 << 19), int8 ? s->tokmax_ctx : nullptr, int8 ? b.mat[1].scales : nullptr,
                     n_tok, s->max_pages, s->H, s->dh, s->cfg.page_tokens, d, max_pos, s->last_n_seq == n_tok ? 1 : 0,
-                    s->d_grp_first, s->d_grp_count, s->n_groups};
+                    s->d_grp_first, s->d_grp_count, s->n_groups, s->d_unit_base, s->total_units, s->max_stages};
         {
             const int ev = prof_begin(s, st);
             if (int rc = launch_attention(aa, s->attn_cap, st)) return rc;
@@ -549,6 +556,20 @@ static int stage_meta(pb_span* s, int n_tok, int n_seq, const int32_t* tok_seq, 
     s->n_groups = ng;
     PB_CHECK_CUDA(cudaMemcpyAsync(s->d_grp_first, gf, sizeof(int32_t) * ng, cudaMemcpyHostToDevice, st));
     PB_CHECK_CUDA(cudaMemcpyAsync(s->d_grp_count, gc, sizeof(int32_t) * ng, cudaMemcpyHostToDevice, st));
+    // stream-K units of the tensor-core attention: H x ceil(keys / 64) per group
+    int64_t* ub = s->h_ub[slot];
+    int64_t tot = 0;
+    int mst = 0;
+    for (int g = 0; g < ng; ++g) {
+        ub[g] = tot;
+        const int stages = (int)ceil_div(tok_pos[gf[g]] + gc[g], 64);
+        mst = std::max(mst, stages);
+        tot += (int64_t)s->H * stages;
+    }
+    ub[ng] = tot;
+    s->total_units = tot;
+    s->max_stages = mst;
+    PB_CHECK_CUDA(cudaMemcpyAsync(s->d_unit_base, ub, sizeof(int64_t) * (ng + 1), cudaMemcpyHostToDevice, st));
     PB_CHECK_CUDA(cudaEventRecord(s->meta_ev[slot], st));
     return PB_OK;
 }

@@ -48,7 +48,7 @@ struct BlockW {
     float gs1 = 0.f, bs1 = 0.f, gs2 = 0.f, bs2 = 0.f;
 };
 
-enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_GELU = 2 };
+enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_GELU = 2, EPI_PLAIN = 3 };
 
 // Epilogue parameters shared by every GEMV/GEMM flavour.
 struct Epi {
@@ -97,6 +97,8 @@ struct ProSrc {
 
 int fill_matrix_gen(Mat& m, uint64_t key, float threshold, float boost, int every, cudaStream_t st);
 int fill_matrix_f32(Mat& m, const float* w, float threshold, cudaStream_t st);
+// same from the transposed matrix wt = W^T [M][K] row-major (the tied LM head's embedding table)
+int fill_matrix_f32_t(Mat& m, const float* wt, float threshold, cudaStream_t st);
 int untile_codes(const Mat& m, int8_t* d_out, cudaStream_t st);
 
 int quantize_blockwise(const float* x, int64_t n, int block, int8_t* codes, float* scales, cudaStream_t st);
@@ -138,6 +140,10 @@ struct AttnArgs {
     const int32_t* grp_first;  // query groups: up to 8 consecutive positions of one sequence
     const int32_t* grp_count;
     int n_groups;
+    // stream-K units of the tensor-core kernel: (group, head, 64-key stage)
+    const int64_t* unit_base;  // [n_groups + 1] first unit of each group
+    int64_t total_units;
+    int max_stages;            // max over groups of ceil(keys / 64)
 };
 int launch_attention(const AttnArgs& a, int64_t part_cap, cudaStream_t st);
 template <int DH>

@@ -40,6 +40,33 @@ struct MatSource {  // row-major f32 [K, M] on the device
     __device__ __forceinline__ float operator()(int64_t k, int64_t o) const { return w[k * M + o]; }
 };
 
+struct TransSource {  // W[k, o] = wt[o * K + k]: row-major W^T [M][K] on the device
+    const float* wt;
+    int64_t K;
+    __device__ __forceinline__ float operator()(int64_t k, int64_t o) const { return wt[o * K + k]; }
+};
+
+// column absmax of W^T (coalesced along k); non-negative floats compare as ints
+__global__ void __launch_bounds__(256) k_col_absmax_t(const float* __restrict__ wt, int64_t K, int64_t M,
+                                                      int rows_per_cta, int* __restrict__ bits) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    const int64_t o0 = (int64_t)blockIdx.y * rows_per_cta, o1 = min(M, o0 + rows_per_cta);
+    float m = 0.f;
+    for (int64_t o = o0; o < o1; ++o) m = fmaxf(m, fabsf(wt[o * K + k]));
+    atomicMax(bits + k, __float_as_int(m));
+}
+
+__global__ void k_scales_from_absmax(const int* __restrict__ bits, int64_t K, float threshold,
+                                     float* __restrict__ scales, uint8_t* __restrict__ outl) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+        const float m = __int_as_float(bits[k]);
+        const bool is_out = m > threshold;  // quant.py:90-93
+        outl[k] = is_out ? 1 : 0;
+        scales[k] = is_out ? 0.f : __fdiv_rn(m, 127.f);
+    }
+}
+
 __global__ void k_gen_tensor(uint64_t key, int64_t first, int64_t n, float* __restrict__ out) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
@@ -142,13 +169,26 @@ static int grid_n(int64_t n, int threads = 256) {
 }
 
 template <class Src>
-static int quantize_matrix(Mat& m, Src src, float threshold, cudaStream_t st) {
+static int quantize_matrix(Mat& m, Src src, float threshold, cudaStream_t st, const float* wt = nullptr) {
     const int64_t K = m.K, M = m.M, KC = m.Kp / 32, MT = m.Mp / 16;
     uint8_t* d_flags = nullptr;
     PB_CHECK_CUDA(cudaMallocAsync(&d_flags, K, st));
     PB_CHECK_CUDA(cudaMemsetAsync(m.scales, 0, sizeof(float) * m.Kp, st));
-    k_feature_absmax<Src><<<grid_n(K * 32), 256, 0, st>>>(src, K, M, threshold, m.scales, d_flags);
-    if (int rc = launch_check("feature_absmax")) return rc;
+    if (wt) {  // transposed source: coalesced column absmax
+        int* bits = nullptr;
+        PB_CHECK_CUDA(cudaMallocAsync(&bits, sizeof(int) * K, st));
+        PB_CHECK_CUDA(cudaMemsetAsync(bits, 0, sizeof(int) * K, st));
+        const int rows = 512;
+        k_col_absmax_t<<<dim3((unsigned)ceil_div(K, 256), (unsigned)ceil_div(M, rows)), 256, 0, st>>>(wt, K, M, rows,
+                                                                                                     bits);
+        if (int rc = launch_check("col_absmax_t")) return rc;
+        k_scales_from_absmax<<<grid_n(K), 256, 0, st>>>(bits, K, threshold, m.scales, d_flags);
+        if (int rc = launch_check("scales_from_absmax")) return rc;
+        PB_CHECK_CUDA(cudaFreeAsync(bits, st));
+    } else {
+        k_feature_absmax<Src><<<grid_n(K * 32), 256, 0, st>>>(src, K, M, threshold, m.scales, d_flags);
+        if (int rc = launch_check("feature_absmax")) return rc;
+    }
     k_quant_tiles<Src><<<grid_n(MT * KC * 32), 256, 0, st>>>(src, K, M, KC, MT, m.scales, m.codes);
     if (int rc = launch_check("quant_tiles")) return rc;
     std::vector<uint8_t> flags(K);
@@ -185,6 +225,11 @@ int fill_matrix_f32(Mat& m, const float* w, float threshold, cudaStream_t st) {
     if (m.int8) return quantize_matrix(m, src, threshold, st);
     PB_CHECK_CUDA(cudaMemcpyAsync(m.w32, w, sizeof(float) * (size_t)m.K * m.M, cudaMemcpyDeviceToDevice, st));
     return PB_OK;
+}
+
+int fill_matrix_f32_t(Mat& m, const float* wt, float threshold, cudaStream_t st) {
+    TransSource src{wt, m.K};
+    return quantize_matrix(m, src, threshold, st, wt);
 }
 
 int untile_codes(const Mat& m, int8_t* d_out, cudaStream_t st) {
