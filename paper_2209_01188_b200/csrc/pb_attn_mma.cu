@@ -30,6 +30,7 @@ constexpr int AM_SK = 64;    // keys per stage
 constexpr int AM_ST = 3;     // stages in flight
 constexpr int AM_WARPS = 4;  // compute warps, 16 keys each per stage
 constexpr int AM_G = 8;      // queries per group
+constexpr int AM_PT = 128;   // page-table window of the producer (pages)
 constexpr int AM_MAXC = 16;  // max CTAs contributing to one (group, head): split workspace slots
 
 __device__ __forceinline__ int kv_chunk_swz(int chunk, int slot) { return chunk ^ (slot & 7); }
@@ -63,7 +64,8 @@ __device__ __forceinline__ void split_h2(float x0, float x1, uint32_t& hi, uint3
 
 template <int DH>
 constexpr size_t attn_mma_smem() {
-    return (size_t)AM_ST * 2 * AM_SK * DH * 2 + (size_t)AM_WARPS * AM_G * (DH + 2) * 4 + 2 * AM_ST * 8 + 64;
+    return (size_t)AM_ST * 2 * AM_SK * DH * 2 + (size_t)AM_WARPS * AM_G * (DH + 2) * 4 + 2 * AM_ST * 8 + 64 +
+           4 * AM_PT;
 }
 
 __device__ __forceinline__ void cons_bar() {  // the AM_WARPS compute warps only
@@ -140,9 +142,12 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
 
     if (warp == AM_WARPS) {
         // ---------------- producer warp: K/V page pieces of every stage of the range.
+        // The segment's page-table entries are staged in shared memory first
+        // (one coalesced load), so issuing a stage never waits on a global load.
         // In a pure decode step the keys before each query's own position were
         // written by earlier steps: stream them while the QKV GEMV (PDL
         // predecessor) is still finishing; wait before the newest key.
+        int* s_pages = reinterpret_cast<int*>(s_flag + 4);  // [AM_PT]
         bool waited = false;
         int it = 0;
         for (int64_t u = u0; u < u1;) {
@@ -153,11 +158,19 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
             const int safe_end = a.decode_only ? pos0 : 0;
             const int32_t* pt = a.pages + (int64_t)a.tok_seq[t0] * a.max_pages;
             const int64_t head_off = (int64_t)sg.h * a.P * DH;
+            int pbase = -1 << 30;  // first page index held in s_pages
             for (int i = sg.i0; i < sg.i0 + sg.n; ++i, ++it) {
-                const int b = it % AM_ST;
-                mbar_wait(&empty[b], ((it / AM_ST) & 1) ^ 1);
                 const int k0 = i * AM_SK;
                 const int k1 = min(jend, k0 + AM_SK);
+                if ((k1 - 1) / a.P >= pbase + AM_PT) {  // refill the page window
+                    __syncwarp();
+                    pbase = k0 / a.P;
+                    const int plast = (min(jend, (sg.i0 + sg.n) * AM_SK) - 1) / a.P;
+                    for (int p = lane; p < AM_PT && pbase + p <= plast; p += 32) s_pages[p] = pt[pbase + p];
+                    __syncwarp();
+                }
+                const int b = it % AM_ST;
+                mbar_wait(&empty[b], ((it / AM_ST) & 1) ^ 1);
                 if (!waited && k1 > safe_end) {
                     pdl_wait();
                     pdl_trigger();
@@ -166,7 +179,7 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
                 if (lane == 0) {
                     mbar_expect_tx(&full[b], (uint32_t)(k1 - k0) * ROWB * 2);
                     for (int j = k0; j < k1;) {
-                        const int page = pt[j / a.P];
+                        const int page = s_pages[j / a.P - pbase];
                         const int jn = min(k1, (j / a.P + 1) * a.P);
                         const half* kp = a.kv + (int64_t)page * 2 * kv_stride + head_off + (int64_t)(j % a.P) * DH;
                         const uint32_t bytes = (uint32_t)(jn - j) * ROWB;
@@ -232,6 +245,11 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
             const int k0 = i * AM_SK;
             mbar_wait(&full[b], (it / AM_ST) & 1);
             const int kb = warp * 16;  // this warp's 16 keys of the stage
+            if (a.debug_nocomp) {  // experiment: memory pipeline only
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[b]);
+                continue;
+            }
             if (k0 + kb + 16 > j1) {
                 // partial last stage: rows past the range hold stale smem; P is 0
                 // there but 0 * NaN would poison O, so clear this warp's V rows
@@ -442,7 +460,13 @@ int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st) 
         configured = true;
     }
     (void)n_groups;
-    return launch_pdl(k_attn_mma<DH>, dim3((unsigned)G), dim3((AM_WARPS + 1) * 32), smem, st, a, (int)G, U);
+    static const int nocomp = [] {
+        const char* e = getenv("PB_ATT_NOCOMP");
+        return e ? atoi(e) : 0;
+    }();
+    AttnArgs aa = a;
+    aa.debug_nocomp = nocomp;
+    return launch_pdl(k_attn_mma<DH>, dim3((unsigned)G), dim3((AM_WARPS + 1) * 32), smem, st, aa, (int)G, U);
 }
 
 template int run_attn_mma<64>(const AttnArgs&, int, int64_t, cudaStream_t);

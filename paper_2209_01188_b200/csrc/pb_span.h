@@ -144,6 +144,7 @@ struct AttnArgs {
     const int64_t* unit_base;  // [n_groups + 1] first unit of each group
     int64_t total_units;
     int max_stages;            // max over groups of ceil(keys / 64)
+    int debug_nocomp = 0;      // experiment knob (PB_ATT_NOCOMP): skip the math, stream only
 };
 int launch_attention(const AttnArgs& a, int64_t part_cap, cudaStream_t st);
 template <int DH>
