@@ -13,7 +13,7 @@ import os
 from .errors import RemoteError, raise_for
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpetals_b200.so")
+LIB_PATH = os.environ.get("PB_LIB") or os.path.join(HERE, "libpetals_b200.so")  # PB_LIB: A/B builds
 
 # every symbol declared in include/petals_b200.h
 EXPORTS = [

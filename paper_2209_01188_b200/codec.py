@@ -155,6 +155,14 @@ def parse_tensor(data: bytes):
     raise ProtocolError(f"unknown tensor encoding {encoding}")
 
 
+def payload_finite(data: bytes) -> bool:
+    """True iff the TensorMsg's values are finite (f32 values, or int8 scales:
+    int8 codes times finite scales are finite)."""
+    enc, _, _, scales, payload = parse_tensor(data)
+    vals = payload if enc == ENC_F32 else scales
+    return bool(np.isfinite(vals).all()) if vals.size else True
+
+
 def decode_tensor(data: bytes, device=None):
     """TensorMsg -> CUDA f32 tensor (int8 decoded on the GPU)."""
     import torch

@@ -165,29 +165,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
         __syncwarp();
     } else {
         // ---------------- converters (warps 1-4): rows 32cw .. 32cw+31 of the tile
+        // int8 canonical core matrices (8 rows x 16 k, pb_weights.cu) -> fp16
+        // canonical core matrices (8 rows x 8 k): one row x 16 k per thread and k half
         const int cw = warp - 1;
-        const int g = lane >> 2, q = lane & 3;
+        const int r = cw * 32 + lane;
         for (int kc = 0; kc < KC; ++kc) {
             const int s = kc % TC_STAGES, f = kc % TC_FSTAGES;
             mbar_wait(&full[s], (kc / TC_STAGES) & 1);
             mbar_wait(&fempty[f], ((kc / TC_FSTAGES) & 1) ^ 1);
             uint8_t* dst = sa16 + f * TC_A16;
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const int mtl = cw * 2 + i;  // local m-tile (16 rows)
-                const uint4 w = *reinterpret_cast<const uint4*>(sa8 + s * TC_A8 + mtl * 512 + lane * 16);
-                const uint32_t words[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-                for (int wi = 0; wi < 4; ++wi) {
-                    // word wi: kt = wi >> 1, k-half kh = wi & 1; bytes {row g, row g} {row g+8, row g+8}
-                    uint32_t lo, hi;
-                    tc_i8x4(words[wi], lo, hi);
-                    const int kt = wi >> 1, kh = wi & 1;
-                    const int kchunk = 2 * kt + kh;  // 8-wide k chunk within the 32-wide tile
-                    uint8_t* base = dst + kchunk * 128 + g * 16 + q * 4;
-                    *reinterpret_cast<uint32_t*>(base + (2 * mtl + 0) * 512) = lo;  // row 16 mtl + g
-                    *reinterpret_cast<uint32_t*>(base + (2 * mtl + 1) * 512) = hi;  // row 16 mtl + g + 8
-                }
+            for (int kh = 0; kh < 2; ++kh) {
+                const uint4 w = *reinterpret_cast<const uint4*>(sa8 + s * TC_A8 + (r >> 3) * 256 + kh * 128 + (r & 7) * 16);
+                uint32_t h[8];
+                tc_i8x4(w.x, h[0], h[1]);
+                tc_i8x4(w.y, h[2], h[3]);
+                tc_i8x4(w.z, h[4], h[5]);
+                tc_i8x4(w.w, h[6], h[7]);
+                uint8_t* base = dst + (r >> 3) * 512 + (2 * kh) * 128 + (r & 7) * 16;
+                *reinterpret_cast<uint4*>(base) = make_uint4(h[0], h[1], h[2], h[3]);
+                *reinterpret_cast<uint4*>(base + 128) = make_uint4(h[4], h[5], h[6], h[7]);
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
             __syncwarp();

@@ -4,22 +4,25 @@
 //
 // Math: y[n, o] = sum_k code[o, k] * (s_k * x[n, k]) + sum_j W[k_j, o] x[n, k_j] + b[o]
 // The per-input-feature scale s_k is folded into the activation (x~ = s ⊙ x)
-// so the weight stream is raw int8 codes. x~ is split hi/lo into two fp16
-// operands after a per-token power-of-two shift (max |x~| -> [2^13, 2^14)),
-// so codes (exact in fp16) times (hi + lo) reproduces the f32 activation to
-// ~22 bits with fp32 accumulation on the tensor cores (mma.m16n8k16); the
-// epilogue undoes the shift exactly.
+// so the weight stream is raw int8 codes. Per token, x~ is scaled by a power
+// of two so max |x~| lies in [2^21, 2^22) and rounded to a 22-bit integer a,
+// written as three balanced int8 digits a = 65536 h + 256 m + l. Every
+// product code x digit is then an exact int8 x int8 tensor-core MMA
+// (mma.m16n8k32.s8, s32 accumulation: |sum| <= 127 * 128 * K < 2^31 for K <
+// 131072), so the GEMV is exact integer arithmetic on a 22-bit fixed-point
+// operand (relative error <= 2^-22 of the token's max |x~|); the epilogue
+// recombines h/m/l and undoes the scale. Split-K partial sums are integers:
+// merged exactly and order-independently.
 //
-// Memory-bound decode: every warp streams 512 B fragment tiles of codes with
-// 128-bit non-allocating loads (one per lane), converts int8 -> fp16 with a
-// PRMT/HSUB2 magic-number trick (exact for |c| <= 127) and issues 2 mma per
-// 16 B of codes per column tile. B fragments are shared by the 4 warps of a
-// CTA through L1. Deterministic split-K: partial tiles go to a workspace and
-// the last-arriving CTA sums the splits in fixed order and runs the epilogue.
+// Memory-bound decode: weights stream in 4 KB canonical tiles (pb_weights.cu)
+// through a cp.async.bulk ring; each consumer warp loads an m16k32 A fragment
+// with one ldmatrix.x4 and issues one IMMA per 8 operand columns -- no int8
+// -> fp16 conversion on the weight stream.
 //
-// B (activation) fragment layout, chunk c of tc tokens (columns: tc hi then tc lo):
-//   uint4 at ((c * KC + kc) * NT + nt) * 32 + lane, NT = 2 tc / 8,
-//   words {kt0: B[2q..2q+1][g], B[2q+8..2q+9][g]; kt1: same +16}, column = 8 nt + g.
+// B (activation) layout, chunk c of TC tokens, columns p * TC + t for digit p
+// (0: h, 1: m, 2: l) of token t, NT = ceil(3 TC / 8) n-tiles of 8 columns:
+//   uint2 at ((c * KC + kc) * NT + nt) * 32 + lane (lane = 4 g + q, column 8 nt + g),
+//   .x = B[k = 4q .. 4q+3][col], .y = B[k = 16 + 4q .. 16 + 4q + 3][col]  (the m16n8k32 B fragment).
 #include "pb_async.cuh"
 #include "pb_common.cuh"
 #include "pb_epi.cuh"
@@ -29,10 +32,20 @@ namespace pb {
 
 
 int choose_tc(int n_tok) {
-    if (n_tok <= 4) return 4;
+    if (n_tok <= 2) return 2;
     if (n_tok <= 8) return 8;
     if (n_tok <= 16) return 16;
     return 32;
+}
+
+__host__ __device__ constexpr int digit_ntiles(int tc) { return (3 * tc + 7) / 8; }
+
+// three balanced int8 digits of a (|a| < 2^22): a = 65536 h + 256 m + l
+__device__ __forceinline__ void digits3(int a, int& h, int& m, int& l) {
+    l = ((a + 128) & 255) - 128;
+    const int a1 = (a - l) >> 8;
+    m = ((a1 + 128) & 255) - 128;
+    h = (a1 - m) >> 8;
 }
 
 // ------------------------------------------------------------------ prologue
@@ -262,8 +275,10 @@ int bound_consts(const float* gamma, const float* beta, const float* scales, int
     return PB_OK;
 }
 
-// hi/lo fp16 B fragments of x~ = y * s * 2^shift (layout in the header comment);
-// one thread per (token, 32-wide k chunk, lane quad q).
+// int8-digit B fragments of a = rint(y * s * 2^(shift + 8)) (layout in the header
+// comment); one thread per (token, 32-wide k tile, lane quad q). The statistics'
+// shift maps max |y s| into [2^13, 2^14) (the fp16 split of the tcgen05 path);
+// 2^8 more gives the 22-bit integer range here.
 __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
     __shared__ float4 s_st;
     // early trigger (default): the GEMV that consumes this operand launches while
@@ -279,13 +294,14 @@ __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
         if (threadIdx.x == 0) {
             s_st = r;
             if (blockIdx.x == 0) {
-                a.back[tok] = r.w;
+                a.back[tok] = r.w * (1.f / 256.f);
                 if (a.src.zero_tokmax) a.src.zero_tokmax[tok] = 0.f;
             }
         }
     }
     __syncthreads();
     const float4 st = s_st;
+    const float z = st.z * 256.f;
     const int KC = a.Kp / 32;
     const int it = blockIdx.x * blockDim.x + threadIdx.x;
     if (blockIdx.x == 0 && a.xo) {
@@ -294,30 +310,29 @@ __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
     }
     if (it >= KC * 4) return;
     const int kc = it >> 2, q = it & 3;
-    const int NT = a.tc / 4;
+    const int NT = digit_ntiles(a.tc);
     const int c = tok / a.tc, col = tok % a.tc;
-    const int nt_hi = col >> 3, g_hi = col & 7;
-    const int nt_lo = (a.tc + col) >> 3, g_lo = (a.tc + col) & 7;
-    uint32_t hw[4], lw[4];
+    uint32_t w[3][2] = {{0u, 0u}, {0u, 0u}, {0u, 0u}};
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-        const int kt = w >> 1, upper = w & 1;
-        const int k0 = kc * 32 + kt * 16 + 2 * q + 8 * upper;
-        float v[2];
+    for (int half_ = 0; half_ < 2; ++half_) {
 #pragma unroll
-        for (int e2 = 0; e2 < 2; ++e2) {
-            const int k = k0 + e2;
-            v[e2] = k < a.K ? (pro_y(a, x, k, st.x, st.y) * a.scales[k]) * st.z : 0.f;
+        for (int i = 0; i < 4; ++i) {
+            const int k = kc * 32 + 16 * half_ + 4 * q + i;
+            const float v = k < a.K ? (pro_y(a, x, k, st.x, st.y) * a.scales[k]) * z : 0.f;
+            int h, m, l;
+            digits3(__float2int_rn(v), h, m, l);
+            w[0][half_] |= (uint32_t)(uint8_t)h << (8 * i);
+            w[1][half_] |= (uint32_t)(uint8_t)m << (8 * i);
+            w[2][half_] |= (uint32_t)(uint8_t)l << (8 * i);
         }
-        const half h0 = __float2half_rn(v[0]), h1 = __float2half_rn(v[1]);
-        const half l0 = __float2half_rn(v[0] - __half2float(h0));
-        const half l1 = __float2half_rn(v[1] - __half2float(h1));
-        hw[w] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-        lw[w] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
     }
+    uint2* frag = reinterpret_cast<uint2*>(a.frag);
     const int64_t base = ((int64_t)c * KC + kc) * NT;
-    a.frag[(base + nt_hi) * 32 + 4 * g_hi + q] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-    a.frag[(base + nt_lo) * 32 + 4 * g_lo + q] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+        const int cc = p * a.tc + col;
+        frag[(base + (cc >> 3)) * 32 + 4 * (cc & 7) + q] = make_uint2(w[p][0], w[p][1]);
+    }
 }
 
 // Same operand, written for the tcgen05 GEMM (pb_gemm_tc.cu): UMMA canonical
@@ -418,25 +433,19 @@ int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int 
 
 // ------------------------------------------------------------------ int8 mma GEMV
 
-__device__ __forceinline__ void mma16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
-                                         uint32_t b1) {
+__device__ __forceinline__ void imma16832(int* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                          uint32_t b1) {
     asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};\n"
-        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// 4 int8 (one word) -> two f16x2: {b0,b1}, {b2,b3}; exact for |c| <= 127.
-__device__ __forceinline__ void i8x4_to_f16x2(uint32_t w, uint32_t& lo, uint32_t& hi) {
-    const uint32_t u = w ^ 0x80808080u;                 // offset binary: c + 128
-    const uint32_t p0 = __byte_perm(u, 0x64646464u, 0x4140);  // {1024 + b0', 1024 + b1'}
-    const uint32_t p1 = __byte_perm(u, 0x64646464u, 0x4342);
-    const half2 bias = __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480));  // 1152
-    half2 r0 = __hsub2(*reinterpret_cast<const half2*>(&p0), bias);
-    half2 r1 = __hsub2(*reinterpret_cast<const half2*>(&p1), bias);
-    lo = *reinterpret_cast<uint32_t*>(&r0);
-    hi = *reinterpret_cast<uint32_t*>(&r1);
+__device__ __forceinline__ void ldsm_x4_i8(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
 }
 
 // ---- TMA-bulk pipelined stream-K GEMV ----------------------------------------
@@ -474,18 +483,18 @@ __device__ __forceinline__ int sk_owner(int64_t u, int G, int64_t total) {
     return (int)(((u + 1) * G - 1) / total);
 }
 
-template <int NT, int SK_KCS, int SK_STAGES>
+template <int TC, int SK_KCS, int SK_STAGES>
 __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
-    constexpr int TC = NT * 4;
-    constexpr int COLS = 2 * TC;
+    constexpr int NT = digit_ntiles(TC);
+    constexpr int COLS = 8 * NT;
     constexpr int SST = COLS + 1;
     constexpr int A_STAGE = SK_KCS * 4096;
-    constexpr int B_STAGE = SK_KCS * NT * 512;
+    constexpr int B_STAGE = SK_KCS * NT * 256;
     constexpr int PER = 128 * COLS;  // floats per partial tile
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* sa = smem;                                        // [STAGES][A_STAGE]
     uint8_t* sb = sa + SK_STAGES * A_STAGE;                    // [STAGES][B_STAGE]
-    float* S = reinterpret_cast<float*>(sb + SK_STAGES * B_STAGE);  // [128][SST]
+    int* S = reinterpret_cast<int*>(sb + SK_STAGES * B_STAGE);  // [128][SST] integer partial sums
     uint64_t* full = reinterpret_cast<uint64_t*>(S + 128 * SST + 3);  // 8-byte aligned below
     full = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(full) + 7) & ~uintptr_t(7));
     uint64_t* empty = full + SK_STAGES;
@@ -516,7 +525,7 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
             uint32_t phase = 0;
             int pk[SK_STAGES];  // k tiles of the stages prefetched before the dependency wait
             int pn[SK_STAGES];
-            const uint8_t* bsrc = reinterpret_cast<const uint8_t*>(a.act.frag) + (int64_t)chunk * a.KC * NT * 512;
+            const uint8_t* bsrc = reinterpret_cast<const uint8_t*>(a.act.frag) + (int64_t)chunk * a.KC * NT * 256;
             bool waited = false;
             for (int64_t u = u0; u < u1;) {
                 const int mg = (int)(u / a.KC);
@@ -525,7 +534,7 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
                 for (int kc = ka; kc < kb; kc += SK_KCS) {
                     const int n = min(SK_KCS, kb - kc);
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], n * (4096 + NT * 512));
+                    mbar_expect_tx(&full[stage], n * (4096 + NT * 256));
                     // weights never depend on the previous kernels: start streaming them
                     // while the operand producer (PDL predecessor) is still running
                     bulk_g2s(sa + stage * A_STAGE, a.codes + ((int64_t)mg * a.KC + kc) * 4096, n * 4096, &full[stage]);
@@ -533,7 +542,7 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
                         pk[issued] = kc;
                         pn[issued] = n;
                     } else {
-                        bulk_g2s(sb + stage * B_STAGE, bsrc + (int64_t)kc * NT * 512, n * NT * 512, &full[stage]);
+                        bulk_g2s(sb + stage * B_STAGE, bsrc + (int64_t)kc * NT * 256, n * NT * 256, &full[stage]);
                     }
                     ++issued;
                     if (!waited && issued == SK_STAGES) {
@@ -541,7 +550,7 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
                         pdl_trigger();
                         waited = true;
                         for (int i = 0; i < SK_STAGES; ++i)
-                            bulk_g2s(sb + i * B_STAGE, bsrc + (int64_t)pk[i] * NT * 512, pn[i] * NT * 512, &full[i]);
+                            bulk_g2s(sb + i * B_STAGE, bsrc + (int64_t)pk[i] * NT * 256, pn[i] * NT * 256, &full[i]);
                     }
                     if (++stage == SK_STAGES) {
                         stage = 0;
@@ -554,7 +563,7 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
                 pdl_wait();
                 pdl_trigger();
                 for (int i = 0; i < issued; ++i)
-                    bulk_g2s(sb + i * B_STAGE, bsrc + (int64_t)pk[i] * NT * 512, pn[i] * NT * 512, &full[i]);
+                    bulk_g2s(sb + i * B_STAGE, bsrc + (int64_t)pk[i] * NT * 256, pn[i] * NT * 256, &full[i]);
             }
         } else {
             pdl_wait();
@@ -568,44 +577,40 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
     pdl_trigger();
     const int cw = warp - 1;  // consumer warp: m-tiles 2cw, 2cw+1 of the group
     const int g = lane >> 2, q = lane & 3;
+    // ldmatrix roles: matrix mi = lane / 8 (row half mi & 1, k half mi >> 1), row ri = lane % 8
+    const uint32_t a_lane = (uint32_t)(((lane >> 3) & 1) * 256 + (lane >> 4) * 128 + (lane & 7) * 16);
+    const uint32_t sa_u = smem_u32(sa);
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t u = u0; u < u1;) {
         const int mg = (int)(u / a.KC);
         const int ka = (int)(u % a.KC);
         const int kb = (int)((int64_t)a.KC < ka + (u1 - u) ? (int64_t)a.KC : ka + (u1 - u));
-        float acc[2][NT][4];
+        int acc[2][NT][4];
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
             for (int j = 0; j < NT; ++j)
 #pragma unroll
-                for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.f;
+                for (int r = 0; r < 4; ++r) acc[i][j][r] = 0;
         for (int kc = ka; kc < kb; kc += SK_KCS) {
             const int n = min(SK_KCS, kb - kc);
             mbar_wait(&full[stage], phase);
-            const uint8_t* As = sa + stage * A_STAGE;
             const uint8_t* Bs = sb + stage * B_STAGE;
+            const uint32_t As = sa_u + stage * A_STAGE;
 #pragma unroll
             for (int kk = 0; kk < SK_KCS; ++kk) {
                 if (kk < n) {
-                    uint4 bv[NT];
+                    uint2 bv[NT];
 #pragma unroll
                     for (int j = 0; j < NT; ++j)
-                        bv[j] = *reinterpret_cast<const uint4*>(Bs + (kk * NT + j) * 512 + lane * 16);
+                        bv[j] = *reinterpret_cast<const uint2*>(Bs + (kk * NT + j) * 256 + lane * 8);
 #pragma unroll
                     for (int i = 0; i < 2; ++i) {
-                        const uint4 av = *reinterpret_cast<const uint4*>(As + kk * 4096 + (cw * 2 + i) * 512 + lane * 16);
-                        uint32_t f[8];
-                        i8x4_to_f16x2(av.x, f[0], f[1]);
-                        i8x4_to_f16x2(av.y, f[2], f[3]);
-                        i8x4_to_f16x2(av.z, f[4], f[5]);
-                        i8x4_to_f16x2(av.w, f[6], f[7]);
+                        uint32_t a0, a1, a2, a3;
+                        ldsm_x4_i8(As + kk * 4096 + (cw * 2 + i) * 512 + a_lane, a0, a1, a2, a3);
 #pragma unroll
-                        for (int j = 0; j < NT; ++j) {
-                            mma16816(acc[i][j], f[0], f[1], f[2], f[3], bv[j].x, bv[j].y);
-                            mma16816(acc[i][j], f[4], f[5], f[6], f[7], bv[j].z, bv[j].w);
-                        }
+                        for (int j = 0; j < NT; ++j) imma16832(acc[i][j], a0, a1, a2, a3, bv[j].x, bv[j].y);
                     }
                 }
             }
@@ -623,13 +628,13 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
         const int c_first = sk_owner(g0, a.G, a.total), c_last = sk_owner(g1 - 1, a.G, a.total);
         if (c_first != c_last) {
             const int slot = (u0 < g0) ? 1 : 0;  // not this CTA's first segment -> slot 1
-            float* mine = a.partials + (((int64_t)chunk * a.G + c) * 2 + slot) * PER;
+            int* mine = reinterpret_cast<int*>(a.partials) + (((int64_t)chunk * a.G + c) * 2 + slot) * PER;
 #pragma unroll
             for (int i = 0; i < 2; ++i)
 #pragma unroll
                 for (int j = 0; j < NT; ++j)
-                    *reinterpret_cast<float4*>(mine + (((cw * 2 + i) * NT + j) * 32 + lane) * 4) =
-                        make_float4(acc[i][j][0], acc[i][j][1], acc[i][j][2], acc[i][j][3]);
+                    *reinterpret_cast<int4*>(mine + (((cw * 2 + i) * NT + j) * 32 + lane) * 4) =
+                        make_int4(acc[i][j][0], acc[i][j][1], acc[i][j][2], acc[i][j][3]);
             __threadfence();
             cons_sync();
             if (threadIdx.x == 32) {
@@ -647,16 +652,17 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
 #pragma unroll
                 for (int j = 0; j < NT; ++j)
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.f;
+                    for (int r = 0; r < 4; ++r) acc[i][j][r] = 0;
             for (int cc = c_first; cc <= c_last; ++cc) {
                 const int64_t cu0 = (int64_t)cc * a.total / a.G;
-                const float* p = a.partials + (((int64_t)chunk * a.G + cc) * 2 + (cu0 < g0 ? 1 : 0)) * PER;
+                const int* p = reinterpret_cast<const int*>(a.partials) +
+                               (((int64_t)chunk * a.G + cc) * 2 + (cu0 < g0 ? 1 : 0)) * PER;
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
 #pragma unroll
                     for (int j = 0; j < NT; ++j) {
-                        const float4 v =
-                            __ldcg(reinterpret_cast<const float4*>(p + (((cw * 2 + i) * NT + j) * 32 + lane) * 4));
+                        const int4 v =
+                            __ldcg(reinterpret_cast<const int4*>(p + (((cw * 2 + i) * NT + j) * 32 + lane) * 4));
                         acc[i][j][0] += v.x;
                         acc[i][j][1] += v.y;
                         acc[i][j][2] += v.z;
@@ -679,15 +685,18 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
         cons_sync();
         const int row_base = mg * 128;
         const bool want_sum = a.epi.pstats != nullptr, want_max = a.epi.tokmax != nullptr;
+        float* Sf = reinterpret_cast<float*>(S);  // column j < TC reused for the epilogue outputs
         for (int t = threadIdx.x - 32; t < 128 * TC; t += SK_CONS * 32) {
             const int r = t % 128, j = t / 128;
             const int o = row_base + r;
             const int tok = chunk * TC + j;
             if (o >= a.epi.M || tok >= a.act.n_tok) continue;
-            const float v = (S[r * SST + j] + S[r * SST + TC + j]) * a.act.back[tok];
+            const double iv = 65536.0 * (double)S[r * SST + j] + 256.0 * (double)S[r * SST + TC + j] +
+                              (double)S[r * SST + 2 * TC + j];
+            const float v = (float)iv * a.act.back[tok];
             const float y = epi_store(a.epi, tok, o, v);
-            if (want_max) S[r * SST + j] = fabsf(y * a.epi.s_next[o]);
-            else if (want_sum) S[r * SST + j] = y;
+            if (want_max) Sf[r * SST + j] = fabsf(y * a.epi.s_next[o]);
+            else if (want_sum) Sf[r * SST + j] = y;
         }
         if (want_sum || want_max) {
             // per-token summary of this 128-row group for the next operand's range / LayerNorm
@@ -698,13 +707,13 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
                 if (tok >= a.act.n_tok) continue;
                 if (want_max) {
                     float m = 0.f;
-                    for (int r = lane; r < nrow; r += 32) m = fmaxf(m, S[r * SST + j]);
+                    for (int r = lane; r < nrow; r += 32) m = fmaxf(m, Sf[r * SST + j]);
                     m = warp_max(m);
                     if (lane == 0) atomicMax(reinterpret_cast<int*>(a.epi.tokmax) + tok, __float_as_int(m));
                 } else {
                     float s = 0.f, mn = INFINITY, mx = -INFINITY;
                     for (int r = lane; r < nrow; r += 32) {
-                        const float y = S[r * SST + j];
+                        const float y = Sf[r * SST + j];
                         s += y;
                         mn = fminf(mn, y);
                         mx = fmaxf(mx, y);
@@ -712,7 +721,7 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
                     const float mean = warp_sum(s) / nrow;
                     float m2 = 0.f;
                     for (int r = lane; r < nrow; r += 32) {
-                        const float dlt = S[r * SST + j] - mean;
+                        const float dlt = Sf[r * SST + j] - mean;
                         m2 = fmaf(dlt, dlt, m2);
                     }
                     m2 = warp_sum(m2);
@@ -725,19 +734,19 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
     }
 }
 
-template <int NT, int SK_KCS, int SK_STAGES>
+template <int TC, int SK_KCS, int SK_STAGES>
 static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
                      int64_t partial_cap, cudaStream_t st) {
-    constexpr int TC = NT * 4;
-    const size_t smem = (size_t)SK_STAGES * (SK_KCS * 4096 + SK_KCS * NT * 512) + 128 * (2 * TC + 1) * 4 + 16 +
+    constexpr int NT = digit_ntiles(TC);
+    const size_t smem = (size_t)SK_STAGES * (SK_KCS * 4096 + SK_KCS * NT * 256) + 128 * (8 * NT + 1) * 4 + 16 +
                         2 * SK_STAGES * 8 + 16;
     static int blocks_per_sm = 0, sms = 0;
     if (!blocks_per_sm) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_gemv_i8<NT, SK_KCS, SK_STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_gemv_i8<NT, SK_KCS, SK_STAGES>, SK_THREADS, smem);
+        cudaFuncSetAttribute(k_gemv_i8<TC, SK_KCS, SK_STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_gemv_i8<TC, SK_KCS, SK_STAGES>, SK_THREADS, smem);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
         // tuning knob: fewer CTAs per SM than fit leaves a slot for the next
         // kernel of the chain (PDL) to become resident and start streaming
@@ -751,39 +760,39 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
     const int chunks = (int)ceil_div(act.n_tok, act.tc);
     int64_t G = std::max<int64_t>(1, (int64_t)sms * blocks_per_sm / chunks);
     G = std::min<int64_t>(G, a.total);
-    const int64_t per_tile = 128 * 2 * TC;
+    const int64_t per_tile = 128 * 8 * NT;
     while (G > 1 && (int64_t)chunks * G * 2 * per_tile > partial_cap) G /= 2;
     a.G = (int)G;
     a.act = act;
     a.epi = epi;
     a.partials = partials;
     a.counters = counters;
-    return launch_pdl(k_gemv_i8<NT, SK_KCS, SK_STAGES>, dim3((unsigned)G, chunks), dim3(SK_THREADS), smem, st, a);
+    return launch_pdl(k_gemv_i8<TC, SK_KCS, SK_STAGES>, dim3((unsigned)G, chunks), dim3(SK_THREADS), smem, st, a);
 }
 
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters, int64_t partial_cap,
                 cudaStream_t st) {
     static int cfg = -1;
     if (cfg < 0) {
-        // tuning knob (k tiles per stage x stages): 0 = 2x4, 1 = 4x4 (default), 2 = 2x8, 3 = 4x6,
-        // 4 = 8x3, 5 = 4x3, 6 = 8x2
+        // tuning knob (k tiles per stage x stages) of the decode (TC = 2) kernel:
+        // 0 = 2x4, 1 = 4x4 (default), 2 = 2x8, 3 = 4x6, 4 = 8x3, 5 = 4x3, 6 = 8x2
         const char* e = getenv("PB_GEMV_CFG");
         cfg = e ? atoi(e) : 1;
     }
-    switch (act.tc / 4) {
-        case 1:
+    switch (act.tc) {
+        case 2:
             switch (cfg) {
-                case 0: return sk_launch<1, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
-                case 2: return sk_launch<1, 2, 8>(m, act, epi, partials, counters, partial_cap, st);
-                case 3: return sk_launch<1, 4, 6>(m, act, epi, partials, counters, partial_cap, st);
-                case 4: return sk_launch<1, 8, 3>(m, act, epi, partials, counters, partial_cap, st);
-                case 5: return sk_launch<1, 4, 3>(m, act, epi, partials, counters, partial_cap, st);
-                case 6: return sk_launch<1, 8, 2>(m, act, epi, partials, counters, partial_cap, st);
-                default: return sk_launch<1, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
+                case 0: return sk_launch<2, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
+                case 2: return sk_launch<2, 2, 8>(m, act, epi, partials, counters, partial_cap, st);
+                case 3: return sk_launch<2, 4, 6>(m, act, epi, partials, counters, partial_cap, st);
+                case 4: return sk_launch<2, 8, 3>(m, act, epi, partials, counters, partial_cap, st);
+                case 5: return sk_launch<2, 4, 3>(m, act, epi, partials, counters, partial_cap, st);
+                case 6: return sk_launch<2, 8, 2>(m, act, epi, partials, counters, partial_cap, st);
+                default: return sk_launch<2, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
             }
-        case 2: return sk_launch<2, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
-        case 4: return sk_launch<4, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
-        case 8: return sk_launch<8, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
+        case 8: return sk_launch<8, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
+        case 16: return sk_launch<16, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
+        case 32: return sk_launch<32, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
         default: set_error("bad column tile"); return PB_ERR_GENERIC;
     }
 }

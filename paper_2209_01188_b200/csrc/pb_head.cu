@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(1024) k_head_bound(const float* __restrict__ x
         bound[t] = (float)(0.5 * s * 1.001 + (double)d * 2.384185791015625e-7 * s2 * (double)emax + 1e-6);
         sel[t * 4 + 0] = ord_of(-INFINITY);
         sel[t * 4 + 1] = 0;
-        sel[t * 4 + 2] = 0;
+        sel[t * 4 + 2] = (isfinite(st.x) && isfinite(st.y)) ? 0 : 1;  // non-finite hidden row
     }
 }
 

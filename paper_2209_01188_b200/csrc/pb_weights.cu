@@ -3,14 +3,16 @@
 //
 // Orientation: the reference quantizes W^T, W = [in, out], with
 // one absmax scale per input feature k (a row of W) and treats a whole input
-// feature as an outlier when max_o |W[k, o]| > threshold. Codes are stored in a
-// fragment-tiled [out, in] layout consumed by the mma GEMV (pb_gemv.cu):
-//   tile (mt, kc) = rows [16 mt, 16 mt + 16) x inputs [32 kc, 32 kc + 32),
-//   512 B at (((mt / 8) * KC + kc) * 8 + mt % 8) * 512, i.e. the eight m-tiles of
-//   a 128-row group are adjacent for each kc (one 4 KB bulk copy per k tile);
-//   lane l = 4g + q owns bytes [16 l, 16 l + 16):
-//   byte 8 kt + i holds A[row(i), 16 kt + col(i)] with the m16n8k16 A-fragment
-//   map row(i) = g + 8((i >> 1) & 1), col(i) = 2q + (i & 1) + 8(i >> 2).
+// feature as an outlier when max_o |W[k, o]| > threshold. Codes are stored
+// [out, in] in 4 KB tiles of 128 output rows x 32 inputs, tile (mg, kc) at
+// (mg * KC + kc) * 4096 (a 128-row group's tiles are consecutive along k: one
+// bulk copy streams a stage). Inside a tile the layout is the UMMA canonical
+// K-major no-swizzle form for 8-bit operands:
+//   byte (r >> 3) * 256 + (k >> 4) * 128 + (r & 7) * 16 + (k & 15)
+// i.e. 8-row x 16-byte core matrices (LBO 128 B along k, SBO 256 B along
+// rows). The same tile feeds tcgen05.mma kind::i8 descriptors directly and
+// the decode GEMV's ldmatrix (each core matrix = one 8x8 b16 ldmatrix tile =
+// the m16n8k32 s8 A fragment quarter).
 // Weights are generated on the fly from the counter-form SplitMix64 stream, so
 // a 176B-shape block never materializes in f32.
 #include <vector>
@@ -92,36 +94,34 @@ __global__ void __launch_bounds__(256) k_feature_absmax(Src src, int64_t K, int6
     }
 }
 
-// pass 2: fragment-tiled codes, one thread per 16-byte lane slot
+// pass 2: tiled codes, one thread per 16-byte core-matrix row (row r, 16-wide k half)
 template <class Src>
-__global__ void __launch_bounds__(256) k_quant_tiles(Src src, int64_t K, int64_t M, int64_t KC, int64_t MT,
+__global__ void __launch_bounds__(256) k_quant_tiles(Src src, int64_t K, int64_t M, int64_t KC, int64_t MG,
                                                      const float* __restrict__ scales, int8_t* __restrict__ codes) {
-    const int64_t total = MT * KC * 32;
+    const int64_t total = MG * KC * 256;  // 128 rows x 2 halves per tile
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += stride) {
-        const int lane = (int)(t & 31);
-        const int64_t tile = t >> 5;
-        const int64_t mt = tile / KC, kc = tile % KC;
-        const int g = lane >> 2, q = lane & 3;
+        const int r = (int)(t & 127), kh = (int)((t >> 7) & 1);
+        const int64_t tile = t >> 8;
+        const int64_t mg = tile / KC, kc = tile % KC;
+        const int64_t o = mg * 128 + r;
         uint32_t words[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
         for (int b = 0; b < 16; ++b) {
-            const int kt = b >> 3, i = b & 7;
-            const int64_t o = mt * 16 + g + 8 * ((i >> 1) & 1);
-            const int64_t k = kc * 32 + kt * 16 + 2 * q + (i & 1) + 8 * (i >> 2);
+            const int64_t k = kc * 32 + kh * 16 + b;
             int code = 0;
             if (o < M && k < K) {
                 const float s = scales[k];
                 if (s > 0.f) {  // quant.py:97-100 (zero scale: outlier or all-zero feature)
                     const double qd = (double)src(k, o) / (double)s;
-                    double r = floor(fabs(qd) + 0.5);
-                    r = r > 127.0 ? 127.0 : r;
-                    code = qd < 0.0 ? -(int)r : (int)r;
+                    double rr = floor(fabs(qd) + 0.5);
+                    rr = rr > 127.0 ? 127.0 : rr;
+                    code = qd < 0.0 ? -(int)rr : (int)rr;
                 }
             }
             words[b >> 2] |= (uint32_t)(uint8_t)(int8_t)code << (8 * (b & 3));
         }
-        const int64_t off = ((((mt >> 3) * KC + kc) * 8 + (mt & 7)) * 32 + lane) * 16;
+        const int64_t off = tile * 4096 + (r >> 3) * 256 + kh * 128 + (r & 7) * 16;
         *reinterpret_cast<uint4*>(codes + off) = make_uint4(words[0], words[1], words[2], words[3]);
     }
 }
@@ -152,14 +152,8 @@ __global__ void k_untile(const int8_t* __restrict__ tiles, int64_t K, int64_t M,
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += stride) {
         const int64_t o = t / K, k = t % K;
-        const int64_t mt = o >> 4, r = o & 15, kc = k >> 5, kk = k & 31;
-        const int kt = (int)(kk >> 4), c = (int)(kk & 15);
-        const int g = (int)(r & 7), hi_r = (int)(r >> 3);
-        const int hi_c = c >> 3, cc = c & 7;
-        const int q = cc >> 1, lo = cc & 1;
-        const int i = lo + 2 * hi_r + 4 * hi_c;
-        const int lane = 4 * g + q;
-        out[t] = tiles[((((mt >> 3) * KC + kc) * 8 + (mt & 7)) * 32 + lane) * 16 + kt * 8 + i];
+        const int64_t mg = o >> 7, r = o & 127, kc = k >> 5, kk = k & 31;
+        out[t] = tiles[(mg * KC + kc) * 4096 + (r >> 3) * 256 + (kk >> 4) * 128 + (r & 7) * 16 + (kk & 15)];
     }
 }
 
@@ -170,7 +164,7 @@ static int grid_n(int64_t n, int threads = 256) {
 
 template <class Src>
 static int quantize_matrix(Mat& m, Src src, float threshold, cudaStream_t st, const float* wt = nullptr) {
-    const int64_t K = m.K, M = m.M, KC = m.Kp / 32, MT = m.Mp / 16;
+    const int64_t K = m.K, M = m.M, KC = m.Kp / 32, MG = m.Mp / 128;
     uint8_t* d_flags = nullptr;
     PB_CHECK_CUDA(cudaMallocAsync(&d_flags, K, st));
     PB_CHECK_CUDA(cudaMemsetAsync(m.scales, 0, sizeof(float) * m.Kp, st));
@@ -189,7 +183,7 @@ static int quantize_matrix(Mat& m, Src src, float threshold, cudaStream_t st, co
         k_feature_absmax<Src><<<grid_n(K * 32), 256, 0, st>>>(src, K, M, threshold, m.scales, d_flags);
         if (int rc = launch_check("feature_absmax")) return rc;
     }
-    k_quant_tiles<Src><<<grid_n(MT * KC * 32), 256, 0, st>>>(src, K, M, KC, MT, m.scales, m.codes);
+    k_quant_tiles<Src><<<grid_n(MG * KC * 256), 256, 0, st>>>(src, K, M, KC, MG, m.scales, m.codes);
     if (int rc = launch_check("quant_tiles")) return rc;
     std::vector<uint8_t> flags(K);
     PB_CHECK_CUDA(cudaMemcpyAsync(flags.data(), d_flags, K, cudaMemcpyDeviceToHost, st));

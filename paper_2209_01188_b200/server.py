@@ -34,6 +34,7 @@ import numpy as np
 from . import codec
 from .errors import (
     ERR_BAD_REQUEST,
+    ERR_GENERIC,
     ERR_BUSY,
     ERR_CAPACITY,
     ERR_DESYNC,
@@ -159,6 +160,7 @@ class _Session:
         self.last_active = time.monotonic()
         self.lock = threading.Lock()
         self.last_step = None  # (start_pos, digest, reply)
+        self.poisoned = False  # a non-finite hidden state entered the caches (reference: NaN KV)
 
 
 class _Job:
@@ -523,6 +525,13 @@ class ServerNode:
             with self._sessions_lock:
                 if self._sessions.get(sid) is not session:
                     raise RemoteError(ERR_UNKNOWN_SESSION, "session evicted")
+            if session.poisoned or not codec.payload_finite(payload[20:]):
+                # the reference computes NaN/inf hidden states and fails encoding the reply
+                # (transport/wire.py:89-90 -> ERR_GENERIC) after advancing the position
+                # (server.py:386-387); every later step of the session fails the same way
+                session.poisoned = True
+                session.position += t
+                raise RemoteError(ERR_GENERIC, "internal error: non-finite tensor")
             x = codec.decode_tensor(payload[20:], device=self.span.device)
             try:
                 out = self.sched.run(session.seq, x)
@@ -562,11 +571,14 @@ class ServerNode:
 
     def _forward(self, payload: bytes) -> bytes:
         try:
+            finite = codec.payload_finite(payload)
             batch = codec.decode_tensor(payload, device=self.span.device)
         except SwarmError as e:
             raise RemoteError(ERR_BAD_REQUEST, str(e)) from e
         if batch.ndim != 3:
             raise RemoteError(ERR_BAD_REQUEST, "FORWARD tensor must be [B, t, d]")
+        if not finite:  # the reference computes NaN/inf and fails encoding the reply (wire.py:89-90)
+            raise RemoteError(ERR_GENERIC, "internal error: non-finite tensor")
         try:
             out = self.span.forward(batch)
         except CapacityError as e:

@@ -237,3 +237,33 @@ def test_forward_rpc_matches_block_forward(swarm):
     for r in range(3):
         want, _, _ = block_forward(swarm.ckpt.blocks[1], batch[r], KvCache.empty(cfg), 0, cfg)
         assert float(np.max(np.abs(acts[r] - want))) <= 1e-3 * float(np.abs(want).max())
+
+
+def test_nonfinite_step_matches_reference(swarm):
+    """A NaN hidden state: the reference computes NaN, fails to encode the reply
+    (transport/wire.py:89-90 -> ERR_GENERIC) after advancing the position, and
+    every later step of that session fails the same way. Same codes here."""
+    from swarmlm.errors import RemoteError
+    from swarmlm.model import embed
+    from swarmlm.transport import MSG, rpc_call
+
+    ck = swarm.ckpt
+
+    def raw_step(address, sid, pos, arr):
+        arr = np.asarray(arr, "<f4")
+        msg = struct.pack(">BB", 0, 2) + struct.pack(">II", *arr.shape) + arr.tobytes()
+        try:
+            rpc_call(address, MSG.STEP, sid + struct.pack(">I", pos) + msg, 10000.0)
+            return 0
+        except RemoteError as e:
+            return e.code
+
+    codes = {}
+    for kind, node in (("ref", swarm.reference((0, 4))), ("b200", swarm.b200((0, 4)))):
+        sid = _open(node.address)
+        bad = embed(ck, [2]).copy()
+        bad[0, 3] = np.nan
+        codes[kind] = [raw_step(node.address, sid, 0, embed(ck, [1, 2, 3])), raw_step(node.address, sid, 3, bad),
+                       raw_step(node.address, sid, 3, bad), raw_step(node.address, sid, 4, embed(ck, [5]))]
+    assert codes["b200"] == codes["ref"], codes
+    assert codes["ref"][0] == 0 and codes["ref"][1] != 0

@@ -79,8 +79,8 @@ void run_bulk(const uint8_t* d, int64_t bytes, int* sink, int ctas_per_sm, int s
         cudaEventElapsedTime(&ms, a, b);
         if (r) best = ms < best ? ms : best;
     }
-    printf("bulk stage=%6d stages=%d ctas/sm=%d smem=%7zu: %.1f GB/s  (%s)\n", STAGE, STAGES, ctas_per_sm, smem,
-           use / best / 1e6, cudaGetErrorString(cudaGetLastError()));
+    printf("bulk stage=%6d stages=%d ctas/sm=%d smem=%7zu: %.1f GB/s %.1f us (%s)\n", STAGE, STAGES, ctas_per_sm, smem,
+           use / best / 1e6, best * 1e3, cudaGetErrorString(cudaGetLastError()));
 }
 
 template <int UNROLL>
@@ -112,6 +112,10 @@ int main() {
     cudaMalloc(&d, bytes);
     cudaMalloc(&sink, 4);
     cudaMemset(d, 1, bytes);
+    for (int64_t mb : {100, 200, 400, 600, 800, 1600}) {  // fixed cost per launch: t = a + bytes / BW
+        printf("size %lld MB: ", (long long)mb);
+        run_bulk<16384, 4>(d, mb << 20, sink, 2, sms);
+    }
     run_bulk<16384, 4>(d, bytes, sink, 2, sms);
     run_bulk<16384, 6>(d, bytes, sink, 2, sms);
     run_bulk<16384, 8>(d, bytes, sink, 1, sms);
