@@ -335,11 +335,13 @@ __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
     }
 }
 
-// Same operand, written for the tcgen05 GEMM (pb_gemm_tc.cu): UMMA canonical
-// K-major no-swizzle layout, per (128-token tile, 32-wide k tile) a 16 KB block
-// of 256 columns (hi of the 128 tokens, then lo); column c, k: byte
-// (c/8)*512 + (k/8)*128 + (c%8)*16 + (k%8)*2. One thread per (token, k tile,
-// 8-wide chunk) -> two 16-byte stores. Padding tokens are written as zeros.
+// Same operand for the tcgen05 GEMM (pb_gemm_tc.cu): the three int8 digit
+// planes of a = rint(y s 2^(shift + 8)), each in the UMMA canonical K-major
+// no-swizzle layout of the weight tiles: per (TC_TOKENS-token tile nt, 32-wide
+// k tile kc, digit p) a TC_TOKENS x 32 B block at ((nt * KC + kc) * 3 + p) *
+// TC_TOKENS * 32, token c, k: byte (c >> 3) * 256 + (k >> 4) * 128 + (c & 7) * 16
+// + (k & 15). One thread per (token, k tile, 16-wide k half) -> three 16-byte
+// stores. Padding tokens are zeros.
 __global__ void __launch_bounds__(256) k_canonwrite(ProArgs a, uint8_t* __restrict__ bcanon, int n_tok) {
     __shared__ float4 s_st;
     const int tok = blockIdx.y;
@@ -350,7 +352,7 @@ __global__ void __launch_bounds__(256) k_canonwrite(ProArgs a, uint8_t* __restri
         if (threadIdx.x == 0) {
             s_st = r;
             if (blockIdx.x == 0) {
-                a.back[tok] = r.w;
+                a.back[tok] = r.w * (1.f / 256.f);
                 if (a.src.zero_tokmax) a.src.zero_tokmax[tok] = 0.f;
             }
         }
@@ -362,31 +364,29 @@ __global__ void __launch_bounds__(256) k_canonwrite(ProArgs a, uint8_t* __restri
         for (int j = threadIdx.x; j < a.n_outl; j += blockDim.x)
             a.xo[(int64_t)tok * a.n_outl + j] = pro_y(a, x, a.outl_idx[j], s_st.x, s_st.y);
     }
-    if (it >= KC * 4) return;
-    const int kc = it >> 2, ch = it & 3;
-    uint32_t hw[4] = {0u, 0u, 0u, 0u}, lw[4] = {0u, 0u, 0u, 0u};
+    if (it >= KC * 2) return;
+    const int kc = it >> 1, kh = it & 1;
+    uint32_t w[3][4] = {};
     if (real) {
         const float4 st = s_st;
+        const float z = st.z * 256.f;
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            float v[2];
-#pragma unroll
-            for (int e2 = 0; e2 < 2; ++e2) {
-                const int k = kc * 32 + ch * 8 + 2 * p + e2;
-                v[e2] = k < a.K ? (pro_y(a, x, k, st.x, st.y) * a.scales[k]) * st.z : 0.f;
-            }
-            const half h0 = __float2half_rn(v[0]), h1 = __float2half_rn(v[1]);
-            const half l0 = __float2half_rn(v[0] - __half2float(h0));
-            const half l1 = __float2half_rn(v[1] - __half2float(h1));
-            hw[p] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-            lw[p] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+        for (int i = 0; i < 16; ++i) {
+            const int k = kc * 32 + kh * 16 + i;
+            const float v = k < a.K ? (pro_y(a, x, k, st.x, st.y) * a.scales[k]) * z : 0.f;
+            int h, m, l;
+            digits3(__float2int_rn(v), h, m, l);
+            w[0][i >> 2] |= (uint32_t)(uint8_t)h << (8 * (i & 3));
+            w[1][i >> 2] |= (uint32_t)(uint8_t)m << (8 * (i & 3));
+            w[2][i >> 2] |= (uint32_t)(uint8_t)l << (8 * (i & 3));
         }
     }
-    const int nt = tok >> 7, c = tok & 127;
-    uint8_t* blk = bcanon + ((int64_t)nt * KC + kc) * 16384 + ch * 128;
-    *reinterpret_cast<uint4*>(blk + (c >> 3) * 512 + (c & 7) * 16) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-    const int cl = c + 128;
-    *reinterpret_cast<uint4*>(blk + (cl >> 3) * 512 + (cl & 7) * 16) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    constexpr int PLANE = TC_TOKENS * 32;
+    const int nt = tok / TC_TOKENS, c = tok % TC_TOKENS;
+    uint8_t* blk = bcanon + ((int64_t)nt * KC + kc) * 3 * PLANE + (c >> 3) * 256 + kh * 128 + (c & 7) * 16;
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+        *reinterpret_cast<uint4*>(blk + p * PLANE) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
 }
 
 // f32-weights mode: plain y = LN(x) (or x) rows for the CUDA-core GEMM
@@ -420,12 +420,13 @@ int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int 
         k_rows_f32<<<dim3((unsigned)ceil_div(K, 256), n_tok), 256, 0, st>>>(a);
         return launch_check("rows_f32");
     }
-    const int items = (Kp / 32) * 4;
     if (bcanon) {
-        k_canonwrite<<<dim3((unsigned)ceil_div(items, 256), (unsigned)round_up(n_tok, 128)), 256, 0, st>>>(a, bcanon,
+        const int items = (Kp / 32) * 2;
+        k_canonwrite<<<dim3((unsigned)ceil_div(items, 256), (unsigned)round_up(n_tok, TC_TOKENS)), 256, 0, st>>>(a, bcanon,
                                                                                                       n_tok);
         return launch_check("canonwrite");
     }
+    const int items = (Kp / 32) * 4;
     return launch_pdl(k_fragwrite, dim3((unsigned)ceil_div(items, 256), n_tok), dim3(256), 0, st, a);
 }
 

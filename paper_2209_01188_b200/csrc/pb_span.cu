@@ -32,7 +32,7 @@ struct pb_span {
     // workspaces
     float *xa = nullptr, *mid = nullptr, *q = nullptr, *ctx = nullptr, *act = nullptr, *xo = nullptr, *y32 = nullptr;
     uint4* frag = nullptr;
-    uint8_t* bcanon = nullptr;  // tcgen05 B operand [ceil(NT/128)][KC][16 KB]
+    uint8_t* bcanon = nullptr;  // tcgen05 B operand [ceil(NT/TC_TOKENS)][KC][3 digit planes][TC_TOKENS x 32 B]
     int tc_min = TC_MIN_TOKENS_DEFAULT;
     float* back = nullptr;
     float4* stats = nullptr;
@@ -183,7 +183,7 @@ int pb_span_create(const pb_span_config* cfg, pb_span** out) {
     const int64_t kp_max = round_up(rd, 32);
     if (!rc && int8) rc = dalloc(s, &s->frag, (int64_t)(NT + 31) * kp_max * 4 / 16 + 64);
     if (const char* e = getenv("PB_TC_MIN")) s->tc_min = atoi(e);
-    if (!rc && int8 && NT >= s->tc_min) rc = dalloc(s, &s->bcanon, ceil_div(NT, 128) * (kp_max / 32) * 16384);
+    if (!rc && int8 && NT >= s->tc_min) rc = dalloc(s, &s->bcanon, ceil_div(NT, TC_TOKENS) * (kp_max / 32) * 3 * TC_TOKENS * 32);
     if (!rc) rc = dalloc(s, &s->back, NT);
     if (!rc) rc = dalloc(s, &s->stats, NT);
     if (!rc) rc = dalloc(s, &s->pst_x, (int64_t)NT * ceil_div(d, 128));
@@ -410,8 +410,8 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                 Act a{nullptr, s->back, n_tok, 0};
                 ev = prof_begin(s, st);
                 int rc = launch_gemm_tc(m, s->bcanon, a, e, st);
-                // tensor roofline: 2 * M * K * (2 columns per token: hi + lo) flops
-                prof_end(s, ev, 5, 2.0 * m.M * m.K * 2.0 * n_tok, st);
+                // tensor roofline: int8 ops issued = 2 * M * K * 3 digit columns per token
+                prof_end(s, ev, 5, 2.0 * m.M * m.K * 3.0 * n_tok, st);
                 return rc;
             }
             if (int8) {

@@ -113,6 +113,7 @@ int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int 
 // tcgen05 GEMM over a canonical-layout B operand (pb_gemm_tc.cu)
 int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Epi& epi, cudaStream_t st);
 constexpr int TC_MIN_TOKENS_DEFAULT = 64;
+constexpr int TC_TOKENS = 80;  // tokens per tcgen05 tile (3 digit accumulators x 80 columns, double-buffered in TMEM)
 // (max_k |gamma_k| s_k, max_k |beta_k| s_k) -> host
 int bound_consts(const float* gamma, const float* beta, const float* scales, int K, float* gs, float* bs,
                  cudaStream_t st);
