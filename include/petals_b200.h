@@ -15,6 +15,8 @@
  *   pb_span_* weights        <- quant.py:81-108,132-149 quantize_weights_int8 / QuantizedBlockWeights.from_block
  *   pb_span_step             <- model.py:314-380 block_forward looped over a span as in server.py:383-385,
  *                               batched over sessions; KV caches = server.py:69-77 _Session.caches
+ *   pb_span_step_tape,
+ *   pb_span_backward         <- server.py:411-450 FORWARD tapes / BACKWARD, model.py:383-418 block_backward
  *   pb_head_*                <- model.py:421-446 embed / lm_head / sample_next("greedy"), the client side of
  *                               client.py:247-250
  */
@@ -125,6 +127,19 @@ int pb_span_step_int8(pb_span* span, int32_t n_tok, int32_t n_seq, const int32_t
                       const int32_t* h_tok_pos, const int32_t* h_pages, const int8_t* d_in_codes,
                       const float* d_in_scales, const float* d_in_f32, int8_t* d_out_codes,
                       float* d_out_scales, float* d_out_f32, void* stream);
+
+/* pb_span_step that also records the FORWARD tape (server.py:418-428): block j's input rows are
+ * copied to d_tape[j][n_tok][hidden] (hosted block order) for pb_span_backward. */
+int pb_span_step_tape(pb_span* span, int32_t n_tok, int32_t n_seq, const int32_t* h_tok_seq,
+                      const int32_t* h_tok_pos, const int32_t* h_pages, const float* d_in, float* d_out,
+                      float* d_tape, void* stream);
+
+/* BACKWARD of one FORWARD row (server.py:431-450 -> model.py:383-418 block_backward over the hosted
+ * blocks in reverse): d_grad_in[t][hidden] = dL/d(span input) given d_grad_out[t][hidden], the row's
+ * tape d_tape[n_blocks][t][hidden] (positions 0 .. t-1, empty cache). Intermediates are recomputed
+ * from the tape in f32 with the span's own weights (int8 spans: dequantized codes + f32 outliers). */
+int pb_span_backward(pb_span* span, const float* d_tape, int32_t t, const float* d_grad_out, float* d_grad_in,
+                     void* stream);
 
 /* Last-launch statistics: number of kernels the last step launched. */
 int32_t pb_span_last_launches(const pb_span* span);

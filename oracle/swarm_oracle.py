@@ -185,6 +185,14 @@ class Int8Matrix:
         self.outlier_rows = w[self.outlier_idx, :].copy()  # [n_outl, out]
         self.shape_in_out = w.shape
 
+    def dense(self) -> np.ndarray:
+        """The [in, out] f32 matrix the int8 path multiplies by: codes x scales,
+        outlier features' rows exact."""
+        w = (self.codes.astype(np.float32) * self.scales[None, :]).T.copy()
+        if self.outlier_idx.size:
+            w[self.outlier_idx, :] = self.outlier_rows
+        return w.astype(np.float32)
+
     def apply(self, x: np.ndarray) -> np.ndarray:
         """x [t, in] -> x @ W via dequantised regular part + f32 outlier rows
         (quant.py:117-129; model.py:305-311)."""
@@ -318,3 +326,81 @@ def forward_span(blocks, x: np.ndarray, shape: Shape, quantized: bool) -> np.nda
     for blk in blocks:
         x = block_step(blk, x, KV(shape), 0, shape, QuantBlock(blk) if quantized else None)
     return x
+
+
+# ------------------------------------------------------------------- training (FORWARD tape / BACKWARD)
+
+
+def gelu_grad(x):
+    """model.py:295-298."""
+    c = np.float32(math.sqrt(2.0 / math.pi))
+    a = np.float32(0.044715)
+    t = np.tanh(c * (x + a * x ** 3))
+    return (0.5 * (1.0 + t) + 0.5 * x * (1.0 - t * t) * c * (1.0 + 3.0 * a * x ** 2)).astype(np.float32)
+
+
+def layer_norm_backward(dy, xhat, inv_std, g):
+    """model.py:279-283."""
+    dxhat = dy * g
+    m1 = dxhat.mean(-1, keepdims=True)
+    m2 = (dxhat * xhat).mean(-1, keepdims=True)
+    return ((dxhat - m1 - xhat * m2) * inv_std).astype(np.float32)
+
+
+def block_backward(blk: Block, x: np.ndarray, grad_out: np.ndarray, shape: Shape) -> np.ndarray:
+    """Gradient of block_forward at empty cache / start 0 (the FORWARD row
+    semantics, server.py:418-425) w.r.t. its input: the forward is recomputed
+    from x (the tape) and model.py:383-418 is applied. f32 numpy like the
+    reference."""
+    t, d = x.shape
+    H, dh = shape.n_heads, shape.head_dim
+    x = x.astype(np.float32)
+
+    def ln(v, g, b):
+        mu = v.mean(-1, keepdims=True)
+        var = v.var(-1, keepdims=True)
+        inv = (1.0 / np.sqrt(var + EPS_LN)).astype(np.float32)
+        xh = ((v - mu) * inv).astype(np.float32)
+        return (g * xh + b).astype(np.float32), xh, inv
+
+    h1, xh1, inv1 = ln(x, blk.ln1_g, blk.ln1_b)
+    qkv = h1 @ blk.wqkv + blk.bqkv
+    q = qkv[:, :d].reshape(t, H, dh)
+    k = qkv[:, d:2 * d].reshape(t, H, dh)
+    v = qkv[:, 2 * d:].reshape(t, H, dh)
+    sc = np.einsum("ihd,jhd->hij", q, k).astype(np.float32) / np.float32(math.sqrt(dh))
+    pos = np.arange(t, dtype=np.float32)
+    rel = pos[None, :] - pos[:, None]
+    sc = sc + alibi(H)[:, None, None] * rel[None]
+    sc = np.where(rel[None] > 0, np.float32(-np.inf), sc)
+    sc = sc - sc.max(-1, keepdims=True)
+    e = np.exp(sc, dtype=np.float32)
+    p = e / e.sum(-1, keepdims=True)
+    ctx = np.einsum("hij,jhd->ihd", p, v).astype(np.float32).reshape(t, d)
+    mid = x + (ctx @ blk.wo + blk.bo)
+    h2, xh2, inv2 = ln(mid, blk.ln2_g, blk.ln2_b)
+    pre = h2 @ blk.wmlp_in + blk.bmlp_in
+    g = grad_out.astype(np.float32)
+    dact = g @ blk.wmlp_out.T
+    dpre = dact * gelu_grad(pre)
+    dh2 = dpre @ blk.wmlp_in.T
+    dmid = g + layer_norm_backward(dh2, xh2, inv2, blk.ln2_g)
+    dctx = (dmid @ blk.wo.T).reshape(t, H, dh)
+    dprobs = np.einsum("ihd,jhd->hij", dctx, v).astype(np.float32)
+    dv = np.einsum("hij,ihd->jhd", p, dctx).astype(np.float32)
+    row = (dprobs * p).sum(-1, keepdims=True)
+    dsc = p * (dprobs - row)
+    inv_sq = np.float32(1.0 / math.sqrt(dh))
+    dq = np.einsum("hij,jhd->ihd", dsc, k).astype(np.float32) * inv_sq
+    dk = np.einsum("hij,ihd->jhd", dsc, q).astype(np.float32) * inv_sq
+    dqkv = np.concatenate([dq.reshape(t, d), dk.reshape(t, d), dv.reshape(t, d)], axis=1)
+    dx = dmid + layer_norm_backward(dqkv @ blk.wqkv.T, xh1, inv1, blk.ln1_g)
+    return dx.astype(np.float32)
+
+
+def dequantized_block(blk: Block) -> Block:
+    """The block a span with int8 weights computes with: codes x feature scales,
+    outlier features kept exact (quant.py:117-129)."""
+    out = Block(*(Int8Matrix(w).dense() for w in (blk.wqkv, blk.wo, blk.wmlp_in, blk.wmlp_out)),
+                blk.wo.shape[0], blk.wmlp_in.shape[1] // blk.wmlp_in.shape[0])
+    return out

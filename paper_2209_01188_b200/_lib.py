@@ -22,6 +22,7 @@ EXPORTS = [
     "pb_span_outliers", "pb_span_read_codes", "pb_span_step", "pb_span_step_int8", "pb_span_last_launches",
     "pb_span_profile", "pb_span_profile_read", "pb_head_create", "pb_head_destroy", "pb_head_device_bytes",
     "pb_head_gen", "pb_head_load", "pb_head_embed", "pb_head_embed_device", "pb_head_logits", "pb_head_greedy",
+    "pb_span_step_tape", "pb_span_backward",
 ]
 
 
@@ -59,6 +60,8 @@ def lib() -> C.CDLL:
         "pb_span_read_codes": [P, I32, I32, P, P],
         "pb_span_step": [P, I32, I32, P, P, P, P, P, VP],
         "pb_span_step_int8": [P, I32, I32, P, P, P, P, P, P, P, P, P, VP],
+        "pb_span_step_tape": [P, I32, I32, P, P, P, P, P, P, VP],
+        "pb_span_backward": [P, P, I32, P, P, VP],
         "pb_span_profile": [P, I32],
         "pb_span_profile_read": [P, I32, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double)],
         "pb_head_create": [I32, I32, I32, I32, C.POINTER(C.c_void_p)],

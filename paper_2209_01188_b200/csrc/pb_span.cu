@@ -22,52 +22,7 @@ void set_error(const std::string& msg) { g_err = msg; }
 
 using namespace pb;
 
-struct pb_span {
-    pb_span_config cfg{};
-    int d = 0, H = 0, dh = 0, rd = 0, max_pages = 0;
-    std::vector<BlockW> blocks;
-    half* kv = nullptr;          // [n_blocks][n_pages][2][H][P][dh]
-    int64_t kv_block_elems = 0;  // elements per block
-    float* slopes = nullptr;
-    // workspaces
-    float *xa = nullptr, *mid = nullptr, *q = nullptr, *ctx = nullptr, *act = nullptr, *xo = nullptr, *y32 = nullptr;
-    uint4* frag = nullptr;
-    uint8_t* bcanon = nullptr;  // tcgen05 B operand [ceil(NT/TC_TOKENS)][KC][3 digit planes][TC_TOKENS x 32 B]
-    int tc_min = TC_MIN_TOKENS_DEFAULT;
-    float* back = nullptr;
-    float4* stats = nullptr;
-    float4 *pst_x = nullptr, *pst_mid = nullptr;  // per-128-row LN summaries [NT][d/128]
-    float *tokmax_ctx = nullptr, *tokmax_act = nullptr;  // operand ranges [NT]
-    float* partials = nullptr;
-    int64_t partial_cap = 0;
-    int* counters = nullptr;
-    float* attn_part = nullptr;
-    int64_t attn_cap = 0;
-    int32_t *d_tok_seq = nullptr, *d_tok_pos = nullptr, *d_pages = nullptr;
-    int32_t *d_grp_first = nullptr, *d_grp_count = nullptr;
-    int n_groups = 0;
-    int64_t* d_unit_base = nullptr;  // stream-K attention units per query group
-    int64_t total_units = 0;
-    int max_stages = 0;
-    static constexpr int NSLOT = 4;  // ring of pinned staging buffers (no host sync per step)
-    int32_t* h_meta[NSLOT] = {nullptr, nullptr, nullptr, nullptr};
-    int64_t* h_ub[NSLOT] = {nullptr, nullptr, nullptr, nullptr};
-    cudaEvent_t meta_ev[NSLOT] = {nullptr, nullptr, nullptr, nullptr};
-    int meta_slot = 0;
-    int64_t meta_ints = 0;
-    // live kernel profiling (CUDA event pairs around launches; bench.py roofline)
-    bool prof_on = false;
-    std::vector<cudaEvent_t> prof_ev;
-    struct ProfRec { int kind; int ev; double bytes; };
-    std::vector<ProfRec> prof;
-    std::vector<int32_t> h_tok_pos_last;
-    int8_t* hop_codes = nullptr;
-    float* hop_scales = nullptr;
-    int64_t bytes = 0;
-    int32_t last_launches = 0;
-    int last_n_seq = 0;
-    std::mutex mu;  // one step at a time per span (the stream is shared)
-};
+#include "pb_span_impl.h"
 
 namespace {
 
@@ -360,7 +315,8 @@ static void prof_end(pb_span* s, int ev, int kind, double bytes, cudaStream_t st
 // qkv operand of block j; attention -> max|ctx s_wo| -> wo operand; wo-GEMV ->
 // LN summaries -> wmlp_in operand; wmlp_in-GEMV -> max|act s_out| -> wmlp_out
 // operand. Only block 0's LN1 needs a separate row-statistics kernel.
-static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float* out, cudaStream_t st) {
+static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float* out, cudaStream_t st,
+                      float* tape = nullptr) {
     const int d = s->d, rd = s->rd;
     const bool int8 = s->cfg.weights == PB_WEIGHTS_INT8;
     const int tc = choose_tc(n_tok);
@@ -371,6 +327,9 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
         BlockW& b = s->blocks[j];
         const float* x_in = j == 0 ? in : s->xa;
         float* x_out = j == s->cfg.n_blocks - 1 ? out : s->xa;
+        if (tape)  // FORWARD tape: block j's input rows (pb_train.cu recomputes the rest)
+            PB_CHECK_CUDA(cudaMemcpyAsync(tape + (int64_t)j * n_tok * d, x_in, sizeof(float) * (size_t)n_tok * d,
+                                          cudaMemcpyDeviceToDevice, st));
         half* kvb = s->kv + s->kv_block_elems * j;
         Epi base{};
         base.n_outl = 0;
@@ -584,6 +543,18 @@ extern "C" int pb_span_step(pb_span* span, int32_t n_tok, int32_t n_seq, const i
     int max_pos = 0;
     if (int rc = stage_meta(span, n_tok, n_seq, h_tok_seq, h_tok_pos, h_pages, &max_pos, st)) return rc;
     return run_blocks(span, n_tok, max_pos, d_in, d_out, st);
+}
+
+extern "C" int pb_span_step_tape(pb_span* span, int32_t n_tok, int32_t n_seq, const int32_t* h_tok_seq,
+                                 const int32_t* h_tok_pos, const int32_t* h_pages, const float* d_in, float* d_out,
+                                 float* d_tape, void* stream) {
+    PB_REQUIRE(span && d_tape, PB_ERR_BAD_REQUEST, "null argument");
+    std::lock_guard<std::mutex> lk(span->mu);
+    PB_CHECK_CUDA(cudaSetDevice(span->cfg.device));
+    auto st = (cudaStream_t)stream;
+    int max_pos = 0;
+    if (int rc = stage_meta(span, n_tok, n_seq, h_tok_seq, h_tok_pos, h_pages, &max_pos, st)) return rc;
+    return run_blocks(span, n_tok, max_pos, d_in, d_out, st, d_tape);
 }
 
 extern "C" int pb_span_step_int8(pb_span* span, int32_t n_tok, int32_t n_seq, const int32_t* h_tok_seq,

@@ -39,6 +39,7 @@ from .errors import (
     ERR_CAPACITY,
     ERR_DESYNC,
     ERR_UNKNOWN_SESSION,
+    ERR_UNKNOWN_TAPE,
     CapacityError,
     InputError,
     RemoteError,
@@ -54,6 +55,7 @@ log = logging.getLogger(__name__)
 DEFAULT_CAPACITY = 64
 DEFAULT_CACHE_BUDGET = 65536
 SESSION_IDLE_TIMEOUT_S = 120.0
+TAPE_TTL_S = 60.0  # server.py:43
 SERVER_VERSION = "0.1.0-b200"
 DEFAULT_NET_BYTES_PER_S = 1.25e8
 DEFAULT_TTL_MS = 30_000
@@ -250,6 +252,8 @@ class ServerNode:
         self.range: BlockRange | None = None
         self._sessions: dict = {}
         self._sessions_lock = threading.Lock()
+        self._tapes: dict[bytes, tuple[float, object]] = {}  # tape_id -> (born, device tape [B, n_blocks, t, d])
+        self._tapes_lock = threading.Lock()
         self._stop = threading.Event()
         self._registry: dict = {}
         self._registry_lock = threading.Lock()
@@ -397,6 +401,9 @@ class ServerNode:
                 victims = [self._sessions.pop(sid) for sid in stale]
             for v in victims:
                 self.span.release(v.seq)
+            with self._tapes_lock:  # server.py:230-233
+                for tid in [tid for tid, (born, _) in self._tapes.items() if now - born > TAPE_TTL_S]:
+                    del self._tapes[tid]
 
     def maybe_rebalance(self) -> bool:
         return False  # allocation/rebalancing is control plane (out of scope)
@@ -443,7 +450,7 @@ class ServerNode:
         if msg_type == MSG.FORWARD:
             return MSG.FORWARD, self._forward(payload)
         if msg_type == MSG.BACKWARD:
-            raise RemoteError(ERR_BAD_REQUEST, "BACKWARD is not served by the B200 span server")
+            return MSG.BACKWARD, self._backward(payload)
         if msg_type == MSG.ANNOUNCE:
             self._remember(json.loads(payload.decode()))
             return MSG.ANNOUNCE, b""
@@ -580,7 +587,27 @@ class ServerNode:
         if not finite:  # the reference computes NaN/inf and fails encoding the reply (wire.py:89-90)
             raise RemoteError(ERR_GENERIC, "internal error: non-finite tensor")
         try:
-            out = self.span.forward(batch)
+            out, tape = self.span.forward(batch, tape=True)
         except CapacityError as e:
             raise RemoteError(ERR_CAPACITY, str(e)) from e
-        return os.urandom(16) + codec.encode_tensor(out, self._reply_encoding())
+        tape_id = os.urandom(16)
+        with self._tapes_lock:  # server.py:426-428
+            self._tapes[tape_id] = (time.monotonic(), tape)
+        return tape_id + codec.encode_tensor(out, self._reply_encoding())
+
+    def _backward(self, payload: bytes) -> bytes:
+        """server.py:431-450: consume-once tape, f32 reply (gradients travel at full precision)."""
+        if len(payload) < 16:
+            raise RemoteError(ERR_BAD_REQUEST, "short BACKWARD payload")
+        with self._tapes_lock:
+            item = self._tapes.pop(payload[:16], None)
+        if item is None:
+            raise RemoteError(ERR_UNKNOWN_TAPE, "unknown or expired tape")
+        _, tape = item
+        try:
+            grad = codec.decode_tensor(payload[16:], device=self.span.device)
+        except SwarmError as e:
+            raise RemoteError(ERR_BAD_REQUEST, str(e)) from e
+        if grad.ndim != 3 or grad.shape[0] != tape.shape[0] or tuple(grad.shape[1:]) != tuple(tape.shape[2:]):
+            raise RemoteError(ERR_BAD_REQUEST, "BACKWARD grad shape mismatch")
+        return codec.encode_tensor(self.span.backward(tape, grad), codec.ENC_F32)

@@ -242,10 +242,12 @@ class BlockSpan:
             for s, t in zip(seqs, lens):
                 s.length += t
 
-    def forward(self, batch):
+    def forward(self, batch, tape: bool = False):
         """Cache-less forward of independent rows (server.py:411-429 semantics):
         batch [B, t, d] -> [B, t, d]. Rows are packed into steps of up to
-        max_tokens positions with temporary KV pages."""
+        max_tokens positions with temporary KV pages. With tape=True also
+        returns the FORWARD tape [B, n_blocks, t, d] (each hosted block's input
+        rows) that `backward` consumes."""
         import torch
 
         B, t, d = batch.shape
@@ -255,14 +257,51 @@ class BlockSpan:
         per = max(1, min(self.max_seqs, self.max_tokens // t if t <= self.max_tokens else 1))
         if t > self.max_tokens:
             raise CapacityError(f"t={t} exceeds the span's max_tokens={self.max_tokens}")
+        tp = torch.empty(B, self.n_blocks, t, d, device=self.device) if tape else None
         for r0 in range(0, B, per):
             rows = range(r0, min(B, r0 + per))
             seqs = [Sequence() for _ in rows]
             try:
-                res = self.step([(s, batch[r]) for s, r in zip(seqs, rows)])
-                for r, y in zip(rows, res):
-                    out[r] = y
+                if tape:
+                    n = len(rows)
+                    x = batch[r0:r0 + n].reshape(n * t, d).to(device=self.device, dtype=torch.float32).contiguous()
+                    y = torch.empty_like(x)
+                    buf = torch.empty(self.n_blocks, n * t, d, device=self.device)
+                    with self._lock:
+                        for s in seqs:
+                            self._reserve(s, t)
+                        n_tok, tok_seq, tok_pos, pages = self._meta(seqs, [t] * n)
+                        st = _lib.stream_ptr(torch.cuda.current_stream(self.device))
+                        _lib.check(_lib.lib().pb_span_step_tape(
+                            self._h, n_tok, n, tok_seq.ctypes.data, tok_pos.ctypes.data, pages.ctypes.data,
+                            _lib.ptr(x), _lib.ptr(y), _lib.ptr(buf), st))
+                        for s in seqs:
+                            s.length += t
+                    out[r0:r0 + n] = y.view(n, t, d)
+                    tp[r0:r0 + n] = buf.view(self.n_blocks, n, t, d).transpose(0, 1)
+                else:
+                    res = self.step([(s, batch[r]) for s, r in zip(seqs, rows)])
+                    for r, y in zip(rows, res):
+                        out[r] = y
             finally:
                 for s in seqs:
                     self.release(s)
+        return (out, tp) if tape else out
+
+    def backward(self, tape, grad):
+        """BACKWARD (server.py:431-450): dL/d(span input) [B, t, d] from the
+        FORWARD tape [B, n_blocks, t, d] and dL/d(span output) [B, t, d], one
+        row at a time through the hosted blocks in reverse (model.py:383-418)."""
+        import torch
+
+        B, nb, t, d = tape.shape
+        if nb != self.n_blocks or grad.shape != (B, t, d):
+            raise InputError("BACKWARD grad shape mismatch")
+        g = grad.to(device=self.device, dtype=torch.float32).contiguous()
+        tape = tape.contiguous()
+        out = torch.empty_like(g)
+        st = _lib.stream_ptr(torch.cuda.current_stream(self.device))
+        for r in range(B):
+            _lib.check(_lib.lib().pb_span_backward(self._h, _lib.ptr(tape[r]), t, _lib.ptr(g[r]), _lib.ptr(out[r]),
+                                                   st))
         return out

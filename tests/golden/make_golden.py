@@ -194,6 +194,35 @@ def make_blocks():
     np.savez_compressed(os.path.join(OUT, "blocks.npz"), **out)
 
 
+def make_train():
+    """FORWARD tapes + BACKWARD (server.py:411-450): per row, block_forward with
+    want_tape over every block (fp32 weights, empty cache), then block_backward
+    in reverse (model.py:383-418) for a random upstream gradient."""
+    out = {}
+    for name, kw in (("tiny", TINY), ("small", SMALL), ("mid", MID)):
+        cfg = M.ModelConfig(**kw)
+        ckpt = M.gen_checkpoint(42, cfg)
+        rng = np.random.default_rng(100 + len(name))
+        B, t = 2, 7
+        batch = np.stack([M.embed(ckpt, rng.integers(0, cfg.vocab, t)) for _ in range(B)])
+        grad = rng.uniform(-1, 1, (B, t, cfg.hidden)).astype(np.float32)
+        fwd = np.empty_like(batch)
+        gin = np.empty_like(batch)
+        for r in range(B):
+            h, tapes = batch[r], []
+            for b in ckpt.blocks:
+                h, _, tape = M.block_forward(b, h, M.KvCache.empty(cfg), 0, cfg, want_tape=True)
+                tapes.append(tape)
+            fwd[r] = h
+            g = grad[r]
+            for b, tape in zip(reversed(ckpt.blocks), reversed(tapes)):
+                g = M.block_backward(b, tape, g, cfg)
+            gin[r] = g
+        out[f"{name}_batch"], out[f"{name}_grad"] = batch, grad
+        out[f"{name}_fwd"], out[f"{name}_grad_in"] = fwd, gin
+    np.savez_compressed(os.path.join(OUT, "train.npz"), **out)
+
+
 def make_c2():
     """Config 2 (BLOOM-560M shape, 24 blocks, h=1024, H=16): int8-weights
     greedy generation with a 128-token prefix, reference qw semantics.
@@ -206,7 +235,7 @@ def make_c2():
 
 
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["codec", "weights", "blocks", "c2"]
+    what = sys.argv[1:] or ["codec", "weights", "blocks", "train", "c2"]
     for w in what:
         print("making", w, flush=True)
         globals()[f"make_{w}"]()

@@ -127,3 +127,24 @@ def test_generate_tokens_match_reference(golden, name):
     shape = SHAPES[name]
     assert O.generate(42, shape, [1, 2, 3], 16, quantized=False) == g[f"{name}_gen_f32"].tolist()
     assert O.generate(42, shape, [1, 2, 3], 16, quantized=True) == g[f"{name}_gen_qw"].tolist()
+
+
+def test_oracle_backward_matches_reference_golden(golden):
+    """oracle.block_backward (recompute from the tape) == the reference's
+    FORWARD/BACKWARD (server.py:411-450) on the same rows (f32; tolerance for
+    numpy summation order only)."""
+    g = golden("train")
+    for name, shape in (("tiny", O.Shape(2, 8, 2, 32, 64)), ("small", O.Shape(4, 16, 2, 32, 128)),
+                        ("mid", O.Shape(3, 256, 4, 512, 256))):
+        blocks = [O.make_block(42, shape, i) for i in range(shape.n_layers)]
+        for r in range(g[f"{name}_batch"].shape[0]):
+            h, tapes = g[f"{name}_batch"][r], []
+            for blk in blocks:
+                tapes.append(h)
+                h = O.block_step(blk, h, O.KV(shape), 0, shape)
+            np.testing.assert_allclose(h, g[f"{name}_fwd"][r], rtol=1e-5, atol=1e-5)
+            gr = g[f"{name}_grad"][r]
+            for blk, x in zip(reversed(blocks), reversed(tapes)):
+                gr = O.block_backward(blk, x, gr, shape)
+            want = g[f"{name}_grad_in"][r]
+            assert np.max(np.abs(gr - want)) <= 1e-5 * max(np.max(np.abs(want)), 1.0), name

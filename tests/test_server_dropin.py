@@ -267,3 +267,71 @@ def test_nonfinite_step_matches_reference(swarm):
                        raw_step(node.address, sid, 3, bad), raw_step(node.address, sid, 4, embed(ck, [5]))]
     assert codes["b200"] == codes["ref"], codes
     assert codes["ref"][0] == 0 and codes["ref"][1] != 0
+
+
+def test_forward_backward_matches_reference_server(swarm):
+    """tests/test_server.py:195-210 over the wire, B200 server vs the
+    reference server on the same checkpoint (f32 weights): activations and
+    input gradients within 1e-3 (the reference pins numpy's own arithmetic
+    bit-exactly; the span carries an fp16 KV cache in FORWARD)."""
+    from swarmlm.transport import ENC_F32, MSG, decode_tensor, encode_tensor, rpc_call
+
+    rng = np.random.default_rng(0)
+    batch = rng.uniform(-0.5, 0.5, (2, 3, 16)).astype(np.float32)
+    grad = rng.uniform(-1, 1, (2, 3, 16)).astype(np.float32)
+    res = {}
+    for kind, node in (("ref", swarm.reference((1, 3))), ("b200", swarm.b200((1, 3)))):
+        reply = rpc_call(node.address, MSG.FORWARD, encode_tensor(batch, ENC_F32), 10000.0)
+        tape_id, acts = reply[:16], decode_tensor(reply[16:])
+        gin = decode_tensor(rpc_call(node.address, MSG.BACKWARD, tape_id + encode_tensor(grad, ENC_F32), 10000.0))
+        res[kind] = (acts, gin)
+    for a, b in zip(res["b200"], res["ref"]):
+        assert float(np.max(np.abs(a - b))) <= 1e-3 * float(np.abs(b).max())
+
+
+def test_backward_consume_once_and_zero_grad(swarm):
+    """tests/test_server.py:212-236: a tape serves one BACKWARD
+    (ERR_UNKNOWN_TAPE after), a zero gradient gives an exactly zero reply."""
+    from swarmlm.errors import ERR_UNKNOWN_TAPE, RemoteError
+    from swarmlm.transport import ENC_F32, MSG, decode_tensor, encode_tensor, rpc_call
+
+    node = swarm.b200((0, 4))
+    rng = np.random.default_rng(1)
+    batch = rng.uniform(-0.5, 0.5, (1, 2, 16)).astype(np.float32)
+    reply = rpc_call(node.address, MSG.FORWARD, encode_tensor(batch, ENC_F32), 10000.0)
+    zero = encode_tensor(np.zeros_like(batch), ENC_F32)
+    gin = decode_tensor(rpc_call(node.address, MSG.BACKWARD, reply[:16] + zero, 10000.0))
+    assert np.array_equal(gin, np.zeros_like(batch))
+    with pytest.raises(RemoteError) as ei:
+        rpc_call(node.address, MSG.BACKWARD, reply[:16] + zero, 10000.0)
+    assert ei.value.code == ERR_UNKNOWN_TAPE
+    with pytest.raises(RemoteError) as ei:
+        rpc_call(node.address, MSG.BACKWARD, os.urandom(16) + zero, 10000.0)
+    assert ei.value.code == ERR_UNKNOWN_TAPE
+
+
+def test_distributed_backward_matches_reference_client(small_ckpt):
+    """The reference client's DistributedModel.forward/backward (client.py:417-498)
+    over two B200 spans equals the same calls over two reference servers."""
+    from swarmlm.client import DistributedModel
+
+    rng = np.random.default_rng(5)
+    batch = rng.uniform(-0.5, 0.5, (2, 4, 16)).astype(np.float32)
+    grad = rng.uniform(-1, 1, (2, 4, 16)).astype(np.float32)
+    outs = {}
+    for kind in ("ref", "b200"):
+        sw = Swarm(small_ckpt)
+        try:
+            for r in ((0, 2), (2, 4)):
+                (sw.reference if kind == "ref" else sw.b200)(r)
+            cl = sw.client()
+            try:
+                dm = DistributedModel(cl)
+                h, handles = dm.forward(batch)
+                outs[kind] = (h, dm.backward(handles, grad))
+            finally:
+                cl.close()
+        finally:
+            sw.close()
+    for a, b in zip(outs["b200"], outs["ref"]):
+        assert float(np.max(np.abs(a - b))) <= 1e-3 * float(np.abs(b).max())
