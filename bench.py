@@ -52,6 +52,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--synthetic-kv", action="store_true", help="skip the real prefill (KV content is synthetic)")
+    p.add_argument("--forward-rows", type=int, default=2, help="rows of the FORWARD sample (C5 shape: 512 tokens each)")
     return p.parse_args()
 
 
@@ -209,7 +210,7 @@ class Pipeline:
         pages_per_seq = -(-cfg.max_seq // 64)
         t0 = time.perf_counter()
         self.span = BlockSpan(cfg, s, e, int8=True, page_tokens=64, n_pages=self.S * self.B * pages_per_seq + 2,
-                              max_tokens=self.chunk * self.B, max_seqs=self.B, device=self.local)
+                              max_tokens=max(self.chunk * self.B, 512), max_seqs=max(self.B, 2), device=self.local)
         self.span.generate_weights(args.seed)
         torch.cuda.synchronize()
         self.gen_s = time.perf_counter() - t0
@@ -381,6 +382,33 @@ def run_ours(args):
         e2e = {"value": K * S * B / (float(te.item()) / 1e3), "unit": unit, "h2d_bytes_per_step": 4 * d * B,
                "d2h_bytes_per_step": d * B, "path": "pb_span_step_int8 C-ABI with pinned host ingress (span 0) and "
                "egress of the int8 hidden (last span), NCCL int8 hops between spans"}
+    # ---- FORWARD sample (C5 shape: rows of 512 tokens through this rank's span, tcgen05 path;
+    # server.py:411-429 semantics, no tape), timed with CUDA events; each rank its own span
+    fwd = None
+    if args.forward_rows > 0:
+        rows, t = args.forward_rows, 512
+        xb = torch.randn(rows, t, cfg.hidden, device=pl.dev) * 0.05
+        pl.span.forward(xb)  # warm-up
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        pl.span.forward(xb)
+        f1.record()
+        torch.cuda.synchronize()
+        f_ms = f0.elapsed_time(f1)
+        pl.span.profile(True)  # separate pass: per-kernel shares
+        pl.span.forward(xb)
+        torch.cuda.synchronize()
+        g_ms, g_n, g_ops = pl.span.profile_read(5)
+        a_ms, _, _ = pl.span.profile_read(pl.span.PROF_ATTN)
+        pl.span.profile(False)
+        s0, s1 = pl.ranges[rank]
+        useful = 2.0 * rows * t * (s1 - s0) * 12 * cfg.hidden * cfg.hidden
+        fwd = {"rows": rows, "tokens_per_row": t, "blocks": s1 - s0, "ms": f_ms,
+               "tokens_per_s": rows * t / (f_ms / 1e3), "useful_tflops": useful / (f_ms / 1e3) / 1e12,
+               "tcgen05_share": g_ms / f_ms, "attention_share": a_ms / f_ms,
+               "note": "FORWARD of rows x 512 tokens through this GPU's span (C5 row shape); useful flops = "
+                       "2*tokens*12h^2 per block (matmuls only; profile pass for the shares)"}
     # ---- report (rank 0)
     if rank != 0:
         if pl.dist:
@@ -431,6 +459,7 @@ def run_ours(args):
                                      "peak_tflops_dense_bf16_measured": measured_tflops(),
                                      "note": "kind::i8 ops issued (3 int8 digit columns per token); useful = "
                                              "2*M*K*tokens of the reference matmul"}},
+        "forward": fwd,
         "device_bytes": pl.span.device_bytes,
     }
     if not args.no_cpu_baseline and N == 1:

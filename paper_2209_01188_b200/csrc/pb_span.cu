@@ -422,7 +422,8 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
         AttnArgs aa{s->q, kvb, s->d_tok_seq, s->d_tok_pos, s->d_pages, s->slopes, s->ctx, s->attn_part,
                     s->counters + (1 << 19), int8 ? s->tokmax_ctx : nullptr, int8 ? b.mat[1].scales : nullptr,
                     n_tok, s->max_pages, s->H, s->dh, s->cfg.page_tokens, d, max_pos, s->last_n_seq == n_tok ? 1 : 0,
-                    s->d_grp_first, s->d_grp_count, s->n_groups, s->d_unit_base, s->total_units, s->max_stages};
+                    s->d_grp_first, s->d_grp_count, s->n_groups, s->d_unit_base, s->total_units, s->max_stages,
+                    s->max_group};
         {
             const int ev = prof_begin(s, st);
             if (int rc = launch_attention(aa, s->attn_cap, st)) return rc;
@@ -504,7 +505,7 @@ static int stage_meta(pb_span* s, int n_tok, int n_seq, const int32_t* tok_seq, 
     int32_t* gc = gf + n_tok;
     int ng = 0;
     for (int i = 0; i < n_tok; ++i) {
-        if (ng > 0 && tok_seq[i] == tok_seq[i - 1] && tok_pos[i] == tok_pos[i - 1] + 1 && gc[ng - 1] < 8) {
+        if (ng > 0 && tok_seq[i] == tok_seq[i - 1] && tok_pos[i] == tok_pos[i - 1] + 1 && gc[ng - 1] < 32) {
             ++gc[ng - 1];
         } else {
             gf[ng] = i;
@@ -528,6 +529,9 @@ static int stage_meta(pb_span* s, int n_tok, int n_seq, const int32_t* tok_seq, 
     ub[ng] = tot;
     s->total_units = tot;
     s->max_stages = mst;
+    int mg_ = 0;
+    for (int g = 0; g < ng; ++g) mg_ = std::max(mg_, (int)gc[g]);
+    s->max_group = mg_;
     PB_CHECK_CUDA(cudaMemcpyAsync(s->d_unit_base, ub, sizeof(int64_t) * (ng + 1), cudaMemcpyHostToDevice, st));
     PB_CHECK_CUDA(cudaEventRecord(s->meta_ev[slot], st));
     return PB_OK;

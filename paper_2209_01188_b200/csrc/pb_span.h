@@ -138,13 +138,14 @@ struct AttnArgs {
     int n_tok, max_pages, H, dh, P, d;
     int max_pos;             // max over tokens of (pos + 1)
     int decode_only;         // every sequence adds one position (older keys are safe to prefetch early)
-    const int32_t* grp_first;  // query groups: up to 8 consecutive positions of one sequence
+    const int32_t* grp_first;  // query groups: up to 32 consecutive positions of one sequence
     const int32_t* grp_count;
     int n_groups;
     // stream-K units of the tensor-core kernel: (group, head, 64-key stage)
     const int64_t* unit_base;  // [n_groups + 1] first unit of each group
     int64_t total_units;
     int max_stages;            // max over groups of ceil(keys / 64)
+    int max_group;             // largest query group (> 8: the prefill kernel, queries split across warps)
     int debug_nocomp = 0;      // experiment knob (PB_ATT_NOCOMP): skip the math, stream only
 };
 int launch_attention(const AttnArgs& a, int64_t part_cap, cudaStream_t st);

@@ -39,6 +39,7 @@ struct pb_span {
     int64_t* d_unit_base = nullptr;  // stream-K attention units per query group
     int64_t total_units = 0;
     int max_stages = 0;
+    int max_group = 0;
     static constexpr int NSLOT = 4;  // ring of pinned staging buffers (no host sync per step)
     int32_t* h_meta[NSLOT] = {nullptr, nullptr, nullptr, nullptr};
     int64_t* h_ub[NSLOT] = {nullptr, nullptr, nullptr, nullptr};
