@@ -386,6 +386,9 @@ def run_ours(args):
     # server.py:411-429 semantics, no tape), timed with CUDA events; each rank its own span
     fwd = None
     if args.forward_rows > 0:
+        for grp in pl.seqs:  # decode sessions are done: their KV pages host the FORWARD rows
+            for sq in grp:
+                pl.span.release(sq)
         rows, t = args.forward_rows, 512
         xb = torch.randn(rows, t, cfg.hidden, device=pl.dev) * 0.05
         pl.span.forward(xb)  # warm-up
@@ -426,7 +429,7 @@ def run_ours(args):
     line = {
         "metric": metric, "value": value, "unit": unit, "n_gpus": N, "steps": K, "warmup": W,
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "int8 weights x fp16(hi+lo) activations, fp32 accumulate; fp16 KV",
+        "dtype": "int8 weights x int8-digit activations (22-bit fixed point, exact s32 accumulate); fp16 KV; f32 residual",
         "data": "synthetic (gen_checkpoint seed 42 weights generated on device; random embedding-like inputs)",
         "config": {"workload": f"{args.shape} ({cfg.n_layers} blocks, h={cfg.hidden}) int8 decode, {S} micro-batch(es) "
                                f"of {B} batch-1 session(s) pipelined over {N} GPU span(s) {pl.ranges}, "
