@@ -226,6 +226,7 @@ class Pipeline:
         self.inputs = torch.randn(64, d, generator=g, device=self.dev) * 0.05  # embedding-like rows
         self.launches = 0
         self.total_jobs = 0
+        self.jobtimes = [] if os.environ.get("PB_BENCH_JOBTIMES") else None  # diagnostic: per-job device times
 
     def payload_bytes(self, t):
         n = t * self.B * self.d
@@ -254,11 +255,18 @@ class Pipeline:
         tmap = dict(jobs)
         r, N = self.rank, self.world
 
+        jt = self.jobtimes
+
         def step(j, inbox):
+            if jt is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                jt.append(e)
             t = tmap[j]
             n = t * self.B
             seqs = self.seqs[j % self.S]
-            oc, os_ = self.views(self.outbox, t)
+            outbox = self.outbox
+            oc, os_ = self.views(outbox, t)
             if inbox is None or r == 0:  # span 0: fresh input (a received ring payload only orders the step)
                 if host_in is not None:
                     self.out[:n].copy_(host_in[:n], non_blocking=True)
@@ -273,6 +281,10 @@ class Pipeline:
                 self.span.step_codes(seqs, [t] * self.B, in_codes=ic, in_scales=is_, out_codes=oc, out_scales=os_,
                                      out_f32=self.out[:n])
             self.launches += self.span.last_launches
+            if jt is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                jt.append(e)
             if r == N - 1 and host_out is not None:
                 host_out[:n * self.d].copy_(oc, non_blocking=True)
                 if sync_out:
@@ -281,8 +293,8 @@ class Pipeline:
                 # ring back-edge: only orders span 0's next step of this session
                 # (stand-in for the client's LM head); fixed size, so prefill
                 # chunks and decode steps of different t always match
-                return self.outbox[:RING_BYTES]
-            return self.outbox[:self.payload_bytes(t)]
+                return outbox[:RING_BYTES]
+            return outbox[:self.payload_bytes(t)]
 
         run_jobs(sched, [j for j, _ in jobs], step, torch_exchange,
                  lambda j: self.inbox[:RING_BYTES] if r == 0 else self.inbox[:self.payload_bytes(tmap[j])])
@@ -343,6 +355,13 @@ def run_ours(args):
         pl.barrier()
     jbase += K * S
     ms = start.elapsed_time(stop)
+    if pl.jobtimes is not None:
+        ev = pl.jobtimes[-2 * K * S:]
+        busy = [ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(K * S)]
+        gaps = [ev[2 * i - 1].elapsed_time(ev[2 * i]) for i in range(1, K * S)]
+        print(f"[rank {rank}] job busy ms mean {statistics.mean(busy):.3f} max {max(busy):.3f} | "
+              f"gap ms mean {statistics.mean(gaps):.3f} max {max(gaps):.3f}", file=sys.stderr, flush=True)
+        pl.jobtimes = None
     launches = pl.launches
     # ---- live per-kernel device times (CUDA events around every launch on the
     # launching stream) over a second, identical pass of K steps; kept out of
