@@ -90,11 +90,32 @@ def encode_header(encoding: int, shape) -> bytes:
     return struct.pack(">BB", encoding, len(shape)) + b"".join(struct.pack(">I", d) for d in shape)
 
 
-def encode_tensor(t, encoding: int = ENC_F32, block_size: int = 64) -> bytes:
-    """TensorMsg bytes (transport/wire.py:87-106). `t` may be a numpy array or a
-    CUDA tensor; int8 encoding runs on the GPU."""
+_PINNED: dict = {}
+
+
+def _pinned(nbytes: int):
+    """Reusable pinned host staging buffer (one per thread, grown on demand)."""
+    import threading
+
     import torch
 
+    key = threading.get_ident()
+    buf = _PINNED.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8).pin_memory()
+        _PINNED[key] = buf
+    return buf
+
+
+def encode_tensor(t, encoding: int = ENC_F32, block_size: int = 64) -> bytes:
+    """TensorMsg bytes (transport/wire.py:87-106). `t` may be a numpy array or a
+    CUDA tensor; int8 encoding runs on the GPU. A CUDA tensor leaves the device
+    in one pinned copy (codes, scales and the finiteness flag together, one
+    stream synchronization)."""
+    import torch
+
+    if encoding not in (ENC_F32, ENC_INT8):
+        raise InputError(f"unknown tensor encoding {encoding}")
     if isinstance(t, np.ndarray):
         arr = np.asarray(t, np.float32)
         shape = arr.shape
@@ -103,24 +124,44 @@ def encode_tensor(t, encoding: int = ENC_F32, block_size: int = 64) -> bytes:
     else:
         arr = None
         shape = tuple(t.shape)
-        if not bool(torch.isfinite(t).all()):
-            raise InputError("non-finite tensor")
     if len(shape) > 255:
         raise InputError("too many dimensions")
     n = int(np.prod(shape)) if shape else 1
     if n and n * 4 > MAX_PAYLOAD:
         raise InputError("tensor exceeds frame cap")
     head = encode_header(encoding, shape)
-    if encoding == ENC_F32:
-        if arr is None:
-            arr = t.detach().to(torch.float32).cpu().numpy()
-        return head + np.ascontiguousarray(arr, "<f4").tobytes()
-    if encoding == ENC_INT8:
-        src = torch.as_tensor(arr) if arr is not None else t
-        q = quantize_blockwise(src, block_size)
+    if arr is not None:
+        if encoding == ENC_F32:
+            return head + np.ascontiguousarray(arr, "<f4").tobytes()
+        q = quantize_blockwise(torch.as_tensor(arr), block_size)
         return (head + struct.pack(">I", block_size) + q.scales.cpu().numpy().astype("<f4").tobytes()
                 + q.codes.cpu().numpy().tobytes())
-    raise InputError(f"unknown tensor encoding {encoding}")
+    x = t.detach().to(torch.float32).contiguous()
+    stream = torch.cuda.current_stream(x.device)
+    flag = (~torch.isfinite(x)).any().to(torch.uint8).reshape(1)
+    if encoding == ENC_F32:
+        buf = _pinned(4 * n + 1)
+        buf[:4 * n].view(torch.float32).copy_(x.reshape(-1), non_blocking=True)
+        buf[4 * n:4 * n + 1].copy_(flag, non_blocking=True)
+        stream.synchronize()
+        if buf[4 * n].item():
+            raise InputError("non-finite tensor")
+        return head + buf[:4 * n].numpy().tobytes()
+    if block_size < 1:
+        raise InputError("block_size must be >= 1")
+    nb = max(1, math.ceil(n / block_size)) if n else 0
+    scales = torch.empty(nb, dtype=torch.float32, device=x.device)
+    codes = torch.empty(n, dtype=torch.int8, device=x.device)
+    _lib.check(_lib.lib().pb_quantize_blockwise(_lib.ptr(x), n, block_size, _lib.ptr(codes), _lib.ptr(scales),
+                                                _lib.stream_ptr(stream)))
+    buf = _pinned(4 * nb + n + 1)
+    buf[:4 * nb].view(torch.float32).copy_(scales, non_blocking=True)
+    buf[4 * nb:4 * nb + n].view(torch.int8).copy_(codes, non_blocking=True)
+    buf[4 * nb + n:4 * nb + n + 1].copy_(flag, non_blocking=True)
+    stream.synchronize()
+    if buf[4 * nb + n].item():
+        raise InputError("non-finite tensor")
+    return head + struct.pack(">I", block_size) + buf[:4 * nb + n].numpy().tobytes()
 
 
 def parse_tensor(data: bytes):

@@ -799,43 +799,105 @@ int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, i
 }
 
 // ------------------------------------------------------------------ f32-weights path
-// quantize in {none, activations}: reference fp32 matmul x @ W, W [K, M] row-major.
-constexpr int F32_TOK = 8;
+// quantize in {none, activations} (the reference's default server mode): fp32
+// x @ W with W [K, M] row-major as in the checkpoint. Memory-bound split-K GEMV:
+// a CTA streams a k-range of 1024 output columns with 128-bit non-allocating
+// loads (8 in flight per thread), up to F32_T tokens per pass from shared
+// memory; partial sums go to a workspace and a second kernel adds the splits in
+// fixed order and runs the fused epilogue.
+constexpr int F32_T = 8;       // tokens per pass
+constexpr int F32_KB = 128;    // k rows staged per shared-memory refill
 
-__global__ void __launch_bounds__(128) k_gemm_f32(const float* __restrict__ w, int K, int M, const float* __restrict__ y,
-                                                  int n_tok, Epi epi) {
-    __shared__ float ys[F32_TOK][64];
-    const int o = blockIdx.x * 128 + threadIdx.x;
-    const int tok0 = blockIdx.y * F32_TOK;
-    float acc[F32_TOK];
+template <int T>
+__global__ void __launch_bounds__(256) k_gemv_f32(const float* __restrict__ w, int K, int M,
+                                                  const float* __restrict__ y, int n_tok, int tok0, int kchunk,
+                                                  float* __restrict__ part) {
+    __shared__ float ys[T][F32_KB];
+    const int o = (blockIdx.x * 256 + threadIdx.x) * 4;
+    const int k0 = blockIdx.y * kchunk, k1 = min(K, k0 + kchunk);
+    const bool vec = (M & 3) == 0 && o + 3 < M;
+    float acc[T][4];
 #pragma unroll
-    for (int j = 0; j < F32_TOK; ++j) acc[j] = 0.f;
-    for (int k0 = 0; k0 < K; k0 += 64) {
+    for (int j = 0; j < T; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[j][c] = 0.f;
+    for (int kb = k0; kb < k1; kb += F32_KB) {
         __syncthreads();
-        for (int t = threadIdx.x; t < F32_TOK * 64; t += 128) {
-            const int j = t / 64, kk = t % 64;
-            const int tok = tok0 + j, k = k0 + kk;
-            ys[j][kk] = (tok < n_tok && k < K) ? y[(int64_t)tok * K + k] : 0.f;
+        for (int e = threadIdx.x; e < T * F32_KB; e += 256) {
+            const int j = e / F32_KB, kk = e % F32_KB;
+            const int tok = tok0 + j, k = kb + kk;
+            ys[j][kk] = (tok < n_tok && k < k1) ? y[(int64_t)tok * K + k] : 0.f;
         }
         __syncthreads();
+        const int kend = min(F32_KB, k1 - kb);
         if (o < M) {
-            const int kend = min(64, K - k0);
+#pragma unroll 8
             for (int kk = 0; kk < kend; ++kk) {
-                const float wv = w[(int64_t)(k0 + kk) * M + o];
+                const float* row = w + (int64_t)(kb + kk) * M + o;
+                float4 wv;
+                if (vec) {
+                    const int4 r = ld_stream_v4(row);
+                    wv = make_float4(__int_as_float(r.x), __int_as_float(r.y), __int_as_float(r.z), __int_as_float(r.w));
+                } else {
+                    wv.x = row[0];
+                    wv.y = o + 1 < M ? row[1] : 0.f;
+                    wv.z = o + 2 < M ? row[2] : 0.f;
+                    wv.w = o + 3 < M ? row[3] : 0.f;
+                }
 #pragma unroll
-                for (int j = 0; j < F32_TOK; ++j) acc[j] = fmaf(ys[j][kk], wv, acc[j]);
+                for (int j = 0; j < T; ++j) {
+                    const float xv = ys[j][kk];
+                    acc[j][0] = fmaf(xv, wv.x, acc[j][0]);
+                    acc[j][1] = fmaf(xv, wv.y, acc[j][1]);
+                    acc[j][2] = fmaf(xv, wv.z, acc[j][2]);
+                    acc[j][3] = fmaf(xv, wv.w, acc[j][3]);
+                }
             }
         }
     }
     if (o >= M) return;
-    for (int j = 0; j < F32_TOK; ++j)
-        if (tok0 + j < n_tok) epi_store(epi, tok0 + j, o, acc[j]);
+    float* p = part + (int64_t)blockIdx.y * F32_T * M;
+#pragma unroll
+    for (int j = 0; j < T; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (o + c < M) p[(int64_t)j * M + o + c] = acc[j][c];
 }
 
-int launch_gemm_f32(const Mat& m, const float* y, int n_tok, const Epi& epi, cudaStream_t st) {
-    dim3 grid((unsigned)ceil_div(m.M, 128), (unsigned)ceil_div(n_tok, F32_TOK));
-    k_gemm_f32<<<grid, 128, 0, st>>>(m.w32, m.K, m.M, y, n_tok, epi);
-    return launch_check("gemm_f32");
+__global__ void k_reduce_f32(const float* __restrict__ part, int S, int M, int n_tok, int tok0, Epi epi) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, tok = tok0 + j;
+    if (o >= M || tok >= n_tok) return;
+    float v = 0.f;
+    for (int s2 = 0; s2 < S; ++s2) v += part[((int64_t)s2 * F32_T + j) * M + o];
+    epi_store(epi, tok, o, v);
+}
+
+int launch_gemm_f32(const Mat& m, const float* y, int n_tok, const Epi& epi, float* part, int64_t part_cap,
+                    cudaStream_t st) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int gx = (int)ceil_div(m.M, 1024);
+    int S = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(4 * sms, gx), ceil_div(m.K, F32_KB)));
+    while (S > 1 && (int64_t)S * F32_T * m.M > part_cap) --S;
+    const int kchunk = (int)round_up(ceil_div(m.K, S), 4);
+    S = (int)ceil_div(m.K, kchunk);
+    for (int tok0 = 0; tok0 < n_tok; tok0 += F32_T) {
+        const int nt = std::min(F32_T, n_tok - tok0);
+        const dim3 grid((unsigned)gx, (unsigned)S);
+        if (nt == 1) k_gemv_f32<1><<<grid, 256, 0, st>>>(m.w32, m.K, m.M, y, n_tok, tok0, kchunk, part);
+        else if (nt == 2) k_gemv_f32<2><<<grid, 256, 0, st>>>(m.w32, m.K, m.M, y, n_tok, tok0, kchunk, part);
+        else if (nt <= 4) k_gemv_f32<4><<<grid, 256, 0, st>>>(m.w32, m.K, m.M, y, n_tok, tok0, kchunk, part);
+        else k_gemv_f32<F32_T><<<grid, 256, 0, st>>>(m.w32, m.K, m.M, y, n_tok, tok0, kchunk, part);
+        if (int rc = launch_check("gemv_f32")) return rc;
+        k_reduce_f32<<<dim3((unsigned)ceil_div(m.M, 256), (unsigned)std::min(F32_T, n_tok - tok0)), 256, 0, st>>>(
+            part, S, m.M, n_tok, tok0, epi);
+        if (int rc = launch_check("reduce_f32")) return rc;
+    }
+    return PB_OK;
 }
 
 }  // namespace pb

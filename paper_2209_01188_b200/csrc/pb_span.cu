@@ -146,7 +146,7 @@ int pb_span_create(const pb_span_config* cfg, pb_span** out) {
     if (!rc) rc = dalloc(s, &s->tokmax_ctx, NT);
     if (!rc) rc = dalloc(s, &s->tokmax_act, NT);
     s->partial_cap = (int64_t)8 << 20;
-    if (!rc && int8) rc = dalloc(s, &s->partials, s->partial_cap);
+    if (!rc) rc = dalloc(s, &s->partials, s->partial_cap);
     if (!rc) rc = dalloc(s, &s->counters, 1 << 20);
     s->attn_cap = attention_part_floats(NT, s->H, s->dh, cfg->max_seq);
     if (!rc) rc = dalloc(s, &s->attn_part, s->attn_cap);
@@ -397,9 +397,9 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
             if (int rc = launch_prologue(mode, ProSrc{}, x, n_tok, K, K, g, be, m, tc, nullptr, s->back, s->stats,
                                          nullptr, s->y32, st))
                 return rc;
-            launches += mode == PRO_LN ? 3 : 1;  // (rowstats + rows) + gemm
+            launches += (mode == PRO_LN ? 2 : 0) + 2 * (int)ceil_div(n_tok, 8);  // (rowstats + rows) + gemv/reduce passes
             const int ev = prof_begin(s, st);
-            int rc = launch_gemm_f32(m, s->y32, n_tok, e, st);
+            int rc = launch_gemm_f32(m, s->y32, n_tok, e, s->partials, s->partial_cap, st);
             prof_end(s, ev, 3, 4.0 * m.M * m.K, st);
             return rc;
         };

@@ -119,7 +119,8 @@ int bound_consts(const float* gamma, const float* beta, const float* scales, int
                  cudaStream_t st);
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
                 int64_t partial_cap, cudaStream_t st);
-int launch_gemm_f32(const Mat& m, const float* y, int n_tok, const Epi& epi, cudaStream_t st);
+int launch_gemm_f32(const Mat& m, const float* y, int n_tok, const Epi& epi, float* part, int64_t part_cap,
+                    cudaStream_t st);
 int choose_tc(int n_tok);
 
 // attention over the paged cache

@@ -56,6 +56,7 @@ DEFAULT_CAPACITY = 64
 DEFAULT_CACHE_BUDGET = 65536
 SESSION_IDLE_TIMEOUT_S = 120.0
 TAPE_TTL_S = 60.0  # server.py:43
+_TIMING = os.environ.get("PB_SERVER_TIMING") == "1"  # diagnostic: per-STEP decode / compute / encode seconds
 SERVER_VERSION = "0.1.0-b200"
 DEFAULT_NET_BYTES_PER_S = 1.25e8
 DEFAULT_TTL_MS = 30_000
@@ -252,6 +253,7 @@ class ServerNode:
         self.range: BlockRange | None = None
         self._sessions: dict = {}
         self._sessions_lock = threading.Lock()
+        self.timing: list = []  # PB_SERVER_TIMING diagnostics
         self._tapes: dict[bytes, tuple[float, object]] = {}  # tape_id -> (born, device tape [B, n_blocks, t, d])
         self._tapes_lock = threading.Lock()
         self._stop = threading.Event()
@@ -539,7 +541,10 @@ class ServerNode:
                 session.poisoned = True
                 session.position += t
                 raise RemoteError(ERR_GENERIC, "internal error: non-finite tensor")
+            tm = [time.perf_counter()] if _TIMING else None
             x = codec.decode_tensor(payload[20:], device=self.span.device)
+            if tm:
+                tm.append(time.perf_counter())
             try:
                 out = self.sched.run(session.seq, x)
             except CapacityError as e:
@@ -547,8 +552,13 @@ class ServerNode:
             except InputError as e:
                 raise RemoteError(ERR_BAD_REQUEST, str(e)) from e
             session.position += t
+            if tm:
+                tm.append(time.perf_counter())
             reply = codec.encode_tensor(out, self._reply_encoding())
             session.last_step = (start_pos, digest, reply)
+            if tm:
+                tm.append(time.perf_counter())
+                self.timing.append(tuple(b - a for a, b in zip(tm, tm[1:])))
         self._enforce_cache_budget()
         return reply
 
