@@ -32,8 +32,12 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "BLOOM-176B int8 decode steps/s (b=1)"
-METRIC_B = "BLOOM-176B int8 decode tokens/s (b={b})"
+METRIC = "{model} int8 decode steps/s (b=1)"
+METRIC_B = "{model} int8 decode tokens/s (b={b})"
+
+
+def model_label(shape: str) -> str:
+    return shape.upper()  # bloom-176b -> BLOOM-176B
 RING_BYTES = 64
 UNIT = "steps/s"
 
@@ -166,7 +170,7 @@ def run_reference(args):
     desc = (f"1 block of the {args.shape} shape, int8 decode t=1 at context {ctx_sample} (oracle port of "
             f"quant.py matmul_mixed + model.py block_forward, random codes), x{cfg.n_layers} blocks extrapolated")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC.format(model=model_label(args.shape)), "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_block * cfg.n_layers * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": {"workload": f"{args.shape} int8 decode b=1 (CPU reference arithmetic)",
@@ -306,7 +310,9 @@ def run_ours(args):
     from paper_2209_01188_b200.model import SHAPES
 
     cfg = SHAPES[args.shape]
-    metric, unit = (METRIC, UNIT) if args.batch == 1 else (METRIC_B.format(b=args.batch), "tokens/s")
+    label = model_label(args.shape)
+    metric, unit = ((METRIC.format(model=label), UNIT) if args.batch == 1
+                    else (METRIC_B.format(model=label, b=args.batch), "tokens/s"))
     pl = Pipeline(args, cfg)
     S, N, rank, B = pl.S, pl.world, pl.rank, pl.B
     K, W = args.steps, args.warmup
