@@ -760,7 +760,14 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
     a.total = (int64_t)a.MG * a.KC;
     const int chunks = (int)ceil_div(act.n_tok, act.tc);
     int64_t G = std::max<int64_t>(1, (int64_t)sms * blocks_per_sm / chunks);
-    G = std::min<int64_t>(G, a.total);
+    // small matrices: at least min_units k tiles per CTA (a CTA then streams whole
+    // 128-row groups instead of splitting every group across many CTAs and paying
+    // the split merge); large matrices keep one CTA per resident slot
+    static const int64_t min_units = [] {
+        const char* e = getenv("PB_GEMV_MINU");  // tuning knob
+        return (int64_t)(e ? atoi(e) : 16);
+    }();
+    G = std::min<int64_t>(G, std::max<int64_t>(1, a.total / std::max<int64_t>(min_units, 1)));
     const int64_t per_tile = 128 * 8 * NT;
     while (G > 1 && (int64_t)chunks * G * 2 * per_tile > partial_cap) G /= 2;
     a.G = (int)G;
