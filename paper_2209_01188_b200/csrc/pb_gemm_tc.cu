@@ -40,14 +40,15 @@ namespace pb {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BN = TC_TOKENS;           // tokens per tile (per digit accumulator)
-constexpr int TC_STAGES = 16;
+constexpr int TC_KT = 4;                   // k tiles per pipeline stage (MMAs issued per wait/commit)
+constexpr int TC_STAGES = 4;
 constexpr int TC_THREADS = 192;
 constexpr int TC_A = 4096;                 // int8 codes per k tile (128 rows x 32)
 constexpr int TC_PLANE = TC_BN * 32;       // one digit plane per k tile
 constexpr int TC_B = 3 * TC_PLANE;
 constexpr int TC_ACC = 256;                // TMEM columns per accumulator set (3 x 80 used)
 constexpr int TC_TMEM_COLS = 512;
-constexpr size_t TC_SMEM = (size_t)TC_STAGES * (TC_A + TC_B) + (2 * TC_STAGES + 4) * 8 + 16;
+constexpr size_t TC_SMEM = (size_t)TC_STAGES * TC_KT * (TC_A + TC_B) + (2 * TC_STAGES + 4) * 8 + 16;
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
@@ -98,9 +99,9 @@ struct TcArgs {
 
 __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* sa = smem;                                // [STAGES][4 KB]
-    uint8_t* sb = sa + TC_STAGES * TC_A;               // [STAGES][3 planes]
-    uint64_t* full = reinterpret_cast<uint64_t*>(sb + TC_STAGES * TC_B);
+    uint8_t* sa = smem;                                // [STAGES][KT][4 KB]
+    uint8_t* sb = sa + TC_STAGES * TC_KT * TC_A;       // [STAGES][KT][3 planes]
+    uint64_t* full = reinterpret_cast<uint64_t*>(sb + TC_STAGES * TC_KT * TC_B);
     uint64_t* empty = full + TC_STAGES;
     uint64_t* accfull = empty + TC_STAGES;  // [2]
     uint64_t* accempty = accfull + 2;       // [2]
@@ -139,12 +140,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
                 const int mg = t / a.NTL, nt = t % a.NTL;
                 const int8_t* asrc = a.codes + (int64_t)mg * KC * TC_A;
                 const uint8_t* bsrc = a.bcanon + (int64_t)nt * KC * TC_B;
-                for (int kc = 0; kc < KC; ++kc, ++it) {
-                    const int s = it % TC_STAGES;
+                for (int kc = 0; kc < KC; kc += TC_KT, ++it) {
+                    const int s = it % TC_STAGES, n = min(TC_KT, KC - kc);
                     mbar_wait(&empty[s], ((it / TC_STAGES) & 1) ^ 1);
-                    mbar_expect_tx(&full[s], TC_A + TC_B);
-                    bulk_g2s(sa + s * TC_A, asrc + (int64_t)kc * TC_A, TC_A, &full[s]);
-                    bulk_g2s(sb + s * TC_B, bsrc + (int64_t)kc * TC_B, TC_B, &full[s]);
+                    mbar_expect_tx(&full[s], n * (TC_A + TC_B));
+                    // consecutive k tiles are contiguous in both operands: one copy each
+                    bulk_g2s(sa + s * TC_KT * TC_A, asrc + (int64_t)kc * TC_A, n * TC_A, &full[s]);
+                    bulk_g2s(sb + s * TC_KT * TC_B, bsrc + (int64_t)kc * TC_B, n * TC_B, &full[s]);
                 }
             }
         }
@@ -157,11 +159,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
                 mbar_wait(&accempty[b], ((i >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t acc = tmem + b * TC_ACC;
-                for (int kc = 0; kc < KC; ++kc, ++it) {
-                    const int s = it % TC_STAGES;
+                for (int kc = 0; kc < KC; kc += TC_KT, ++it) {
+                    const int s = it % TC_STAGES, n = min(TC_KT, KC - kc);
                     mbar_wait(&full[s], (it / TC_STAGES) & 1);
                     tc_fence_after();
-                    tc_mma(acc, umma_desc(smem_u32(sa + s * TC_A)), umma_desc(smem_u32(sb + s * TC_B)), kc != 0);
+                    const uint32_t a0 = smem_u32(sa + s * TC_KT * TC_A), b0 = smem_u32(sb + s * TC_KT * TC_B);
+                    for (int k = 0; k < n; ++k)
+                        tc_mma(acc, umma_desc(a0 + k * TC_A), umma_desc(b0 + k * TC_B), (kc | k) != 0);
                     tc_commit(&empty[s]);
                 }
                 tc_commit(&accfull[b]);
