@@ -96,24 +96,6 @@ __device__ __forceinline__ float block_max(float v, float* red) {
     return red[0];
 }
 
-struct ProArgs {
-    int mode;
-    const float* x;
-    int K, Kp;
-    const float* gamma;
-    const float* beta;
-    const float* scales;  // nullptr in f32 mode
-    int n_outl;
-    const int32_t* outl_idx;
-    int tc;
-    uint4* frag;
-    float* back;   // [n_tok] 2^-shift (epilogue rescale)
-    float4* stats; // [n_tok] {mu, inv, 2^shift, 2^-shift}
-    float* xo;
-    float* y32;
-    ProSrc src;
-    int early;
-};
 
 __device__ __forceinline__ float pro_y(const ProArgs& a, const float* x, int k, float mu, float inv) {
     if (a.mode == PRO_LN) return fmaf(a.gamma[k], (x[k] - mu) * inv, a.beta[k]);  // model.py:271-276
@@ -275,41 +257,14 @@ int bound_consts(const float* gamma, const float* beta, const float* scales, int
     return PB_OK;
 }
 
-// int8-digit B fragments of a = rint(y * s * 2^(shift + 8)) (layout in the header
-// comment); one thread per (token, 32-wide k tile, lane quad q). The statistics'
-// shift maps max |y s| into [2^13, 2^14) (the fp16 split of the tcgen05 path);
-// 2^8 more gives the 22-bit integer range here.
-__global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
-    __shared__ float4 s_st;
-    // early trigger (default): the GEMV that consumes this operand launches while
-    // this kernel still waits for its producer and starts streaming weights
-    // (its own griddepcontrol.wait still orders it after this grid completes)
-    if (a.early) pdl_trigger();
-    pdl_wait();
-    if (!a.early) pdl_trigger();
-    const int tok = blockIdx.y;
+// One B-fragment item of the int8-digit operand a = rint(y * s * 2^(shift + 8))
+// (layout in the header comment): token tok, 32-wide k tile kc, lane quad q.
+// The statistics' shift maps max |y s| into [2^13, 2^14) (the fp16 split of the
+// tcgen05 path); 2^8 more gives the 22-bit integer range here.
+__device__ __forceinline__ void frag_item(const ProArgs& a, int tok, int kc, int q, const float4 st) {
     const float* x = a.x + (int64_t)tok * a.K;
-    if (threadIdx.x < 32) {
-        const float4 r = resolve_stats(a, tok);
-        if (threadIdx.x == 0) {
-            s_st = r;
-            if (blockIdx.x == 0) {
-                a.back[tok] = r.w * (1.f / 256.f);
-                if (a.src.zero_tokmax) a.src.zero_tokmax[tok] = 0.f;
-            }
-        }
-    }
-    __syncthreads();
-    const float4 st = s_st;
     const float z = st.z * 256.f;
     const int KC = a.Kp / 32;
-    const int it = blockIdx.x * blockDim.x + threadIdx.x;
-    if (blockIdx.x == 0 && a.xo) {
-        for (int j = threadIdx.x; j < a.n_outl; j += blockDim.x)
-            a.xo[(int64_t)tok * a.n_outl + j] = pro_y(a, x, a.outl_idx[j], st.x, st.y);
-    }
-    if (it >= KC * 4) return;
-    const int kc = it >> 2, q = it & 3;
     const int NT = digit_ntiles(a.tc);
     const int c = tok / a.tc, col = tok % a.tc;
     uint32_t w[3][2] = {{0u, 0u}, {0u, 0u}, {0u, 0u}};
@@ -333,6 +288,44 @@ __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
         const int cc = p * a.tc + col;
         frag[(base + (cc >> 3)) * 32 + 4 * (cc & 7) + q] = make_uint2(w[p][0], w[p][1]);
     }
+}
+
+// Per-token side outputs of the operand writer: 2^-(shift + 8), the reset of
+// the next producer's range accumulator, the f32 activations at the outlier
+// features.
+__device__ __forceinline__ void operand_token_outputs(const ProArgs& a, int tok, const float4 st, int tid,
+                                                      int nthr) {
+    if (tid == 0) {
+        a.back[tok] = st.w * (1.f / 256.f);
+        if (a.src.zero_tokmax) a.src.zero_tokmax[tok] = 0.f;
+    }
+    if (a.xo) {
+        const float* x = a.x + (int64_t)tok * a.K;
+        for (int j = tid; j < a.n_outl; j += nthr) a.xo[(int64_t)tok * a.n_outl + j] = pro_y(a, x, a.outl_idx[j], st.x, st.y);
+    }
+}
+
+// k_fragwrite: one thread per (token, 32-wide k tile, lane quad q)
+__global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
+    __shared__ float4 s_st;
+    // early trigger (default): the GEMV that consumes this operand launches while
+    // this kernel still waits for its producer and starts streaming weights
+    // (its own griddepcontrol.wait still orders it after this grid completes)
+    if (a.early) pdl_trigger();
+    pdl_wait();
+    if (!a.early) pdl_trigger();
+    const int tok = blockIdx.y;
+    if (threadIdx.x < 32) {
+        const float4 r = resolve_stats(a, tok);
+        if (threadIdx.x == 0) s_st = r;
+    }
+    __syncthreads();
+    const float4 st = s_st;
+    if (blockIdx.x == 0) operand_token_outputs(a, tok, st, threadIdx.x, blockDim.x);
+    const int KC = a.Kp / 32;
+    const int it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (it >= KC * 4) return;
+    frag_item(a, tok, it >> 2, it & 3, st);
 }
 
 // Same operand for the tcgen05 GEMM (pb_gemm_tc.cu): the three int8 digit
@@ -516,10 +509,7 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
     if (u0 >= u1) {
         pdl_wait();
         pdl_trigger();
-        return;
-    }
-
-    if (warp == 0) {
+    } else if (warp == 0) {
         // ---------------- producer
         if (lane == 0) {
             int stage = 0, issued = 0;
@@ -570,9 +560,7 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
             pdl_wait();
             pdl_trigger();
         }
-        return;
-    }
-
+    } else {
     // ---------------- consumers
     pdl_wait();
     pdl_trigger();
@@ -733,6 +721,7 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
             }
         }
     }
+    }  // consumers
 }
 
 template <int TC, int SK_KCS, int SK_STAGES>
@@ -753,7 +742,7 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
         // kernel of the chain (PDL) to become resident and start streaming
         if (const char* e = getenv("PB_GEMV_CTAS")) blocks_per_sm = std::max(1, std::min(blocks_per_sm, atoi(e)));
     }
-    SkArgs a;
+    SkArgs a{};
     a.codes = m.codes;
     a.MG = m.Mp / 128;
     a.KC = m.Kp / 32;

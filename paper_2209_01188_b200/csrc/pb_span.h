@@ -117,6 +117,26 @@ constexpr int TC_TOKENS = 80;  // tokens per tcgen05 tile (3 digit accumulators 
 // (max_k |gamma_k| s_k, max_k |beta_k| s_k) -> host
 int bound_consts(const float* gamma, const float* beta, const float* scales, int K, float* gs, float* bs,
                  cudaStream_t st);
+// Operand-writer arguments (k_fragwrite / k_canonwrite).
+struct ProArgs {
+    int mode;
+    const float* x;
+    int K, Kp;
+    const float* gamma;
+    const float* beta;
+    const float* scales;  // nullptr in f32 mode
+    int n_outl;
+    const int32_t* outl_idx;
+    int tc;
+    uint4* frag;
+    float* back;   // [n_tok] 2^-shift (epilogue rescale)
+    float4* stats; // [n_tok] {mu, inv, 2^shift, 2^-shift}
+    float* xo;
+    float* y32;
+    ProSrc src;
+    int early;
+};
+
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
                 int64_t partial_cap, cudaStream_t st);
 int launch_gemm_f32(const Mat& m, const float* y, int n_tok, const Epi& epi, float* part, int64_t part_cap,
