@@ -104,7 +104,8 @@ __device__ __forceinline__ float pro_y(const ProArgs& a, const float* x, int k, 
 
 // Row statistics, one CTA per token: LayerNorm mean / inverse std (population
 // variance, eps 1e-5; accumulated in f64) and the power-of-two shift that maps
-// max |y * s| into [2^13, 2^14) for the hi/lo fp16 split.
+// max |y * s| into [2^13, 2^14) (the operand writers scale by 2^8 more for the
+// 22-bit fixed-point digits).
 constexpr int STATS_THREADS = 1024;
 
 __global__ void __launch_bounds__(STATS_THREADS) k_rowstats(ProArgs a) {

@@ -9,7 +9,7 @@
 // their error rigorously, and rescores only the candidates inside the bound
 // against the f32 rows in f64:
 //   |approx_v - exact_v| <= sum_k |y_k| s_k / 2          (code rounding, s_k = feature scale)
-//                          + K 2^-22 sum_k |y_k| max|E|  (hi/lo operand split + f32 accumulation)
+//                          + K 2^-22 sum_k |y_k| max|E|  (22-bit fixed-point operand + f32 recombination)
 //   candidates = { v : approx_v >= max_u approx_u - 2 B }
 // so the winner (largest exact logit, lowest index on ties) is always a
 // candidate. If more than HEAD_CAP rows qualify (degenerate hidden states)
@@ -267,7 +267,7 @@ int sms_of(int dev) {
 }
 
 // LN statistics of the hidden rows (k_rowstats through the GEMV prologue) and
-// the hi/lo fragments of the normalized rows
+// the int8-digit fragments of the normalized rows
 int head_prologue(pb_head* h, const float* x, int n, cudaStream_t st) {
     ProSrc src;  // SRC_STATS: exact row statistics
     return launch_prologue(PRO_LN, src, x, n, h->d, h->et.Kp, h->gamma, h->beta, h->et, choose_tc(n), h->frag,

@@ -75,7 +75,7 @@ struct Epi {
 
 // B-operand (activation) layout parameters for one GEMV launch.
 struct Act {
-    const uint4* frag;      // hi/lo f16 fragments, see pb_gemv.cu
+    const uint4* frag;      // int8-digit B fragments (m16n8k32), see pb_gemv.cu
     const float* back;      // [n_tok] 2^-shift per token
     int n_tok;
     int tc;                 // tokens per column chunk (4, 8, 16, 32)
@@ -105,7 +105,7 @@ int quantize_blockwise(const float* x, int64_t n, int block, int8_t* codes, floa
 int dequantize_blockwise(const int8_t* codes, const float* scales, int64_t n, int block, float* out,
                          cudaStream_t st);
 
-// prologue: y = LN(x) (PRO_LN) or x (PRO_SCALE); writes hi/lo fragments of
+// prologue: y = LN(x) (PRO_LN) or x (PRO_SCALE); writes the int8-digit operand of
 // y * scales, the per-token 2^-shift, outlier activations xo, and (f32 mode) y.
 int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int K, int Kp, const float* gamma,
                     const float* beta, const Mat& m, int tc, uint4* frag, float* back, float4* stats, float* xo,

@@ -4,7 +4,7 @@ oracle.
 
 Tolerances (north_star: <= 1e-2 relative): hidden states are compared with
 max-abs error relative to max |reference| and must be <= 1e-3 here (observed
-~1e-5..1e-4: activations are carried as hi/lo fp16 pairs with fp32
+~1e-5..1e-4: matmul operands are 22-bit fixed-point int8 digits with exact s32
 accumulation; K/V are fp16). Greedy token ids must be identical.
 """
 
