@@ -298,3 +298,30 @@ def test_tcgen05_prefill_matches_gemv_path(shape_name, t, monkeypatch):
     for i in range(3):
         err = rel_err(outs["64"][i], outs["100000"][i])
         assert err <= TOL, (shape_name, i, err)  # fp16 KV rounding can flip on 1-ulp f32 differences
+
+
+def test_bloom176b_tcgen05_prefill_vs_f64_reference():
+    """One 176B-shape block (h=14336, H=112): a 160-token prefill through the
+    tcgen05 kind::i8 GEMM (two 80-token tiles) and the prefill attention
+    kernel, then two decode steps, against a float64 restatement built from
+    the span's own codes (C5's row shape, shortened)."""
+    import torch
+
+    from paper_2209_01188_b200.model import SHAPES as S
+    from paper_2209_01188_b200.span import BlockSpan
+    from torch_ref import RefBlock
+
+    cfg = S["bloom-176b"]
+    span = BlockSpan(cfg, 0, 1, int8=True, page_tokens=64, max_tokens=160, n_pages=8)
+    span.generate_weights(42)
+    ref = RefBlock(span, 0)
+    g = torch.Generator(device="cuda").manual_seed(4)
+    x = torch.randn(162, cfg.hidden, device="cuda", generator=g) * 0.05
+    seq = span.new_sequence()
+    kv = [None, None]
+    for a, b in ((0, 160), (160, 161), (161, 162)):
+        got = span.step([(seq, x[a:b])])[0].double()
+        want = ref.step(x[a:b].double(), kv, a)
+        err = float((got - want).abs().max() / want.abs().max())
+        assert err <= TOL, (a, err)
+    span.close()
