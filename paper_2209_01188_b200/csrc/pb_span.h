@@ -170,6 +170,9 @@ struct AttnArgs {
     int debug_nocomp = 0;      // experiment knob (PB_ATT_NOCOMP): skip the math, stream only
 };
 int launch_attention(const AttnArgs& a, int64_t part_cap, cudaStream_t st);
+
+
+
 template <int DH>
 int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st);
 // the tensor-core attention (head_dim 64/128) reads KV rows whose 16-byte
