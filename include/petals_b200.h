@@ -152,6 +152,16 @@ int32_t pb_span_last_launches(const pb_span* span);
 int pb_span_profile(pb_span* span, int32_t on);
 int pb_span_profile_read(pb_span* span, int32_t kind, double* ms, int64_t* launches, double* bytes);
 
+/* Diagnostics (not a reference interface): per-CTA globaltimer stamps of the
+ * decode kernels (int8 GEMV, attention, operand writer) into a device buffer
+ * of cap_words u64 (NULL: off). Each traced launch takes 8 u64 per CTA
+ * (entry, dependency released, first stage, end: globaltimer ns; SM id);
+ * pb_trace_meta writes {kind, ctas, word offset} triples for the launches
+ * traced since pb_trace_set and returns their number. Process-wide, for
+ * single-threaded probes only. */
+int pb_trace_set(void* d_buf, int64_t cap_words);
+int64_t pb_trace_meta(int64_t* h_out, int64_t cap_triples);
+
 /* ---- client head: embedding, final LayerNorm + tied LM head, greedy ---- */
 typedef struct pb_head pb_head;
 

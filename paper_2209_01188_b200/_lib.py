@@ -22,7 +22,7 @@ EXPORTS = [
     "pb_span_outliers", "pb_span_read_codes", "pb_span_step", "pb_span_step_int8", "pb_span_last_launches",
     "pb_span_profile", "pb_span_profile_read", "pb_head_create", "pb_head_destroy", "pb_head_device_bytes",
     "pb_head_gen", "pb_head_load", "pb_head_embed", "pb_head_embed_device", "pb_head_logits", "pb_head_greedy",
-    "pb_span_step_tape", "pb_span_backward",
+    "pb_span_step_tape", "pb_span_backward", "pb_trace_set", "pb_trace_meta",
 ]
 
 
@@ -63,6 +63,7 @@ def lib() -> C.CDLL:
         "pb_span_step_tape": [P, I32, I32, P, P, P, P, P, P, VP],
         "pb_span_backward": [P, P, I32, P, P, VP],
         "pb_span_profile": [P, I32],
+        "pb_trace_set": [P, I64],
         "pb_span_profile_read": [P, I32, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double)],
         "pb_head_create": [I32, I32, I32, I32, C.POINTER(C.c_void_p)],
         "pb_head_destroy": [P],
@@ -81,6 +82,8 @@ def lib() -> C.CDLL:
     L.pb_span_device_bytes.restype = C.c_int64
     L.pb_head_device_bytes.argtypes = [P]
     L.pb_head_device_bytes.restype = C.c_int64
+    L.pb_trace_meta.argtypes = [P, I64]
+    L.pb_trace_meta.restype = C.c_int64
     L.pb_span_last_launches.argtypes = [P]
     L.pb_span_last_launches.restype = C.c_int32
     _lib = L

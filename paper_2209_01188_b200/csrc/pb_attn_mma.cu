@@ -52,6 +52,7 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
     const int64_t kv_stride = (int64_t)a.H * a.P * DH;
 
     if (threadIdx.x == 0) {
+        trace_stamp(a.trace, c, 0);
         for (int b = 0; b < AM_ST; ++b) {
             mbar_init(&full[b], 1);
             mbar_init(&empty[b], AM_WARPS);
@@ -121,6 +122,7 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
     // ---------------- compute warps
     pdl_wait();
     pdl_trigger();
+    if (threadIdx.x == 32) trace_stamp(a.trace, c, 1);
     const int g = lane >> 2, qd = lane & 3;
     const uint32_t ks_base = smem_u32(Ks), vs_base = smem_u32(Vs);
     const int mi = lane >> 3, ri = lane & 7;  // ldmatrix lane roles: matrix mi, row ri
@@ -353,6 +355,7 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
         }
         u += sg.n;
     }
+    if (threadIdx.x == 32) trace_stamp(a.trace, c, 3);
 }
 
 // Prefill variant (query groups of up to AP_G = 32 consecutive positions of
@@ -683,6 +686,7 @@ int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st) 
     }();
     AttnArgs aa = a;
     aa.debug_nocomp = nocomp;
+    aa.trace = trace_region(TR_ATTN, (int)G);
     return launch_pdl(k_attn_mma<DH>, dim3((unsigned)G), dim3((AM_WARPS + 1) * 32), smem, st, aa, (int)G, U);
 }
 

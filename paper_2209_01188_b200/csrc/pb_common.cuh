@@ -110,6 +110,29 @@ __device__ __forceinline__ int8_t wire_code(float x, float s, float amax) {
     return (int8_t)(x < 0.f ? -m : m);
 }
 
+// Diagnostics (pb_trace_set): per-CTA globaltimer stamps of the decode
+// kernels, TRACE_WORDS u64 per CTA, written only when the launch got a trace region.
+__device__ __forceinline__ uint64_t gtime() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+constexpr int TRACE_WORDS = 8;  // per CTA: entry, released, first stage, end, SM id
+__device__ __forceinline__ void trace_stamp(uint64_t* tr, int cta, int i) {
+    if (tr) {
+        tr[cta * TRACE_WORDS + i] = gtime();
+        if (i == 0) tr[cta * TRACE_WORDS + 4] = smid();
+    }
+}
+// host: the next region of the trace buffer for a launch of `ctas` CTAs (or nullptr)
+uint64_t* trace_region(int kind, int ctas);
+enum TraceKind { TR_GEMV = 0, TR_ATTN = 1, TR_FRAG = 2 };
+
 // Programmatic dependent launch (PDL): kernels of the decode chain are launched
 // with cudaLaunchAttributeProgrammaticStreamSerialization, may start while the
 // previous kernel drains, and must execute pdl_wait() before touching anything

@@ -201,9 +201,12 @@ __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
     // early trigger (default): the GEMV that consumes this operand launches while
     // this kernel still waits for its producer and starts streaming weights
     // (its own griddepcontrol.wait still orders it after this grid completes)
+    const int tcta = blockIdx.y * gridDim.x + blockIdx.x;
+    if (threadIdx.x == 0) trace_stamp(a.trace, tcta, 0);
     if (a.early) pdl_trigger();
     pdl_wait();
     if (!a.early) pdl_trigger();
+    if (threadIdx.x == 0) trace_stamp(a.trace, tcta, 1);
     const int tok = blockIdx.y;
     if (threadIdx.x < 32) {
         const float4 r = resolve_stats(a, tok);
@@ -214,8 +217,11 @@ __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
     if (blockIdx.x == 0) operand_token_outputs(a, tok, st, threadIdx.x, blockDim.x);
     const int KC = a.Kp / 32;
     const int it = blockIdx.x * blockDim.x + threadIdx.x;
-    if (it >= KC * 4) return;
-    frag_item(a, tok, it >> 2, it & 3, st);
+    if (it < KC * 4) frag_item(a, tok, it >> 2, it & 3, st);
+    if (a.trace) {
+        __syncthreads();
+        if (threadIdx.x == 0) trace_stamp(a.trace, tcta, 3);
+    }
 }
 
 // Same operand for the tcgen05 GEMM (pb_gemm_tc.cu): the three int8 digit
@@ -310,6 +316,7 @@ int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int 
         return launch_check("canonwrite");
     }
     const int items = (Kp / 32) * 4;
+    a.trace = trace_region(TR_FRAG, (int)ceil_div(items, 256) * n_tok);
     return launch_pdl(k_fragwrite, dim3((unsigned)ceil_div(items, 256), n_tok), dim3(256), 0, st, a);
 }
 
@@ -346,10 +353,84 @@ struct SkArgs {
     Epi epi;
     float* partials;  // [chunk][G][2][128 * 2tc]
     int* counters;    // [chunk][MG]
+    uint64_t* trace;  // diagnostics (pb_trace_set), usually null
 };
 
 __device__ __forceinline__ int sk_owner(int64_t u, int G, int64_t total) {
     return (int)(((u + 1) * G - 1) / total);
+}
+
+// Fused epilogue of one 128-row group (consumer warps only): the integer
+// digit sums acc -> f64 recombination -> bias / outliers / residual / GELU /
+// q|k|v + KV append, plus the per-token summary for the next operand.
+template <int TC>
+__device__ __forceinline__ void sk_epilogue(const SkArgs& a, int (&acc)[2][digit_ntiles(TC)][4], int mg, int chunk,
+                                            int* S) {
+    constexpr int NT = digit_ntiles(TC);
+    constexpr int SST = 8 * NT + 1;
+    const int lane = threadIdx.x & 31, cw = (threadIdx.x >> 5) - 1;
+    const int g = lane >> 2, q = lane & 3;
+    // ---- fused epilogue of the 128-row group
+    cons_sync();  // S is free (previous epilogue done)
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int row = (cw * 2 + i) * 16 + g + 8 * (r >> 1);
+                const int col = j * 8 + 2 * q + (r & 1);
+                S[row * SST + col] = acc[i][j][r];
+            }
+    cons_sync();
+    const int row_base = mg * 128;
+    const bool want_sum = a.epi.pstats != nullptr, want_max = a.epi.tokmax != nullptr;
+    float* Sf = reinterpret_cast<float*>(S);  // column j < TC reused for the epilogue outputs
+    for (int t = threadIdx.x - 32; t < 128 * TC; t += SK_CONS * 32) {
+        const int r = t % 128, j = t / 128;
+        const int o = row_base + r;
+        const int tok = chunk * TC + j;
+        if (o >= a.epi.M || tok >= a.act.n_tok) continue;
+        const double iv = 65536.0 * (double)S[r * SST + j] + 256.0 * (double)S[r * SST + TC + j] +
+                          (double)S[r * SST + 2 * TC + j];
+        const float v = (float)iv * a.act.back[tok];
+        const float y = epi_store(a.epi, tok, o, v);
+        if (want_max) Sf[r * SST + j] = fabsf(y * a.epi.s_next[o]);
+        else if (want_sum) Sf[r * SST + j] = y;
+    }
+    if (want_sum || want_max) {
+        // per-token summary of this 128-row group for the next operand's range / LayerNorm
+        cons_sync();
+        const int nrow = min(128, a.epi.M - row_base);
+        for (int j = cw; j < TC; j += SK_CONS) {
+            const int tok = chunk * TC + j;
+            if (tok >= a.act.n_tok) continue;
+            if (want_max) {
+                float m = 0.f;
+                for (int r = lane; r < nrow; r += 32) m = fmaxf(m, Sf[r * SST + j]);
+                m = warp_max(m);
+                if (lane == 0) atomicMax(reinterpret_cast<int*>(a.epi.tokmax) + tok, __float_as_int(m));
+            } else {
+                float s = 0.f, mn = INFINITY, mx = -INFINITY;
+                for (int r = lane; r < nrow; r += 32) {
+                    const float y = Sf[r * SST + j];
+                    s += y;
+                    mn = fminf(mn, y);
+                    mx = fmaxf(mx, y);
+                }
+                const float mean = warp_sum(s) / nrow;
+                float m2 = 0.f;
+                for (int r = lane; r < nrow; r += 32) {
+                    const float dlt = Sf[r * SST + j] - mean;
+                    m2 = fmaf(dlt, dlt, m2);
+                }
+                m2 = warp_sum(m2);
+                mn = -warp_max(-mn);
+                mx = warp_max(mx);
+                if (lane == 0) a.epi.pstats[(int64_t)tok * ((a.epi.M + 127) / 128) + mg] = make_float4(mean, m2, mn, mx);
+            }
+        }
+    }
 }
 
 template <int TC, int SK_KCS, int SK_STAGES>
@@ -373,7 +454,9 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
     const int chunk = blockIdx.y;
     const int c = blockIdx.x;
     const int64_t u0 = (int64_t)c * a.total / a.G, u1 = (int64_t)(c + 1) * a.total / a.G;
+    const int tcta = chunk * a.G + c;
     if (threadIdx.x == 0) {
+        trace_stamp(a.trace, tcta, 0);
         for (int s = 0; s < SK_STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], SK_CONS);
@@ -439,6 +522,8 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
     // ---------------- consumers
     pdl_wait();
     pdl_trigger();
+    if (threadIdx.x == 32) trace_stamp(a.trace, tcta, 1);
+    bool first_stage = true;
     const int cw = warp - 1;  // consumer warp: m-tiles 2cw, 2cw+1 of the group
     const int g = lane >> 2, q = lane & 3;
     // ldmatrix roles: matrix mi = lane / 8 (row half mi & 1, k half mi >> 1), row ri = lane % 8
@@ -460,6 +545,10 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
         for (int kc = ka; kc < kb; kc += SK_KCS) {
             const int n = min(SK_KCS, kb - kc);
             mbar_wait(&full[stage], phase);
+            if (first_stage) {
+                if (threadIdx.x == 32) trace_stamp(a.trace, tcta, 2);
+                first_stage = false;
+            }
             const uint8_t* Bs = sb + stage * B_STAGE;
             const uint32_t As = sa_u + stage * A_STAGE;
 #pragma unroll
@@ -534,70 +623,12 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
                     }
             }
         }
-        // ---- fused epilogue of the 128-row group
-        cons_sync();  // S is free (previous epilogue done)
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int j = 0; j < NT; ++j)
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const int row = (cw * 2 + i) * 16 + g + 8 * (r >> 1);
-                    const int col = j * 8 + 2 * q + (r & 1);
-                    S[row * SST + col] = acc[i][j][r];
-                }
-        cons_sync();
-        const int row_base = mg * 128;
-        const bool want_sum = a.epi.pstats != nullptr, want_max = a.epi.tokmax != nullptr;
-        float* Sf = reinterpret_cast<float*>(S);  // column j < TC reused for the epilogue outputs
-        for (int t = threadIdx.x - 32; t < 128 * TC; t += SK_CONS * 32) {
-            const int r = t % 128, j = t / 128;
-            const int o = row_base + r;
-            const int tok = chunk * TC + j;
-            if (o >= a.epi.M || tok >= a.act.n_tok) continue;
-            const double iv = 65536.0 * (double)S[r * SST + j] + 256.0 * (double)S[r * SST + TC + j] +
-                              (double)S[r * SST + 2 * TC + j];
-            const float v = (float)iv * a.act.back[tok];
-            const float y = epi_store(a.epi, tok, o, v);
-            if (want_max) Sf[r * SST + j] = fabsf(y * a.epi.s_next[o]);
-            else if (want_sum) Sf[r * SST + j] = y;
-        }
-        if (want_sum || want_max) {
-            // per-token summary of this 128-row group for the next operand's range / LayerNorm
-            cons_sync();
-            const int nrow = min(128, a.epi.M - row_base);
-            for (int j = cw; j < TC; j += SK_CONS) {
-                const int tok = chunk * TC + j;
-                if (tok >= a.act.n_tok) continue;
-                if (want_max) {
-                    float m = 0.f;
-                    for (int r = lane; r < nrow; r += 32) m = fmaxf(m, Sf[r * SST + j]);
-                    m = warp_max(m);
-                    if (lane == 0) atomicMax(reinterpret_cast<int*>(a.epi.tokmax) + tok, __float_as_int(m));
-                } else {
-                    float s = 0.f, mn = INFINITY, mx = -INFINITY;
-                    for (int r = lane; r < nrow; r += 32) {
-                        const float y = Sf[r * SST + j];
-                        s += y;
-                        mn = fminf(mn, y);
-                        mx = fmaxf(mx, y);
-                    }
-                    const float mean = warp_sum(s) / nrow;
-                    float m2 = 0.f;
-                    for (int r = lane; r < nrow; r += 32) {
-                        const float dlt = Sf[r * SST + j] - mean;
-                        m2 = fmaf(dlt, dlt, m2);
-                    }
-                    m2 = warp_sum(m2);
-                    mn = -warp_max(-mn);
-                    mx = warp_max(mx);
-                    if (lane == 0) a.epi.pstats[(int64_t)tok * ((a.epi.M + 127) / 128) + mg] = make_float4(mean, m2, mn, mx);
-                }
-            }
-        }
+        sk_epilogue<TC>(a, acc, mg, chunk, S);
     }
+    if (threadIdx.x == 32) trace_stamp(a.trace, tcta, 3);
     }  // consumers
 }
+
 
 template <int TC, int SK_KCS, int SK_STAGES>
 static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
@@ -639,6 +670,7 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
     a.epi = epi;
     a.partials = partials;
     a.counters = counters;
+    a.trace = trace_region(TR_GEMV, (int)G * chunks);
     return launch_pdl(k_gemv_i8<TC, SK_KCS, SK_STAGES>, dim3((unsigned)G, chunks), dim3(SK_THREADS), smem, st, a);
 }
 

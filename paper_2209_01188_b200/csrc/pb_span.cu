@@ -18,9 +18,36 @@ namespace pb {
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 
+static uint64_t* g_trace = nullptr;
+static int64_t g_trace_cap = 0, g_trace_used = 0;
+static std::vector<int64_t> g_trace_meta;
+
+uint64_t* trace_region(int kind, int ctas) {
+    if (!g_trace || g_trace_used + TRACE_WORDS * (int64_t)ctas > g_trace_cap) return nullptr;
+    uint64_t* p = g_trace + g_trace_used;
+    g_trace_meta.insert(g_trace_meta.end(), {(int64_t)kind, (int64_t)ctas, g_trace_used});
+    g_trace_used += TRACE_WORDS * (int64_t)ctas;
+    return p;
+}
+
 }  // namespace pb
 
 using namespace pb;
+
+extern "C" int pb_trace_set(void* d_buf, int64_t cap_words) {
+    g_trace = static_cast<uint64_t*>(d_buf);
+    g_trace_cap = d_buf ? cap_words : 0;
+    g_trace_used = 0;
+    g_trace_meta.clear();
+    return PB_OK;
+}
+
+extern "C" int64_t pb_trace_meta(int64_t* h_out, int64_t cap_triples) {
+    const int64_t n = (int64_t)g_trace_meta.size() / 3;
+    if (h_out)
+        for (int64_t i = 0; i < std::min(n, cap_triples) * 3; ++i) h_out[i] = g_trace_meta[i];
+    return n;
+}
 
 #include "pb_span_impl.h"
 

@@ -135,6 +135,7 @@ struct ProArgs {
     float* y32;
     ProSrc src;
     int early;
+    uint64_t* trace = nullptr;  // diagnostics (pb_trace_set)
 };
 
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
@@ -168,6 +169,7 @@ struct AttnArgs {
     int max_stages;            // max over groups of ceil(keys / 64)
     int max_group;             // largest query group (> 8: the prefill kernel, queries split across warps)
     int debug_nocomp = 0;      // experiment knob (PB_ATT_NOCOMP): skip the math, stream only
+    uint64_t* trace = nullptr; // diagnostics (pb_trace_set)
 };
 int launch_attention(const AttnArgs& a, int64_t part_cap, cudaStream_t st);
 
