@@ -154,8 +154,9 @@ int pb_span_profile_read(pb_span* span, int32_t kind, double* ms, int64_t* launc
 
 /* Diagnostics (not a reference interface): per-CTA globaltimer stamps of the
  * decode kernels (int8 GEMV, attention, operand writer) into a device buffer
- * of cap_words u64 (NULL: off). Each traced launch takes 8 u64 per CTA
- * (entry, dependency released, first stage, end: globaltimer ns; SM id);
+ * of cap_words u64 (NULL: off). Each traced launch takes 16 u64 per CTA
+ * (entry, dependency released, first stage, end: globaltimer ns; SM id;
+ * kernel-specific stamps);
  * pb_trace_meta writes {kind, ctas, word offset} triples for the launches
  * traced since pb_trace_set and returns their number. Process-wide, for
  * single-threaded probes only. */

@@ -48,17 +48,23 @@ static inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b
 
 // ---------------------------------------------------------------- device helpers
 
+// Warp reductions reconverge the warp first (__syncwarp): after divergent
+// code the compiler's shuffle otherwise takes its non-converged path, traced
+// at ~1.5-3 us per reduction on the operand writer's critical path.
 __device__ __forceinline__ float warp_max(float v) {
+    __syncwarp();
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
 __device__ __forceinline__ float warp_sum(float v) {
+    __syncwarp();
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
 __device__ __forceinline__ double warp_sum_d(double v) {
+    __syncwarp();
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
@@ -122,10 +128,10 @@ __device__ __forceinline__ uint32_t smid() {
     asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
     return r;
 }
-constexpr int TRACE_WORDS = 8;  // per CTA: entry, released, first stage, end, SM id
+constexpr int TRACE_WORDS = 16;  // per CTA: entry, released, first stage, end, SM id, kernel-specific
 __device__ __forceinline__ void trace_stamp(uint64_t* tr, int cta, int i) {
     if (tr) {
-        tr[cta * TRACE_WORDS + i] = gtime();
+        tr[cta * TRACE_WORDS + i] = gtime();  // i = 5..7: kernel-specific extra stamps
         if (i == 0) tr[cta * TRACE_WORDS + 4] = smid();
     }
 }

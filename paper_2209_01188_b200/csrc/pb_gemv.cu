@@ -195,8 +195,14 @@ int bound_consts(const float* gamma, const float* beta, const float* scales, int
     return PB_OK;
 }
 
-// k_fragwrite: one thread per (token, 32-wide k tile, lane quad q)
+// k_fragwrite: one thread per (token, 32-wide k tile, lane quad q).
+// Specialised per (operand mode, statistics source) so the code on the
+// dependency-release critical path is compact (it runs cold in the
+// instruction cache once per matrix; MODE/SRC = -1: runtime values).
+template <int MODE, int SRC>
 __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
+    if (MODE >= 0) a.mode = MODE;
+    if (SRC >= 0) a.src.kind = SRC;
     __shared__ float4 s_st;
     // early trigger (default): the GEMV that consumes this operand launches while
     // this kernel still waits for its producer and starts streaming weights
@@ -204,6 +210,10 @@ __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
     const int tcta = blockIdx.y * gridDim.x + blockIdx.x;
     if (threadIdx.x == 0) trace_stamp(a.trace, tcta, 0);
     if (a.early) pdl_trigger();
+    const int KC = a.Kp / 32;
+    const int it = blockIdx.x * blockDim.x + threadIdx.x;
+    FragParams fp;
+    if (it < KC * 4) frag_params(a, it >> 2, it & 3, fp);  // weights: before the dependency wait
     pdl_wait();
     if (!a.early) pdl_trigger();
     if (threadIdx.x == 0) trace_stamp(a.trace, tcta, 1);
@@ -211,13 +221,17 @@ __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
     if (threadIdx.x < 32) {
         const float4 r = resolve_stats(a, tok);
         if (threadIdx.x == 0) s_st = r;
+        if (a.trace) {
+            asm volatile("" ::"f"(r.x), "f"(r.y), "f"(r.z));
+            if (threadIdx.x == 0) trace_stamp(a.trace, blockIdx.y * gridDim.x + blockIdx.x, 2);
+        }
     }
     __syncthreads();
+    if (threadIdx.x == 0) trace_stamp(a.trace, tcta, 5);
     const float4 st = s_st;
     if (blockIdx.x == 0) operand_token_outputs(a, tok, st, threadIdx.x, blockDim.x);
-    const int KC = a.Kp / 32;
-    const int it = blockIdx.x * blockDim.x + threadIdx.x;
-    if (it < KC * 4) frag_item(a, tok, it >> 2, it & 3, st);
+    if (it < KC * 4) frag_item(a, tok, it >> 2, it & 3, st, fp);
+    if (threadIdx.x == 0) trace_stamp(a.trace, tcta, 6);
     if (a.trace) {
         __syncthreads();
         if (threadIdx.x == 0) trace_stamp(a.trace, tcta, 3);
@@ -317,7 +331,12 @@ int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int 
     }
     const int items = (Kp / 32) * 4;
     a.trace = trace_region(TR_FRAG, (int)ceil_div(items, 256) * n_tok);
-    return launch_pdl(k_fragwrite, dim3((unsigned)ceil_div(items, 256), n_tok), dim3(256), 0, st, a);
+    const dim3 grid((unsigned)ceil_div(items, 256), n_tok);
+    if (a.mode == PRO_LN && a.src.kind == SRC_PARTIALS)
+        return launch_pdl(k_fragwrite<PRO_LN, SRC_PARTIALS>, grid, dim3(256), 0, st, a);
+    if (a.mode == PRO_SCALE && a.src.kind == SRC_TOKMAX)
+        return launch_pdl(k_fragwrite<PRO_SCALE, SRC_TOKMAX>, grid, dim3(256), 0, st, a);
+    return launch_pdl(k_fragwrite<-1, -1>, grid, dim3(256), 0, st, a);
 }
 
 // ------------------------------------------------------------------ epilogue
@@ -354,6 +373,7 @@ struct SkArgs {
     float* partials;  // [chunk][G][2][128 * 2tc]
     int* counters;    // [chunk][MG]
     uint64_t* trace;  // diagnostics (pb_trace_set), usually null
+    int64_t l2pf_bytes;  // weight bytes per CTA prefetched into L2 while waiting for the operand
 };
 
 __device__ __forceinline__ int sk_owner(int64_t u, int G, int64_t total) {
@@ -495,6 +515,13 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
                     }
                     ++issued;
                     if (!waited && issued == SK_STAGES) {
+                        // the ring is full and the operand is not ready: pull the next
+                        // stages of this CTA's (contiguous) range into L2 meanwhile, so
+                        // HBM works through the previous kernel's tail
+                        const int64_t pf0 = (u + (kc + n - ka)) * 4096;
+                        const int64_t pf1 = u1 * 4096 < pf0 + a.l2pf_bytes ? u1 * 4096 : pf0 + a.l2pf_bytes;
+                        for (int64_t b = pf0; b < pf1; b += 16384)
+                            bulk_prefetch_l2(a.codes + b, (uint32_t)(pf1 - b < 16384 ? pf1 - b : 16384));
                         pdl_wait();
                         pdl_trigger();
                         waited = true;
@@ -654,7 +681,13 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
     a.KC = m.Kp / 32;
     a.total = (int64_t)a.MG * a.KC;
     const int chunks = (int)ceil_div(act.n_tok, act.tc);
-    int64_t G = std::max<int64_t>(1, (int64_t)sms * blocks_per_sm / chunks);
+    // waves > 1: more CTAs than resident slots; the hardware hands the later
+    // waves to whichever SMs finish first (per-SM streaming rates differ)
+    static const int waves = [] {
+        const char* e = getenv("PB_GEMV_WAVES");  // tuning knob
+        return e ? std::max(1, atoi(e)) : 1;
+    }();
+    int64_t G = std::max<int64_t>(1, (int64_t)sms * blocks_per_sm * waves / chunks);
     // small matrices: at least min_units k tiles per CTA (a CTA then streams whole
     // 128-row groups instead of splitting every group across many CTAs and paying
     // the split merge); large matrices keep one CTA per resident slot
@@ -671,6 +704,11 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
     a.partials = partials;
     a.counters = counters;
     a.trace = trace_region(TR_GEMV, (int)G * chunks);
+    static const int64_t l2pf = [] {
+        const char* e = getenv("PB_GEMV_L2PF");  // tuning knob: KB per CTA (measured: no gain, off)
+        return (int64_t)(e ? atoi(e) : 0) * 1024;
+    }();
+    a.l2pf_bytes = l2pf;
     return launch_pdl(k_gemv_i8<TC, SK_KCS, SK_STAGES>, dim3((unsigned)G, chunks), dim3(SK_THREADS), smem, st, a);
 }
 

@@ -30,6 +30,33 @@ __device__ __forceinline__ int shift_for(float bound) {
     return 14 - e;
 }
 
+// Compensated f32 sum (Knuth TwoSum per addition; hi + lo carries ~48 bits).
+struct CSum {
+    float hi = 0.f, lo = 0.f;
+    __device__ __forceinline__ static void two_sum(float a, float b, float& s, float& e) {
+        s = __fadd_rn(a, b);  // _rn intrinsics: no contraction or reassociation
+        const float bb = __fsub_rn(s, a);
+        e = __fadd_rn(__fsub_rn(a, __fsub_rn(s, bb)), __fsub_rn(b, bb));
+    }
+    __device__ __forceinline__ void add(float v) {
+        float s, e;
+        two_sum(hi, v, s, e);
+        hi = s;
+        lo = __fadd_rn(lo, e);
+    }
+    __device__ __forceinline__ void warp_reduce() {
+        __syncwarp();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float oh = __shfl_xor_sync(0xffffffffu, hi, o), ol = __shfl_xor_sync(0xffffffffu, lo, o);
+            float s, e;
+            two_sum(hi, oh, s, e);
+            hi = s;
+            lo = __fadd_rn(__fadd_rn(lo, ol), e);
+        }
+    }
+};
+
 // Resolve {mu, inv, 2^shift, 2^-shift} of one token inside the operand
 // producer (warp 0), from the producing epilogue's partial summaries
 // (deterministic lane-strided + fixed shuffle-tree merge) or from the exact
@@ -42,41 +69,91 @@ __device__ inline float4 resolve_stats(const ProArgs& a, int tok) {
     }
     if (a.src.kind == SRC_STATS) return a.stats[tok];
     // parallel two-pass combination of the 128-row group summaries:
-    // mean = sum n_g mean_g / N ; M2 = sum M2_g + n_g (mean_g - mean)^2 (f64;
-    // butterfly sums are commutative, so every lane gets the same bits)
+    // mean = sum n_g mean_g / N ; M2 = sum M2_g + n_g (mean_g - mean)^2, as
+    // compensated (hi, lo) f32 sums -- f64 accuracy without the FP64 pipe's
+    // latency on this critical path (traced: 6 us per resolve in f64). Lane
+    // order is fixed and the butterfly steps are symmetric (TwoSum's error
+    // term is exact), so every lane gets the same bits.
     const float4* ps = a.src.pstats + (int64_t)tok * a.src.MG;
-    double s1 = 0.0;
+    CSum s1, s2;
     float mn = INFINITY, mx = -INFINITY;
-    for (int g = lane; g < a.src.MG; g += 32) {
-        const float4 p = ps[g];
-        s1 += (double)min(128, a.src.M - g * 128) * (double)p.x;
-        mn = fminf(mn, p.z);
-        mx = fmaxf(mx, p.w);
+    // MG <= 128 (hidden <= 16384): the summaries stay in registers for the
+    // second pass -- one L2 round trip on this critical path instead of five
+    const bool inreg = a.src.MG <= 128;
+    float4 p[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int g = lane + 32 * i;
+        p[i] = g < a.src.MG ? ps[g] : make_float4(0.f, 0.f, INFINITY, -INFINITY);
     }
-    s1 = warp_sum_d(s1);
+    for (int g0 = 0; g0 < a.src.MG; g0 += 128) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int g = g0 + lane + 32 * i;
+            const float4 q = g0 == 0 ? p[i] : (g < a.src.MG ? ps[g] : make_float4(0.f, 0.f, INFINITY, -INFINITY));
+            if (g < a.src.MG) s1.add(__fmul_rn((float)min(128, a.src.M - g * 128), q.x));
+            mn = fminf(mn, q.z);
+            mx = fmaxf(mx, q.w);
+        }
+    }
+    if (a.trace) {  // diagnostics: the stamp depends on the loaded summaries
+        asm volatile("" ::"f"(s1.hi), "f"(mn), "f"(mx));
+        if (lane == 0) trace_stamp(a.trace, blockIdx.y * gridDim.x + blockIdx.x, 7);
+    }
+    s1.warp_reduce();
     mn = -warp_max(-mn);
     mx = warp_max(mx);
-    const double mean = s1 / a.src.M;
-    double s2 = 0.0;
-    for (int g = lane; g < a.src.MG; g += 32) {
-        const float4 p = ps[g];
-        const double dm = (double)p.x - mean;
-        s2 += (double)p.y + (double)min(128, a.src.M - g * 128) * dm * dm;
+    const float mu = (s1.hi + s1.lo) / (float)a.src.M;
+    if (inreg) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int g = lane + 32 * i;
+            if (g < a.src.MG) {
+                const float dm = p[i].x - mu;
+                s2.add(p[i].y);
+                s2.add(__fmul_rn(__fmul_rn((float)min(128, a.src.M - g * 128), dm), dm));
+            }
+        }
+    } else {
+        for (int g = lane; g < a.src.MG; g += 32) {
+            const float4 q = ps[g];
+            const float dm = q.x - mu;
+            s2.add(q.y);
+            s2.add(__fmul_rn(__fmul_rn((float)min(128, a.src.M - g * 128), dm), dm));
+        }
     }
-    s2 = warp_sum_d(s2);
-    const float mu = (float)mean;
-    const float var = (float)(s2 / a.src.M);
+    s2.warp_reduce();
+    const float var = (s2.hi + s2.lo) / (float)a.src.M;
     const float inv = 1.0f / sqrtf(var + 1e-5f);
     const float dev = fmaxf(mx - mu, mu - mn);
     const int sh = shift_for(a.src.gs * dev * inv + a.src.bs);
     return make_float4(mu, inv, ldexpf(1.f, sh), ldexpf(1.f, -sh));
 }
 
+// Weight-side inputs of one B-fragment item (k tile kc, lane quad q: the 8
+// features 4q..4q+3 and 16+4q..16+4q+3): per-feature scales and, for
+// LayerNorm operands, gamma/beta. They do not depend on the previous kernel,
+// so the operand writer loads them before its PDL dependency wait.
+struct FragParams {
+    float s[8], g[8], b[8];
+};
+__device__ __forceinline__ void frag_params(const ProArgs& a, int kc, int q, FragParams& p) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int k = kc * 32 + 16 * (e >> 2) + 4 * q + (e & 3);
+        const bool in = k < a.K;
+        p.s[e] = in ? a.scales[k] : 0.f;
+        p.g[e] = in && a.mode == PRO_LN ? a.gamma[k] : 1.f;
+        p.b[e] = in && a.mode == PRO_LN ? a.beta[k] : 0.f;
+    }
+}
+
 // One B-fragment item of the int8-digit operand a = rint(y * s * 2^(shift + 8))
 // (layout in the header comment): token tok, 32-wide k tile kc, lane quad q.
 // The statistics' shift maps max |y s| into [2^13, 2^14) (the fp16 split of the
 // tcgen05 path); 2^8 more gives the 22-bit integer range here.
-__device__ __forceinline__ void frag_item(const ProArgs& a, int tok, int kc, int q, const float4 st) {
+__device__ __forceinline__ void frag_item(const ProArgs& a, int tok, int kc, int q, const float4 st,
+                                          const FragParams& p) {
     const float* x = a.x + (int64_t)tok * a.K;
     const float z = st.z * 256.f;
     const int KC = a.Kp / 32;
@@ -84,24 +161,22 @@ __device__ __forceinline__ void frag_item(const ProArgs& a, int tok, int kc, int
     const int c = tok / a.tc, col = tok % a.tc;
     uint32_t w[3][2] = {{0u, 0u}, {0u, 0u}, {0u, 0u}};
 #pragma unroll
-    for (int half_ = 0; half_ < 2; ++half_) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int k = kc * 32 + 16 * half_ + 4 * q + i;
-            const float v = k < a.K ? (pro_y(a, x, k, st.x, st.y) * a.scales[k]) * z : 0.f;
-            int h, m, l;
-            digits3(__float2int_rn(v), h, m, l);
-            w[0][half_] |= (uint32_t)(uint8_t)h << (8 * i);
-            w[1][half_] |= (uint32_t)(uint8_t)m << (8 * i);
-            w[2][half_] |= (uint32_t)(uint8_t)l << (8 * i);
-        }
+    for (int e = 0; e < 8; ++e) {
+        const int k = kc * 32 + 16 * (e >> 2) + 4 * q + (e & 3);
+        float y = 0.f;
+        if (k < a.K) y = a.mode == PRO_LN ? fmaf(p.g[e], (x[k] - st.x) * st.y, p.b[e]) : x[k];  // model.py:271-276
+        int h, m, l;
+        digits3(__float2int_rn((y * p.s[e]) * z), h, m, l);
+        w[0][e >> 2] |= (uint32_t)(uint8_t)h << (8 * (e & 3));
+        w[1][e >> 2] |= (uint32_t)(uint8_t)m << (8 * (e & 3));
+        w[2][e >> 2] |= (uint32_t)(uint8_t)l << (8 * (e & 3));
     }
     uint2* frag = reinterpret_cast<uint2*>(a.frag);
     const int64_t base = ((int64_t)c * KC + kc) * NT;
 #pragma unroll
-    for (int p = 0; p < 3; ++p) {
-        const int cc = p * a.tc + col;
-        frag[(base + (cc >> 3)) * 32 + 4 * (cc & 7) + q] = make_uint2(w[p][0], w[p][1]);
+    for (int pp = 0; pp < 3; ++pp) {
+        const int cc = pp * a.tc + col;
+        frag[(base + (cc >> 3)) * 32 + 4 * (cc & 7) + q] = make_uint2(w[pp][0], w[pp][1]);
     }
 }
 

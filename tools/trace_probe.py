@@ -70,7 +70,7 @@ def main():
     recs = []
     for i in range(n):
         kind, ctas, off = meta[3 * i], meta[3 * i + 1], meta[3 * i + 2]
-        recs.append((KIND.get(kind, str(kind)), t[off:off + 8 * ctas].reshape(ctas, 8)))
+        recs.append((KIND.get(kind, str(kind)), t[off:off + 16 * ctas].reshape(ctas, 16)))
     base = min(r[:, 0][r[:, 0] > 0].min() for _, r in recs)
     us = lambda v: (v - base) / 1e3  # noqa: E731
 
@@ -92,6 +92,10 @@ def main():
         print(f"{i:3d}  {k:4s} {r.shape[0]:5d} | {spread(r[:, 0])} | {spread(r[:, 1])} | {spread(r[:, 2])} | "
               f"{spread(r[:, 3])} | {busy:6.1f} {gap}")
         prev_end = emax
+        if k == "frag" and (r[:, 5] > 0).any():
+            print(f"          frag summaries loaded {spread(r[:, 7])} | stats (warp 0) {spread(r[:, 2])} | "
+                  f"CTA barrier {spread(r[:, 5])} | "
+                  f"items written {spread(r[:, 6])}")
     if args.sm:
         sm_rates([r for k, r in recs if k == "gemv"], np)
     span.close()
