@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--seed", type=int, default=42)
     p.add_argument("--prefill-chunk", type=int, default=256)
     p.add_argument("--batch", type=int, default=1, help="batch-1 sessions per pipeline micro-batch")
+    p.add_argument("--hop", default="p2p", choices=["p2p", "nccl"],
+                   help="span-to-span hop: NVLink peer-memory mailboxes (pb_hop.cu) or NCCL send/recv")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--synthetic-kv", action="store_true", help="skip the real prefill (KV content is synthetic)")
@@ -231,6 +233,11 @@ class Pipeline:
         self.launches = 0
         self.total_jobs = 0
         self.jobtimes = [] if os.environ.get("PB_BENCH_JOBTIMES") else None  # diagnostic: per-job device times
+        self.ring = None
+        if self.world > 1 and args.hop == "p2p":
+            from paper_2209_01188_b200.pipeline import P2PRing
+
+            self.ring = P2PRing(self.rank, self.world, self.S, cap, self.local, dist)
 
     def payload_bytes(self, t):
         n = t * self.B * self.d
@@ -300,8 +307,60 @@ class Pipeline:
                 return outbox[:RING_BYTES]
             return outbox[:self.payload_bytes(t)]
 
+        if self.ring is not None:
+            self.run_p2p(sched, jobs, tmap, x_for, host_in, host_out, sync_out)
+            return
         run_jobs(sched, [j for j, _ in jobs], step, torch_exchange,
                  lambda j: self.inbox[:RING_BYTES] if r == 0 else self.inbox[:self.payload_bytes(tmap[j])])
+
+    def run_p2p(self, sched, jobs, tmap, x_for, host_in, host_out, sync_out):
+        """The same ring over NVLink mailboxes: span r's wire quantizer stores
+        job j's codes/scales straight into span r+1's slot, a signal kernel
+        publishes it, span r+1's stream waits on it -- no host sync, no NCCL."""
+        import torch
+
+        from paper_2209_01188_b200 import _lib
+        from paper_2209_01188_b200.pipeline import DevPtr
+
+        r, N, ring = self.rank, self.world, self.ring
+        st = _lib.stream_ptr(torch.cuda.current_stream())
+
+        def views(addr, t):
+            n = t * self.B * self.d
+            return DevPtr(addr), DevPtr(addr + -(-n // 16) * 16)
+
+        for j, t in jobs:
+            src, dst = sched.recv_from(j), sched.send_to(j)
+            if src is not None:
+                ring.wait(j, st)
+            n = t * self.B
+            seqs = self.seqs[j % self.S]
+            if dst is not None and r < N - 1:
+                oc, os_ = views(ring.peer_slot(j), t)
+            else:
+                oc, os_ = self.views(self.outbox, t)
+            if r == 0:
+                if host_in is not None:
+                    self.out[:n].copy_(host_in[:n], non_blocking=True)
+                    inp = self.out[:n]
+                elif x_for is not None:
+                    inp = x_for(j, n)
+                else:
+                    inp = self.inputs[j % 64: j % 64 + 1].expand(n, self.d).contiguous()
+                self.span.step_codes(seqs, [t] * self.B, in_f32=inp, out_codes=oc, out_scales=os_, out_f32=self.out[:n])
+            else:
+                ic, is_ = views(ring.local_slot(j), t)
+                self.span.step_codes(seqs, [t] * self.B, in_codes=ic, in_scales=is_, out_codes=oc, out_scales=os_,
+                                     out_f32=self.out[:n])
+            self.launches += self.span.last_launches + (1 if src is not None else 0) + (1 if dst is not None else 0)
+            if r == N - 1 and host_out is not None:
+                host_out[:n * self.d].copy_(oc, non_blocking=True)
+                if sync_out:
+                    torch.cuda.current_stream().synchronize()
+            if dst is not None:
+                # forward edge: job j's payload; ring back-edge (last span -> span 0):
+                # orders the session's next step j + S (stand-in for the client's head)
+                ring.signal(j if r < N - 1 else j + self.S, st)
 
 
 def run_ours(args):
@@ -406,7 +465,7 @@ def run_ours(args):
             pl.dist.all_reduce(te, op=pl.dist.ReduceOp.MAX)
         e2e = {"value": K * S * B / (float(te.item()) / 1e3), "unit": unit, "h2d_bytes_per_step": 4 * d * B,
                "d2h_bytes_per_step": d * B, "path": "pb_span_step_int8 C-ABI with pinned host ingress (span 0) and "
-               "egress of the int8 hidden (last span), NCCL int8 hops between spans"}
+               "egress of the int8 hidden (last span), " + ("NVLink peer-memory" if pl.ring is not None else "NCCL") + " int8 hops between spans"}
     # ---- FORWARD sample (C5 shape: rows of 512 tokens through this rank's span, tcgen05 path;
     # server.py:411-429 semantics, no tape), timed with CUDA events; each rank its own span
     fwd = None

@@ -152,6 +152,21 @@ int32_t pb_span_last_launches(const pb_span* span);
 int pb_span_profile(pb_span* span, int32_t on);
 int pb_span_profile_read(pb_span* span, int32_t kind, double* ms, int64_t* launches, double* bytes);
 
+/* ---- span-to-span hop over NVLink peer memory (replaces the client relay,
+ * client.py:312-331, for spans on one box; pipeline.P2PRing) ----
+ * pb_hop_alloc: zeroed device mailbox + its 64-byte CUDA IPC handle (h_handle).
+ * pb_hop_open / pb_hop_close: map / unmap a peer process's mailbox.
+ * pb_hop_signal: after the payload kernels on `stream`, publish seq to a (peer)
+ * u64 flag with a system-scope release. pb_hop_wait: stream waits (one-thread
+ * kernel, system-scope acquire) until *d_flag >= seq; after timeout_ms the
+ * kernel traps (a missing signal fails loudly instead of hanging). */
+int pb_hop_alloc(int64_t bytes, int32_t device, void** d_ptr, void* h_handle);
+int pb_hop_free(void* d_ptr);
+int pb_hop_open(const void* h_handle, int32_t device, void** d_ptr);
+int pb_hop_close(void* d_ptr);
+int pb_hop_wait(const uint64_t* d_flag, uint64_t seq, int64_t timeout_ms, void* stream);
+int pb_hop_signal(uint64_t* d_peer_flag, uint64_t seq, void* stream);
+
 /* Diagnostics (not a reference interface): per-CTA globaltimer stamps of the
  * decode kernels (int8 GEMV, attention, operand writer) into a device buffer
  * of cap_words u64 (NULL: off). Each traced launch takes 16 u64 per CTA

@@ -23,6 +23,7 @@ EXPORTS = [
     "pb_span_profile", "pb_span_profile_read", "pb_head_create", "pb_head_destroy", "pb_head_device_bytes",
     "pb_head_gen", "pb_head_load", "pb_head_embed", "pb_head_embed_device", "pb_head_logits", "pb_head_greedy",
     "pb_span_step_tape", "pb_span_backward", "pb_trace_set", "pb_trace_meta",
+    "pb_hop_alloc", "pb_hop_free", "pb_hop_open", "pb_hop_close", "pb_hop_wait", "pb_hop_signal",
 ]
 
 
@@ -64,6 +65,12 @@ def lib() -> C.CDLL:
         "pb_span_backward": [P, P, I32, P, P, VP],
         "pb_span_profile": [P, I32],
         "pb_trace_set": [P, I64],
+        "pb_hop_alloc": [I64, I32, C.POINTER(C.c_void_p), P],
+        "pb_hop_free": [P],
+        "pb_hop_open": [P, I32, C.POINTER(C.c_void_p)],
+        "pb_hop_close": [P],
+        "pb_hop_wait": [P, U64, I64, VP],
+        "pb_hop_signal": [P, U64, VP],
         "pb_span_profile_read": [P, I32, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double)],
         "pb_head_create": [I32, I32, I32, I32, C.POINTER(C.c_void_p)],
         "pb_head_destroy": [P],

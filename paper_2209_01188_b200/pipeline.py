@@ -91,3 +91,75 @@ def torch_exchange(ops):
     p2p = [dist.P2POp(dist.isend if op == "send" else dist.irecv, buf, peer) for op, buf, peer in ops]
     for w in dist.batch_isend_irecv(p2p):
         w.wait()
+
+
+class DevPtr:
+    """A raw device address where the span API expects a tensor (data_ptr())."""
+
+    def __init__(self, addr: int):
+        self.addr = int(addr)
+
+    def data_ptr(self) -> int:
+        return self.addr
+
+
+class P2PRing:
+    """The RingSchedule's hops over NVLink peer memory (pb_hop.cu) instead of
+    NCCL: every rank exports one mailbox (u64 flags + `slots` payload slots)
+    by CUDA IPC handle and maps its successor's. Job j's payload goes to slot
+    j % slots of the receiver; its flag there is set to j + 1 (monotonic per
+    slot). slots = sessions + 1 is enough without flow control: only
+    `sessions` jobs are in flight around the ring, so job j + slots cannot be
+    sent before job j was consumed."""
+
+    FLAGS = 64
+
+    def __init__(self, rank: int, world: int, sessions: int, slot_bytes: int, device: int, dist, timeout_ms=120000):
+        import ctypes as C
+
+        from . import _lib
+
+        self.rank, self.world, self.S = rank, world, sessions
+        self.slots = sessions + 1
+        assert self.slots <= self.FLAGS
+        self.slot_bytes = -(-slot_bytes // 256) * 256
+        self.timeout_ms = timeout_ms
+        self.L = _lib.lib()
+        total = 8 * self.FLAGS + self.slots * self.slot_bytes
+        base, handle = C.c_void_p(), (C.c_char * 64)()
+        _lib.check(self.L.pb_hop_alloc(total, device, C.byref(base), handle))
+        self.base = base.value
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(handle))
+        peer = C.c_void_p()
+        succ = (rank + 1) % world
+        _lib.check(self.L.pb_hop_open(C.create_string_buffer(handles[succ], 64), device, C.byref(peer)))
+        self.peer = peer.value
+
+    def _slot(self, base: int, j: int) -> int:
+        return base + 8 * self.FLAGS + (j % self.slots) * self.slot_bytes
+
+    def local_slot(self, j: int) -> int:
+        return self._slot(self.base, j)
+
+    def peer_slot(self, j: int) -> int:
+        return self._slot(self.peer, j)
+
+    def wait(self, j: int, stream: int) -> None:
+        from . import _lib
+
+        _lib.check(self.L.pb_hop_wait(self.base + 8 * (j % self.slots), j + 1, self.timeout_ms, stream))
+
+    def signal(self, j: int, stream: int) -> None:
+        """Publish job j (payload already stored in the successor's slot j % slots)."""
+        from . import _lib
+
+        _lib.check(self.L.pb_hop_signal(self.peer + 8 * (j % self.slots), j + 1, stream))
+
+    def close(self) -> None:
+        if getattr(self, "peer", None):
+            self.L.pb_hop_close(self.peer)
+            self.peer = None
+        if getattr(self, "base", None):
+            self.L.pb_hop_free(self.base)
+            self.base = None
