@@ -48,7 +48,7 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
 
     const int c = blockIdx.x;
     const int64_t u0 = (int64_t)c * U / G, u1 = (int64_t)(c + 1) * U / G;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = warp_uniform_id();
     const int64_t kv_stride = (int64_t)a.H * a.P * DH;
 
     if (threadIdx.x == 0) {
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_pf(AttnArgs a, int
 
     const int c = blockIdx.x;
     const int64_t u0 = (int64_t)c * U / G, u1 = (int64_t)(c + 1) * U / G;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = warp_uniform_id();
     const int64_t kv_stride = (int64_t)a.H * a.P * DH;
 
     if (threadIdx.x == 0) {

@@ -48,6 +48,11 @@ static inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b
 
 // ---------------------------------------------------------------- device helpers
 
+// Warp index the compiler can prove warp-uniform (a lane-0 broadcast): code
+// under `if (warp == w)` is then known to be converged, so shuffles there
+// compile to the plain SHFL instead of BRA.DIV + the collective fallback.
+__device__ __forceinline__ int warp_uniform_id() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0); }
+
 // Warp reductions reconverge the warp first (__syncwarp): after divergent
 // code the compiler's shuffle otherwise takes its non-converged path, traced
 // at ~1.5-3 us per reduction on the operand writer's critical path.

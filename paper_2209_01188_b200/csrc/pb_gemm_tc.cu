@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
     uint64_t* accempty = accfull + 2;       // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = warp_uniform_id(), lane = threadIdx.x & 31;
     const int KC = a.KC;
     const int G = gridDim.x;
 

@@ -203,7 +203,6 @@ template <int MODE, int SRC>
 __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
     if (MODE >= 0) a.mode = MODE;
     if (SRC >= 0) a.src.kind = SRC;
-    __shared__ float4 s_st;
     // early trigger (default): the GEMV that consumes this operand launches while
     // this kernel still waits for its producer and starts streaming weights
     // (its own griddepcontrol.wait still orders it after this grid completes)
@@ -218,17 +217,11 @@ __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
     if (!a.early) pdl_trigger();
     if (threadIdx.x == 0) trace_stamp(a.trace, tcta, 1);
     const int tok = blockIdx.y;
-    if (threadIdx.x < 32) {
-        const float4 r = resolve_stats(a, tok);
-        if (threadIdx.x == 0) s_st = r;
-        if (a.trace) {
-            asm volatile("" ::"f"(r.x), "f"(r.y), "f"(r.z));
-            if (threadIdx.x == 0) trace_stamp(a.trace, blockIdx.y * gridDim.x + blockIdx.x, 2);
-        }
-    }
-    __syncthreads();
+    // every warp resolves the statistics itself (warp-uniform code, no CTA
+    // barrier; a lane-divergent region made the shuffles take the compiler's
+    // non-converged path: ncu showed WARPSYNC.COLLECTIVE, ~5 us per resolve)
+    const float4 st = resolve_stats(a, tok);
     if (threadIdx.x == 0) trace_stamp(a.trace, tcta, 5);
-    const float4 st = s_st;
     if (blockIdx.x == 0) operand_token_outputs(a, tok, st, threadIdx.x, blockDim.x);
     if (it < KC * 4) frag_item(a, tok, it >> 2, it & 3, st, fp);
     if (threadIdx.x == 0) trace_stamp(a.trace, tcta, 6);
@@ -388,7 +381,7 @@ __device__ __forceinline__ void sk_epilogue(const SkArgs& a, int (&acc)[2][digit
                                             int* S) {
     constexpr int NT = digit_ntiles(TC);
     constexpr int SST = 8 * NT + 1;
-    const int lane = threadIdx.x & 31, cw = (threadIdx.x >> 5) - 1;
+    const int lane = threadIdx.x & 31, cw = warp_uniform_id() - 1;
     const int g = lane >> 2, q = lane & 3;
     // ---- fused epilogue of the 128-row group
     cons_sync();  // S is free (previous epilogue done)
@@ -470,7 +463,7 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
     uint64_t* empty = full + SK_STAGES;
     int* s_flag = reinterpret_cast<int*>(empty + SK_STAGES);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = warp_uniform_id(), lane = threadIdx.x & 31;
     const int chunk = blockIdx.y;
     const int c = blockIdx.x;
     const int64_t u0 = (int64_t)c * a.total / a.G, u1 = (int64_t)(c + 1) * a.total / a.G;

@@ -58,7 +58,7 @@ struct CSum {
 };
 
 // Resolve {mu, inv, 2^shift, 2^-shift} of one token inside the operand
-// producer (warp 0), from the producing epilogue's partial summaries
+// producer (any full warp; warp-uniform control flow), from the producing epilogue's partial summaries
 // (deterministic lane-strided + fixed shuffle-tree merge) or from the exact
 // atomicMax of |x s|.
 __device__ inline float4 resolve_stats(const ProArgs& a, int tok) {
@@ -91,7 +91,7 @@ __device__ inline float4 resolve_stats(const ProArgs& a, int tok) {
         for (int i = 0; i < 4; ++i) {
             const int g = g0 + lane + 32 * i;
             const float4 q = g0 == 0 ? p[i] : (g < a.src.MG ? ps[g] : make_float4(0.f, 0.f, INFINITY, -INFINITY));
-            if (g < a.src.MG) s1.add(__fmul_rn((float)min(128, a.src.M - g * 128), q.x));
+            s1.add(g < a.src.MG ? __fmul_rn((float)min(128, a.src.M - g * 128), q.x) : 0.f);  // branch-free
             mn = fminf(mn, q.z);
             mx = fmaxf(mx, q.w);
         }
@@ -108,11 +108,10 @@ __device__ inline float4 resolve_stats(const ProArgs& a, int tok) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int g = lane + 32 * i;
-            if (g < a.src.MG) {
-                const float dm = p[i].x - mu;
-                s2.add(p[i].y);
-                s2.add(__fmul_rn(__fmul_rn((float)min(128, a.src.M - g * 128), dm), dm));
-            }
+            const bool in = g < a.src.MG;
+            const float dm = p[i].x - mu;
+            s2.add(in ? p[i].y : 0.f);
+            s2.add(in ? __fmul_rn(__fmul_rn((float)min(128, a.src.M - g * 128), dm), dm) : 0.f);
         }
     } else {
         for (int g = lane; g < a.src.MG; g += 32) {
