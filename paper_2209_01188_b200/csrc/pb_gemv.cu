@@ -710,24 +710,33 @@ int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, i
     static int cfg = -1;
     if (cfg < 0) {
         // tuning knob (k tiles per stage x stages) of the decode (TC = 2) kernel:
-        // 0 = 2x4, 1 = 4x4 (default), 2 = 2x8, 3 = 4x6, 4 = 8x3, 5 = 4x3, 6 = 8x2, 7 = 4x8, 8 = 4x12
+        // 1 = 4x4 (three CTAs per SM), 6 = 8x2, 8 = 4x12, 10 = 6x3, 11 = 8x4 (default),
+        // 12 = 16x3, 14 = 8x6 (sweep: profiles/r1_gemv_timeline_and_tail.txt)
         const char* e = getenv("PB_GEMV_CFG");
-        cfg = e ? atoi(e) : 1;
+        cfg = e ? atoi(e) : 11;  // 8 k tiles (32 KB) x 4 stages, one CTA per SM (profiles/r1_gemv_timeline_and_tail.txt)
+    }
+    static int cfg8 = -1;
+    if (cfg8 < 0) {
+        const char* e = getenv("PB_GEMV_CFG8");  // tuning knob of the 3..8-token kernel: 0 = 4x4, 1 = 8x4, 2 = 8x2 (default)
+        cfg8 = e ? atoi(e) : 2;
     }
     switch (act.tc) {
         case 2:
             switch (cfg) {
-                case 0: return sk_launch<2, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
-                case 2: return sk_launch<2, 2, 8>(m, act, epi, partials, counters, partial_cap, st);
-                case 3: return sk_launch<2, 4, 6>(m, act, epi, partials, counters, partial_cap, st);
-                case 4: return sk_launch<2, 8, 3>(m, act, epi, partials, counters, partial_cap, st);
-                case 5: return sk_launch<2, 4, 3>(m, act, epi, partials, counters, partial_cap, st);
                 case 6: return sk_launch<2, 8, 2>(m, act, epi, partials, counters, partial_cap, st);
-                case 7: return sk_launch<2, 4, 8>(m, act, epi, partials, counters, partial_cap, st);
                 case 8: return sk_launch<2, 4, 12>(m, act, epi, partials, counters, partial_cap, st);
-                default: return sk_launch<2, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
+                case 10: return sk_launch<2, 6, 3>(m, act, epi, partials, counters, partial_cap, st);
+                case 12: return sk_launch<2, 16, 3>(m, act, epi, partials, counters, partial_cap, st);
+                case 14: return sk_launch<2, 8, 6>(m, act, epi, partials, counters, partial_cap, st);
+                case 1: return sk_launch<2, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
+                default: return sk_launch<2, 8, 4>(m, act, epi, partials, counters, partial_cap, st);
             }
-        case 8: return sk_launch<8, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
+        case 8:
+            switch (cfg8) {
+                case 1: return sk_launch<8, 8, 4>(m, act, epi, partials, counters, partial_cap, st);
+                case 2: return sk_launch<8, 8, 2>(m, act, epi, partials, counters, partial_cap, st);
+                default: return sk_launch<8, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
+            }
         case 16: return sk_launch<16, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
         case 32: return sk_launch<32, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
         default: set_error("bad column tile"); return PB_ERR_GENERIC;
