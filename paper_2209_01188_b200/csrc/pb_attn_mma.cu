@@ -27,24 +27,24 @@
 
 namespace pb {
 
-template <int DH>
+template <int DH, int ST>
 constexpr size_t attn_mma_smem() {
-    return (size_t)AM_ST * 2 * AM_SK * DH * 2 + (size_t)AM_WARPS * AM_G * (DH + 2) * 4 + 2 * AM_ST * 8 + 64 +
+    return (size_t)ST * 2 * AM_SK * DH * 2 + (size_t)AM_WARPS * AM_G * (DH + 2) * 4 + 2 * ST * 8 + 64 +
            4 * AM_PT;
 }
 
-template <int DH>
+template <int DH, int ST>
 __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, int G, int64_t U) {
     constexpr int NKT = DH / 16;  // k-steps of S
     constexpr int NNT = DH / 8;   // n-tiles of O
     constexpr int ROWB = DH * 2;  // bytes per K/V row
     extern __shared__ __align__(128) uint8_t smem[];
     half* Ks = reinterpret_cast<half*>(smem);                         // [ST][SK][DH]
-    half* Vs = Ks + AM_ST * AM_SK * DH;                               // [ST][SK][DH]
-    float* wst = reinterpret_cast<float*>(Vs + AM_ST * AM_SK * DH);   // [WARPS][G][DH + 2]
+    half* Vs = Ks + ST * AM_SK * DH;                               // [ST][SK][DH]
+    float* wst = reinterpret_cast<float*>(Vs + ST * AM_SK * DH);   // [WARPS][G][DH + 2]
     uint64_t* full = reinterpret_cast<uint64_t*>(wst + AM_WARPS * AM_G * (DH + 2));
-    uint64_t* empty = full + AM_ST;
-    int* s_flag = reinterpret_cast<int*>(empty + AM_ST);
+    uint64_t* empty = full + ST;
+    int* s_flag = reinterpret_cast<int*>(empty + ST);
 
     const int c = blockIdx.x;
     const int64_t u0 = (int64_t)c * U / G, u1 = (int64_t)(c + 1) * U / G;
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
 
     if (threadIdx.x == 0) {
         trace_stamp(a.trace, c, 0);
-        for (int b = 0; b < AM_ST; ++b) {
+        for (int b = 0; b < ST; ++b) {
             mbar_init(&full[b], 1);
             mbar_init(&empty[b], AM_WARPS);
         }
@@ -90,8 +90,8 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
                     for (int p = lane; p < AM_PT && pbase + p <= plast; p += 32) s_pages[p] = pt[pbase + p];
                     __syncwarp();
                 }
-                const int b = it % AM_ST;
-                mbar_wait(&empty[b], ((it / AM_ST) & 1) ^ 1);
+                const int b = it % ST;
+                mbar_wait(&empty[b], ((it / ST) & 1) ^ 1);
                 if (!waited && k1 > safe_end) {
                     pdl_wait();
                     pdl_trigger();
@@ -163,9 +163,9 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
 #pragma unroll
             for (int r = 0; r < 4; ++r) o[n][r] = 0.f;
         for (int i = sg.i0; i < sg.i0 + sg.n; ++i, ++it) {
-            const int b = it % AM_ST;
+            const int b = it % ST;
             const int k0 = i * AM_SK;
-            mbar_wait(&full[b], (it / AM_ST) & 1);
+            mbar_wait(&full[b], (it / ST) & 1);
             const int kb = warp * 16;  // this warp's 16 keys of the stage
             if (a.debug_nocomp) {  // experiment: memory pipeline only
                 __syncwarp();
@@ -652,20 +652,21 @@ int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st) 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     static const int per_sm = [] {
-        const char* e = getenv("PB_ATTM_CTAS");  // tuning knob: CTAs per SM (smem allows 2)
+        const char* e = getenv("PB_ATTM_CTAS");  // tuning knob: 1 (6-stage ring) or 2 (3 stages, default) CTAs per SM
         return e ? atoi(e) : 2;
     }();
     const int64_t U = a.total_units;
     if (U <= 0) return PB_OK;
     // CTAs: fill the machine, but keep every (group, head) within AM_MAXC contributors
-    int64_t G = std::min<int64_t>(U, (int64_t)per_sm * sms);
+    const bool prefill = a.max_group > AM_G;  // prefill groups: queries split across warps (3-stage ring, 2 per SM)
+    int64_t G = std::min<int64_t>(U, (int64_t)(prefill ? 2 : per_sm) * sms);
     while (G > 1 && ceil_div(a.max_stages, U / G) + 1 > AM_MAXC) --G;
     if ((int64_t)a.n_tok * a.H * AM_MAXC * (DH + 2) > cap) {
         set_error("attention workspace too small");
         return PB_ERR_CAPACITY;
     }
     (void)n_groups;
-    if (a.max_group > AM_G) {  // prefill groups: queries split across warps
+    if (prefill) {
         constexpr size_t smem = attn_pf_smem<DH>();
         static bool configured = false;
         if (!configured) {
@@ -674,10 +675,15 @@ int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st) 
         }
         return launch_pdl(k_attn_pf<DH>, dim3((unsigned)G), dim3((AM_WARPS + 1) * 32), smem, st, a, (int)G, U);
     }
-    constexpr size_t smem = attn_mma_smem<DH>();
+    // two CTAs per SM with 3-stage rings (default) or one with 6 stages: the
+    // same K/V bytes in flight per SM; one CTA has a smaller tail but only 4
+    // compute warps per SM and measured slower (176B 442 vs 444 us/block)
+    constexpr size_t smem = attn_mma_smem<DH, 3>();
+    constexpr size_t smem6 = attn_mma_smem<DH, 6>();
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_attn_mma<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_attn_mma<DH, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_attn_mma<DH, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem6);
         configured = true;
     }
     static const int nocomp = [] {
@@ -687,7 +693,9 @@ int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st) 
     AttnArgs aa = a;
     aa.debug_nocomp = nocomp;
     aa.trace = trace_region(TR_ATTN, (int)G);
-    return launch_pdl(k_attn_mma<DH>, dim3((unsigned)G), dim3((AM_WARPS + 1) * 32), smem, st, aa, (int)G, U);
+    if (per_sm == 1)
+        return launch_pdl(k_attn_mma<DH, 6>, dim3((unsigned)G), dim3((AM_WARPS + 1) * 32), smem6, st, aa, (int)G, U);
+    return launch_pdl(k_attn_mma<DH, 3>, dim3((unsigned)G), dim3((AM_WARPS + 1) * 32), smem, st, aa, (int)G, U);
 }
 
 template int run_attn_mma<64>(const AttnArgs&, int, int64_t, cudaStream_t);
