@@ -294,6 +294,19 @@ __global__ void __launch_bounds__(256) k_rows_f32(ProArgs a) {
         a.y32[(int64_t)tok * a.K + k] = pro_y(a, x, k, st.x, st.y);
 }
 
+int prepare_fused_operand(int mode, const ProSrc& src, const float* x, int n_tok, int K, int Kp, const float* gamma,
+                          const float* beta, const Mat& m, int tc, float* back, float4* stats, float* xo,
+                          cudaStream_t st, ProArgs* out) {
+    ProArgs a{mode, x, K, Kp, gamma, beta, m.scales, m.n_outl, m.outl_idx, tc, nullptr, back, stats, xo, nullptr, src, 1};
+    a.src.zero_tokmax = nullptr;  // the fused QKV launch resets both ranges (launch_gemv_fused zero_a/zero_b)
+    if (a.src.kind == SRC_STATS) {
+        k_rowstats<<<n_tok, STATS_THREADS, 0, st>>>(a);
+        if (int rc = launch_check("rowstats")) return rc;
+    }
+    *out = a;
+    return PB_OK;
+}
+
 int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int K, int Kp, const float* gamma,
                     const float* beta, const Mat& m, int tc, uint4* frag, float* back, float4* stats, float* xo,
                     float* y32, cudaStream_t st, uint8_t* bcanon) {
@@ -367,6 +380,11 @@ struct SkArgs {
     int* counters;    // [chunk][MG]
     uint64_t* trace;  // diagnostics (pb_trace_set), usually null
     int64_t l2pf_bytes;  // weight bytes per CTA prefetched into L2 while waiting for the operand
+    // fused operand (k_gemv_i8<.., FUSED>): an operand warp builds the B fragments of
+    // every stage in shared memory from the activations (no k_fragwrite launch)
+    ProArgs pro;
+    float* zero_a;  // accumulators of later producers reset by this launch (QKV: max|ctx s|, max|act s|)
+    float* zero_b;
 };
 
 __device__ __forceinline__ int sk_owner(int64_t u, int G, int64_t total) {
@@ -446,8 +464,125 @@ __device__ __forceinline__ void sk_epilogue(const SkArgs& a, int (&acc)[2][digit
     }
 }
 
+// Fused-operand warps (decode, TC = 2 tokens per column chunk): after
+// the dependency wait each resolves the chunk's token statistics itself (LN
+// summaries / atomicMax range of the producing kernel, as k_fragwrite does);
+// warp 0 writes the per-token side outputs. Then, for its own stages (every
+// SK_OPW-th in the producer's order), a warp loads the stage's inputs, waits
+// for the ring slot, and writes the m16n8k32 B fragments of the stage's k
+// tiles straight into shared memory: the same digits as frag_item, bit for
+// bit. Lane l owns features 4l..4l+3 of each 128-feature slice; one float4 of
+// x (+ gamma, beta) and scales per slice.
+constexpr int SK_OPW = 4;  // operand warps of the fused GEMV: warp w fills the stages s = w (mod 4)
+
 template <int TC, int SK_KCS, int SK_STAGES>
-__global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
+__device__ __forceinline__ void sk_operand_warp(const SkArgs& a, int64_t u0, int64_t u1, int chunk, uint8_t* sb,
+                                                uint64_t* full, uint64_t* empty, int ow) {
+    constexpr int NT = digit_ntiles(TC);
+    constexpr int B_STAGE = SK_KCS * NT * 256;
+    // a warp reuses only its own ring slots, so it can never run two rounds ahead
+    // of the consumers (mbarrier parity waits cannot tell those rounds apart)
+    static_assert(SK_STAGES % SK_OPW == 0, "operand warps must own whole ring slots");
+    const ProArgs& p = a.pro;
+    const int lane = threadIdx.x & 31;
+    float4 st[TC];
+#pragma unroll
+    for (int t = 0; t < TC; ++t) {
+        const int tok = chunk * TC + t;
+        st[t] = tok < a.act.n_tok ? resolve_stats(p, tok) : make_float4(0.f, 1.f, 0.f, 0.f);  // warp-uniform
+        if (tok < a.act.n_tok && ow == 0) {
+            if (lane == 0) p.back[tok] = st[t].w * (1.f / 256.f);
+            if (p.xo) {
+                const float* x = p.x + (int64_t)tok * p.K;
+                for (int j = lane; j < p.n_outl; j += 32)
+                    p.xo[(int64_t)tok * p.n_outl + j] = pro_y(p, x, p.outl_idx[j], st[t].x, st[t].y);
+            }
+        }
+    }
+    if (a.zero_a && blockIdx.x == 0 && ow == 0 && lane < TC && chunk * TC + lane < a.act.n_tok) {
+        a.zero_a[chunk * TC + lane] = 0.f;
+        a.zero_b[chunk * TC + lane] = 0.f;
+    }
+    const bool ln = p.mode == PRO_LN;
+    int stage = 0, seq = 0;
+    uint32_t phase = 0;
+    for (int64_t u = u0; u < u1;) {
+        const int ka = (int)(u % a.KC);
+        const int kb = (int)((int64_t)a.KC < ka + (u1 - u) ? (int64_t)a.KC : ka + (u1 - u));
+        for (int kc = ka; kc < kb; kc += SK_KCS, ++seq) {
+            const int n = min(SK_KCS, kb - kc);
+            if (seq % SK_OPW != ow) {  // another operand warp's stage
+                if (++stage == SK_STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+                continue;
+            }
+            // inputs first (they do not depend on the ring slot): their L2 latency
+            // overlaps the wait for the consumers to free this stage
+            constexpr int NI = (SK_KCS + 3) / 4;  // 128-feature slices per stage
+            float4 sc[NI], g4[NI], b4[NI], x4[NI][TC];
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const int krel = 128 * i + 4 * lane;
+                const int k = kc * 32 + krel;
+                const bool in = krel < n * 32 && k < p.K;  // K % 4 == 0 (launcher): slices are in or out
+                sc[i] = in ? *reinterpret_cast<const float4*>(p.scales + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+                g4[i] = in && ln ? *reinterpret_cast<const float4*>(p.gamma + k) : make_float4(1.f, 1.f, 1.f, 1.f);
+                b4[i] = in && ln ? *reinterpret_cast<const float4*>(p.beta + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int t = 0; t < TC; ++t) {
+                    const int tok = chunk * TC + t;
+                    x4[i][t] = in && tok < a.act.n_tok ? *reinterpret_cast<const float4*>(p.x + (int64_t)tok * p.K + k)
+                                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint32_t* B = reinterpret_cast<uint32_t*>(sb + stage * B_STAGE);
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const int krel = 128 * i + 4 * lane;
+                if (krel >= n * 32) continue;
+                const int kk = krel >> 5, kt = krel & 31, half_ = kt >> 4, q = (kt & 15) >> 2;
+#pragma unroll
+                for (int t = 0; t < TC; ++t) {
+                    const int tok = chunk * TC + t;
+                    if (tok >= a.act.n_tok) continue;
+                    const float xs[4] = {x4[i][t].x, x4[i][t].y, x4[i][t].z, x4[i][t].w},
+                                gs[4] = {g4[i].x, g4[i].y, g4[i].z, g4[i].w},
+                                bs[4] = {b4[i].x, b4[i].y, b4[i].z, b4[i].w},
+                                ss[4] = {sc[i].x, sc[i].y, sc[i].z, sc[i].w};
+                    const float z = st[t].z * 256.f;
+                    uint32_t w[3] = {0u, 0u, 0u};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float y = ln ? fmaf(gs[e], (xs[e] - st[t].x) * st[t].y, bs[e]) : xs[e];  // model.py:271-276
+                        int h, m, l;
+                        digits3(__float2int_rn((y * ss[e]) * z), h, m, l);
+                        w[0] |= (uint32_t)(uint8_t)h << (8 * e);
+                        w[1] |= (uint32_t)(uint8_t)m << (8 * e);
+                        w[2] |= (uint32_t)(uint8_t)l << (8 * e);
+                    }
+#pragma unroll
+                    for (int pp = 0; pp < 3; ++pp) {
+                        const int cc = pp * TC + t;
+                        B[((kk * NT + (cc >> 3)) * 32 + 4 * (cc & 7) + q) * 2 + half_] = w[pp];
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[stage]);
+            if (++stage == SK_STAGES) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+        u += kb - ka;
+    }
+}
+
+template <int TC, int SK_KCS, int SK_STAGES, bool FUSED = false>
+__global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv_i8(SkArgs a) {
     constexpr int NT = digit_ntiles(TC);
     constexpr int COLS = 8 * NT;
     constexpr int SST = COLS + 1;
@@ -471,7 +606,7 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
     if (threadIdx.x == 0) {
         trace_stamp(a.trace, tcta, 0);
         for (int s = 0; s < SK_STAGES; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], FUSED ? 2 : 1);  // fused: + the stage's operand-warp arrival
             mbar_init(&empty[s], SK_CONS);
         }
         mbar_fence_init();
@@ -480,6 +615,33 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
     if (u0 >= u1) {
         pdl_wait();
         pdl_trigger();
+    } else if (FUSED && warp > SK_CONS) {
+        // ---------------- operand warps
+        pdl_wait();
+        pdl_trigger();
+        sk_operand_warp<TC, SK_KCS, SK_STAGES>(a, u0, u1, chunk, sb, full, empty, warp - SK_CONS - 1);
+    } else if (FUSED && warp == 0) {
+        // ---------------- producer: weights only (they never depend on earlier kernels)
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t u = u0; u < u1;) {
+                const int mg = (int)(u / a.KC);
+                const int ka = (int)(u % a.KC);
+                const int kb = (int)((int64_t)a.KC < ka + (u1 - u) ? (int64_t)a.KC : ka + (u1 - u));
+                for (int kc = ka; kc < kb; kc += SK_KCS) {
+                    const int n = min(SK_KCS, kb - kc);
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], n * 4096);
+                    bulk_g2s(sa + stage * A_STAGE, a.codes + ((int64_t)mg * a.KC + kc) * 4096, n * 4096, &full[stage]);
+                    if (++stage == SK_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                u += kb - ka;
+            }
+        }
     } else if (warp == 0) {
         // ---------------- producer
         if (lane == 0) {
@@ -650,9 +812,11 @@ __global__ void __launch_bounds__(SK_THREADS) k_gemv_i8(SkArgs a) {
 }
 
 
-template <int TC, int SK_KCS, int SK_STAGES>
+template <int TC, int SK_KCS, int SK_STAGES, bool FUSED = false>
 static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
-                     int64_t partial_cap, cudaStream_t st) {
+                     int64_t partial_cap, cudaStream_t st, const ProArgs* pro = nullptr, float* zero_a = nullptr,
+                     float* zero_b = nullptr) {
+    constexpr int THREADS = SK_THREADS + (FUSED ? 32 * SK_OPW : 0);
     constexpr int NT = digit_ntiles(TC);
     const size_t smem = (size_t)SK_STAGES * (SK_KCS * 4096 + SK_KCS * NT * 256) + 128 * (8 * NT + 1) * 4 + 16 +
                         2 * SK_STAGES * 8 + 16;
@@ -661,8 +825,8 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_gemv_i8<TC, SK_KCS, SK_STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_gemv_i8<TC, SK_KCS, SK_STAGES>, SK_THREADS, smem);
+        cudaFuncSetAttribute(k_gemv_i8<TC, SK_KCS, SK_STAGES, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_gemv_i8<TC, SK_KCS, SK_STAGES, FUSED>, THREADS, smem);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
         // tuning knob: fewer CTAs per SM than fit leaves a slot for the next
         // kernel of the chain (PDL) to become resident and start streaming
@@ -702,7 +866,31 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
         return (int64_t)(e ? atoi(e) : 0) * 1024;
     }();
     a.l2pf_bytes = l2pf;
-    return launch_pdl(k_gemv_i8<TC, SK_KCS, SK_STAGES>, dim3((unsigned)G, chunks), dim3(SK_THREADS), smem, st, a);
+    if (FUSED) {
+        a.pro = *pro;
+        a.pro.trace = nullptr;
+        a.zero_a = zero_a;
+        a.zero_b = zero_b;
+    }
+    return launch_pdl(k_gemv_i8<TC, SK_KCS, SK_STAGES, FUSED>, dim3((unsigned)G, chunks), dim3(THREADS), smem, st, a);
+}
+
+bool gemv_fusable(const Act& act, int K) {
+    static const bool off = getenv("PB_NO_FUSED_OPERAND") != nullptr;  // A/B knob: separate k_fragwrite
+    const char* e = getenv("PB_GEMV_CFG");
+    if (off || (K & 3) != 0) return false;
+    // 2 tokens per column chunk only: the 8-token variant measured slower (operand
+    // warps compute-bound: 560M batch 8 68 -> 117 us/block)
+    return act.tc == 2 && (!e || atoi(e) == 11);
+}
+
+int launch_gemv_fused(const Mat& m, const Act& act, const Epi& epi, const ProArgs& pro, float* zero_a,
+                      float* zero_b, float* partials, int* counters, int64_t partial_cap, cudaStream_t st) {
+    if (!gemv_fusable(act, pro.K)) {
+        set_error("fused-operand GEMV: unsupported shape");
+        return PB_ERR_GENERIC;
+    }
+    return sk_launch<2, 8, 4, true>(m, act, epi, partials, counters, partial_cap, st, &pro, zero_a, zero_b);
 }
 
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters, int64_t partial_cap,

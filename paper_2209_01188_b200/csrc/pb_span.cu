@@ -405,12 +405,38 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                 e.outl_idx = m.outl_idx;
                 e.outl_rows = m.outl_rows;
                 e.xo = s->xo;
+                Act a{s->frag, s->back, n_tok, tc};
+                // measured (profiles/r1_gemv_timeline_and_tail.txt): fused wins where the
+                // kernel boundaries dominate (560M -12 %, 7B1 -8 % per block) but costs ~1 %
+                // at the 176B shape in a sustained run (its operand warps' extra power lowers
+                // the capped SM clock), so the switch is by hidden size
+                static const int fuse_max_d = [] {
+                    const char* e = getenv("PB_FUSED_MAX_HIDDEN");
+                    return e ? atoi(e) : 8192;
+                }();
+                if (d <= fuse_max_d && gemv_fusable(a, K)) {
+                    // decode: the GEMV's operand warp builds the int8-digit operand itself;
+                    // the QKV launch resets the two range accumulators of this block
+                    // (attention -> wo, wmlp_in epilogue -> wmlp_out), whose previous
+                    // readers (block j-1) have completed by then
+                    ProArgs pa;
+                    if (int rc = prepare_fused_operand(mode, src, x, n_tok, K, m.Kp, g, be, m, tc, s->back, s->stats,
+                                                       s->xo, st, &pa))
+                        return rc;
+                    launches += src.kind == SRC_STATS ? 2 : 1;  // (rowstats +) gemv
+                    const int ev = prof_begin(s, st);
+                    const double bytes = (double)m.M * m.K + 4.0 * m.K + 4.0 * m.M + 4.0 * m.n_outl * m.M;
+                    int rc = launch_gemv_fused(m, a, e, pa, mi == 0 ? s->tokmax_ctx : nullptr,
+                                               mi == 0 ? s->tokmax_act : nullptr, s->partials, s->counters,
+                                               s->partial_cap, st);
+                    prof_end(s, ev, 0, bytes, st);
+                    return rc;
+                }
                 int ev = prof_begin(s, st);
                 if (int rc = launch_prologue(mode, src, x, n_tok, K, m.Kp, g, be, m, tc, s->frag, s->back, s->stats,
                                              s->xo, nullptr, st))
                     return rc;
                 prof_end(s, ev, 2, 4.0 * n_tok * K, st);
-                Act a{s->frag, s->back, n_tok, tc};
                 launches += src.kind == SRC_STATS ? 3 : 2;  // (rowstats +) fragwrite + gemv
                 ev = prof_begin(s, st);
                 // algorithmic bytes: codes + per-feature scales + bias (+ f32 outlier rows)

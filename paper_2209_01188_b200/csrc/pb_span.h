@@ -140,6 +140,15 @@ struct ProArgs {
 
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
                 int64_t partial_cap, cudaStream_t st);
+// decode (<= 2 tokens per column chunk): the operand is built inside the GEMV
+// by an operand warp (no k_fragwrite launch); prepare_fused_operand runs the
+// block-0 row statistics if needed and returns the operand description
+bool gemv_fusable(const Act& act, int K);
+int prepare_fused_operand(int mode, const ProSrc& src, const float* x, int n_tok, int K, int Kp, const float* gamma,
+                          const float* beta, const Mat& m, int tc, float* back, float4* stats, float* xo,
+                          cudaStream_t st, ProArgs* out);
+int launch_gemv_fused(const Mat& m, const Act& act, const Epi& epi, const ProArgs& pro, float* zero_a,
+                      float* zero_b, float* partials, int* counters, int64_t partial_cap, cudaStream_t st);
 int launch_gemm_f32(const Mat& m, const float* y, int n_tok, const Epi& epi, float* part, int64_t part_cap,
                     cudaStream_t st);
 int choose_tc(int n_tok);
