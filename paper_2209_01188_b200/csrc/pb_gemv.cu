@@ -480,9 +480,6 @@ __device__ __forceinline__ void sk_operand_warp(const SkArgs& a, int64_t u0, int
                                                 uint64_t* full, uint64_t* empty, int ow) {
     constexpr int NT = digit_ntiles(TC);
     constexpr int B_STAGE = SK_KCS * NT * 256;
-    // a warp reuses only its own ring slots, so it can never run two rounds ahead
-    // of the consumers (mbarrier parity waits cannot tell those rounds apart)
-    static_assert(SK_STAGES % SK_OPW == 0, "operand warps must own whole ring slots");
     const ProArgs& p = a.pro;
     const int lane = threadIdx.x & 31;
     float4 st[TC];
@@ -583,6 +580,9 @@ __device__ __forceinline__ void sk_operand_warp(const SkArgs& a, int64_t u0, int
 
 template <int TC, int SK_KCS, int SK_STAGES, bool FUSED = false>
 __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv_i8(SkArgs a) {
+    // an operand warp reuses only its own ring slots, so it can never run two rounds
+    // ahead of the consumers (mbarrier parity waits cannot tell those rounds apart)
+    static_assert(!FUSED || SK_STAGES % SK_OPW == 0, "operand warps must own whole ring slots");
     constexpr int NT = digit_ntiles(TC);
     constexpr int COLS = 8 * NT;
     constexpr int SST = COLS + 1;
