@@ -304,9 +304,9 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
         bool finalize = cf == cl;
         if (!finalize) {
             // ---- last contributor of (g, h) merges the pieces in CTA order
-            __threadfence();
-            cons_bar();
+            cons_bar();  // every thread's partial stores precede the counter (fence by one thread, as in a grid sync)
             if (tid == 0) {
+                __threadfence();
                 int* ctr = a.counters + (int64_t)t0 * a.H + h;
                 const int prev = atomicAdd(ctr, 1);
                 const int last = prev == cl - cf;
@@ -603,9 +603,9 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_pf(AttnArgs a, int
                     out[2 + n * 8 + 2 * qd + 1] = o[n][1] + o[n][3];
                 }
             }
-            __threadfence();
             cons_bar();
             if (threadIdx.x == 0) {
+                __threadfence();
                 int* ctr = a.counters + (int64_t)t0 * a.H + h;
                 const int prev = atomicAdd(ctr, 1);
                 const int last = prev == cl - cf;

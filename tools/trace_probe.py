@@ -24,6 +24,7 @@ def main():
     p.add_argument("--batch", type=int, default=1)
     p.add_argument("--steps", type=int, default=2, help="traced steps (the last one is printed)")
     p.add_argument("--sm", action="store_true", help="per-SM GEMV streaming rates: are slow SMs the same every launch?")
+    p.add_argument("--attn", action="store_true", help="per-CTA attention durations: which CTAs form the tail")
     args = p.parse_args()
     import numpy as np
     import torch
@@ -98,6 +99,23 @@ def main():
                   f"items written {spread(r[:, 6])}")
     if args.sm:
         sm_rates([r for k, r in recs if k == "gemv"], np)
+    if args.attn:
+        for k, r in recs:
+            if k != "attn":
+                continue
+            ok = (r[:, 1] > 0) & (r[:, 3] > 0)
+            dur = (r[:, 3] - r[:, 1]) / 1e3
+            idx = np.where(ok)[0]
+            order = idx[np.argsort(-dur[idx])]
+            sm = r[:, 4].astype(int)
+            # CTAs sharing an SM: how much slower is the slower of a pair?
+            pairs = {}
+            for c in idx:
+                pairs.setdefault(sm[c], []).append(dur[c])
+            gaps = [max(v) - min(v) for v in pairs.values() if len(v) == 2]
+            print(f"attn: release->end p50 {np.median(dur[idx]):.1f} p90 {np.percentile(dur[idx], 90):.1f} "
+                  f"max {dur[idx].max():.1f} us; same-SM pair gap median {np.median(gaps) if gaps else 0:.1f} us; "
+                  f"slowest CTAs (index, SM, us): " + ", ".join(f"{c}/{sm[c]}/{dur[c]:.1f}" for c in order[:10]))
     span.close()
 
 
