@@ -237,7 +237,17 @@ class Pipeline:
         if self.world > 1 and args.hop == "p2p":
             from paper_2209_01188_b200.pipeline import P2PRing
 
-            self.ring = P2PRing(self.rank, self.world, self.S, cap, self.local, dist)
+            ok = 1
+            try:
+                self.ring = P2PRing(self.rank, self.world, self.S, cap, self.local, dist)
+            except Exception as e:  # e.g. no CUDA IPC between the processes: every rank falls back together
+                print(f"[rank {self.rank}] peer-memory hop unavailable ({e}); using NCCL send/recv", file=sys.stderr)
+                ok = 0
+            flag = torch.tensor([ok], device=self.dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if not int(flag.item()) and self.ring is not None:
+                self.ring.close()
+                self.ring = None
 
     def payload_bytes(self, t):
         n = t * self.B * self.d

@@ -127,10 +127,15 @@ class P2PRing:
         self.L = _lib.lib()
         total = 8 * self.FLAGS + self.slots * self.slot_bytes
         base, handle = C.c_void_p(), (C.c_char * 64)()
-        _lib.check(self.L.pb_hop_alloc(total, device, C.byref(base), handle))
-        self.base = base.value
-        handles = [None] * world
-        dist.all_gather_object(handles, bytes(handle))
+        self.base = self.peer = None
+        rc = self.L.pb_hop_alloc(total, device, C.byref(base), handle)
+        if rc == 0:
+            self.base = base.value
+        handles = [None] * world  # collective on every rank, even after a local failure
+        dist.all_gather_object(handles, bytes(handle) if rc == 0 else None)
+        if any(h is None for h in handles):
+            self.close()
+            raise RuntimeError("mailbox allocation failed on a rank")
         peer = C.c_void_p()
         succ = (rank + 1) % world
         _lib.check(self.L.pb_hop_open(C.create_string_buffer(handles[succ], 64), device, C.byref(peer)))
