@@ -48,6 +48,10 @@ __device__ __forceinline__ void split_h2(float x0, float x1, uint32_t& hi, uint3
 __device__ __forceinline__ void cons_bar() {  // the AM_WARPS compute warps only
     asm volatile("bar.sync 1, %0;" ::"n"(AM_WARPS * 32) : "memory");
 }
+template <int NW>
+__device__ __forceinline__ void cons_bar_n() {  // NW compute warps
+    asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+}
 
 // Stream-K decomposition: the work units are (query group, head, 64-key
 // stage), numbered group-major (unit_base[g] = first unit of group g, every

@@ -27,14 +27,18 @@
 
 namespace pb {
 
-template <int DH, int ST>
+template <int DH, int ST, int CW>
 constexpr size_t attn_mma_smem() {
-    return (size_t)ST * 2 * AM_SK * DH * 2 + (size_t)AM_WARPS * AM_G * (DH + 2) * 4 + 2 * ST * 8 + 64 +
+    return (size_t)ST * 2 * AM_SK * DH * 2 + (size_t)CW * AM_G * (DH + 2) * 4 + 2 * ST * 8 + 64 +
            4 * AM_PT;
 }
 
-template <int DH, int ST>
-__global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, int G, int64_t U) {
+template <int DH, int ST, int CW>
+__global__ void __launch_bounds__((CW + 1) * 32) k_attn_mma(AttnArgs a, int G, int64_t U) {
+    // CW = 4: four compute warps, 16 keys of every stage each. CW = 8 (one CTA per SM):
+    // two groups of four warps take alternate stages (more warps per SM hide the
+    // per-stage MMA / softmax latency); each warp keeps its own online softmax.
+    constexpr int GW = CW > 4 ? 4 : CW;  // warps per stage
     constexpr int NKT = DH / 16;  // k-steps of S
     constexpr int NNT = DH / 8;   // n-tiles of O
     constexpr int ROWB = DH * 2;  // bytes per K/V row
@@ -42,7 +46,7 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
     half* Ks = reinterpret_cast<half*>(smem);                         // [ST][SK][DH]
     half* Vs = Ks + ST * AM_SK * DH;                               // [ST][SK][DH]
     float* wst = reinterpret_cast<float*>(Vs + ST * AM_SK * DH);   // [WARPS][G][DH + 2]
-    uint64_t* full = reinterpret_cast<uint64_t*>(wst + AM_WARPS * AM_G * (DH + 2));
+    uint64_t* full = reinterpret_cast<uint64_t*>(wst + CW * AM_G * (DH + 2));
     uint64_t* empty = full + ST;
     int* s_flag = reinterpret_cast<int*>(empty + ST);
 
@@ -55,13 +59,13 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
         trace_stamp(a.trace, c, 0);
         for (int b = 0; b < ST; ++b) {
             mbar_init(&full[b], 1);
-            mbar_init(&empty[b], AM_WARPS);
+            mbar_init(&empty[b], GW);
         }
         mbar_fence_init();
     }
     __syncthreads();
 
-    if (warp == AM_WARPS) {
+    if (warp == CW) {
         // ---------------- producer warp: K/V page pieces of every stage of the range.
         // The segment's page-table entries are staged in shared memory first
         // (one coalesced load), so issuing a stage never waits on a global load.
@@ -127,10 +131,11 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
     const uint32_t ks_base = smem_u32(Ks), vs_base = smem_u32(Vs);
     const int mi = lane >> 3, ri = lane & 7;  // ldmatrix lane roles: matrix mi, row ri
     const float isq = 1.0f / sqrtf((float)DH);
-    int it = 0;
-    for (int64_t u = u0; u < u1;) {
+    int it = 0, nseg = 0;
+    for (int64_t u = u0; u < u1; ++nseg) {
         const AmSeg sg = am_seg(a, u, u1);
         const int h = sg.h;
+        if (threadIdx.x == 32 && nseg < 2) trace_stamp(a.trace, c, 5 + 3 * nseg);  // diagnostics: segment start
         const int t0 = a.grp_first[sg.g], nq = a.grp_count[sg.g];
         const int pos0 = a.tok_pos[t0];
         const int j1 = pos0 + nq;
@@ -163,10 +168,12 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
 #pragma unroll
             for (int r = 0; r < 4; ++r) o[n][r] = 0.f;
         for (int i = sg.i0; i < sg.i0 + sg.n; ++i, ++it) {
+            if (CW > GW && (it & 1) != (warp >> 2)) continue;  // the other warp group's stage
             const int b = it % ST;
             const int k0 = i * AM_SK;
             mbar_wait(&full[b], (it / ST) & 1);
-            const int kb = warp * 16;  // this warp's 16 keys of the stage
+            if (threadIdx.x == 32 && nseg < 2 && i == sg.i0) trace_stamp(a.trace, c, 6 + 3 * nseg);  // first data
+            const int kb = (warp & (GW - 1)) * 16;  // this warp's 16 keys of the stage
             if (a.debug_nocomp) {  // experiment: memory pipeline only
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[b]);
@@ -269,7 +276,7 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
                 w[2 + n * 8 + 2 * qd + 1] = o[n][1] + o[n][3];
             }
         }
-        cons_bar();
+        cons_bar_n<CW>();
         // ---- merge the 4 warps per query (fixed order); this CTA's piece of (g, h)
         const int cf = am_owner(sg.a, G, U), cl = am_owner(sg.a + sg.ns - 1, G, U);
         const int tid = threadIdx.x;  // 0 .. 127
@@ -279,20 +286,20 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
         for (int q = 0; q < nq; ++q) {
             float M = -INFINITY;
 #pragma unroll
-            for (int w = 0; w < AM_WARPS; ++w) M = fmaxf(M, wst[(w * AM_G + q) * (DH + 2)]);
-            float sw[AM_WARPS];
+            for (int w = 0; w < CW; ++w) M = fmaxf(M, wst[(w * AM_G + q) * (DH + 2)]);
+            float sw[CW];
             float L = 0.f;
 #pragma unroll
-            for (int w = 0; w < AM_WARPS; ++w) {
+            for (int w = 0; w < CW; ++w) {
                 const float mw = wst[(w * AM_G + q) * (DH + 2)];
                 sw[w] = mw == -INFINITY ? 0.f : expf(mw - M);
                 L += wst[(w * AM_G + q) * (DH + 2) + 1] * sw[w];
             }
             float* out = a.part + (((int64_t)(t0 + q) * a.H + h) * AM_MAXC + (c - cf)) * (DH + 2);
-            for (int e = tid; e < DH; e += AM_WARPS * 32) {
+            for (int e = tid; e < DH; e += CW * 32) {
                 float acc = 0.f;
 #pragma unroll
-                for (int w = 0; w < AM_WARPS; ++w) acc += wst[(w * AM_G + q) * (DH + 2) + 2 + e] * sw[w];
+                for (int w = 0; w < CW; ++w) acc += wst[(w * AM_G + q) * (DH + 2) + 2 + e] * sw[w];
                 if (cf == cl) mloc[q] = fmaxf(mloc[q], am_final<DH>(a, t0 + q, h, e, acc, L));
                 else out[2 + e] = acc;
             }
@@ -304,7 +311,7 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
         bool finalize = cf == cl;
         if (!finalize) {
             // ---- last contributor of (g, h) merges the pieces in CTA order
-            cons_bar();  // every thread's partial stores precede the counter (fence by one thread, as in a grid sync)
+            cons_bar_n<CW>();  // every thread's partial stores precede the counter (fence by one thread, as in a grid sync)
             if (tid == 0) {
                 __threadfence();
                 int* ctr = a.counters + (int64_t)t0 * a.H + h;
@@ -313,7 +320,7 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
                 if (last) *ctr = 0;
                 *s_flag = last;
             }
-            cons_bar();
+            cons_bar_n<CW>();
             finalize = *s_flag != 0;
             if (finalize) {
                 __threadfence();
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
                         const float ms = __ldcg(pp + s * (DH + 2));
                         if (ms != -INFINITY) L += __ldcg(pp + s * (DH + 2) + 1) * expf(ms - M);
                     }
-                    for (int e = tid; e < DH; e += AM_WARPS * 32) {
+                    for (int e = tid; e < DH; e += CW * 32) {
                         float acc = 0.f;
                         for (int s = 0; s < np; ++s) {
                             const float ms = __ldcg(pp + s * (DH + 2));
@@ -338,21 +345,22 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_mma(AttnArgs a, in
                 }
             }
         }
-        cons_bar();  // wst free; every warp past the merge
+        cons_bar_n<CW>();  // wst free; every warp past the merge
         if (finalize && a.tokmax) {
             // operand range of the wo GEMV: exact, order-independent max per token
             for (int q = 0; q < nq; ++q) {
                 const float v = warp_max(mloc[q]);
-                if (lane == 0) wst[q * 8 + warp] = v;
+                if (lane == 0) wst[q * CW + warp] = v;
             }
-            cons_bar();
+            cons_bar_n<CW>();
             if (tid < nq) {
                 float v = 0.f;
-                for (int w = 0; w < AM_WARPS; ++w) v = fmaxf(v, wst[tid * 8 + w]);
+                for (int w = 0; w < CW; ++w) v = fmaxf(v, wst[tid * CW + w]);
                 atomicMax(reinterpret_cast<int*>(a.tokmax) + t0 + tid, __float_as_int(v));
             }
-            cons_bar();
+            cons_bar_n<CW>();
         }
+        if (threadIdx.x == 32 && nseg < 2) trace_stamp(a.trace, c, 7 + 3 * nseg);  // segment done
         u += sg.n;
     }
     if (threadIdx.x == 32) trace_stamp(a.trace, c, 3);
@@ -652,7 +660,7 @@ int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st) 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     static const int per_sm = [] {
-        const char* e = getenv("PB_ATTM_CTAS");  // tuning knob: 1 (6-stage ring) or 2 (3 stages, default) CTAs per SM
+        const char* e = getenv("PB_ATTM_CTAS");  // tuning knob: 1 (6 stages, 8 compute warps) or 2 (3 stages, 4 warps)
         return e ? atoi(e) : 2;
     }();
     const int64_t U = a.total_units;
@@ -675,15 +683,14 @@ int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st) 
         }
         return launch_pdl(k_attn_pf<DH>, dim3((unsigned)G), dim3((AM_WARPS + 1) * 32), smem, st, a, (int)G, U);
     }
-    // two CTAs per SM with 3-stage rings (default) or one with 6 stages: the
-    // same K/V bytes in flight per SM; one CTA has a smaller tail but only 4
-    // compute warps per SM and measured slower (176B 442 vs 444 us/block)
-    constexpr size_t smem = attn_mma_smem<DH, 3>();
-    constexpr size_t smem6 = attn_mma_smem<DH, 6>();
+    // two CTAs per SM with 3-stage rings and 4 compute warps each (default), or one
+    // CTA per SM with 6 stages and 8 compute warps (two groups on alternate stages)
+    constexpr size_t smem = attn_mma_smem<DH, 3, 4>();
+    constexpr size_t smem6 = attn_mma_smem<DH, 6, 8>();
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_attn_mma<DH, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_attn_mma<DH, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem6);
+        cudaFuncSetAttribute(k_attn_mma<DH, 3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_attn_mma<DH, 6, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem6);
         configured = true;
     }
     static const int nocomp = [] {
@@ -694,8 +701,8 @@ int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st) 
     aa.debug_nocomp = nocomp;
     aa.trace = trace_region(TR_ATTN, (int)G);
     if (per_sm == 1)
-        return launch_pdl(k_attn_mma<DH, 6>, dim3((unsigned)G), dim3((AM_WARPS + 1) * 32), smem6, st, aa, (int)G, U);
-    return launch_pdl(k_attn_mma<DH, 3>, dim3((unsigned)G), dim3((AM_WARPS + 1) * 32), smem, st, aa, (int)G, U);
+        return launch_pdl(k_attn_mma<DH, 6, 8>, dim3((unsigned)G), dim3(9 * 32), smem6, st, aa, (int)G, U);
+    return launch_pdl(k_attn_mma<DH, 3, 4>, dim3((unsigned)G), dim3(5 * 32), smem, st, aa, (int)G, U);
 }
 
 template int run_attn_mma<64>(const AttnArgs&, int, int64_t, cudaStream_t);

@@ -113,6 +113,14 @@ def main():
             for c in idx:
                 pairs.setdefault(sm[c], []).append(dur[c])
             gaps = [max(v) - min(v) for v in pairs.values() if len(v) == 2]
+            cross = idx[r[idx, 8] > 0]  # CTAs with a second segment
+            if cross.size:
+                rel = lambda col: (r[cross, col] - r[cross, 1]) / 1e3  # noqa: E731
+                n1 = lambda col: np.median(rel(col))  # noqa: E731
+                print(f"attn: {cross.size} CTAs cross a head boundary; median us after release: seg0 start "
+                      f"{n1(5):.1f} data {n1(6):.1f} done {n1(7):.1f} | seg1 start {n1(8):.1f} data {n1(9):.1f} "
+                      f"done {n1(10):.1f} | end {n1(3):.1f}; single-segment CTAs end "
+                      f"{np.median((r[idx[r[idx, 8] == 0], 3] - r[idx[r[idx, 8] == 0], 1]) / 1e3):.1f}")
             print(f"attn: release->end p50 {np.median(dur[idx]):.1f} p90 {np.percentile(dur[idx], 90):.1f} "
                   f"max {dur[idx].max():.1f} us; same-SM pair gap median {np.median(gaps) if gaps else 0:.1f} us; "
                   f"slowest CTAs (index, SM, us): " + ", ".join(f"{c}/{sm[c]}/{dur[c]:.1f}" for c in order[:10]))
