@@ -668,10 +668,13 @@ int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st) 
     // CTAs: fill the machine, but keep every (group, head) within AM_MAXC contributors
     const bool prefill = a.max_group > AM_G;  // prefill groups: queries split across warps (3-stage ring, 2 per SM)
     int64_t G = std::min<int64_t>(U, (int64_t)(prefill ? 2 : per_sm) * sms);
-    // one query group (batch-1 decode): a multiple of the head count, so no CTA's
-    // range crosses a head boundary (traced: such CTAs finish ~10 us after the rest)
+    // decode with equally long query groups (batch-1, or a batch at one context
+    // length): G a multiple of the (group, head) count, so no CTA's range crosses
+    // a head boundary (traced: such CTAs finish ~10 us after the rest)
     static const bool head_aligned = getenv("PB_ATT_NO_ALIGN") == nullptr;
-    if (head_aligned && !prefill && a.n_groups == 1 && G >= a.H && (U / a.H) >= G / a.H) G = G / a.H * a.H;
+    const int64_t pairs = (int64_t)a.n_groups * a.H;
+    if (head_aligned && !prefill && U == pairs * a.max_stages && G >= pairs)
+        G = std::min<int64_t>(G / pairs, a.max_stages) * pairs;
     while (G > 1 && ceil_div(a.max_stages, U / G) + 1 > AM_MAXC) --G;
     if ((int64_t)a.n_tok * a.H * AM_MAXC * (DH + 2) > cap) {
         set_error("attention workspace too small");
