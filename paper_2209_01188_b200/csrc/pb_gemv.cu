@@ -848,9 +848,10 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
     // small matrices: at least min_units k tiles per CTA (a CTA then streams whole
     // 128-row groups instead of splitting every group across many CTAs and paying
     // the split merge); large matrices keep one CTA per resident slot
+    // (sweep, profiles/r1_gemv_timeline_and_tail.txt: 32 for <= 2 tokens, 64 for 8)
     static const int64_t min_units = [] {
         const char* e = getenv("PB_GEMV_MINU");  // tuning knob
-        return (int64_t)(e ? atoi(e) : 16);
+        return (int64_t)(e ? atoi(e) : (TC >= 8 ? 64 : 32));
     }();
     G = std::min<int64_t>(G, std::max<int64_t>(1, a.total / std::max<int64_t>(min_units, 1)));
     const int64_t per_tile = 128 * 8 * NT;
