@@ -909,6 +909,11 @@ int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, i
         const char* e = getenv("PB_GEMV_CFG8");  // tuning knob of the 3..8-token kernel: 0 = 4x4, 1 = 8x4, 2 = 8x2 (default)
         cfg8 = e ? atoi(e) : 2;
     }
+    static int cfg32 = -1;
+    if (cfg32 < 0) {
+        const char* e = getenv("PB_GEMV_CFG32");  // tuning knob of the 17..32-token kernel: 0 = 2x4, 1 = 4x4, 2 = 8x2
+        cfg32 = e ? atoi(e) : 0;
+    }
     switch (act.tc) {
         case 2:
             switch (cfg) {
@@ -927,7 +932,12 @@ int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, i
                 default: return sk_launch<8, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
             }
         case 16: return sk_launch<16, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
-        case 32: return sk_launch<32, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
+        case 32:
+            switch (cfg32) {
+                case 1: return sk_launch<32, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
+                case 2: return sk_launch<32, 8, 2>(m, act, epi, partials, counters, partial_cap, st);
+                default: return sk_launch<32, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
+            }
         default: set_error("bad column tile"); return PB_ERR_GENERIC;
     }
 }
