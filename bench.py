@@ -213,7 +213,7 @@ class Pipeline:
         self.chunk = max(1, args.prefill_chunk // self.B)  # prefill positions per sequence per step
         self.ranges = split_blocks(cfg.n_layers, self.world)
         s, e = self.ranges[self.rank]
-        pages_per_seq = -(-cfg.max_seq // 64)
+        pages_per_seq = -(-min(cfg.max_seq, args.ctx + 64) // 64)  # KV pool sized for the benchmarked context
         t0 = time.perf_counter()
         self.span = BlockSpan(cfg, s, e, int8=True, page_tokens=64, n_pages=self.S * self.B * pages_per_seq + 2,
                               max_tokens=max(self.chunk * self.B, 512), max_seqs=max(self.B, 2), device=self.local)
