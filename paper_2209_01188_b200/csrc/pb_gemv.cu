@@ -473,7 +473,7 @@ __device__ __forceinline__ void sk_epilogue(const SkArgs& a, int (&acc)[2][digit
 // tiles straight into shared memory: the same digits as frag_item, bit for
 // bit. Lane l owns features 4l..4l+3 of each 128-feature slice; one float4 of
 // x (+ gamma, beta) and scales per slice.
-constexpr int SK_OPW = 4;  // operand warps of the fused GEMV: warp w fills the stages s = w (mod 4)
+constexpr int SK_OPW = 4;  // operand warps of the fused GEMV: warp w fills the stages s = w (mod SK_OPW)
 
 template <int TC, int SK_KCS, int SK_STAGES>
 __device__ __forceinline__ void sk_operand_warp(const SkArgs& a, int64_t u0, int64_t u1, int chunk, uint8_t* sb,
