@@ -73,6 +73,25 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
+// arrive on the same-offset mbarrier of every CTA in the (2-CTA) cluster
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+// global -> shared of both CTAs of the pair (same offset), complete_tx on each CTA's mbarrier at bar's offset
+__device__ __forceinline__ void bulk_g2s_pair(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
+        "%4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"((uint16_t)3)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
@@ -93,11 +112,19 @@ struct TcArgs {
     const uint8_t* bcanon;  // [token tiles][KC][3][TC_PLANE]
     int KC, MG, NTL;        // k tiles, row groups, token tiles
     int tiles;              // MG * NTL
+    int l2pf;               // L2 prefetch distance in k tiles (0: off)
     Act act;
     Epi epi;
 };
 
-__global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
+// PAIR: CTAs 2p and 2p + 1 form a cluster on row groups 2 mg' and 2 mg' + 1
+// of the same token tile; each loads its own weight k tiles and HALF of the
+// shared digit planes, multicast into both CTAs' shared memory, so a CTA pulls
+// 4 + 3.75 KB per k tile through L2 instead of 4 + 7.5 KB. A stage is free
+// again once both CTAs' MMAs have read it (empty barrier count 2, commits
+// multicast to the pair).
+template <bool PAIR>
+__device__ __forceinline__ void gemm_tc_body(const TcArgs& a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sa = smem;                                // [STAGES][KT][4 KB]
     uint8_t* sb = sa + TC_STAGES * TC_KT * TC_A;       // [STAGES][KT][3 planes]
@@ -109,12 +136,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
 
     const int warp = warp_uniform_id(), lane = threadIdx.x & 31;
     const int KC = a.KC;
-    const int G = gridDim.x;
+    // tile schedule: unit u = cta, cta + NU, ...; PAIR units are (row-group pair, token tile)
+    const int rank = PAIR ? (int)(blockIdx.x & 1) : 0;
+    const int cta = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int NU = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    const int units = PAIR ? a.tiles / 2 : a.tiles;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < TC_STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);  // MMA commit
+            mbar_init(&empty[s], PAIR ? 2 : 1);  // MMA commit (both CTAs' when PAIR)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&accfull[b], 1);   // MMA commit after a tile's last k step
@@ -128,7 +159,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
-    __syncthreads();
+    if (PAIR)
+        cluster_sync();  // the peer's barriers are initialised before any multicast reaches them
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -136,17 +170,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
         // ---------------- TMA producer
         if (lane == 0) {
             int it = 0;
-            for (int t = blockIdx.x; t < a.tiles; t += G) {
-                const int mg = t / a.NTL, nt = t % a.NTL;
+            for (int u = cta; u < units; u += NU) {
+                const int mg = PAIR ? 2 * (u / a.NTL) + rank : u / a.NTL, nt = u % a.NTL;
                 const int8_t* asrc = a.codes + (int64_t)mg * KC * TC_A;
                 const uint8_t* bsrc = a.bcanon + (int64_t)nt * KC * TC_B;
                 for (int kc = 0; kc < KC; kc += TC_KT, ++it) {
                     const int s = it % TC_STAGES, n = min(TC_KT, KC - kc);
+                    if (a.l2pf) {
+                        // pull k tiles l2pf ahead of the ring into L2: the ring (4 stages, ~1 us of MMA) is
+                        // shorter than an HBM miss under load
+                        const int kp = kc + a.l2pf;
+                        if (kp < KC) {
+                            const int np = min(TC_KT, KC - kp);
+                            bulk_prefetch_l2(asrc + (int64_t)kp * TC_A, np * TC_A);
+                            if (PAIR)
+                                bulk_prefetch_l2(bsrc + (int64_t)kp * TC_B + rank * np * (TC_B / 2), np * (TC_B / 2));
+                            else
+                                bulk_prefetch_l2(bsrc + (int64_t)kp * TC_B, np * TC_B);
+                        }
+                    }
                     mbar_wait(&empty[s], ((it / TC_STAGES) & 1) ^ 1);
                     mbar_expect_tx(&full[s], n * (TC_A + TC_B));
                     // consecutive k tiles are contiguous in both operands: one copy each
                     bulk_g2s(sa + s * TC_KT * TC_A, asrc + (int64_t)kc * TC_A, n * TC_A, &full[s]);
-                    bulk_g2s(sb + s * TC_KT * TC_B, bsrc + (int64_t)kc * TC_B, n * TC_B, &full[s]);
+                    if (PAIR) {
+                        const uint32_t half = n * (TC_B / 2);  // n * 3840 B: 16-B multiple
+                        bulk_g2s_pair(sb + s * TC_KT * TC_B + rank * half, bsrc + (int64_t)kc * TC_B + rank * half,
+                                      half, &full[s]);
+                    } else {
+                        bulk_g2s(sb + s * TC_KT * TC_B, bsrc + (int64_t)kc * TC_B, n * TC_B, &full[s]);
+                    }
                 }
             }
         }
@@ -154,7 +207,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
         // ---------------- MMA issuer: tile i accumulates in set i & 1 (digit p at column 80 p)
         if (lane == 0) {
             int it = 0, i = 0;
-            for (int t = blockIdx.x; t < a.tiles; t += G, ++i) {
+            for (int u = cta; u < units; u += NU, ++i) {
                 const int b = i & 1;
                 mbar_wait(&accempty[b], ((i >> 1) & 1) ^ 1);
                 tc_fence_after();
@@ -166,7 +219,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
                     const uint32_t a0 = smem_u32(sa + s * TC_KT * TC_A), b0 = smem_u32(sb + s * TC_KT * TC_B);
                     for (int k = 0; k < n; ++k)
                         tc_mma(acc, umma_desc(a0 + k * TC_A), umma_desc(b0 + k * TC_B), (kc | k) != 0);
-                    tc_commit(&empty[s]);
+                    if (PAIR)
+                        tc_commit_pair(&empty[s]);
+                    else
+                        tc_commit(&empty[s]);
                 }
                 tc_commit(&accfull[b]);
             }
@@ -178,8 +234,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
         const int row = quarter * 32 + lane;
         const bool want_max = a.epi.tokmax != nullptr;
         int i = 0;
-        for (int t = blockIdx.x; t < a.tiles; t += G, ++i) {
-            const int mg = t / a.NTL, nt = t % a.NTL;
+        for (int u = cta; u < units; u += NU, ++i) {
+            const int mg = PAIR ? 2 * (u / a.NTL) + rank : u / a.NTL, nt = u % a.NTL;
             const int b = i & 1;
             mbar_wait(&accfull[b], (i >> 1) & 1);
             tc_fence_after();
@@ -212,23 +268,59 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if (PAIR)
+        cluster_sync();  // no multicast copy or commit may still target an exited peer
+    else
+        __syncthreads();
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS));
     }
 }
 
+__global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) { gemm_tc_body<false>(a); }
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) k_gemm_tc_pair(TcArgs a) {
+    gemm_tc_body<true>(a);
+}
+
 int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Epi& epi, cudaStream_t st) {
-    static int sms = 0;
+    static int sms = 0, pair_clusters = 0;
     if (!sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM);
+        cudaFuncSetAttribute(k_gemm_tc_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM);
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3((unsigned)sms);
+        cfg.blockDim = dim3(TC_THREADS);
+        cfg.dynamicSmemBytes = TC_SMEM;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&pair_clusters, (void*)k_gemm_tc_pair, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            pair_clusters = 0;
+        }
     }
-    TcArgs a{m.codes, bcanon, m.Kp / 32, m.Mp / 128, (int)ceil_div(act.n_tok, TC_BN), 0, act, epi};
+    TcArgs a{m.codes, bcanon, m.Kp / 32, m.Mp / 128, (int)ceil_div(act.n_tok, TC_BN), 0, 0, act, epi};
     a.tiles = a.MG * a.NTL;
+    if (const char* pf = getenv("PB_TC_L2PF")) a.l2pf = std::max(0, atoi(pf));  // tuning knob (k tiles ahead)
+    // A/B knob (read per launch): 1 = 2-CTA clusters with multicast digit planes. Measured equal to the
+    // one-CTA kernel (176B prefill 1224 vs 1224 ms, profiles/r1_tcgen05_pair_l2pf.txt): L2 -> SM bytes are
+    // not what bounds this GEMM, so the default stays the simpler kernel.
+    const char* e = getenv("PB_TC_PAIR");
+    const bool pair_on = e && atoi(e) == 1;
+    if (pair_on && pair_clusters > 0 && a.MG % 2 == 0) {
+        // persistent: one 2-CTA cluster per SM pair, as many as can be co-resident
+        const int grid = 2 * std::min(a.tiles / 2, pair_clusters);
+        k_gemm_tc_pair<<<grid, TC_THREADS, TC_SMEM, st>>>(a);
+        return launch_check("gemm_tc_pair");
+    }
     const int grid = std::min(a.tiles, sms);  // persistent: one CTA per SM (TMEM 512 columns)
     k_gemm_tc<<<grid, TC_THREADS, TC_SMEM, st>>>(a);
     return launch_check("gemm_tc");

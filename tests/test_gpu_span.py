@@ -300,6 +300,35 @@ def test_tcgen05_prefill_matches_gemv_path(shape_name, t, monkeypatch):
         assert err <= TOL, (shape_name, i, err)  # fp16 KV rounding can flip on 1-ulp f32 differences
 
 
+@pytest.mark.parametrize("shape_name,t", [("mid", 200), ("bloom-7b1", 300)])
+def test_tcgen05_pair_multicast_bit_identical(shape_name, t, monkeypatch):
+    """The 2-CTA cluster tcgen05 GEMM (digit planes multicast to both CTAs of
+    a row-group pair, PB_TC_PAIR=1) computes the same integers as the default
+    one-CTA-per-tile kernel: prefill + one decode step are bit-identical."""
+    import torch
+
+    from paper_2209_01188_b200.model import SHAPES as S
+    from paper_2209_01188_b200.span import BlockSpan
+
+    cfg, end = (cfg_of(SHAPES["mid"]), SHAPES["mid"].n_layers) if shape_name == "mid" else (S[shape_name], 2)
+    monkeypatch.setenv("PB_TC_MIN", "64")
+    outs = {}
+    for pair in ("0", "1"):
+        monkeypatch.setenv("PB_TC_PAIR", pair)
+        span = BlockSpan(cfg, 0, end, int8=True, page_tokens=64, max_tokens=max(t, 64), n_pages=16)
+        span.generate_weights(42)
+        rng = np.random.default_rng(3)
+        x = torch.from_numpy(rng.normal(size=(t + 1, cfg.hidden)).astype(np.float32) * 0.05).cuda()
+        seq = span.new_sequence()
+        a = span.step([(seq, x[:t])])[0].cpu().numpy()
+        b = span.step([(seq, x[t:])])[0].cpu().numpy()
+        outs[pair] = (a, b)
+        span.close()
+        torch.cuda.empty_cache()
+    for i in range(2):
+        assert np.array_equal(outs["0"][i].view(np.uint32), outs["1"][i].view(np.uint32)), (shape_name, i)
+
+
 def test_bloom176b_tcgen05_prefill_vs_f64_reference():
     """One 176B-shape block (h=14336, H=112): a 160-token prefill through the
     tcgen05 kind::i8 GEMM (two 80-token tiles) and the prefill attention
