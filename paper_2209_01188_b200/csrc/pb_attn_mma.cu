@@ -673,8 +673,27 @@ int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st) 
     // a head boundary (traced: such CTAs finish ~10 us after the rest)
     static const bool head_aligned = getenv("PB_ATT_NO_ALIGN") == nullptr;
     const int64_t pairs = (int64_t)a.n_groups * a.H;
-    if (head_aligned && !prefill && U == pairs * a.max_stages && G >= pairs)
-        G = std::min<int64_t>(G / pairs, a.max_stages) * pairs;
+    static const int parts_knob = [] {
+        const char* e = getenv("PB_ATT_PARTS");  // tuning knob: CTAs per (group, head); -1 = wave-balanced choice
+        return e ? atoi(e) : 0;
+    }();
+    if (head_aligned && !prefill && U == pairs * a.max_stages && G >= pairs) {
+        const int64_t slots = G;  // co-resident CTAs
+        int64_t k = std::min<int64_t>(slots / pairs, a.max_stages);
+        if (parts_knob > 0) {
+            k = std::min<int64_t>(parts_knob, a.max_stages);
+        } else if (parts_knob < 0) {
+            // more CTAs than slots run in waves: pick k minimising waves(k) / k, the per-CTA share of a
+            // head on the busiest SM (176B: k = 5 -> 560 CTAs in 2 waves of 296, 0.4 of a head vs 0.5 at k = 2)
+            double best = 1e30;
+            for (int64_t c = 1; c <= std::min<int64_t>(a.max_stages, 12); ++c) {
+                if (ceil_div(a.max_stages, a.max_stages / c) + 1 > AM_MAXC) break;
+                const double cost = (double)ceil_div(c * pairs, slots) / (double)c;
+                if (cost < best - 1e-9) best = cost, k = c;
+            }
+        }
+        G = k * pairs;
+    }
     while (G > 1 && ceil_div(a.max_stages, U / G) + 1 > AM_MAXC) --G;
     if ((int64_t)a.n_tok * a.H * AM_MAXC * (DH + 2) > cap) {
         set_error("attention workspace too small");
