@@ -113,6 +113,7 @@ struct TcArgs {
     int KC, MG, NTL;        // k tiles, row groups, token tiles
     int tiles;              // MG * NTL
     int l2pf;               // L2 prefetch distance in k tiles (0: off)
+    int ntg;                // token tiles per pass (NTL: one pass)
     Act act;
     Epi epi;
 };
@@ -123,6 +124,19 @@ struct TcArgs {
 // 4 + 3.75 KB per k tile through L2 instead of 4 + 7.5 KB. A stage is free
 // again once both CTAs' MMAs have read it (empty barrier count 2, commits
 // multicast to the pair).
+// Unit u -> (row group, token tile). Units run in passes over ntg token tiles:
+// within a pass the token tiles of one row group are neighbours (they share
+// the weight k tiles in L2), and the pass's digit planes (ntg x KC x 7.5 KB)
+// stay L2-resident across the row groups instead of every wave of CTAs
+// re-streaming all NTL token tiles' planes from HBM.
+__device__ __forceinline__ void tc_unit(const TcArgs& a, int u, int mgs, int& mgu, int& nt) {
+    const int per = mgs * a.ntg;
+    const int g = u / per, r = u - g * per;
+    const int n_here = min(a.ntg, a.NTL - g * a.ntg);
+    mgu = r / n_here;
+    nt = g * a.ntg + (r - mgu * n_here);
+}
+
 template <bool PAIR>
 __device__ __forceinline__ void gemm_tc_body(const TcArgs& a) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -141,6 +155,7 @@ __device__ __forceinline__ void gemm_tc_body(const TcArgs& a) {
     const int cta = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
     const int NU = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     const int units = PAIR ? a.tiles / 2 : a.tiles;
+    const int mgs = PAIR ? a.MG / 2 : a.MG;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < TC_STAGES; ++s) {
@@ -171,7 +186,9 @@ __device__ __forceinline__ void gemm_tc_body(const TcArgs& a) {
         if (lane == 0) {
             int it = 0;
             for (int u = cta; u < units; u += NU) {
-                const int mg = PAIR ? 2 * (u / a.NTL) + rank : u / a.NTL, nt = u % a.NTL;
+                int mgu, nt;
+                tc_unit(a, u, mgs, mgu, nt);
+                const int mg = PAIR ? 2 * mgu + rank : mgu;
                 const int8_t* asrc = a.codes + (int64_t)mg * KC * TC_A;
                 const uint8_t* bsrc = a.bcanon + (int64_t)nt * KC * TC_B;
                 for (int kc = 0; kc < KC; kc += TC_KT, ++it) {
@@ -235,7 +252,9 @@ __device__ __forceinline__ void gemm_tc_body(const TcArgs& a) {
         const bool want_max = a.epi.tokmax != nullptr;
         int i = 0;
         for (int u = cta; u < units; u += NU, ++i) {
-            const int mg = PAIR ? 2 * (u / a.NTL) + rank : u / a.NTL, nt = u % a.NTL;
+            int mgu, nt;
+            tc_unit(a, u, mgs, mgu, nt);
+            const int mg = PAIR ? 2 * mgu + rank : mgu;
             const int b = i & 1;
             mbar_wait(&accfull[b], (i >> 1) & 1);
             tc_fence_after();
@@ -307,8 +326,20 @@ int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Ep
             pair_clusters = 0;
         }
     }
-    TcArgs a{m.codes, bcanon, m.Kp / 32, m.Mp / 128, (int)ceil_div(act.n_tok, TC_BN), 0, 0, act, epi};
+    TcArgs a{m.codes, bcanon, m.Kp / 32, m.Mp / 128, (int)ceil_div(act.n_tok, TC_BN), 0, 0, 0, act, epi};
     a.tiles = a.MG * a.NTL;
+    // passes of ntg token tiles whose digit planes fit a 32 MB L2 budget (176B, 2048 tokens: 9 of 26
+    // tiles per pass at K = 14336; 743 -> 789-800 useful TFLOP/s, profiles/r1_tcgen05_ntg_sweep.txt)
+    int budget_mb = 32;
+    if (const char* g = getenv("PB_TC_NTG")) {  // tuning knob: N > 0 token tiles per pass, -MB plane budget, 0 one pass
+        const int v = atoi(g);
+        budget_mb = v < 0 ? -v : 0;
+        a.ntg = v > 0 ? std::min(a.NTL, v) : a.NTL;
+    }
+    if (budget_mb > 0)
+        a.ntg = (int)std::max<int64_t>(1, std::min<int64_t>(a.NTL, ((int64_t)budget_mb << 20) / ((int64_t)a.KC * TC_B)));
+    else if (a.ntg <= 0)
+        a.ntg = a.NTL;
     if (const char* pf = getenv("PB_TC_L2PF")) a.l2pf = std::max(0, atoi(pf));  // tuning knob (k tiles ahead)
     // A/B knob (read per launch): 1 = 2-CTA clusters with multicast digit planes. Measured equal to the
     // one-CTA kernel (176B prefill 1224 vs 1224 ms, profiles/r1_tcgen05_pair_l2pf.txt): L2 -> SM bytes are
