@@ -30,6 +30,7 @@
 // Canonical K-major (SWIZZLE_NONE) operand layout: 8-row x 16-byte core
 // matrices, LBO = 128 B (k direction), SBO = 256 B (8-row groups).
 #include <algorithm>
+#include <cstdint>
 
 #include "pb_async.cuh"
 #include "pb_common.cuh"
@@ -328,22 +329,28 @@ int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Ep
     }
     TcArgs a{m.codes, bcanon, m.Kp / 32, m.Mp / 128, (int)ceil_div(act.n_tok, TC_BN), 0, 0, 0, act, epi};
     a.tiles = a.MG * a.NTL;
-    // passes of ntg token tiles whose digit planes fit a 32 MB L2 budget (176B, 2048 tokens: 9 of 26
-    // tiles per pass at K = 14336; 743 -> 789-800 useful TFLOP/s, profiles/r1_tcgen05_ntg_sweep.txt)
-    int budget_mb = 32;
-    if (const char* g = getenv("PB_TC_NTG")) {  // tuning knob: N > 0 token tiles per pass, -MB plane budget, 0 one pass
-        const int v = atoi(g);
-        budget_mb = v < 0 ? -v : 0;
-        a.ntg = v > 0 ? std::min(a.NTL, v) : a.NTL;
-    }
-    if (budget_mb > 0)
-        a.ntg = (int)std::max<int64_t>(1, std::min<int64_t>(a.NTL, ((int64_t)budget_mb << 20) / ((int64_t)a.KC * TC_B)));
-    else if (a.ntg <= 0)
+    // Token-tile passes chosen by an HBM-traffic model: a pass of ntg tiles reads every weight byte once
+    // (its row group's token tiles run on neighbouring CTAs) and its digit planes once if they fit an L2
+    // budget (64 MB), otherwise once per wave of CTAs. 176B, 2048 tokens, K = 14336: 3 passes of 9
+    // tiles, DRAM 14.3 -> 3.4 GB per mlp_in launch, 4.83 -> 4.10 ms (profiles/r1_tcgen05_ntg_sweep.txt).
+    {
+        const char* g = getenv("PB_TC_NTG");  // tuning knob: N > 0 token tiles per pass, 0 one pass
+        const int v = g ? atoi(g) : -1;
         a.ntg = a.NTL;
-    if (const char* pf = getenv("PB_TC_L2PF")) a.l2pf = std::max(0, atoi(pf));  // tuning knob (k tiles ahead)
-    // A/B knob (read per launch): 1 = 2-CTA clusters with multicast digit planes. Measured equal to the
-    // one-CTA kernel (176B prefill 1224 vs 1224 ms, profiles/r1_tcgen05_pair_l2pf.txt): L2 -> SM bytes are
-    // not what bounds this GEMM, so the default stays the simpler kernel.
+        if (v > 0) {
+            a.ntg = std::min(a.NTL, v);
+        } else if (v < 0) {
+            const int64_t a_all = (int64_t)a.MG * a.KC * TC_A, plane = (int64_t)a.KC * TC_B;
+            const int64_t budget = 64ll << 20, slots = sms;
+            int64_t best = INT64_MAX;
+            for (int n = a.NTL; n >= 1; --n) {
+                const int64_t passes = ceil_div(a.NTL, n), bp = n * plane;
+                const int64_t waves = ceil_div((int64_t)a.MG * n, slots);
+                const int64_t cost = passes * a_all + (bp <= budget ? (int64_t)a.NTL * plane : passes * waves * bp);
+                if (cost < best) best = cost, a.ntg = n;
+            }
+        }
+    }
     const char* e = getenv("PB_TC_PAIR");
     const bool pair_on = e && atoi(e) == 1;
     if (pair_on && pair_clusters > 0 && a.MG % 2 == 0) {
