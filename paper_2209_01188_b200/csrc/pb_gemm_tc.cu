@@ -9,11 +9,12 @@
 // (canonical K-major int8, pb_weights.cu) and the digit planes (k_canonwrite)
 // are UMMA operands as they land in shared memory: no conversion pass.
 //
-// Persistent grid, one CTA per SM (TMEM 512 columns). Tile t = (row group
-// t / NTL, token tile t % NTL); CTA c takes tiles c, c + G, c + 2G, ... so the
-// NTL token tiles of one row group run on neighbouring CTAs at the same time
-// and share each weight k tile through L2: HBM streams every weight byte once
-// per launch however many token tiles there are. Two TMEM accumulator sets (3
+// Persistent grid, one CTA per SM (TMEM 512 columns). Tiles run in passes of
+// ntg token tiles (tc_unit); within a pass tile = (row group, token tile) with
+// the token tiles of one row group on neighbouring CTAs (CTA c takes tiles c,
+// c + G, ...), so they share each weight k tile through L2, and the pass's
+// digit planes stay L2-resident across row groups. ntg comes from an HBM
+// traffic model in launch_gemm_tc (one pass for <= 13 token tiles). Two TMEM accumulator sets (3
 // digits x 80 columns each) let the epilogue of tile i run while the tensor
 // core accumulates tile i + 1.
 //
