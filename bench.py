@@ -51,7 +51,8 @@ def parse():
     p.add_argument("--shape", default="bloom-176b")
     p.add_argument("--ctx", type=int, default=2048)
     p.add_argument("--seed", type=int, default=42)
-    p.add_argument("--prefill-chunk", type=int, default=256)
+    # a multiple of the tcgen05 GEMM's 80-token tile (256 padded 4 tiles to 320 tokens)
+    p.add_argument("--prefill-chunk", type=int, default=240)
     p.add_argument("--batch", type=int, default=1, help="batch-1 sessions per pipeline micro-batch")
     p.add_argument("--hop", default="p2p", choices=["p2p", "nccl"],
                    help="span-to-span hop: NVLink peer-memory mailboxes (pb_hop.cu) or NCCL send/recv")
