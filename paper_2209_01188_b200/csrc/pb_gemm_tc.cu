@@ -272,7 +272,8 @@ __device__ __forceinline__ void gemm_tc_body(const TcArgs& a) {
                     const int tok = nt * TC_BN + c0 + j;
                     float mx = 0.f;
                     if (tok < a.act.n_tok && o < a.epi.M) {
-                        const double iv = 65536.0 * (double)h[j] + 256.0 * (double)m[j] + (double)l[j];
+                        // exact integer (|iv| < 2^47), one rounding to f32: same value as the f64 sum
+                        const long long iv = ((long long)h[j] << 16) + ((long long)m[j] << 8) + (long long)l[j];
                         const float y = epi_store(a.epi, tok, o, (float)iv * a.act.back[tok]);
                         if (want_max) mx = fabsf(y * a.epi.s_next[o]);
                     }
