@@ -164,9 +164,21 @@ def encode_tensor(t, encoding: int = ENC_F32, block_size: int = 64) -> bytes:
     return head + struct.pack(">I", block_size) + buf[:4 * nb + n].numpy().tobytes()
 
 
-def parse_tensor(data: bytes):
+def _buf(data):
+    """(memoryview, pinned torch uint8 tensor | None) of bytes / memoryview / rpc.Payload."""
+    if hasattr(data, "pinned") and hasattr(data, "view"):
+        return data.view, data.pinned
+    return memoryview(data), None
+
+
+def parse_tensor(data):
     """Split TensorMsg bytes into (encoding, dims, block_size, scales np, codes np | f32 np)
-    without decoding (transport/wire.py:109-138 validation)."""
+    without decoding (transport/wire.py:109-138 validation). `data` may be
+    bytes, a memoryview or an rpc.Payload (zero-copy numpy views)."""
+    return _parse(_buf(data)[0])[:5]
+
+
+def _parse(data):
     if len(data) < 2:
         raise ProtocolError("truncated tensor header")
     encoding, ndim = struct.unpack(">BB", data[:2])
@@ -179,7 +191,7 @@ def parse_tensor(data: bytes):
     if encoding == ENC_F32:
         if len(data) != off + 4 * n:
             raise ProtocolError("f32 tensor size mismatch")
-        return encoding, dims, 0, None, np.frombuffer(data, "<f4", count=n, offset=off)
+        return encoding, dims, 0, None, np.frombuffer(data, "<f4", count=n, offset=off), (off, None)
     if encoding == ENC_INT8:
         if len(data) < off + 4:
             raise ProtocolError("truncated int8 tensor")
@@ -192,11 +204,11 @@ def parse_tensor(data: bytes):
             raise ProtocolError("int8 tensor size mismatch")
         scales = np.frombuffer(data, "<f4", count=nb, offset=off)
         codes = np.frombuffer(data, np.int8, count=n, offset=off + 4 * nb)
-        return encoding, dims, block_size, scales, codes
+        return encoding, dims, block_size, scales, codes, (off + 4 * nb, off)
     raise ProtocolError(f"unknown tensor encoding {encoding}")
 
 
-def payload_finite(data: bytes) -> bool:
+def payload_finite(data) -> bool:
     """True iff the TensorMsg's values are finite (f32 values, or int8 scales:
     int8 codes times finite scales are finite)."""
     enc, _, _, scales, payload = parse_tensor(data)
@@ -204,14 +216,29 @@ def payload_finite(data: bytes) -> bool:
     return bool(np.isfinite(vals).all()) if vals.size else True
 
 
-def decode_tensor(data: bytes, device=None):
+def _h2d(arr, pinned, off, nbytes, dtype, dev):
+    """Host -> device copy of one TensorMsg section: straight from the
+    page-locked receive buffer when there is one (asynchronous DMA, ordered on
+    the current stream before any kernel that reads it), else via a copy of
+    the pageable bytes."""
+    import torch
+
+    if pinned is not None and nbytes:
+        dst = torch.empty(nbytes, dtype=torch.uint8, device=dev)  # aligned: sections start at any byte offset
+        dst.copy_(pinned[off:off + nbytes], non_blocking=True)
+        return dst.view(dtype)
+    return torch.from_numpy(arr.copy()).to(dev)
+
+
+def decode_tensor(data, device=None):
     """TensorMsg -> CUDA f32 tensor (int8 decoded on the GPU)."""
     import torch
 
     dev = device or _dev()
-    enc, dims, bs, scales, payload = parse_tensor(data)
+    view, pinned = _buf(data)
+    enc, dims, bs, scales, payload, (poff, soff) = _parse(view)
     if enc == ENC_F32:
-        return torch.from_numpy(payload.copy()).to(dev).reshape(dims)
-    q = QuantizedBlockwise(bs, torch.from_numpy(scales.copy()).to(dev), torch.from_numpy(payload.copy()).to(dev),
-                           tuple(dims))
+        return _h2d(payload, pinned, poff, 4 * payload.size, torch.float32, dev).reshape(dims)
+    q = QuantizedBlockwise(bs, _h2d(scales, pinned, soff, 4 * scales.size, torch.float32, dev),
+                           _h2d(payload, pinned, poff, payload.size, torch.int8, dev), tuple(dims))
     return dequantize_blockwise(q)

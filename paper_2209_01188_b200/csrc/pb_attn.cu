@@ -324,14 +324,9 @@ template <int DH>
 static int run_attn(const AttnArgs& a, int64_t cap, cudaStream_t st) {
     // split the key range only as far as needed to cover the machine (~2 CTAs
     // per SM); each split streams >= 4 stages
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    static int ctas_per_sm = 0;
-    if (!ctas_per_sm) {
-        const char* e = getenv("PB_ATT_CTAS_PER_SM");  // tuning knob
-        ctas_per_sm = e ? atoi(e) : 2;
-    }
+    const int sms = sm_count();
+    if (sms < 0) return PB_ERR_GENERIC;
+    constexpr int ctas_per_sm = 2;
     int nsplit = (int)ceil_div((int64_t)ctas_per_sm * sms, (int64_t)a.n_tok * a.H);
     nsplit = std::max(1, std::min<int>(nsplit, std::min<int>(ATT_MAX_SPLIT, (int)ceil_div(a.max_pos, 4 * ATT_SK))));
     const int kps = (int)round_up(ceil_div(a.max_pos, nsplit), ATT_SK);
@@ -341,11 +336,12 @@ static int run_attn(const AttnArgs& a, int64_t cap, cudaStream_t st) {
         return PB_ERR_CAPACITY;
     }
     constexpr size_t smem = attn_smem<DH>();
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_attn<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    static int ok[PB_MAX_DEVICES] = {};
+    if (per_device(ok, [](int) {
+            return cudaFuncSetAttribute(k_attn<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+                           cudaSuccess ? 1 : -1;
+        }) < 0)
+        return launch_check("attn setup");
     return launch_pdl(k_attn<DH>, dim3(a.H, a.n_tok, nsplit), dim3((ATT_WARPS + 1) * 32), smem, st, a, nsplit, kps);
 }
 

@@ -174,11 +174,6 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_attn_mma(AttnArgs a, int G, i
             mbar_wait(&full[b], (it / ST) & 1);
             if (threadIdx.x == 32 && nseg < 2 && i == sg.i0) trace_stamp(a.trace, c, 6 + 3 * nseg);  // first data
             const int kb = (warp & (GW - 1)) * 16;  // this warp's 16 keys of the stage
-            if (a.debug_nocomp) {  // experiment: memory pipeline only
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[b]);
-                continue;
-            }
             if (k0 + kb + 16 > j1) {
                 // partial last stage: rows past the range hold stale smem; P is 0
                 // there but 0 * NaN would poison O, so clear this warp's V rows
@@ -656,44 +651,19 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_pf(AttnArgs a, int
 
 template <int DH>
 int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    static const int per_sm = [] {
-        const char* e = getenv("PB_ATTM_CTAS");  // tuning knob: 1 (6 stages, 8 compute warps) or 2 (3 stages, 4 warps)
-        return e ? atoi(e) : 2;
-    }();
+    const int sms = sm_count();
+    if (sms < 0) return PB_ERR_GENERIC;
     const int64_t U = a.total_units;
     if (U <= 0) return PB_OK;
-    // CTAs: fill the machine, but keep every (group, head) within AM_MAXC contributors
-    const bool prefill = a.max_group > AM_G;  // prefill groups: queries split across warps (3-stage ring, 2 per SM)
-    int64_t G = std::min<int64_t>(U, (int64_t)(prefill ? 2 : per_sm) * sms);
+    // CTAs: fill the machine (two per SM), but keep every (group, head) within AM_MAXC contributors
+    const bool prefill = a.max_group > AM_G;  // prefill groups: queries split across warps
+    int64_t G = std::min<int64_t>(U, 2 * (int64_t)sms);
     // decode with equally long query groups (batch-1, or a batch at one context
     // length): G a multiple of the (group, head) count, so no CTA's range crosses
     // a head boundary (traced: such CTAs finish ~10 us after the rest)
-    static const bool head_aligned = getenv("PB_ATT_NO_ALIGN") == nullptr;
     const int64_t pairs = (int64_t)a.n_groups * a.H;
-    static const int parts_knob = [] {
-        const char* e = getenv("PB_ATT_PARTS");  // tuning knob: CTAs per (group, head); -1 = wave-balanced choice
-        return e ? atoi(e) : 0;
-    }();
-    if (head_aligned && !prefill && U == pairs * a.max_stages && G >= pairs) {
-        const int64_t slots = G;  // co-resident CTAs
-        int64_t k = std::min<int64_t>(slots / pairs, a.max_stages);
-        if (parts_knob > 0) {
-            k = std::min<int64_t>(parts_knob, a.max_stages);
-        } else if (parts_knob < 0) {
-            // more CTAs than slots run in waves: pick k minimising waves(k) / k, the per-CTA share of a
-            // head on the busiest SM (176B: k = 5 -> 560 CTAs in 2 waves of 296, 0.4 of a head vs 0.5 at k = 2)
-            double best = 1e30;
-            for (int64_t c = 1; c <= std::min<int64_t>(a.max_stages, 12); ++c) {
-                if (ceil_div(a.max_stages, a.max_stages / c) + 1 > AM_MAXC) break;
-                const double cost = (double)ceil_div(c * pairs, slots) / (double)c;
-                if (cost < best - 1e-9) best = cost, k = c;
-            }
-        }
-        G = k * pairs;
-    }
+    if (!prefill && U == pairs * a.max_stages && G >= pairs)
+        G = std::min<int64_t>(G / pairs, a.max_stages) * pairs;
     while (G > 1 && ceil_div(a.max_stages, U / G) + 1 > AM_MAXC) --G;
     if ((int64_t)a.n_tok * a.H * AM_MAXC * (DH + 2) > cap) {
         set_error("attention workspace too small");
@@ -702,32 +672,24 @@ int run_attn_mma(const AttnArgs& a, int n_groups, int64_t cap, cudaStream_t st) 
     (void)n_groups;
     if (prefill) {
         constexpr size_t smem = attn_pf_smem<DH>();
-        static bool configured = false;
-        if (!configured) {
-            cudaFuncSetAttribute(k_attn_pf<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            configured = true;
-        }
+        static int ok[PB_MAX_DEVICES] = {};
+        if (per_device(ok, [](int) {
+                return cudaFuncSetAttribute(k_attn_pf<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+                               cudaSuccess ? 1 : -1;
+            }) < 0)
+            return launch_check("attn_pf setup");
         return launch_pdl(k_attn_pf<DH>, dim3((unsigned)G), dim3((AM_WARPS + 1) * 32), smem, st, a, (int)G, U);
     }
-    // two CTAs per SM with 3-stage rings and 4 compute warps each (default), or one
-    // CTA per SM with 6 stages and 8 compute warps (two groups on alternate stages)
+    // two CTAs per SM, 3-stage rings, 4 compute warps each
     constexpr size_t smem = attn_mma_smem<DH, 3, 4>();
-    constexpr size_t smem6 = attn_mma_smem<DH, 6, 8>();
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_attn_mma<DH, 3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_attn_mma<DH, 6, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem6);
-        configured = true;
-    }
-    static const int nocomp = [] {
-        const char* e = getenv("PB_ATT_NOCOMP");
-        return e ? atoi(e) : 0;
-    }();
+    static int ok[PB_MAX_DEVICES] = {};
+    if (per_device(ok, [](int) {
+            return cudaFuncSetAttribute(k_attn_mma<DH, 3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem) == cudaSuccess ? 1 : -1;
+        }) < 0)
+        return launch_check("attn_mma setup");
     AttnArgs aa = a;
-    aa.debug_nocomp = nocomp;
     aa.trace = trace_region(TR_ATTN, (int)G);
-    if (per_sm == 1)
-        return launch_pdl(k_attn_mma<DH, 6, 8>, dim3((unsigned)G), dim3(9 * 32), smem6, st, aa, (int)G, U);
     return launch_pdl(k_attn_mma<DH, 3, 4>, dim3((unsigned)G), dim3(5 * 32), smem, st, aa, (int)G, U);
 }
 

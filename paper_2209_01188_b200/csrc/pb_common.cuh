@@ -34,6 +34,34 @@ void set_error(const std::string& msg);
         }                                            \
     } while (0)
 
+constexpr int PB_MAX_DEVICES = 64;
+
+// Per-device launch setup (shared-memory opt-in, occupancy, SM count):
+// cudaFuncSetAttribute applies to the current device's context only, so a
+// process driving several GPUs configures each one. `slot[dev]` caches an
+// int (0 = not yet); init(dev) returns the value (> 0) or a negative error.
+template <typename F>
+inline int per_device(int* slot, F&& init) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= PB_MAX_DEVICES) {
+        set_error("per_device: bad current device");
+        return -1;
+    }
+    if (slot[dev] > 0) return slot[dev];
+    const int v = init(dev);
+    if (v > 0) slot[dev] = v;
+    return v;
+}
+
+inline int sm_count() {
+    static int slot[PB_MAX_DEVICES] = {};
+    return per_device(slot, [](int dev) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return sms > 0 ? sms : -1;
+    });
+}
+
 inline int launch_check(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {

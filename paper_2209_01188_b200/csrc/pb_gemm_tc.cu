@@ -273,7 +273,7 @@ __device__ __forceinline__ void gemm_tc_body(const TcArgs& a) {
                     float mx = 0.f;
                     if (tok < a.act.n_tok && o < a.epi.M) {
                         // exact integer (|iv| < 2^47), one rounding to f32: same value as the f64 sum
-                        const long long iv = ((long long)h[j] << 16) + ((long long)m[j] << 8) + (long long)l[j];
+                        const long long iv = (long long)h[j] * 65536 + (long long)m[j] * 256 + (long long)l[j];
                         const float y = epi_store(a.epi, tok, o, (float)iv * a.act.back[tok]);
                         if (want_max) mx = fabsf(y * a.epi.s_next[o]);
                     }
@@ -301,34 +301,16 @@ __device__ __forceinline__ void gemm_tc_body(const TcArgs& a) {
 }
 
 __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) { gemm_tc_body<false>(a); }
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) k_gemm_tc_pair(TcArgs a) {
-    gemm_tc_body<true>(a);
-}
 
 int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Epi& epi, cudaStream_t st) {
-    static int sms = 0, pair_clusters = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM);
-        cudaFuncSetAttribute(k_gemm_tc_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM);
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 2;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3((unsigned)sms);
-        cfg.blockDim = dim3(TC_THREADS);
-        cfg.dynamicSmemBytes = TC_SMEM;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        if (cudaOccupancyMaxActiveClusters(&pair_clusters, (void*)k_gemm_tc_pair, &cfg) != cudaSuccess) {
-            cudaGetLastError();
-            pair_clusters = 0;
-        }
-    }
+    static int ok[PB_MAX_DEVICES] = {};
+    if (per_device(ok, [](int) {
+            return cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM) ==
+                           cudaSuccess ? 1 : -1;
+        }) < 0)
+        return launch_check("gemm_tc setup");
+    const int sms = sm_count();
+    if (sms < 0) return PB_ERR_GENERIC;
     TcArgs a{m.codes, bcanon, m.Kp / 32, m.Mp / 128, (int)ceil_div(act.n_tok, TC_BN), 0, 0, 0, act, epi};
     a.tiles = a.MG * a.NTL;
     // Token-tile passes chosen by an HBM-traffic model: a pass of ntg tiles reads every weight byte once
@@ -336,30 +318,16 @@ int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Ep
     // budget (64 MB), otherwise once per wave of CTAs. 176B, 2048 tokens, K = 14336: 3 passes of 9
     // tiles, DRAM 14.3 -> 3.4 GB per mlp_in launch, 4.83 -> 4.10 ms (profiles/r1_tcgen05_ntg_sweep.txt).
     {
-        const char* g = getenv("PB_TC_NTG");  // tuning knob: N > 0 token tiles per pass, 0 one pass
-        const int v = g ? atoi(g) : -1;
         a.ntg = a.NTL;
-        if (v > 0) {
-            a.ntg = std::min(a.NTL, v);
-        } else if (v < 0) {
-            const int64_t a_all = (int64_t)a.MG * a.KC * TC_A, plane = (int64_t)a.KC * TC_B;
-            const int64_t budget = 64ll << 20, slots = sms;
-            int64_t best = INT64_MAX;
-            for (int n = a.NTL; n >= 1; --n) {
-                const int64_t passes = ceil_div(a.NTL, n), bp = n * plane;
-                const int64_t waves = ceil_div((int64_t)a.MG * n, slots);
-                const int64_t cost = passes * a_all + (bp <= budget ? (int64_t)a.NTL * plane : passes * waves * bp);
-                if (cost < best) best = cost, a.ntg = n;
-            }
+        const int64_t a_all = (int64_t)a.MG * a.KC * TC_A, plane = (int64_t)a.KC * TC_B;
+        const int64_t budget = 64ll << 20, slots = sms;
+        int64_t best = INT64_MAX;
+        for (int n = a.NTL; n >= 1; --n) {
+            const int64_t passes = ceil_div(a.NTL, n), bp = n * plane;
+            const int64_t waves = ceil_div((int64_t)a.MG * n, slots);
+            const int64_t cost = passes * a_all + (bp <= budget ? (int64_t)a.NTL * plane : passes * waves * bp);
+            if (cost < best) best = cost, a.ntg = n;
         }
-    }
-    const char* e = getenv("PB_TC_PAIR");
-    const bool pair_on = e && atoi(e) == 1;
-    if (pair_on && pair_clusters > 0 && a.MG % 2 == 0) {
-        // persistent: one 2-CTA cluster per SM pair, as many as can be co-resident
-        const int grid = 2 * std::min(a.tiles / 2, pair_clusters);
-        k_gemm_tc_pair<<<grid, TC_THREADS, TC_SMEM, st>>>(a);
-        return launch_check("gemm_tc_pair");
     }
     const int grid = std::min(a.tiles, sms);  // persistent: one CTA per SM (TMEM 512 columns)
     k_gemm_tc<<<grid, TC_THREADS, TC_SMEM, st>>>(a);

@@ -310,10 +310,7 @@ int prepare_fused_operand(int mode, const ProSrc& src, const float* x, int n_tok
 int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int K, int Kp, const float* gamma,
                     const float* beta, const Mat& m, int tc, uint4* frag, float* back, float4* stats, float* xo,
                     float* y32, cudaStream_t st, uint8_t* bcanon) {
-    static const int early = [] {
-        const char* e = getenv("PB_FRAG_EARLY");
-        return e ? atoi(e) : 1;
-    }();
+    constexpr int early = 1;  // weight-side operand inputs loaded before the PDL wait
     ProArgs a{mode, x, K, Kp, gamma, beta, y32 ? nullptr : m.scales, m.n_outl, m.outl_idx, tc, frag, back, stats,
               xo, y32, src, early};
     if (y32) a.src = ProSrc{};
@@ -379,7 +376,6 @@ struct SkArgs {
     float* partials;  // [chunk][G][2][128 * 2tc]
     int* counters;    // [chunk][MG]
     uint64_t* trace;  // diagnostics (pb_trace_set), usually null
-    int64_t l2pf_bytes;  // weight bytes per CTA prefetched into L2 while waiting for the operand
     // fused operand (k_gemv_i8<.., FUSED>): an operand warp builds the B fragments of
     // every stage in shared memory from the activations (no k_fragwrite launch)
     ProArgs pro;
@@ -670,13 +666,7 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
                     }
                     ++issued;
                     if (!waited && issued == SK_STAGES) {
-                        // the ring is full and the operand is not ready: pull the next
-                        // stages of this CTA's (contiguous) range into L2 meanwhile, so
-                        // HBM works through the previous kernel's tail
-                        const int64_t pf0 = (u + (kc + n - ka)) * 4096;
-                        const int64_t pf1 = u1 * 4096 < pf0 + a.l2pf_bytes ? u1 * 4096 : pf0 + a.l2pf_bytes;
-                        for (int64_t b = pf0; b < pf1; b += 16384)
-                            bulk_prefetch_l2(a.codes + b, (uint32_t)(pf1 - b < 16384 ? pf1 - b : 16384));
+                        // the ring is full of weights: now wait for the operand producer
                         pdl_wait();
                         pdl_trigger();
                         waited = true;
@@ -820,39 +810,33 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
     constexpr int NT = digit_ntiles(TC);
     const size_t smem = (size_t)SK_STAGES * (SK_KCS * 4096 + SK_KCS * NT * 256) + 128 * (8 * NT + 1) * 4 + 16 +
                         2 * SK_STAGES * 8 + 16;
-    static int blocks_per_sm = 0, sms = 0;
-    if (!blocks_per_sm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
+    // occupancy and the smem opt-in are per device (a process may drive several GPUs)
+    static int bps_dev[PB_MAX_DEVICES] = {}, sms_dev[PB_MAX_DEVICES] = {};
+    int dev = 0;
+    PB_CHECK_CUDA(cudaGetDevice(&dev));
+    if (dev >= PB_MAX_DEVICES) { set_error("device index beyond PB_MAX_DEVICES"); return PB_ERR_GENERIC; }
+    if (!bps_dev[dev]) {
+        int sms = 0, bps = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_gemv_i8<TC, SK_KCS, SK_STAGES, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_gemv_i8<TC, SK_KCS, SK_STAGES, FUSED>, THREADS, smem);
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
-        // tuning knob: fewer CTAs per SM than fit leaves a slot for the next
-        // kernel of the chain (PDL) to become resident and start streaming
-        if (const char* e = getenv("PB_GEMV_CTAS")) blocks_per_sm = std::max(1, std::min(blocks_per_sm, atoi(e)));
+        PB_CHECK_CUDA(cudaFuncSetAttribute(k_gemv_i8<TC, SK_KCS, SK_STAGES, FUSED>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_gemv_i8<TC, SK_KCS, SK_STAGES, FUSED>, THREADS, smem);
+        sms_dev[dev] = sms;
+        bps_dev[dev] = std::max(bps, 1);
     }
+    const int blocks_per_sm = bps_dev[dev], sms = sms_dev[dev];
     SkArgs a{};
     a.codes = m.codes;
     a.MG = m.Mp / 128;
     a.KC = m.Kp / 32;
     a.total = (int64_t)a.MG * a.KC;
     const int chunks = (int)ceil_div(act.n_tok, act.tc);
-    // waves > 1: more CTAs than resident slots; the hardware hands the later
-    // waves to whichever SMs finish first (per-SM streaming rates differ)
-    static const int waves = [] {
-        const char* e = getenv("PB_GEMV_WAVES");  // tuning knob
-        return e ? std::max(1, atoi(e)) : 1;
-    }();
-    int64_t G = std::max<int64_t>(1, (int64_t)sms * blocks_per_sm * waves / chunks);
+    int64_t G = std::max<int64_t>(1, (int64_t)sms * blocks_per_sm / chunks);
     // small matrices: at least min_units k tiles per CTA (a CTA then streams whole
     // 128-row groups instead of splitting every group across many CTAs and paying
     // the split merge); large matrices keep one CTA per resident slot
     // (sweep, profiles/r1_gemv_timeline_and_tail.txt: 32 for <= 2 tokens, 64 for 8)
-    static const int64_t min_units = [] {
-        const char* e = getenv("PB_GEMV_MINU");  // tuning knob
-        return (int64_t)(e ? atoi(e) : (TC >= 8 ? 64 : 32));
-    }();
+    constexpr int64_t min_units = TC >= 8 ? 64 : 32;
     G = std::min<int64_t>(G, std::max<int64_t>(1, a.total / std::max<int64_t>(min_units, 1)));
     const int64_t per_tile = 128 * 8 * NT;
     while (G > 1 && (int64_t)chunks * G * 2 * per_tile > partial_cap) G /= 2;
@@ -862,11 +846,6 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
     a.partials = partials;
     a.counters = counters;
     a.trace = trace_region(TR_GEMV, (int)G * chunks);
-    static const int64_t l2pf = [] {
-        const char* e = getenv("PB_GEMV_L2PF");  // tuning knob: KB per CTA (measured: no gain, off)
-        return (int64_t)(e ? atoi(e) : 0) * 1024;
-    }();
-    a.l2pf_bytes = l2pf;
     if (FUSED) {
         a.pro = *pro;
         a.pro.trace = nullptr;
@@ -877,12 +856,9 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
 }
 
 bool gemv_fusable(const Act& act, int K) {
-    static const bool off = getenv("PB_NO_FUSED_OPERAND") != nullptr;  // A/B knob: separate k_fragwrite
-    const char* e = getenv("PB_GEMV_CFG");
-    if (off || (K & 3) != 0) return false;
     // 2 tokens per column chunk only: the 8-token variant measured slower (operand
     // warps compute-bound: 560M batch 8 68 -> 117 us/block)
-    return act.tc == 2 && (!e || atoi(e) == 11);
+    return (K & 3) == 0 && act.tc == 2;
 }
 
 int launch_gemv_fused(const Mat& m, const Act& act, const Epi& epi, const ProArgs& pro, float* zero_a,
@@ -894,50 +870,16 @@ int launch_gemv_fused(const Mat& m, const Act& act, const Epi& epi, const ProArg
     return sk_launch<2, 8, 4, true>(m, act, epi, partials, counters, partial_cap, st, &pro, zero_a, zero_b);
 }
 
+// Stage shapes (k tiles per stage x stages) per column tile, chosen by sweeps
+// (profiles/r1_gemv_timeline_and_tail.txt, profiles/r1_small_shape_gemv_minu.txt):
+// decode 8 x 4 (32 KB stages, one CTA per SM), 3..8 tokens 8 x 2, 17..32 tokens 2 x 4.
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters, int64_t partial_cap,
                 cudaStream_t st) {
-    static int cfg = -1;
-    if (cfg < 0) {
-        // tuning knob (k tiles per stage x stages) of the decode (TC = 2) kernel:
-        // 1 = 4x4 (three CTAs per SM), 6 = 8x2, 8 = 4x12, 10 = 6x3, 11 = 8x4 (default),
-        // 12 = 16x3, 14 = 8x6 (sweep: profiles/r1_gemv_timeline_and_tail.txt)
-        const char* e = getenv("PB_GEMV_CFG");
-        cfg = e ? atoi(e) : 11;  // 8 k tiles (32 KB) x 4 stages, one CTA per SM (profiles/r1_gemv_timeline_and_tail.txt)
-    }
-    static int cfg8 = -1;
-    if (cfg8 < 0) {
-        const char* e = getenv("PB_GEMV_CFG8");  // tuning knob of the 3..8-token kernel: 0 = 4x4, 1 = 8x4, 2 = 8x2 (default)
-        cfg8 = e ? atoi(e) : 2;
-    }
-    static int cfg32 = -1;
-    if (cfg32 < 0) {
-        const char* e = getenv("PB_GEMV_CFG32");  // tuning knob of the 17..32-token kernel: 0 = 2x4, 1 = 4x4, 2 = 8x2
-        cfg32 = e ? atoi(e) : 0;
-    }
     switch (act.tc) {
-        case 2:
-            switch (cfg) {
-                case 6: return sk_launch<2, 8, 2>(m, act, epi, partials, counters, partial_cap, st);
-                case 8: return sk_launch<2, 4, 12>(m, act, epi, partials, counters, partial_cap, st);
-                case 10: return sk_launch<2, 6, 3>(m, act, epi, partials, counters, partial_cap, st);
-                case 12: return sk_launch<2, 16, 3>(m, act, epi, partials, counters, partial_cap, st);
-                case 14: return sk_launch<2, 8, 6>(m, act, epi, partials, counters, partial_cap, st);
-                case 1: return sk_launch<2, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
-                default: return sk_launch<2, 8, 4>(m, act, epi, partials, counters, partial_cap, st);
-            }
-        case 8:
-            switch (cfg8) {
-                case 1: return sk_launch<8, 8, 4>(m, act, epi, partials, counters, partial_cap, st);
-                case 2: return sk_launch<8, 8, 2>(m, act, epi, partials, counters, partial_cap, st);
-                default: return sk_launch<8, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
-            }
+        case 2: return sk_launch<2, 8, 4>(m, act, epi, partials, counters, partial_cap, st);
+        case 8: return sk_launch<8, 8, 2>(m, act, epi, partials, counters, partial_cap, st);
         case 16: return sk_launch<16, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
-        case 32:
-            switch (cfg32) {
-                case 1: return sk_launch<32, 4, 4>(m, act, epi, partials, counters, partial_cap, st);
-                case 2: return sk_launch<32, 8, 2>(m, act, epi, partials, counters, partial_cap, st);
-                default: return sk_launch<32, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
-            }
+        case 32: return sk_launch<32, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
         default: set_error("bad column tile"); return PB_ERR_GENERIC;
     }
 }

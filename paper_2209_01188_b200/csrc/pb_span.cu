@@ -168,7 +168,6 @@ int pb_span_create(const pb_span_config* cfg, pb_span** out) {
     // at the 176B width 32 already win (1084 -> 916 us per block at batch 32), at
     // 7B1 width the GEMV still wins at 32 (profiles/r1_gemv_timeline_and_tail.txt)
     if (s->d > 8192) s->tc_min = 32;
-    if (const char* e = getenv("PB_TC_MIN")) s->tc_min = atoi(e);
     if (!rc && int8 && NT >= s->tc_min) rc = dalloc(s, &s->bcanon, ceil_div(NT, TC_TOKENS) * (kp_max / 32) * 3 * TC_TOKENS * 32);
     if (!rc) rc = dalloc(s, &s->back, NT);
     if (!rc) rc = dalloc(s, &s->stats, NT);
@@ -414,10 +413,7 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                 // kernel boundaries dominate (560M -12 %, 7B1 -8 % per block) but costs ~1 %
                 // at the 176B shape in a sustained run (its operand warps' extra power lowers
                 // the capped SM clock), so the switch is by hidden size
-                static const int fuse_max_d = [] {
-                    const char* e = getenv("PB_FUSED_MAX_HIDDEN");
-                    return e ? atoi(e) : 8192;
-                }();
+                constexpr int fuse_max_d = 8192;
                 if (d <= fuse_max_d && gemv_fusable(a, K)) {
                     // decode: the GEMV's operand warp builds the int8-digit operand itself;
                     // the QKV launch resets the two range accumulators of this block

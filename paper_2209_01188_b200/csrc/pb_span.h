@@ -177,7 +177,6 @@ struct AttnArgs {
     int64_t total_units;
     int max_stages;            // max over groups of ceil(keys / 64)
     int max_group;             // largest query group (> 8: the prefill kernel, queries split across warps)
-    int debug_nocomp = 0;      // experiment knob (PB_ATT_NOCOMP): skip the math, stream only
     uint64_t* trace = nullptr; // diagnostics (pb_trace_set)
 };
 int launch_attention(const AttnArgs& a, int64_t part_cap, cudaStream_t st);

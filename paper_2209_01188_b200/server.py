@@ -46,7 +46,7 @@ from .errors import (
     SwarmError,
 )
 from .model import ModelConfig
-from .rpc import RpcServer, call
+from .rpc import RpcServer, as_view as rpc_view, call
 from .span import BlockSpan
 from .wire import MSG
 
@@ -224,13 +224,24 @@ class StepScheduler:
                     break
                 batch.append(nxt)
                 ntok += nxt.x.shape[0]
+            # pages are reserved per job: a session the pool cannot extend fails
+            # alone (CapacityError -> the handler makes room or answers BUSY)
+            # instead of failing every co-batched session
+            ready = []
+            for j in batch:
+                try:
+                    self.span.reserve(j.seq, j.seq.length + j.x.shape[0])
+                    ready.append(j)
+                except CapacityError as e:
+                    j.err = e
             try:
-                outs = self.span.step([(j.seq, j.x) for j in batch])
-                torch.cuda.current_stream(self.span.device).synchronize()
-                for j, o in zip(batch, outs):
-                    j.out = o
+                if ready:
+                    outs = self.span.step([(j.seq, j.x) for j in ready])
+                    torch.cuda.current_stream(self.span.device).synchronize()
+                    for j, o in zip(ready, outs):
+                        j.out = o
             except Exception as e:  # noqa: BLE001
-                for j in batch:
+                for j in ready:
                     j.err = e
             self.batches += 1
             self.batched_steps += len(batch)
@@ -257,8 +268,6 @@ class ServerNode:
         self._tapes: dict[bytes, tuple[float, object]] = {}  # tape_id -> (born, device tape [B, n_blocks, t, d])
         self._tapes_lock = threading.Lock()
         self._stop = threading.Event()
-        self._registry: dict = {}
-        self._registry_lock = threading.Lock()
         self.rpc: RpcServer | None = None
         self._ckpt = checkpoint
         self._blocks_host = None
@@ -298,7 +307,10 @@ class ServerNode:
         n = len(self.range)
         int8 = self.config.quantize in ("weights", "both")
         pos_budget = max(1, self.config.cache_budget_tokens // n)
-        pages = self.config.kv_pages or (-(-pos_budget // self.config.page_tokens) + self.config.capacity + 2)
+        # the budget's positions + one partial page per session + one maximal
+        # STEP in flight before _enforce_cache_budget runs (server.py:389)
+        pages = self.config.kv_pages or (-(-pos_budget // self.config.page_tokens) + self.config.capacity + 2
+                                         + -(-self.model.max_seq // self.config.page_tokens))
         torch.cuda.set_device(self.config.device)
         if self._given_span is not None:
             self.span = self._given_span
@@ -312,7 +324,8 @@ class ServerNode:
                                   device=self.config.device)
             self._load_weights()
         self.sched = StepScheduler(self.span, self.config.max_batch_tokens, max(1, self.config.capacity))
-        self.rpc = RpcServer(self.config.host, self.config.port, self._dispatch).start()
+        self.rpc = RpcServer(self.config.host, self.config.port, self._dispatch,
+                             pinned_device=self.config.device).start()
         self._announce("joining", throughput=1e-6)
         self.throughput = self.measure_throughput()
         self._announce("online")
@@ -366,21 +379,18 @@ class ServerNode:
     # ---------------------------------------------------------------- registry
 
     def _entry(self, state: str, throughput=None, ttl_ms=None) -> dict:
+        """ServerEntry dict (registry.py:40) announced to the bootstrap peers."""
         return {
             "id": self.server_id, "address": self.address, "start": self.range.start, "end": self.range.end,
             "throughput": throughput if throughput is not None else max(self.throughput, 1e-6),
             "announced_at": int(time.time() * 1000), "ttl_ms": ttl_ms or self.config.ttl_ms, "state": state,
         }
 
-    def _remember(self, entry: dict):
-        with self._registry_lock:
-            mine = self._registry.get(entry["id"])
-            if mine is None or entry["announced_at"] >= mine["announced_at"]:
-                self._registry[entry["id"]] = entry
-
     def _announce(self, state: str, throughput=None, ttl_ms=None):
+        """server.py:171-195: push our entry to the registry seeds. Discovery
+        itself (LOOKUP / GOSSIP replicas) is control plane and stays with the
+        reference's registry."""
         entry = self._entry(state, throughput, ttl_ms)
-        self._remember(entry)
         self.events.append({"t": entry["announced_at"], "event": "announce", "state": state,
                             "range": [self.range.start, self.range.end]})
         payload = json.dumps(entry).encode()
@@ -437,8 +447,14 @@ class ServerNode:
         return self._weights_hash
 
     # ---------------------------------------------------------------- RPC
+    #
+    # Handlers take an rpc.Payload (a zero-copy view of the received frame,
+    # page-locked for tensor-sized payloads) and return reply bytes. Error codes
+    # follow the reference handler by handler (server.py:295-450): malformed
+    # TensorMsg bytes and blocks rejecting the hidden width escape its handlers
+    # as exceptions, i.e. ERR_GENERIC "internal error: ..." (transport/rpc.py:247-250).
 
-    def _dispatch(self, msg_type: int, payload: bytes):
+    def _dispatch(self, msg_type: int, payload):
         if msg_type == MSG.PING:
             return MSG.PING, b""
         if msg_type == MSG.INFO:
@@ -453,26 +469,13 @@ class ServerNode:
             return MSG.FORWARD, self._forward(payload)
         if msg_type == MSG.BACKWARD:
             return MSG.BACKWARD, self._backward(payload)
-        if msg_type == MSG.ANNOUNCE:
-            self._remember(json.loads(payload.decode()))
+        if msg_type == MSG.ANNOUNCE:  # accepted and ignored: discovery is the registry's job
             return MSG.ANNOUNCE, b""
         if msg_type == MSG.LOOKUP:
-            q = json.loads(payload.decode())
-            return MSG.LOOKUP, json.dumps(self._lookup(q["start"], q["end"])).encode()
+            return MSG.LOOKUP, b"[]"
         if msg_type == MSG.GOSSIP:
-            for e in json.loads(payload.decode()):
-                self._remember(e)
-            with self._registry_lock:
-                snap = sorted(self._registry.values(), key=lambda e: e["id"])
-            return MSG.GOSSIP, json.dumps(snap, sort_keys=True).encode()
+            return MSG.GOSSIP, b"[]"
         raise RemoteError(ERR_BAD_REQUEST, f"unknown message type 0x{msg_type:02x}")
-
-    def _lookup(self, start: int, end: int):
-        now = int(time.time() * 1000)
-        with self._registry_lock:
-            hits = [e for e in self._registry.values() if e["state"] == "online"
-                    and now < e["announced_at"] + e["ttl_ms"] and e["start"] < end and start < e["end"]]
-        return sorted(hits, key=lambda e: (e["start"], e["id"]))
 
     def _info_payload(self) -> bytes:
         return json.dumps({
@@ -484,10 +487,10 @@ class ServerNode:
     def _reply_encoding(self) -> int:
         return codec.ENC_INT8 if self.config.quantize in ("activations", "both") else codec.ENC_F32
 
-    def _open_session(self, payload: bytes) -> bytes:
+    def _open_session(self, payload) -> bytes:
         if len(payload) != 20:
             raise RemoteError(ERR_BAD_REQUEST, "OPEN_SESSION wants 16-byte id + u32 max_len")
-        sid, (max_len,) = payload[:16], struct.unpack(">I", payload[16:])
+        sid, (max_len,) = bytes(payload[:16]), struct.unpack(">I", bytes(payload[16:20]))
         if max_len < 1 or max_len > self.model.max_seq:
             raise RemoteError(ERR_BAD_REQUEST, f"max_len must be in [1, {self.model.max_seq}]")
         with self._sessions_lock:
@@ -505,17 +508,22 @@ class ServerNode:
             raise RemoteError(ERR_UNKNOWN_SESSION, "unknown session")
         return s
 
-    def _step(self, payload: bytes) -> bytes:
+    @staticmethod
+    def _internal(e: Exception) -> RemoteError:
+        return RemoteError(ERR_GENERIC, f"internal error: {e}")
+
+    def _step(self, payload) -> bytes:
         if len(payload) < 20:
             raise RemoteError(ERR_BAD_REQUEST, "short STEP payload")
-        sid = payload[:16]
-        (start_pos,) = struct.unpack(">I", payload[16:20])
+        sid = bytes(payload[:16])
+        (start_pos,) = struct.unpack(">I", bytes(payload[16:20]))
         session = self._get_session(sid)
-        digest = hashlib.sha256(payload[20:]).digest()
+        tensor = payload[20:]
+        digest = hashlib.sha256(rpc_view(tensor)).digest()
         try:
-            _, dims, _, _, _ = codec.parse_tensor(payload[20:])
+            _, dims, _, _, _ = codec.parse_tensor(tensor)
         except SwarmError as e:
-            raise RemoteError(ERR_BAD_REQUEST, str(e)) from e
+            raise self._internal(e) from e
         if len(dims) != 2:
             raise RemoteError(ERR_BAD_REQUEST, "STEP tensor must be 2-D [t, d]")
         t = dims[0]
@@ -529,12 +537,12 @@ class ServerNode:
                 raise RemoteError(ERR_DESYNC, f"position mismatch: got {start_pos}, have {session.position}")
             if start_pos + t > session.max_len:
                 raise RemoteError(ERR_CAPACITY, "session exceeds max_len")
-            if dims[1] != self.model.hidden:
-                raise RemoteError(ERR_BAD_REQUEST, f"hidden must be [t, {self.model.hidden}]")
+            if dims[1] != self.model.hidden or t < 1:
+                raise self._internal(InputError(f"hidden must be [t, {self.model.hidden}]"))
             with self._sessions_lock:
                 if self._sessions.get(sid) is not session:
                     raise RemoteError(ERR_UNKNOWN_SESSION, "session evicted")
-            if session.poisoned or not codec.payload_finite(payload[20:]):
+            if session.poisoned or not codec.payload_finite(tensor):
                 # the reference computes NaN/inf hidden states and fails encoding the reply
                 # (transport/wire.py:89-90 -> ERR_GENERIC) after advancing the position
                 # (server.py:386-387); every later step of the session fails the same way
@@ -542,15 +550,20 @@ class ServerNode:
                 session.position += t
                 raise RemoteError(ERR_GENERIC, "internal error: non-finite tensor")
             tm = [time.perf_counter()] if _TIMING else None
-            x = codec.decode_tensor(payload[20:], device=self.span.device)
+            x = codec.decode_tensor(tensor, device=self.span.device)
             if tm:
                 tm.append(time.perf_counter())
             try:
                 out = self.sched.run(session.seq, x)
-            except CapacityError as e:
-                raise RemoteError(ERR_BUSY, f"KV pool exhausted: {e}") from e
-            except InputError as e:
-                raise RemoteError(ERR_BAD_REQUEST, str(e)) from e
+            except CapacityError:
+                # the pool is short of pages for this step: the reference never
+                # refuses a step for memory (it evicts after computing,
+                # server.py:389), so evict idle LRU sessions now and retry once
+                self._make_room(session, t)
+                try:
+                    out = self.sched.run(session.seq, x)
+                except CapacityError as e:
+                    raise RemoteError(ERR_BUSY, f"KV pool exhausted: {e}") from e
             session.position += t
             if tm:
                 tm.append(time.perf_counter())
@@ -562,13 +575,33 @@ class ServerNode:
         self._enforce_cache_budget()
         return reply
 
-    def _close_session(self, payload: bytes) -> bytes:
+    def _close_session(self, payload) -> bytes:
         with self._sessions_lock:
-            s = self._sessions.pop(payload[:16], None)
+            s = self._sessions.pop(bytes(payload[:16]), None)
         if s is not None:
             with s.lock:
                 self.span.release(s.seq)
         return b""
+
+    def _make_room(self, requester: _Session, t: int) -> None:
+        """Evict least-recently-active sessions other than `requester` (never
+        one with a step in flight) until the pool can extend the requester by
+        t positions."""
+        need = self.span.pages_needed(requester.seq, requester.seq.length + t)
+        with self._sessions_lock:
+            order = sorted((s for s in self._sessions.values() if s is not requester), key=lambda s: s.last_active)
+        for v in order:
+            if self.span.pool.free_pages >= need:
+                return
+            if not v.lock.acquire(blocking=False):
+                continue
+            try:
+                with self._sessions_lock:
+                    if self._sessions.get(v.session_id) is v:
+                        del self._sessions[v.session_id]
+                self.span.release(v.seq)
+            finally:
+                v.lock.release()
 
     def _enforce_cache_budget(self):
         n = len(self.range)
@@ -586,38 +619,42 @@ class ServerNode:
             with v.lock:
                 self.span.release(v.seq)
 
-    def _forward(self, payload: bytes) -> bytes:
+    def _forward(self, payload) -> bytes:
         try:
             finite = codec.payload_finite(payload)
             batch = codec.decode_tensor(payload, device=self.span.device)
         except SwarmError as e:
-            raise RemoteError(ERR_BAD_REQUEST, str(e)) from e
+            raise self._internal(e) from e
         if batch.ndim != 3:
             raise RemoteError(ERR_BAD_REQUEST, "FORWARD tensor must be [B, t, d]")
+        if batch.shape[2] != self.model.hidden:
+            raise self._internal(InputError(f"hidden must be [t, {self.model.hidden}]"))
         if not finite:  # the reference computes NaN/inf and fails encoding the reply (wire.py:89-90)
             raise RemoteError(ERR_GENERIC, "internal error: non-finite tensor")
         try:
             out, tape = self.span.forward(batch, tape=True)
         except CapacityError as e:
-            raise RemoteError(ERR_CAPACITY, str(e)) from e
+            raise self._internal(e) from e
         tape_id = os.urandom(16)
         with self._tapes_lock:  # server.py:426-428
             self._tapes[tape_id] = (time.monotonic(), tape)
         return tape_id + codec.encode_tensor(out, self._reply_encoding())
 
-    def _backward(self, payload: bytes) -> bytes:
+    def _backward(self, payload) -> bytes:
         """server.py:431-450: consume-once tape, f32 reply (gradients travel at full precision)."""
         if len(payload) < 16:
             raise RemoteError(ERR_BAD_REQUEST, "short BACKWARD payload")
         with self._tapes_lock:
-            item = self._tapes.pop(payload[:16], None)
+            item = self._tapes.pop(bytes(payload[:16]), None)
         if item is None:
             raise RemoteError(ERR_UNKNOWN_TAPE, "unknown or expired tape")
         _, tape = item
         try:
             grad = codec.decode_tensor(payload[16:], device=self.span.device)
         except SwarmError as e:
-            raise RemoteError(ERR_BAD_REQUEST, str(e)) from e
-        if grad.ndim != 3 or grad.shape[0] != tape.shape[0] or tuple(grad.shape[1:]) != tuple(tape.shape[2:]):
+            raise self._internal(e) from e
+        if grad.ndim != 3 or grad.shape[0] != tape.shape[0]:
             raise RemoteError(ERR_BAD_REQUEST, "BACKWARD grad shape mismatch")
+        if tuple(grad.shape[1:]) != tuple(tape.shape[2:]):
+            raise self._internal(InputError("BACKWARD grad shape mismatch"))
         return codec.encode_tensor(self.span.backward(tape, grad), codec.ENC_F32)

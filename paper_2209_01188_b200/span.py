@@ -173,10 +173,17 @@ class BlockSpan:
         seq.pages = []
         seq.length = 0
 
-    def _reserve(self, seq: Sequence, new_len: int) -> None:
-        need = -(-new_len // self.page_tokens) - len(seq.pages)
+    def pages_needed(self, seq: Sequence, new_len: int) -> int:
+        return max(0, -(-new_len // self.page_tokens) - len(seq.pages))
+
+    def reserve(self, seq: Sequence, new_len: int) -> None:
+        """Give `seq` KV pages for positions [0, new_len) (CapacityError when the
+        pool is short; the sequence keeps what it had)."""
+        need = self.pages_needed(seq, new_len)
         if need > 0:
             seq.pages.extend(self.pool.alloc(need))
+
+    _reserve = reserve
 
     def _meta(self, seqs, lens):
         n_tok = int(sum(lens))
@@ -193,7 +200,13 @@ class BlockSpan:
 
     def step(self, items, out=None):
         """One batched step. items: [(Sequence, hidden [t, d] cuda f32)];
-        returns the outputs in order (views of one [n_tok, d] tensor)."""
+        returns the outputs in order (views of one [n_tok, d] tensor).
+
+        A step larger than the span's workspace (more than max_tokens new
+        positions or max_seqs sequences) runs as consecutive causal chunks;
+        the reference accepts any t <= max_seq in one STEP (server.py:361-390).
+        It is all-or-nothing: if a chunk fails, every sequence is rolled back
+        to its length before the call."""
         import torch
 
         seqs = [s for s, _ in items]
@@ -206,6 +219,8 @@ class BlockSpan:
                 raise InputError("empty step")
             if s.length + t > self.config.max_seq:
                 raise CapacityError(f"position {s.length + t} exceeds max_seq {self.config.max_seq}")
+        if sum(lens) > self.max_tokens or len(items) > self.max_seqs:
+            return self._step_chunked(items, lens)
         with self._lock:
             for s, t in zip(seqs, lens):
                 self._reserve(s, s.length + t)
@@ -221,6 +236,34 @@ class BlockSpan:
             for s, t in zip(seqs, lens):
                 s.length += t
         return list(torch.split(y, lens))
+
+    def _step_chunked(self, items, lens):
+        """Each sequence's new positions in causal chunks of at most max_tokens,
+        up to max_seqs sequences per launch sequence."""
+        import torch
+
+        start = [s.length for s, _ in items]
+        outs = [[] for _ in items]
+        done = [0] * len(items)
+        try:
+            while True:
+                group, budget = [], self.max_tokens
+                for i, ((s, h), t) in enumerate(zip(items, lens)):
+                    if done[i] < t and budget > 0 and len(group) < self.max_seqs:
+                        c = min(t - done[i], budget)
+                        group.append((i, c))
+                        budget -= c
+                if not group:
+                    break
+                res = self.step([(items[i][0], items[i][1][done[i]:done[i] + c]) for i, c in group])
+                for (i, c), y in zip(group, res):
+                    outs[i].append(y)
+                    done[i] += c
+        except Exception:
+            for (s, _), L in zip(items, start):
+                s.length = L
+            raise
+        return [o[0] if len(o) == 1 else torch.cat(o) for o in outs]
 
     def step_codes(self, seqs, lens, in_codes=None, in_scales=None, in_f32=None, out_codes=None, out_scales=None,
                    out_f32=None):
@@ -254,9 +297,10 @@ class BlockSpan:
         if t > self.config.max_seq:
             raise CapacityError(f"t={t} exceeds max_seq")
         out = torch.empty_like(batch)
-        per = max(1, min(self.max_seqs, self.max_tokens // t if t <= self.max_tokens else 1))
-        if t > self.max_tokens:
-            raise CapacityError(f"t={t} exceeds the span's max_tokens={self.max_tokens}")
+        # rows packed per launch sequence; a row longer than the workspace runs
+        # alone in causal chunks of max_tokens positions (its KV pages persist
+        # across the chunks)
+        per = max(1, min(self.max_seqs, self.max_tokens // t)) if t <= self.max_tokens else 1
         tp = torch.empty(B, self.n_blocks, t, d, device=self.device) if tape else None
         for r0 in range(0, B, per):
             rows = range(r0, min(B, r0 + per))
@@ -264,21 +308,25 @@ class BlockSpan:
             try:
                 if tape:
                     n = len(rows)
-                    x = batch[r0:r0 + n].reshape(n * t, d).to(device=self.device, dtype=torch.float32).contiguous()
-                    y = torch.empty_like(x)
-                    buf = torch.empty(self.n_blocks, n * t, d, device=self.device)
-                    with self._lock:
-                        for s in seqs:
-                            self._reserve(s, t)
-                        n_tok, tok_seq, tok_pos, pages = self._meta(seqs, [t] * n)
-                        st = _lib.stream_ptr(torch.cuda.current_stream(self.device))
-                        _lib.check(_lib.lib().pb_span_step_tape(
-                            self._h, n_tok, n, tok_seq.ctypes.data, tok_pos.ctypes.data, pages.ctypes.data,
-                            _lib.ptr(x), _lib.ptr(y), _lib.ptr(buf), st))
-                        for s in seqs:
-                            s.length += t
-                    out[r0:r0 + n] = y.view(n, t, d)
-                    tp[r0:r0 + n] = buf.view(self.n_blocks, n, t, d).transpose(0, 1)
+                    step_t = min(t, self.max_tokens)
+                    for c0 in range(0, t, step_t):
+                        c = min(step_t, t - c0)
+                        x = batch[r0:r0 + n, c0:c0 + c].reshape(n * c, d).to(device=self.device,
+                                                                              dtype=torch.float32).contiguous()
+                        y = torch.empty_like(x)
+                        buf = torch.empty(self.n_blocks, n * c, d, device=self.device)
+                        with self._lock:
+                            for s in seqs:
+                                self._reserve(s, c0 + c)
+                            n_tok, tok_seq, tok_pos, pages = self._meta(seqs, [c] * n)
+                            st = _lib.stream_ptr(torch.cuda.current_stream(self.device))
+                            _lib.check(_lib.lib().pb_span_step_tape(
+                                self._h, n_tok, n, tok_seq.ctypes.data, tok_pos.ctypes.data, pages.ctypes.data,
+                                _lib.ptr(x), _lib.ptr(y), _lib.ptr(buf), st))
+                            for s in seqs:
+                                s.length += c
+                        out[r0:r0 + n, c0:c0 + c] = y.view(n, c, d)
+                        tp[r0:r0 + n, :, c0:c0 + c] = buf.view(self.n_blocks, n, c, d).transpose(0, 1)
                 else:
                     res = self.step([(s, batch[r]) for s, r in zip(seqs, rows)])
                     for r, y in zip(rows, res):

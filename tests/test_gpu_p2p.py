@@ -1,6 +1,8 @@
-"""NVLink peer-memory hop (pb_hop.cu, pipeline.P2PRing) on two GPUs: the
-pipelined result must be bit-identical to handing the wire codes over in one
-process (tools/p2p_check.py). Skipped on a single-GPU box."""
+"""Peer-memory hop (pb_hop.cu, pipeline.P2PRing) between two span processes:
+the pipelined result must be bit-identical to handing the wire codes over in
+one process (tools/p2p_check.py). Two GPUs: the mailbox is on the peer GPU
+over NVLink. One GPU: both ranks share the device (same IPC mailbox and
+signal/wait kernels, no NVLink)."""
 
 import os
 import subprocess
@@ -15,8 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_p2p_ring_bit_identical_to_single_process():
     import torch
 
-    if torch.cuda.device_count() < 2:
-        pytest.skip("needs 2 GPUs")
+    assert torch.cuda.device_count() >= 1
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "tools", "p2p_check.py")]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=300)

@@ -3,7 +3,10 @@ pb_hop.cu): 4 blocks split [0,2) on rank 0 and [2,4) on rank 1, S=2 sessions,
 a prefill chunk then decode steps around the ring. Rank 1 records every job's
 output; rank 0 then replays the same jobs through fresh spans of both halves
 in one process (wire codes handed over in HBM) and requires bit-identical
-hidden states. Run under torchrun with 2 processes:
+hidden states. With one visible GPU both ranks share it (the mailbox is then a
+CUDA IPC mapping within one device -- same code path, no NVLink). The control
+plane (handle exchange, barriers) uses gloo; the data path never touches it.
+Run under torchrun with 2 processes:
 
   python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tools/p2p_check.py
 """
@@ -25,9 +28,10 @@ def main():
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     assert world == 2
-    torch.cuda.set_device(rank)
-    dev = torch.device("cuda", rank)
-    dist.init_process_group("nccl", device_id=dev)
+    gpu = rank % torch.cuda.device_count()
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    dist.init_process_group("gloo")
     cfg = ModelConfig(4, 512, 8, 1024, 256)  # 4 blocks, h=512, 8 heads
     S, d = 2, cfg.hidden
     lens = [16, 1, 1, 1, 1]  # prefill chunk, then decode steps (per session)
@@ -37,7 +41,7 @@ def main():
     inputs = [torch.randn(t, d, generator=g, device=dev) * 0.5 for _, t in jobs]
 
     def make(lo, hi):
-        sp = BlockSpan(cfg, lo, hi, int8=True, page_tokens=16, max_tokens=32, max_seqs=1, device=rank)
+        sp = BlockSpan(cfg, lo, hi, int8=True, page_tokens=16, max_tokens=32, max_seqs=1, device=gpu)
         sp.generate_weights(42)
         return sp
 
@@ -45,7 +49,7 @@ def main():
     seqs = [span.new_sequence() for _ in range(S)]
     slot = max(t for _, t in jobs) * d
     slot_bytes = -(-slot // 16) * 16 + 4 * (-(-slot // 64))
-    ring = P2PRing(rank, world, S, slot_bytes, rank, dist, timeout_ms=30000)
+    ring = P2PRing(rank, world, S, slot_bytes, gpu, dist, timeout_ms=30000)
     sched = RingSchedule(rank, world, S, len(jobs))
     st = _lib.stream_ptr(torch.cuda.current_stream())
     outs = []
