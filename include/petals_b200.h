@@ -120,13 +120,15 @@ int pb_span_step(pb_span* span, int32_t n_tok, int32_t n_seq, const int32_t* h_t
                  void* stream);
 
 /* Same as pb_span_step but the hidden states arrive / leave as wire-codec
- * int8 (codes [n_tok*hidden], scales [n_tok*hidden/64]), block 64; the
- * decode is fused into the first block's prologue input path and the encode
- * runs on the last block's output. Either codec side may be NULL (f32 then). */
+ * int8 (codes [n_tok*hidden], scales [n_tok*hidden/64]), block 64 -- the
+ * span-to-span hop payload (client.py:312-331 relays exactly these bytes).
+ * Either codec side may be NULL (f32 then); in/out pointers may live in a
+ * peer GPU's mailbox (pb_hop_*). d_tape (nullable) records the FORWARD tape
+ * as pb_span_step_tape does. */
 int pb_span_step_int8(pb_span* span, int32_t n_tok, int32_t n_seq, const int32_t* h_tok_seq,
                       const int32_t* h_tok_pos, const int32_t* h_pages, const int8_t* d_in_codes,
                       const float* d_in_scales, const float* d_in_f32, int8_t* d_out_codes,
-                      float* d_out_scales, float* d_out_f32, void* stream);
+                      float* d_out_scales, float* d_out_f32, float* d_tape, void* stream);
 
 /* pb_span_step that also records the FORWARD tape (server.py:418-428): block j's input rows are
  * copied to d_tape[j][n_tok][hidden] (hosted block order) for pb_span_backward. */

@@ -60,7 +60,7 @@ def lib() -> C.CDLL:
         "pb_span_outliers": [P, I32, I32, P, I32, C.POINTER(C.c_int32)],
         "pb_span_read_codes": [P, I32, I32, P, P],
         "pb_span_step": [P, I32, I32, P, P, P, P, P, VP],
-        "pb_span_step_int8": [P, I32, I32, P, P, P, P, P, P, P, P, P, VP],
+        "pb_span_step_int8": [P, I32, I32, P, P, P, P, P, P, P, P, P, P, VP],
         "pb_span_step_tape": [P, I32, I32, P, P, P, P, P, P, VP],
         "pb_span_backward": [P, P, I32, P, P, VP],
         "pb_span_profile": [P, I32],

@@ -617,7 +617,7 @@ extern "C" int pb_span_step_tape(pb_span* span, int32_t n_tok, int32_t n_seq, co
 extern "C" int pb_span_step_int8(pb_span* span, int32_t n_tok, int32_t n_seq, const int32_t* h_tok_seq,
                                  const int32_t* h_tok_pos, const int32_t* h_pages, const int8_t* d_in_codes,
                                  const float* d_in_scales, const float* d_in_f32, int8_t* d_out_codes,
-                                 float* d_out_scales, float* d_out_f32, void* stream) {
+                                 float* d_out_scales, float* d_out_f32, float* d_tape, void* stream) {
     PB_REQUIRE(span, PB_ERR_BAD_REQUEST, "null span");
     PB_REQUIRE(d_in_codes || d_in_f32, PB_ERR_BAD_REQUEST, "no input");
     PB_REQUIRE(d_out_codes || d_out_f32, PB_ERR_BAD_REQUEST, "no output");
@@ -639,7 +639,7 @@ extern "C" int pb_span_step_int8(pb_span* span, int32_t n_tok, int32_t n_seq, co
         ++extra;
     }
     float* out = d_out_f32 ? d_out_f32 : span->xa;
-    if (int rc = run_blocks(span, n_tok, max_pos, in, out, st)) return rc;
+    if (int rc = run_blocks(span, n_tok, max_pos, in, out, st, d_tape)) return rc;
     if (d_out_codes) {
         const int ev = prof_begin(span, st);
         if (int rc = quantize_blockwise(out, n, 64, d_out_codes, d_out_scales, st)) return rc;

@@ -103,6 +103,22 @@ class DevPtr:
         return self.addr
 
 
+class _CudaArray:
+    __slots__ = ("__cuda_array_interface__",)
+
+    def __init__(self, addr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (int(addr), False),
+                                         "version": 3, "strides": None}
+
+
+def dev_view(addr: int, nbytes: int, device):
+    """A torch uint8 tensor aliasing `nbytes` of device memory at `addr`
+    (e.g. a mailbox slot allocated by pb_hop_alloc); no copy, no ownership."""
+    import torch
+
+    return torch.as_tensor(_CudaArray(addr, nbytes), device=device)
+
+
 class P2PRing:
     """The RingSchedule's hops over NVLink peer memory (pb_hop.cu) instead of
     NCCL: every rank exports one mailbox (u64 flags + `slots` payload slots)

@@ -318,12 +318,8 @@ class ServerNode:
                 raise InputError("given span does not match the configured range / quantize mode")
             self._weights_hash = hashlib.sha256(f"span:{self.model}:{self.range}".encode()).hexdigest()
         else:
-            self.span = BlockSpan(self.model, self.range.start, self.range.end, int8=int8,
-                                  page_tokens=self.config.page_tokens, n_pages=pages,
-                                  max_tokens=self.config.max_batch_tokens, max_seqs=max(1, self.config.capacity),
-                                  device=self.config.device)
-            self._load_weights()
-        self.sched = StepScheduler(self.span, self.config.max_batch_tokens, max(1, self.config.capacity))
+            self.span = self._make_span(int8, pages)
+        self.sched = self._make_scheduler()
         self.rpc = RpcServer(self.config.host, self.config.port, self._dispatch,
                              pinned_device=self.config.device).start()
         self._announce("joining", throughput=1e-6)
@@ -334,6 +330,19 @@ class ServerNode:
         log.info("b200 server %s serving blocks [%d, %d) at %s", self.server_id[:8], self.range.start,
                  self.range.end, self.address)
         return self
+
+    def _make_span(self, int8: bool, pages: int):
+        """The hosted blocks on this process's GPU (overridden by the box front end)."""
+        span = BlockSpan(self.model, self.range.start, self.range.end, int8=int8,
+                         page_tokens=self.config.page_tokens, n_pages=pages,
+                         max_tokens=self.config.max_batch_tokens, max_seqs=max(1, self.config.capacity),
+                         device=self.config.device)
+        self.span = span
+        self._load_weights()
+        return span
+
+    def _make_scheduler(self):
+        return StepScheduler(self.span, self.config.max_batch_tokens, max(1, self.config.capacity))
 
     def _load_weights(self):
         if self.config.seed is not None and self._ckpt is None:
@@ -414,8 +423,12 @@ class ServerNode:
             for v in victims:
                 self.span.release(v.seq)
             with self._tapes_lock:  # server.py:230-233
-                for tid in [tid for tid, (born, _) in self._tapes.items() if now - born > TAPE_TTL_S]:
-                    del self._tapes[tid]
+                expired = [self._tapes.pop(tid)[1] for tid, (born, _) in list(self._tapes.items())
+                           if now - born > TAPE_TTL_S]
+            drop = getattr(self.span, "drop_tape", None)  # tapes held on other GPUs (box front end)
+            for tape in expired:
+                if drop is not None:
+                    drop(tape)
 
     def maybe_rebalance(self) -> bool:
         return False  # allocation/rebalancing is control plane (out of scope)

@@ -266,11 +266,12 @@ class BlockSpan:
         return [o[0] if len(o) == 1 else torch.cat(o) for o in outs]
 
     def step_codes(self, seqs, lens, in_codes=None, in_scales=None, in_f32=None, out_codes=None, out_scales=None,
-                   out_f32=None):
+                   out_f32=None, tape=None):
         """Batched step whose input and/or output hidden states are the wire
         codec (codes [n_tok*d] int8, scales [ceil(n_tok*d/64)] f32) on the
         device (pb_span_step_int8): the span-to-span hop payload. Sequences'
-        tokens are concatenated in `seqs` order (lens[i] new positions each)."""
+        tokens are concatenated in `seqs` order (lens[i] new positions each).
+        tape (nullable, [n_blocks, n_tok, d] f32): record the FORWARD tape."""
         import torch
 
         with self._lock:
@@ -281,7 +282,7 @@ class BlockSpan:
             _lib.check(_lib.lib().pb_span_step_int8(
                 self._h, n_tok, len(seqs), tok_seq.ctypes.data, tok_pos.ctypes.data, pages.ctypes.data,
                 _lib.ptr(in_codes), _lib.ptr(in_scales), _lib.ptr(in_f32), _lib.ptr(out_codes), _lib.ptr(out_scales),
-                _lib.ptr(out_f32), st))
+                _lib.ptr(out_f32), _lib.ptr(tape), st))
             for s, t in zip(seqs, lens):
                 s.length += t
 

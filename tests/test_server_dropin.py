@@ -337,3 +337,33 @@ def test_distributed_backward_matches_reference_client(small_ckpt):
             sw.close()
     for a, b in zip(outs["b200"], outs["ref"]):
         assert float(np.max(np.abs(a - b))) <= 1e-3 * float(np.abs(b).max())
+
+
+def test_box_serves_reference_client_in_one_hop(small_ckpt):
+    """The box front end (two sub-span processes, peer-memory hop) announces
+    ONE ServerEntry [0, 4) to the reference registry; the reference client's
+    plan is a single hop, and its generate() equals reference_generate
+    (client.py:230-257, registry.py:40)."""
+    from swarmlm.model import reference_generate
+
+    from paper_2209_01188_b200.box import LocalBox
+    from paper_2209_01188_b200.model import ModelConfig
+    from paper_2209_01188_b200.server import ServerConfig
+
+    sw = Swarm(small_ckpt)
+    box = None
+    try:
+        cfg = ServerConfig(seed=42, model=ModelConfig(4, 16, 2, 32, 128), bootstrap=[sw.seed.address],
+                           measure_steps=3, page_tokens=16)
+        box = LocalBox(cfg, 2)
+        c = sw.client()
+        try:
+            plan = c.plan()
+            assert len(plan) == 1 and (plan[0].entry.range.start, plan[0].entry.range.end) == (0, 4)
+            assert c.generate([1, 2, 3], 16) == reference_generate(small_ckpt, [1, 2, 3], 16)
+        finally:
+            c.close()
+    finally:
+        if box is not None:
+            assert box.stop() == [0, 0]
+        sw.close()
