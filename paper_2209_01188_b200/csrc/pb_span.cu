@@ -168,6 +168,7 @@ int pb_span_create(const pb_span_config* cfg, pb_span** out) {
     // at the 176B width 32 already win (1084 -> 916 us per block at batch 32), at
     // 7B1 width the GEMV still wins at 32 (profiles/r1_gemv_timeline_and_tail.txt)
     if (s->d > 8192) s->tc_min = 32;
+    if (cfg->tc_min_tokens > 0) s->tc_min = cfg->tc_min_tokens;
     if (!rc && int8 && NT >= s->tc_min) rc = dalloc(s, &s->bcanon, ceil_div(NT, TC_TOKENS) * (kp_max / 32) * 3 * TC_TOKENS * 32);
     if (!rc) rc = dalloc(s, &s->back, NT);
     if (!rc) rc = dalloc(s, &s->stats, NT);

@@ -263,12 +263,12 @@ def test_large_shape_block_vs_f64_reference(shape_name):
 
 
 @pytest.mark.parametrize("shape_name,t", [("mid", 200), ("bloom-7b1", 300)])
-def test_tcgen05_prefill_matches_gemv_path(shape_name, t, monkeypatch):
+def test_tcgen05_prefill_matches_gemv_path(shape_name, t):
     """Prefill through the tcgen05 GEMM (TMA-fed, TMEM accumulators) equals the
-    mma.sync GEMV path on the same span weights (both carry f32-accurate
+    IMMA GEMV path on the same span weights (both carry f32-accurate
     operands; only accumulation order differs), and the subsequent decode
     steps (GEMV path) agree too -- i.e. the KV cache written by the tcgen05
-    epilogue is the same."""
+    epilogue is the same. The path is chosen per span (tc_min_tokens)."""
     import torch
 
     from paper_2209_01188_b200.model import SHAPES as S
@@ -282,51 +282,26 @@ def test_tcgen05_prefill_matches_gemv_path(shape_name, t, monkeypatch):
         cfg = S[shape_name]
         end = 2
     outs = {}
-    for tc_min in ("64", "100000"):
-        monkeypatch.setenv("PB_TC_MIN", tc_min)
-        span = BlockSpan(cfg, 0, end, int8=True, page_tokens=64, max_tokens=max(t, 64), n_pages=16)
+    for tc_min in (64, 100000):
+        span = BlockSpan(cfg, 0, end, int8=True, page_tokens=64, max_tokens=max(t, 64), n_pages=16,
+                         tc_min_tokens=tc_min)
         span.generate_weights(42)
         rng = np.random.default_rng(1)
         x = torch.from_numpy(rng.normal(size=(t + 2, cfg.hidden)).astype(np.float32) * 0.05).cuda()
         seq = span.new_sequence()
+        span.profile(True)
         a = span.step([(seq, x[:t])])[0].cpu().numpy()
+        tc_launches = span.profile_read(5)[1]
+        span.profile(False)
+        assert (tc_launches > 0) == (tc_min == 64), tc_launches  # the two paths really differ
         b = span.step([(seq, x[t:t + 1])])[0].cpu().numpy()
         c = span.step([(seq, x[t + 1:t + 2])])[0].cpu().numpy()
         outs[tc_min] = (a, b, c)
         span.close()
         torch.cuda.empty_cache()
     for i in range(3):
-        err = rel_err(outs["64"][i], outs["100000"][i])
+        err = rel_err(outs[64][i], outs[100000][i])
         assert err <= TOL, (shape_name, i, err)  # fp16 KV rounding can flip on 1-ulp f32 differences
-
-
-@pytest.mark.parametrize("shape_name,t", [("mid", 200), ("bloom-7b1", 300)])
-def test_tcgen05_pair_multicast_bit_identical(shape_name, t, monkeypatch):
-    """The 2-CTA cluster tcgen05 GEMM (digit planes multicast to both CTAs of
-    a row-group pair, PB_TC_PAIR=1) computes the same integers as the default
-    one-CTA-per-tile kernel: prefill + one decode step are bit-identical."""
-    import torch
-
-    from paper_2209_01188_b200.model import SHAPES as S
-    from paper_2209_01188_b200.span import BlockSpan
-
-    cfg, end = (cfg_of(SHAPES["mid"]), SHAPES["mid"].n_layers) if shape_name == "mid" else (S[shape_name], 2)
-    monkeypatch.setenv("PB_TC_MIN", "64")
-    outs = {}
-    for pair in ("0", "1"):
-        monkeypatch.setenv("PB_TC_PAIR", pair)
-        span = BlockSpan(cfg, 0, end, int8=True, page_tokens=64, max_tokens=max(t, 64), n_pages=16)
-        span.generate_weights(42)
-        rng = np.random.default_rng(3)
-        x = torch.from_numpy(rng.normal(size=(t + 1, cfg.hidden)).astype(np.float32) * 0.05).cuda()
-        seq = span.new_sequence()
-        a = span.step([(seq, x[:t])])[0].cpu().numpy()
-        b = span.step([(seq, x[t:])])[0].cpu().numpy()
-        outs[pair] = (a, b)
-        span.close()
-        torch.cuda.empty_cache()
-    for i in range(2):
-        assert np.array_equal(outs["0"][i].view(np.uint32), outs["1"][i].view(np.uint32)), (shape_name, i)
 
 
 def test_bloom176b_tcgen05_prefill_vs_f64_reference():
