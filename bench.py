@@ -1,4 +1,5 @@
-"""Headline benchmark: BLOOM-176B-shape int8 decode steps/s (BASELINE.json).
+"""Headline benchmark: BLOOM-176B-shape int8 decode steps/s (b=1) and tokens/s
+(b=32), as a fraction of the HBM roofline (BASELINE.json).
 
 Workload (N GPUs, one process per GPU): the 70-block 176B-shape model
 (h=14336, H=112, int8 weights generated on device from the reference's
@@ -6,14 +7,22 @@ SplitMix64 streams) is split into N contiguous block spans, one per GPU
 (N=1: all 70 blocks on one B200). N batch-1 sessions are in flight (one per
 pipeline stage, "weak" scaling: per-GPU work is constant), each decoding at a
 context that ends at --ctx (default 2048). A step is one decode token of one
-session through all 70 blocks; span-to-span hops carry the hidden state as
-the reference's blockwise int8 wire codec over NCCL send/recv (the last span
-hands the result back to span 0, which closes the ring for the next token).
+session through all 70 blocks; span-to-span hops carry the hidden state as the
+reference's blockwise int8 wire codec through peer-memory mailboxes over
+NVLink (pb_hop.cu; `--hop nccl` for NCCL send/recv); the last span hands the
+result back to span 0, closing the ring for the session's next token.
 
-value = session-steps/s over all GPUs (b=1 per session) measured with CUDA
-events between barriers, max over ranks. e2e = same metric through the
-server's STEP handler with host bytes in/out (N=1) or with pinned-host
-ingress/egress copies at the pipeline ends (N>1).
+value = session-steps/s over all GPUs, CUDA events between barriers, max over
+ranks (inputs resident in HBM). Sub-records on the same line:
+  e2e    the same metric through the server's public API: client threads send
+         STEP frames (int8 TensorMsg, host bytes) over TCP to the span server
+         (N=1: ServerNode; N>1: the box front end, ONE server for [0, 70)
+         whose hops stay on the GPUs) and read the replies;
+  b32    tokens/s with 32 batch-1 sessions per micro-batch (BASELINE's b=32);
+  c2     BLOOM-560M shape on one GPU, 128-token prefix, batch 1 (config 2);
+  forward  C5-style FORWARD rows of 512 tokens through the pipeline;
+  cpu_baseline  the reference's arithmetic (oracle port) on the host cores at
+         the same context, one block, extrapolated.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -34,12 +43,12 @@ sys.path.insert(0, ROOT)
 
 METRIC = "{model} int8 decode steps/s (b=1)"
 METRIC_B = "{model} int8 decode tokens/s (b={b})"
+RING_BYTES = 64
+UNIT = "steps/s"
 
 
 def model_label(shape: str) -> str:
     return shape.upper()  # bloom-176b -> BLOOM-176B
-RING_BYTES = 64
-UNIT = "steps/s"
 
 
 def parse():
@@ -53,13 +62,17 @@ def parse():
     p.add_argument("--seed", type=int, default=42)
     # a multiple of the tcgen05 GEMM's 80-token tile (256 padded 4 tiles to 320 tokens)
     p.add_argument("--prefill-chunk", type=int, default=240)
-    p.add_argument("--batch", type=int, default=1, help="batch-1 sessions per pipeline micro-batch")
+    p.add_argument("--batch", type=int, default=1, help="batch-1 sessions per pipeline micro-batch (headline)")
     p.add_argument("--hop", default="p2p", choices=["p2p", "nccl"],
                    help="span-to-span hop: NVLink peer-memory mailboxes (pb_hop.cu) or NCCL send/recv")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-b32", action="store_true")
+    p.add_argument("--no-c2", action="store_true")
+    p.add_argument("--b32-ctx", type=int, default=64,
+                   help="context of the b=32 sessions (N=1: 172.7 GB of weights leave ~8 GB of HBM for KV)")
     p.add_argument("--synthetic-kv", action="store_true", help="skip the real prefill (KV content is synthetic)")
-    p.add_argument("--forward-rows", type=int, default=2, help="rows of the FORWARD sample (C5 shape: 512 tokens each)")
+    p.add_argument("--forward-rows", type=int, default=4, help="C5 rows of 512 tokens per GPU")
     return p.parse_args()
 
 
@@ -69,10 +82,10 @@ def parse():
 from paper_2209_01188_b200.pipeline import split_blocks  # noqa: E402
 
 
-def bytes_per_step(cfg, ctx_tokens_per_session):
+def bytes_per_step(cfg, ctx_tokens_per_session, n_layers=None):
     """sum_blocks [12h^2 codes + 7h*4 scales + 13h*4 bias/LN]
     + sum_sessions sum_blocks 2*T*h*2 (fp16 K+V)."""
-    h, L = cfg.hidden, cfg.n_layers
+    h, L = cfg.hidden, n_layers or cfg.n_layers
     w = L * (12 * h * h + 7 * h * 4 + 13 * h * 4)
     kv = sum(L * 2 * T * h * 2 for T in ctx_tokens_per_session)
     return w, kv
@@ -102,7 +115,7 @@ class ClockSampler:
                     self.samples.append([v.strip() for v in out.stdout.strip().split(",")])
             except Exception:  # noqa: BLE001
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __exit__(self, *a):
         self._stop.set()
@@ -123,7 +136,7 @@ def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:  # noqa: BLE001
         return 6650.0, "fallback"
 
@@ -147,38 +160,79 @@ def committed_traffic():
 # ------------------------------------------------------------------ CPU legs (oracle port)
 
 
-def cpu_block_sample(cfg, ctx_sample):
+def cpu_info():
+    """CPU model, cores, numpy / BLAS build and thread count."""
+    import numpy as np
+
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = []
+    try:
+        from threadpoolctl import threadpool_info
+
+        blas = [{k: i.get(k) for k in ("internal_api", "version", "num_threads", "threading_layer")}
+                for i in threadpool_info() if i.get("user_api") == "blas"]
+    except Exception:  # noqa: BLE001
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "numpy": np.__version__, "blas": blas}
+
+
+def cpu_block_sample(cfg, ctx):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import cpu_baseline
 
-    return cpu_baseline.BlockSample(cfg.hidden, cfg.n_heads, ctx_sample, cfg.mlp_ratio), cpu_baseline.cores()
+    return cpu_baseline.BlockSample(cfg.hidden, cfg.n_heads, ctx, cfg.mlp_ratio), cpu_baseline.cores()
+
+
+def cpu_step_seconds(sample, reps, threads=None):
+    """Best of `reps` timed samples (OpenBLAS timings are noisy), optionally
+    with the BLAS pool limited to `threads`."""
+    if threads is None:
+        return min(sample.step_seconds() for _ in range(reps))
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(limits=threads, user_api="blas"):
+        return min(sample.step_seconds() for _ in range(reps))
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU arithmetic (oracle port of
-    block_forward(qw) / matmul_mixed) on the host cores; rank 0 only."""
+    """--impl reference: the reference's CPU arithmetic for one decode step at
+    the SAME context (oracle port of block_forward(qw) / matmul_mixed, full
+    f32 KV cache concat as model.py:137-151 does), on all host cores; rank 0
+    only. A step is a bounded sample: ONE block, timed; value = 1 / (70 x the
+    sample time). ms_per_step is the measured sample time, so steps x
+    ms_per_step is the timed region."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_2209_01188_b200.model import SHAPES
 
     cfg = SHAPES[args.shape]
-    ctx_sample = 128
-    sample, ncores = cpu_block_sample(cfg, ctx_sample)
+    ctx = args.ctx
+    sample, ncores = cpu_block_sample(cfg, ctx)
     for _ in range(args.warmup):
         sample.step_seconds()
     ts = [sample.step_seconds() for _ in range(args.steps)]
-    per_block = min(ts)  # best case for the CPU (OpenBLAS timings are noisy)
+    per_block = statistics.median(ts)
     value = 1.0 / (per_block * cfg.n_layers)
-    desc = (f"1 block of the {args.shape} shape, int8 decode t=1 at context {ctx_sample} (oracle port of "
-            f"quant.py matmul_mixed + model.py block_forward, random codes), x{cfg.n_layers} blocks extrapolated")
+    desc = (f"1 block of the {args.shape} shape per step, int8-weights decode t=1 at context {ctx} (oracle port of "
+            f"quant.py matmul_mixed + model.py block_forward with its f32 KV concat), median of {args.steps}; "
+            f"value = 1 / ({cfg.n_layers} x block time)")
     line = {
-        "impl": "reference", "metric": METRIC.format(model=model_label(args.shape)), "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_block * cfg.n_layers * 1e3,
+        "impl": "reference", "metric": METRIC.format(model=model_label(args.shape)), "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_block * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": {"workload": f"{args.shape} int8 decode b=1 (CPU reference arithmetic)",
-                                        "ctx": ctx_sample},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port", "sample": desc},
+                                        "ctx": ctx, "sample": "one block per step, extrapolated x70"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port", "sample": desc,
+                         **cpu_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -188,9 +242,10 @@ def run_reference(args):
 
 
 class Pipeline:
-    """One span of the 70-block model per GPU; jobs follow the deadlock-free
-    ring schedule of paper_2209_01188_b200.pipeline (grouped NCCL send/recv of
-    the int8 wire payload: codes then f32 scales in one byte buffer)."""
+    """One span of the model per GPU; jobs follow the deadlock-free ring
+    schedule of paper_2209_01188_b200.pipeline. Job ids increase across
+    phases (the mailbox flags are monotonic); each phase is its own
+    RingSchedule [first, end)."""
 
     def __init__(self, args, cfg):
         import torch
@@ -207,33 +262,32 @@ class Pipeline:
         if self.world > 1:
             import datetime
 
-            dist.init_process_group("nccl", device_id=self.dev, timeout=datetime.timedelta(seconds=180))
+            dist.init_process_group("nccl", device_id=self.dev, timeout=datetime.timedelta(seconds=300))
         self.dist = dist if self.world > 1 else None
         self.S = self.world  # micro-batches in flight (one per pipeline stage)
         self.B = args.batch  # batch-1 sessions per micro-batch
-        self.chunk = max(1, args.prefill_chunk // self.B)  # prefill positions per sequence per step
+        self.chunk = args.prefill_chunk  # tokens per prefill job (all sessions of the micro-batch)
         self.ranges = split_blocks(cfg.n_layers, self.world)
         s, e = self.ranges[self.rank]
         pages_per_seq = -(-min(cfg.max_seq, args.ctx + 64) // 64)  # KV pool sized for the benchmarked context
         t0 = time.perf_counter()
         self.span = BlockSpan(cfg, s, e, int8=True, page_tokens=64, n_pages=self.S * self.B * pages_per_seq + 2,
-                              max_tokens=max(self.chunk * self.B, 512), max_seqs=max(self.B, 2), device=self.local)
+                              max_tokens=max(self.chunk, 512), max_seqs=64, device=self.local)
         self.span.generate_weights(args.seed)
         torch.cuda.synchronize()
         self.gen_s = time.perf_counter() - t0
-        self.seqs = [[self.span.new_sequence() for _ in range(self.B)] for _ in range(self.S)]
+        self.set_batch(self.B)
         d = cfg.hidden
         self.d = d
-        cap = self.payload_bytes(self.chunk)
+        cap = self.payload_bytes(max(self.chunk, 512), 1)
         self.inbox = torch.empty(cap, dtype=torch.uint8, device=self.dev)
         self.outbox = torch.empty(cap, dtype=torch.uint8, device=self.dev)
-        self.out = torch.empty(self.chunk * self.B, d, dtype=torch.float32, device=self.dev)
+        self.out = torch.empty(max(self.chunk, 512), d, dtype=torch.float32, device=self.dev)
         g = torch.Generator(device=self.dev)
         g.manual_seed(7)
         self.inputs = torch.randn(64, d, generator=g, device=self.dev) * 0.05  # embedding-like rows
         self.launches = 0
-        self.total_jobs = 0
-        self.jobtimes = [] if os.environ.get("PB_BENCH_JOBTIMES") else None  # diagnostic: per-job device times
+        self.next_job = 0
         self.ring = None
         if self.world > 1 and args.hop == "p2p":
             from paper_2209_01188_b200.pipeline import P2PRing
@@ -250,14 +304,24 @@ class Pipeline:
                 self.ring.close()
                 self.ring = None
 
-    def payload_bytes(self, t):
-        n = t * self.B * self.d
+    def set_batch(self, B):
+        """B batch-1 sessions per micro-batch (fresh sequences; the old ones' pages go back)."""
+        for grp in getattr(self, "seqs", []):
+            for s in grp:
+                self.span.release(s)
+        self.B = B
+        self.seqs = [[self.span.new_sequence() for _ in range(B)] for _ in range(self.S)]
+
+    def payload_bytes(self, t, B=None):
+        n = t * (B or self.B) * self.d
         return -(-n // 16) * 16 + 4 * (-(-n // 64))
 
     def views(self, buf, t):
+        import torch
+
         n = t * self.B * self.d
         off = -(-n // 16) * 16
-        return buf[:n].view(__import__("torch").int8), buf[off:off + 4 * (-(-n // 64))].view(__import__("torch").float32)
+        return buf[:n].view(torch.int8), buf[off:off + 4 * (-(-n // 64))].view(torch.float32)
 
     def barrier(self):
         import torch
@@ -267,66 +331,63 @@ class Pipeline:
             self.dist.barrier()
         torch.cuda.synchronize()
 
-    def run(self, jobs, x_for=None, host_in=None, host_out=None, sync_out=False):
-        """jobs: [(job id, new positions t per sequence)]; x_for(j, n) -> span-0 input rows."""
+    def phase(self, lens, fresh=False):
+        """One phase: for each entry t of `lens`, one job per micro-batch (S
+        jobs), t new positions per session. fresh: release the micro-batch's
+        sequences after each job (cache-less FORWARD rows)."""
+        first = self.next_job
+        jobs = [(first + i * self.S + m, t) for i, t in enumerate(lens) for m in range(self.S)]
+        self.next_job = first + len(jobs)
+        self.run(jobs, first, self.next_job, fresh=fresh)
+
+    def _input(self, j, n):
+        import torch
+
+        if n <= 64:
+            return self.inputs[j % 64: j % 64 + 1].expand(n, self.d).contiguous() if n == 1 else self.inputs[:n]
+        g = torch.Generator(device=self.dev)
+        g.manual_seed(j)
+        return torch.randn(n, self.d, device=self.dev, generator=g) * 0.05
+
+    def run(self, jobs, first, end, fresh=False):
         import torch
 
         from paper_2209_01188_b200.pipeline import RingSchedule, run_jobs, torch_exchange
 
-        sched = RingSchedule(self.rank, self.world, self.S, self.total_jobs)
+        sched = RingSchedule(self.rank, self.world, self.S, end, first)
+        if self.ring is not None:
+            return self.run_p2p(sched, jobs, fresh)
         tmap = dict(jobs)
         r, N = self.rank, self.world
 
-        jt = self.jobtimes
-
         def step(j, inbox):
-            if jt is not None:
-                e = torch.cuda.Event(enable_timing=True)
-                e.record()
-                jt.append(e)
             t = tmap[j]
             n = t * self.B
             seqs = self.seqs[j % self.S]
-            outbox = self.outbox
-            oc, os_ = self.views(outbox, t)
+            oc, os_ = self.views(self.outbox, t)
             if inbox is None or r == 0:  # span 0: fresh input (a received ring payload only orders the step)
-                if host_in is not None:
-                    self.out[:n].copy_(host_in[:n], non_blocking=True)
-                    inp = self.out[:n]
-                elif x_for is not None:
-                    inp = x_for(j, n)
-                else:
-                    inp = self.inputs[j % 64: j % 64 + 1].expand(n, self.d).contiguous()
-                self.span.step_codes(seqs, [t] * self.B, in_f32=inp, out_codes=oc, out_scales=os_, out_f32=self.out[:n])
+                self.span.step_codes(seqs, [t] * self.B, in_f32=self._input(j, n), out_codes=oc, out_scales=os_,
+                                     out_f32=self.out[:n])
             else:
                 ic, is_ = self.views(inbox, t)
                 self.span.step_codes(seqs, [t] * self.B, in_codes=ic, in_scales=is_, out_codes=oc, out_scales=os_,
                                      out_f32=self.out[:n])
             self.launches += self.span.last_launches
-            if jt is not None:
-                e = torch.cuda.Event(enable_timing=True)
-                e.record()
-                jt.append(e)
-            if r == N - 1 and host_out is not None:
-                host_out[:n * self.d].copy_(oc, non_blocking=True)
-                if sync_out:
-                    torch.cuda.current_stream().synchronize()  # result readable on the host
+            if fresh:
+                for s in seqs:
+                    self.span.release(s)
             if r == N - 1:
                 # ring back-edge: only orders span 0's next step of this session
-                # (stand-in for the client's LM head); fixed size, so prefill
-                # chunks and decode steps of different t always match
-                return outbox[:RING_BYTES]
-            return outbox[:self.payload_bytes(t)]
+                # (stand-in for the client's LM head); fixed size
+                return self.outbox[:RING_BYTES]
+            return self.outbox[:self.payload_bytes(t)]
 
-        if self.ring is not None:
-            self.run_p2p(sched, jobs, tmap, x_for, host_in, host_out, sync_out)
-            return
         run_jobs(sched, [j for j, _ in jobs], step, torch_exchange,
                  lambda j: self.inbox[:RING_BYTES] if r == 0 else self.inbox[:self.payload_bytes(tmap[j])])
 
-    def run_p2p(self, sched, jobs, tmap, x_for, host_in, host_out, sync_out):
-        """The same ring over NVLink mailboxes: span r's wire quantizer stores
-        job j's codes/scales straight into span r+1's slot, a signal kernel
+    def run_p2p(self, sched, jobs, fresh):
+        """The ring over NVLink mailboxes: span r's wire quantizer stores job
+        j's codes/scales straight into span r+1's slot, a signal kernel
         publishes it, span r+1's stream waits on it -- no host sync, no NCCL."""
         import torch
 
@@ -351,27 +412,252 @@ class Pipeline:
             else:
                 oc, os_ = self.views(self.outbox, t)
             if r == 0:
-                if host_in is not None:
-                    self.out[:n].copy_(host_in[:n], non_blocking=True)
-                    inp = self.out[:n]
-                elif x_for is not None:
-                    inp = x_for(j, n)
-                else:
-                    inp = self.inputs[j % 64: j % 64 + 1].expand(n, self.d).contiguous()
-                self.span.step_codes(seqs, [t] * self.B, in_f32=inp, out_codes=oc, out_scales=os_, out_f32=self.out[:n])
+                self.span.step_codes(seqs, [t] * self.B, in_f32=self._input(j, n), out_codes=oc, out_scales=os_,
+                                     out_f32=self.out[:n])
             else:
                 ic, is_ = views(ring.local_slot(j), t)
                 self.span.step_codes(seqs, [t] * self.B, in_codes=ic, in_scales=is_, out_codes=oc, out_scales=os_,
                                      out_f32=self.out[:n])
             self.launches += self.span.last_launches + (1 if src is not None else 0) + (1 if dst is not None else 0)
-            if r == N - 1 and host_out is not None:
-                host_out[:n * self.d].copy_(oc, non_blocking=True)
-                if sync_out:
-                    torch.cuda.current_stream().synchronize()
+            if fresh:
+                for s in seqs:
+                    self.span.release(s)
             if dst is not None:
                 # forward edge: job j's payload; ring back-edge (last span -> span 0):
                 # orders the session's next step j + S (stand-in for the client's head)
                 ring.signal(j if r < N - 1 else j + self.S, st)
+
+    def timed(self, lens, clk_index=None):
+        """Run one phase between barriers; returns (max-over-ranks ms, launches, clocks)."""
+        import torch
+
+        self.barrier()
+        self.launches = 0
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clk = ClockSampler(self.local if clk_index is None else clk_index)
+        with clk:
+            start.record()
+            self.phase(lens)
+            stop.record()
+            self.barrier()
+        ms = start.elapsed_time(stop)
+        t = torch.tensor([ms], device=self.dev)
+        if self.dist:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item()), self.launches, clk.summary()
+
+    def prefill(self, T0):
+        lens, left = [], T0
+        per = max(1, self.chunk // self.B)
+        while left > 0:
+            lens.append(min(per, left))
+            left -= lens[-1]
+        self.phase(lens)
+
+
+# ------------------------------------------------------------------ sub-records
+
+
+def c2_record(args):
+    """Config 2: BLOOM-560M shape, all 24 blocks on one GPU, int8,
+    128-token prefix then batch-1 decode; steps/s and the fraction of the
+    per-step HBM roofline (0.317 GB at T=128 + 0.013 GB KV)."""
+    import torch
+
+    from paper_2209_01188_b200.model import SHAPES
+    from paper_2209_01188_b200.span import BlockSpan
+
+    cfg = SHAPES["bloom-560m"]
+    span = BlockSpan(cfg, 0, cfg.n_layers, int8=True, page_tokens=64, n_pages=8, max_tokens=128, max_seqs=2)
+    span.generate_weights(args.seed)
+    seq = span.new_sequence()
+    g = torch.Generator(device="cuda").manual_seed(3)
+    prompt = torch.randn(128, cfg.hidden, device="cuda", generator=g) * 0.05
+    x1 = torch.randn(1, cfg.hidden, device="cuda", generator=g) * 0.05
+    out = torch.empty_like(x1)
+    span.step([(seq, prompt)])
+    K, W = max(args.steps, 50), max(args.warmup, 5)
+    for _ in range(W):
+        span.step([(seq, x1)], out=out)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(K):
+        span.step([(seq, x1)], out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    ctx = 128 + W + K // 2
+    w, kv = bytes_per_step(cfg, [ctx])
+    peak, _ = measured_peaks()
+    ceiling_ms = (w + kv) / (peak * 1e9) * 1e3
+    span.close()
+    return {"metric": "BLOOM-560M int8 decode steps/s (b=1)", "value": 1e3 / ms, "unit": "steps/s",
+            "ms_per_step": ms, "us_per_block": 1e3 * ms / cfg.n_layers, "ctx": ctx,
+            "bytes_per_step": w + kv, "roofline_frac": ceiling_ms / ms,
+            "note": "24 blocks h=1024 on one GPU, 128-token prefix, batch-1 decode timed with CUDA events"}
+
+
+def b32_record(pl, args, cfg):
+    """BASELINE's tokens/s (b=32): each micro-batch is 32 batch-1 sessions
+    stepped together (one launch sequence per block for all 32 tokens)."""
+    B, T = 32, args.b32_ctx
+    pl.set_batch(B)
+    T0 = T - (args.warmup + args.steps) - 1
+    lens, left = [], T0
+    while left > 0:
+        lens.append(min(pl.chunk // B, left))
+        left -= lens[-1]
+    pl.phase(lens)
+    pl.phase([1] * args.warmup)
+    ms, launches, clk = pl.timed([1] * args.steps)
+    N, S, K = pl.world, pl.S, args.steps
+    tokens = K * S * B
+    w, kv = bytes_per_step(cfg, [T0 + args.warmup + K // 2] * B)  # one micro-batch through all blocks
+    peak, _ = measured_peaks()
+    # every GPU streams its span's weights + its KV once per micro-batch step
+    agg_ceiling_s = (w / N + kv / N) / (peak * 1e9)
+    step_s = (ms / 1e3) / (K * S)
+    pl.set_batch(args.batch)
+    return {"metric": METRIC_B.format(model=model_label(args.shape), b=B), "value": tokens / (ms / 1e3),
+            "unit": "tokens/s", "sessions": S * B, "ctx_end": T, "ms_per_microbatch_step": step_s * 1e3 * N,
+            "bytes_per_step": w + kv, "roofline_frac": agg_ceiling_s / step_s, "gpu_launches": launches,
+            "clocks": clk, "note": f"{S} micro-batch(es) x {B} sessions, context {T0}->{T}; roofline = every GPU "
+                                   f"streaming its span's int8 weights + KV once per micro-batch step"}
+
+
+def forward_record(pl, args, cfg):
+    """C5-style FORWARD: rows of 512 tokens (server.py:411-429 semantics,
+    cache-less, no tape) through the pipeline, S rows in flight."""
+    import torch
+
+    rows = max(1, args.forward_rows) * pl.S
+    pl.set_batch(1)
+    per_mb = rows // pl.S
+    pl.span.profile(True)
+    pl.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    pl.phase([512] * per_mb, fresh=True)
+    e1.record()
+    pl.barrier()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device=pl.dev)
+    if pl.dist:
+        pl.dist.all_reduce(t, op=pl.dist.ReduceOp.MAX)
+    ms = float(t.item())
+    g_ms, g_n, g_ops = pl.span.profile_read(5)
+    a_ms, _, _ = pl.span.profile_read(pl.span.PROF_ATTN)
+    pl.span.profile(False)
+    tokens = rows * 512
+    useful = 2.0 * tokens * cfg.n_layers * 12 * cfg.hidden * cfg.hidden
+    return {"rows": rows, "tokens_per_row": 512, "ms": ms, "tokens_per_s": tokens / (ms / 1e3),
+            "useful_tflops_per_gpu": useful / pl.world / (ms / 1e3) / 1e12,
+            "tcgen05_gemm": {"launches": g_n, "ms": g_ms,
+                             "useful_tflops": g_ops / 3.0 / max(g_ms, 1e-9) / 1e9 if g_n else None},
+            "tcgen05_share": g_ms / ms, "attention_share": a_ms / ms,
+            "peak_tflops_dense_bf16_measured": measured_tflops(),
+            "note": "C5 rows of 512 tokens through all 70 blocks, one 512-token job per row, rows pipelined over "
+                    "the spans; useful flops = 2*tokens*12h^2 per block (matmuls only); the event-profiled "
+                    "pass that gives the tcgen05/attention shares is the timed one"}
+
+
+def e2e_record(pl, args, cfg, T0):
+    """The headline metric through the server's public API: S client threads
+    each open a session, prefill T0 tokens with one int8 STEP frame, then send
+    W + K one-token STEP frames (int8 TensorMsg built on the host) and read the
+    replies. N=1: ServerNode on the resident span; N>1: the box front end (one
+    ServerEntry [0, 70), rank 0 accepts TCP, the hops stay on the GPUs)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2209_01188_b200.box import BoxFrontEnd, BoxPlan, RankState, payload_bytes, serve_rank, FMT_F32
+    from paper_2209_01188_b200.client import SpanClient
+    from paper_2209_01188_b200.server import ServerConfig, ServerNode
+    from paper_2209_01188_b200 import codec
+
+    N, S, K, W = pl.world, pl.S, args.steps, args.warmup
+    pl.set_batch(1)
+    for grp in pl.seqs:
+        for s in grp:
+            pl.span.release(s)
+    scfg = ServerConfig(seed=args.seed, model=cfg, blocks=(0, cfg.n_layers), quantize="both", capacity=max(S, 4),
+                        cache_budget_tokens=cfg.n_layers * (args.ctx + 64) * (S + 1), max_batch_tokens=pl.chunk,
+                        measure_steps=3, page_tokens=64, device=pl.local)
+    node = None
+    if N == 1:
+        node = ServerNode(scfg, span=pl.span).start()
+    else:
+        gloo = dist.new_group(backend="gloo")
+        plan = BoxPlan(scfg, N)
+        from paper_2209_01188_b200.pipeline import P2PRing
+
+        ring = P2PRing(pl.rank, N, plan.in_flight, payload_bytes(pl.chunk, cfg.hidden, FMT_F32), pl.local, dist)
+        state = RankState(plan, pl.rank, pl.span, ring, dist, group=gloo, owns_span=False)
+        if pl.rank > 0:
+            serve_rank(plan, pl.rank, dist, state=state)
+            return None
+        node = BoxFrontEnd(scfg, N, dist, state=state).start()
+    rng = np.random.default_rng(11)
+    d = cfg.hidden
+    prefill_msg = codec.encode_tensor(rng.standard_normal((T0, d)).astype(np.float32) * 0.05, codec.ENC_INT8)
+    step_msgs = [codec.encode_tensor(rng.standard_normal((1, d)).astype(np.float32) * 0.05, codec.ENC_INT8)
+                 for _ in range(8)]
+    ready, go = threading.Barrier(S + 1), threading.Event()
+    times, errors = [0.0] * S, []
+
+    def client(i):
+        c = SpanClient(node.address, codec.ENC_INT8, timeout_ms=600_000)
+        try:
+            sid = c.open_session(args.ctx)
+            c.step_raw(sid, 0, prefill_msg)
+            pos = T0
+            for k in range(W):
+                c.step_raw(sid, pos, step_msgs[k % 8])
+                pos += 1
+            ready.wait()
+            go.wait()
+            t0 = time.perf_counter()
+            for k in range(K):
+                reply = c.step_raw(sid, pos, step_msgs[k % 8])
+                codec.parse_tensor(reply)  # the host reads the int8 reply (codes + scales)
+                pos += 1
+            times[i] = time.perf_counter() - t0
+            c.close_session(sid)
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+            try:
+                ready.abort()
+            except Exception:  # noqa: BLE001
+                pass
+        finally:
+            c.close()
+
+    ts = [threading.Thread(target=client, args=(i,)) for i in range(S)]
+    for t in ts:
+        t.start()
+    try:
+        ready.wait(timeout=900)
+    except threading.BrokenBarrierError:
+        pass
+    t_start = time.perf_counter()
+    go.set()
+    for t in ts:
+        t.join()
+    wall = time.perf_counter() - t_start
+    node.stop()
+    if errors:
+        return {"error": errors[0]}
+    step_bytes = len(step_msgs[0])
+    return {"value": K * S / wall, "unit": UNIT, "h2d_bytes_per_step": step_bytes, "d2h_bytes_per_step": step_bytes,
+            "wall_s": wall, "sessions": S, "ctx_end": T0 + W + K,
+            "path": ("TCP STEP frames (int8 TensorMsg) -> " + ("ServerNode" if N == 1 else
+                     f"box front end over {N} GPUs (one ServerEntry [0, 70), peer-memory hops)") +
+                     " -> reply frames read by the client threads; prefill via one int8 STEP per session, untimed")}
+
+
+# ------------------------------------------------------------------ main
 
 
 def run_ours(args):
@@ -383,131 +669,51 @@ def run_ours(args):
     label = model_label(args.shape)
     metric, unit = ((METRIC.format(model=label), UNIT) if args.batch == 1
                     else (METRIC_B.format(model=label, b=args.batch), "tokens/s"))
+    rank0 = int(os.environ.get("RANK", "0")) == 0
+    c2 = None
+    if not args.no_c2 and rank0 and args.shape == "bloom-176b":
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        c2 = c2_record(args)  # before the 176B span: HBM is nearly full with it
+        torch.cuda.empty_cache()
     pl = Pipeline(args, cfg)
     S, N, rank, B = pl.S, pl.world, pl.rank, pl.B
     K, W = args.steps, args.warmup
-    T0 = args.ctx - (W + 2 * K) - (0 if args.no_e2e else K) - 1
+    T0 = args.ctx - (W + 2 * K) - 1
     if T0 < 1:
         raise SystemExit("--ctx too small for warmup+steps")
-    # ---- prefill every session to T0 through the pipeline (untimed)
+    # ---- prefill every session to T0 through the pipeline (untimed; tcgen05 GEMM device time recorded)
     t_pf = time.perf_counter()
-    pl.span.profile(True)  # prefill runs the tcgen05 GEMM: record its live device time
+    pl.span.profile(True)
     if args.synthetic_kv:
         for grp in pl.seqs:
             for s in grp:
-                pl.span._reserve(s, T0)
+                pl.span.reserve(s, T0)
                 s.length = T0
     else:
-        chunks = []
-        left = T0
-        while left > 0:
-            c = min(pl.chunk, left)
-            chunks.append(c)
-            left -= c
-        # job order: for each chunk round, every session (keeps the ring pattern)
-        jobs = [(ci * S + m, c) for ci, c in enumerate(chunks) for m in range(S)]
-        pl.total_jobs = len(jobs) + S * (W + 2 * K + (0 if args.no_e2e else K))
-        # all prefill jobs, then decode jobs continue numbering
-        pl.run(jobs, x_for=lambda j, n: pl.inputs[:n] if n <= 64 else torch.randn(n, cfg.hidden, device=pl.dev) * 0.05)
-        jbase = len(jobs)
+        pl.prefill(T0)
     torch.cuda.synchronize()
     pf_s = time.perf_counter() - t_pf
     tc_ms, tc_n, tc_flop = pl.span.profile_read(5)
     pl.span.profile(False)
-    if args.synthetic_kv:
-        jbase = 0
-        pl.total_jobs = S * (W + 2 * K + (0 if args.no_e2e else K))
-    # ---- warmup decode
-    pl.run([(jbase + i, 1) for i in range(W * S)])
-    jbase += W * S
-    # ---- timed decode (device-resident inputs)
-    pl.barrier()
-    pl.launches = 0
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(pl.local) as clk:
-        start.record()
-        pl.run([(jbase + i, 1) for i in range(K * S)])
-        stop.record()
-        pl.barrier()
-    jbase += K * S
-    ms = start.elapsed_time(stop)
-    if pl.jobtimes is not None:
-        ev = pl.jobtimes[-2 * K * S:]
-        busy = [ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(K * S)]
-        gaps = [ev[2 * i - 1].elapsed_time(ev[2 * i]) for i in range(1, K * S)]
-        print(f"[rank {rank}] job busy ms mean {statistics.mean(busy):.3f} max {max(busy):.3f} | "
-              f"gap ms mean {statistics.mean(gaps):.3f} max {max(gaps):.3f}", file=sys.stderr, flush=True)
-        pl.jobtimes = None
-    launches = pl.launches
+    # ---- warmup + timed decode (device-resident inputs)
+    pl.phase([1] * W)
+    ms_max, launches, clocks = pl.timed([1] * K)
     # ---- live per-kernel device times (CUDA events around every launch on the
-    # launching stream) over a second, identical pass of K steps; kept out of
-    # the value's timed region so the events do not perturb it
+    # launching stream) over a second, identical pass of K steps, outside the
+    # value's timed region so the events do not perturb it
     pl.span.profile(True)
-    pl.run([(jbase + i, 1) for i in range(K * S)])
+    pl.phase([1] * K)
     pl.barrier()
-    jbase += K * S
     gemv = pl.span.profile_read(pl.span.PROF_GEMV)
     attn = pl.span.profile_read(pl.span.PROF_ATTN)
     pro = pl.span.profile_read(pl.span.PROF_PROLOGUE)
     codec_p = pl.span.profile_read(pl.span.PROF_CODEC)
     pl.span.profile(False)
-    t = torch.tensor([ms], device=pl.dev)
-    if pl.dist:
-        pl.dist.all_reduce(t, op=pl.dist.ReduceOp.MAX)
-    ms_max = float(t.item())
     value = K * S * B / (ms_max / 1e3)  # session-steps (= tokens) per second over all GPUs
-    # ---- e2e: host bytes in/out
-    e2e = None
-    if not args.no_e2e:
-        d = cfg.hidden
-        host_in = torch.randn(B, d).mul_(0.05).pin_memory()
-        host_out = torch.empty(B * d, dtype=torch.int8).pin_memory()
-        pl.barrier()
-        t0 = time.perf_counter()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        pl.run([(jbase + i, 1) for i in range(K * S)], host_in=host_in if rank == 0 else None,
-               host_out=host_out if rank == N - 1 else None, sync_out=True)
-        e1.record()
-        pl.barrier()
-        wall = time.perf_counter() - t0
-        te = torch.tensor([max(e0.elapsed_time(e1), wall * 1e3)], device=pl.dev)
-        if pl.dist:
-            pl.dist.all_reduce(te, op=pl.dist.ReduceOp.MAX)
-        e2e = {"value": K * S * B / (float(te.item()) / 1e3), "unit": unit, "h2d_bytes_per_step": 4 * d * B,
-               "d2h_bytes_per_step": d * B, "path": "pb_span_step_int8 C-ABI with pinned host ingress (span 0) and "
-               "egress of the int8 hidden (last span), " + ("NVLink peer-memory" if pl.ring is not None else "NCCL") + " int8 hops between spans"}
-    # ---- FORWARD sample (C5 shape: rows of 512 tokens through this rank's span, tcgen05 path;
-    # server.py:411-429 semantics, no tape), timed with CUDA events; each rank its own span
-    fwd = None
-    if args.forward_rows > 0:
-        for grp in pl.seqs:  # decode sessions are done: their KV pages host the FORWARD rows
-            for sq in grp:
-                pl.span.release(sq)
-        rows, t = args.forward_rows, 512
-        xb = torch.randn(rows, t, cfg.hidden, device=pl.dev) * 0.05
-        pl.span.forward(xb)  # warm-up
-        torch.cuda.synchronize()
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record()
-        pl.span.forward(xb)
-        f1.record()
-        torch.cuda.synchronize()
-        f_ms = f0.elapsed_time(f1)
-        pl.span.profile(True)  # separate pass: per-kernel shares
-        pl.span.forward(xb)
-        torch.cuda.synchronize()
-        g_ms, g_n, g_ops = pl.span.profile_read(5)
-        a_ms, _, _ = pl.span.profile_read(pl.span.PROF_ATTN)
-        pl.span.profile(False)
-        s0, s1 = pl.ranges[rank]
-        useful = 2.0 * rows * t * (s1 - s0) * 12 * cfg.hidden * cfg.hidden
-        fwd = {"rows": rows, "tokens_per_row": t, "blocks": s1 - s0, "ms": f_ms,
-               "tokens_per_s": rows * t / (f_ms / 1e3), "useful_tflops": useful / (f_ms / 1e3) / 1e12,
-               "tcgen05_share": g_ms / f_ms, "attention_share": a_ms / f_ms,
-               "note": "FORWARD of rows x 512 tokens through this GPU's span (C5 row shape); useful flops = "
-                       "2*tokens*12h^2 per block (matmuls only; profile pass for the shares)"}
-    # ---- report (rank 0)
+    # ---- sub-records
+    e2e = None if args.no_e2e else e2e_record(pl, args, cfg, T0)
+    b32 = None if args.no_b32 else b32_record(pl, args, cfg)
+    fwd = forward_record(pl, args, cfg) if args.forward_rows > 0 else None
     if rank != 0:
         if pl.dist:
             pl.dist.barrier()
@@ -518,8 +724,8 @@ def run_ours(args):
     achieved = (g_b / g_n) / ((g_ms / g_n) / 1e3) / 1e9 if g_n else 0.0
     traffic = committed_traffic()
     w_bytes, kv_bytes = bytes_per_step(cfg, [args.ctx - K // 2] * (S * B))
-    step_s = (ms_max / 1e3) / (K * S)  # one micro-batch step through all blocks
-    seq_ceiling = (w_bytes + kv_bytes / S) / (peak * 1e9)  # one micro-batch through all blocks, one GPU busy
+    step_s = (ms_max / 1e3) / (K * S)
+    seq_ceiling = (w_bytes + kv_bytes / S) / (peak * 1e9)
     agg_ceiling = (w_bytes / N + kv_bytes / N / S) / (peak * 1e9)
     line = {
         "metric": metric, "value": value, "unit": unit, "n_gpus": N, "steps": K, "warmup": W,
@@ -531,23 +737,22 @@ def run_ours(args):
                                f"context {T0}->{args.ctx}",
                    "sessions": S * B, "batch_per_microbatch": B, "ctx_end": args.ctx, "prefill_tokens": T0,
                    "l2": "weights stream 172.7 GB per step >> 126 MB L2 (no flush needed)",
-                   "parallelism": f"pipeline{N} (block spans)"},
+                   "parallelism": f"pipeline{N} (block spans)", "hop": "p2p" if pl.ring is not None else "nccl"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None,
                      "traffic": traffic.get("gemv_i8_bytes_per_launch") if traffic else None,
                      "kernel": "k_gemv_i8 (int8 GEMV, all 4 matrices of every block)",
                      "launches": g_n, "avg_launch_us": 1e3 * g_ms / max(g_n, 1),
                      "algorithmic_bytes_per_launch": g_b / max(g_n, 1), "peak_source": peak_kind},
-        # sequential: one session's step latency (each session stepped K times in the timed
-        # region) vs all of its bytes through one GPU; aggregate: job throughput vs every GPU
-        # streaming its own span's bytes for every micro-batch step
         "step_roofline": {"bytes_per_step": w_bytes + kv_bytes / S, "sequential_frac": seq_ceiling / (ms_max / 1e3 / K),
                           "aggregate_frac": agg_ceiling / step_s,
                           "kernel_share": {"gemv": g_ms / ms_max, "attention": attn[0] / ms_max,
                                            "prologue": pro[0] / ms_max, "codec": codec_p[0] / ms_max}},
         "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "clocks": clocks,
         "e2e": e2e,
+        "b32": b32,
+        "c2": c2,
         "setup_s": {"weights_gen_quant": pl.gen_s, "prefill": pf_s},
         "prefill": {"tokens": T0 * S * B, "wall_s": pf_s, "tokens_per_s_wall": T0 * S * B / max(pf_s, 1e-9),
                     "tcgen05_gemm": {"launches": tc_n, "ms": tc_ms,
@@ -561,14 +766,16 @@ def run_ours(args):
         "device_bytes": pl.span.device_bytes,
     }
     if not args.no_cpu_baseline and N == 1:
-        sample, ncores = cpu_block_sample(cfg, 128)
+        sample, ncores = cpu_block_sample(cfg, args.ctx)
         sample.step_seconds()
-        ts = [sample.step_seconds() for _ in range(2)]
-        per_block = min(ts)
+        all_t = cpu_step_seconds(sample, 2)
+        one_t = cpu_step_seconds(sample, 1, threads=1)
         line["cpu_baseline"] = {
-            "value": 1.0 / (per_block * cfg.n_layers), "unit": unit, "cores": ncores, "kind": "port",
-            "sample": f"oracle port of block_forward(qw) for 1 {args.shape} block, decode t=1 at context 128, "
-                      f"best of 2, extrapolated x{cfg.n_layers} blocks"}
+            "value": 1.0 / (all_t * cfg.n_layers), "unit": unit, "cores": ncores, "kind": "port",
+            "sample": f"oracle port of block_forward(qw) (f32 KV concat, dequantized-matrix matmuls) for 1 "
+                      f"{args.shape} block, decode t=1 at context {args.ctx}, best of 2, extrapolated x{cfg.n_layers}",
+            "one_thread": {"value": 1.0 / (one_t * cfg.n_layers), "block_s": one_t},
+            "all_threads_block_s": all_t, **cpu_info()}
     print(json.dumps(line), flush=True)
     if pl.dist:
         pl.dist.barrier()

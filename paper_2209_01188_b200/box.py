@@ -105,9 +105,14 @@ class RankState:
     """One rank's sub-span, its mailbox ring and its session / tape tables.
     `apply` executes a descriptor (ranks 1..N-1 and, through BoxScheduler, rank 0)."""
 
-    def __init__(self, plan: BoxPlan, rank: int, span: BlockSpan, ring: P2PRing, dist):
+    def __init__(self, plan: BoxPlan, rank: int, span: BlockSpan, ring: P2PRing, dist, group=None,
+                 owns_span: bool = True):
+        """dist: torch.distributed; group: the (gloo) process group of the
+        control plane, None for the default group; owns_span: close the
+        sub-span on shutdown (False when the caller keeps using it)."""
         self.plan, self.rank, self.world = plan, rank, plan.world
-        self.span, self.ring, self.dist = span, ring, dist
+        self.span, self.ring, self.dist, self.group = span, ring, dist, group
+        self.owns_span = owns_span
         self.d = span.config.hidden
         self.seqs: dict[int, Sequence] = {}
         self.fwd: dict[tuple, Sequence] = {}
@@ -120,7 +125,8 @@ class RankState:
 
     def close(self) -> None:
         self.ring.close()
-        self.span.close()
+        if self.owns_span:
+            self.span.close()
 
     def seq(self, slot: int) -> Sequence:
         s = self.seqs.get(slot)
@@ -249,10 +255,10 @@ class RankState:
         tape = self.tapes.pop(key)
         src = 0 if self.rank == self.world - 1 else self.rank + 1
         g = torch.empty(B, t, self.d)
-        self.dist.recv(g, src=src)
+        self.dist.recv(g, src=src, group=self.group)
         gin = self.span.backward(tape, g.to(self.span.device))
         if self.rank > 0:
-            self.dist.send(gin.cpu(), dst=self.rank - 1)
+            self.dist.send(gin.cpu(), dst=self.rank - 1, group=self.group)
             return None
         return gin
 
@@ -266,7 +272,7 @@ def serve_rank(plan: BoxPlan, rank: int, dist, state=None) -> None:
     buf = torch.empty(desc_len(plan.max_seqs), dtype=torch.int64)
     try:
         while True:
-            dist.recv(buf, src=0)
+            dist.recv(buf, src=0, group=state.group)
             if int(buf[0]) == OP_STOP:
                 break
             state.apply(buf.clone())
@@ -377,7 +383,7 @@ class BoxScheduler:
         import torch.distributed as dist
 
         for r in range(1, self.plan.world):
-            self._pending_sends.append(dist.isend(desc, dst=r))
+            self._pending_sends.append(dist.isend(desc, dst=r, group=self.state.group))
         if len(self._pending_sends) > 256:
             for w in self._pending_sends:
                 w.wait()
@@ -447,7 +453,7 @@ class BoxScheduler:
                     self._flush_sends()
                     import torch.distributed as dist
 
-                    dist.send(grad.detach().cpu().contiguous(), dst=self.plan.world - 1)
+                    dist.send(grad.detach().cpu().contiguous(), dst=self.plan.world - 1, group=self.state.group)
                     ev.out = self.state.apply(desc)
             except Exception as e:  # noqa: BLE001
                 ev.err = e
@@ -627,11 +633,13 @@ class BoxFrontEnd(ServerNode):
     """Rank 0 of the box: the reference ServerNode protocol (sessions, STEP
     semantics, budget, FORWARD/BACKWARD, announcements) over a BoxSpan."""
 
-    def __init__(self, config: ServerConfig, world: int, dist):
-        if config.seed is None and not config.checkpoint_path:
+    def __init__(self, config: ServerConfig, world: int, dist, state: RankState | None = None):
+        """state: rank 0's prebuilt RankState (sub-span + ring + control group),
+        e.g. the bench reusing its resident spans; None builds it."""
+        if state is None and config.seed is None and not config.checkpoint_path:
             raise InputError("the box front end loads weights per GPU: give a seed or a checkpoint path")
         super().__init__(config)
-        self.world, self.dist = world, dist
+        self.world, self.dist, self._state = world, dist, state
 
     def _pick_range(self):
         r = super()._pick_range()
@@ -642,7 +650,7 @@ class BoxFrontEnd(ServerNode):
         import hashlib
 
         plan = BoxPlan(self.config, self.world)
-        state = _build_rank(plan, 0, self.dist)
+        state = self._state or _build_rank(plan, 0, self.dist)
         h = hashlib.sha256(f"box:{self.config.seed}:{self.model}:{self.range}:{self.config.checkpoint_path}".encode())
         self._weights_hash = h.hexdigest()
         return BoxSpan(plan, state, self.range.start, self.range.end)

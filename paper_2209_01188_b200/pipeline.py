@@ -19,8 +19,12 @@ from __future__ import annotations
 
 
 class RingSchedule:
-    def __init__(self, rank: int, world: int, sessions: int, total_jobs: int):
+    """Jobs first .. total_jobs-1 (job ids keep increasing across phases: the
+    peer-memory flags are monotonic)."""
+
+    def __init__(self, rank: int, world: int, sessions: int, total_jobs: int, first: int = 0):
         self.rank, self.world, self.sessions, self.total_jobs = rank, world, sessions, total_jobs
+        self.first = first
 
     def recv_from(self, j: int):
         """Peer to receive job j's hidden from, or None (span 0 starting a session)."""
@@ -28,7 +32,7 @@ class RingSchedule:
             return None
         if self.rank > 0:
             return self.rank - 1
-        return self.world - 1 if j >= self.sessions else None
+        return self.world - 1 if j >= self.first + self.sessions else None
 
     def send_to(self, j: int):
         """Peer to send job j's output to, or None (session finished / single span)."""

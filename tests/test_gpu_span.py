@@ -204,7 +204,8 @@ def test_capacity_errors():
 
 def test_c2_bloom560m_tokens_bit_exact(golden):
     """Config 2: BLOOM-560M shape, int8 weights generated on device, 128-token
-    prefix, greedy tokens equal the reference's qw-mode generation."""
+    prefix then 39 decode steps (40 greedy tokens), equal to the reference's
+    qw-mode generation (tests/golden/c2.npz)."""
     import torch
 
     from paper_2209_01188_b200 import codec

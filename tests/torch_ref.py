@@ -40,14 +40,18 @@ class RefBlock:
         self.H = span.config.n_heads
         self.d = span.config.hidden
 
-    def step(self, x, kv, start):
-        """x [t, d] f64; kv = [k [T, H, dh], v] f64 lists (mutated)."""
+    def step(self, x, kv, start, kv_fp16=False):
+        """x [t, d] f64; kv = [k [T, H, dh], v] f64 lists (mutated). kv_fp16:
+        round the cached K/V to fp16 as the span's paged cache stores them
+        (isolates the kernels' arithmetic from the storage format)."""
         t, d = x.shape
         H, dh = self.H, d // self.H
         qkv = layer_norm(x) @ self.w[0]
         q = qkv[:, :d].reshape(t, H, dh)
         kn = qkv[:, d:2 * d].reshape(t, H, dh)
         vn = qkv[:, 2 * d:].reshape(t, H, dh)
+        if kv_fp16:
+            kn, vn = kn.half().double(), vn.half().double()
         kv[0] = torch.cat([kv[0], kn]) if kv[0] is not None else kn
         kv[1] = torch.cat([kv[1], vn]) if kv[1] is not None else vn
         K, V = kv
