@@ -115,6 +115,9 @@ def _worker(rank, port, q):
         sch.call("release", seqs[1])
         sch.run(seqs[2], torch.zeros(3, D))
         sch.stop()
+        # plain Python / numpy only: tensors would travel as shared-memory handles
+        # that vanish when this process exits before the parent reads them
+        results = {k: (v.numpy() if torch.is_tensor(v) else [r.numpy() for r in v]) for k, v in results.items()}
         q.put(("rank0", (st.log, results, sch.batches, sch.batched_steps, span.pool.free_pages)))
     dist.destroy_process_group()
 
@@ -147,7 +150,7 @@ def test_box_control_plane_mirrors_rank0():
     assert all(f1 >= f0 for (*_, f0), (*_, f1) in zip(log0, log1))
     # the long prompt ran as causal chunks 4 + 4 + 1 on sequence 0
     assert [(L, t) for _, L, t, _ in log0[:3]] == [([0], [4]), ([4], [4]), ([8], [1])]
-    assert torch.equal(results["long"], torch.arange(9 * D, dtype=torch.float32).view(9, D) + 1)
+    assert (results["long"] == torch.arange(9 * D, dtype=torch.float32).view(9, D).numpy() + 1).all()
     for i in range(3):
         assert [float(r[0, 0]) for r in results[i]] == [i * 10 + k + 1.0 for k in range(5)]
     # concurrent decode steps of distinct sessions were coalesced into shared jobs
