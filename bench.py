@@ -601,7 +601,11 @@ def e2e_record(pl, args, cfg, T0):
         node = BoxFrontEnd(scfg, N, dist, state=state).start()
     rng = np.random.default_rng(11)
     d = cfg.hidden
-    prefill_msg = codec.encode_tensor(rng.standard_normal((T0, d)).astype(np.float32) * 0.05, codec.ENC_INT8)
+    # a TensorMsg is capped at 64 MiB counted as f32 (transport/wire.py:93-94, even for int8), i.e. 1170
+    # tokens at h=14336: the client sends a long prompt as consecutive STEPs
+    per_frame = max(1, (64 * 1024 * 1024) // (4 * d) - 1)
+    prefill_msgs = [codec.encode_tensor(rng.standard_normal((min(per_frame, T0 - p), d)).astype(np.float32) * 0.05,
+                                        codec.ENC_INT8) for p in range(0, T0, per_frame)]
     step_msgs = [codec.encode_tensor(rng.standard_normal((1, d)).astype(np.float32) * 0.05, codec.ENC_INT8)
                  for _ in range(8)]
     ready, go = threading.Barrier(S + 1), threading.Event()
@@ -611,8 +615,10 @@ def e2e_record(pl, args, cfg, T0):
         c = SpanClient(node.address, codec.ENC_INT8, timeout_ms=600_000)
         try:
             sid = c.open_session(args.ctx)
-            c.step_raw(sid, 0, prefill_msg)
-            pos = T0
+            pos = 0
+            for msg in prefill_msgs:
+                c.step_raw(sid, pos, msg)
+                pos += min(per_frame, T0 - pos)
             for k in range(W):
                 c.step_raw(sid, pos, step_msgs[k % 8])
                 pos += 1
@@ -654,7 +660,7 @@ def e2e_record(pl, args, cfg, T0):
             "wall_s": wall, "sessions": S, "ctx_end": T0 + W + K,
             "path": ("TCP STEP frames (int8 TensorMsg) -> " + ("ServerNode" if N == 1 else
                      f"box front end over {N} GPUs (one ServerEntry [0, 70), peer-memory hops)") +
-                     " -> reply frames read by the client threads; prefill via one int8 STEP per session, untimed")}
+                     " -> reply frames read by the client threads; prefill via int8 STEPs of <= 1169 tokens per session, untimed")}
 
 
 # ------------------------------------------------------------------ main
@@ -737,7 +743,8 @@ def run_ours(args):
                                f"context {T0}->{args.ctx}",
                    "sessions": S * B, "batch_per_microbatch": B, "ctx_end": args.ctx, "prefill_tokens": T0,
                    "l2": "weights stream 172.7 GB per step >> 126 MB L2 (no flush needed)",
-                   "parallelism": f"pipeline{N} (block spans)", "hop": "p2p" if pl.ring is not None else "nccl"},
+                   "parallelism": f"pipeline{N} (block spans)",
+                   "hop": "none" if N == 1 else ("p2p" if pl.ring is not None else "nccl")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None,
                      "traffic": traffic.get("gemv_i8_bytes_per_launch") if traffic else None,
