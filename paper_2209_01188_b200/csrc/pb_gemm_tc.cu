@@ -30,6 +30,15 @@
 //               release the accumulator set.
 // Canonical K-major (SWIZZLE_NONE) operand layout: 8-row x 16-byte core
 // matrices, LBO = 128 B (k direction), SBO = 256 B (8-row groups).
+//
+// k_gemm_tc_sk<BN>: the same MMA for batched decode (BN = 16 or 32 tokens: one
+// token tile, N = 3 BN = 48 / 96 digit columns instead of padding to 80
+// tokens), memory-bound on the weight stream. Stream-K over (row group, k
+// tile) units so all 148 SMs stream equal byte counts whatever the row-group
+// count (wo / wmlp_out of 176B have 112 row groups); a row group split across
+// CTAs leaves s32 digit partials, and the last contributor (per 32-row TMEM
+// lane quarter, atomic counter) adds them -- exact integers, so the merge order
+// does not matter -- and runs the fused epilogue.
 #include <algorithm>
 #include <cstdint>
 
@@ -63,36 +72,23 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
 // and one MMA per k tile reads the weight tile from shared memory once.
 constexpr uint32_t TC_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)((3 * TC_BN) >> 3) << 17) |
                               ((uint32_t)(TC_BM >> 4) << 24);
+static_assert(TC_IDESC == ((2u << 4) | (1u << 7) | (1u << 10) | (30u << 17) | (8u << 24)), "idesc");
 
+constexpr uint32_t tc_idesc_i8(int n) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+}
+
+template <uint32_t IDESC>
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(TC_IDESC), "r"(accumulate));
+        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
 }
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
-}
-// arrive on the same-offset mbarrier of every CTA in the (2-CTA) cluster
-__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-            smem_u32(bar)),
-        "h"((uint16_t)3)
-        : "memory");
-}
-// global -> shared of both CTAs of the pair (same offset), complete_tx on each CTA's mbarrier at bar's offset
-__device__ __forceinline__ void bulk_g2s_pair(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
-        "%4;" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"((uint16_t)3)
-        : "memory");
-}
-__device__ __forceinline__ void cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -114,18 +110,11 @@ struct TcArgs {
     const uint8_t* bcanon;  // [token tiles][KC][3][TC_PLANE]
     int KC, MG, NTL;        // k tiles, row groups, token tiles
     int tiles;              // MG * NTL
-    int l2pf;               // L2 prefetch distance in k tiles (0: off)
     int ntg;                // token tiles per pass (NTL: one pass)
     Act act;
     Epi epi;
 };
 
-// PAIR: CTAs 2p and 2p + 1 form a cluster on row groups 2 mg' and 2 mg' + 1
-// of the same token tile; each loads its own weight k tiles and HALF of the
-// shared digit planes, multicast into both CTAs' shared memory, so a CTA pulls
-// 4 + 3.75 KB per k tile through L2 instead of 4 + 7.5 KB. A stage is free
-// again once both CTAs' MMAs have read it (empty barrier count 2, commits
-// multicast to the pair).
 // Unit u -> (row group, token tile). Units run in passes over ntg token tiles:
 // within a pass the token tiles of one row group are neighbours (they share
 // the weight k tiles in L2), and the pass's digit planes (ntg x KC x 7.5 KB)
@@ -139,8 +128,7 @@ __device__ __forceinline__ void tc_unit(const TcArgs& a, int u, int mgs, int& mg
     nt = g * a.ntg + (r - mgu * n_here);
 }
 
-template <bool PAIR>
-__device__ __forceinline__ void gemm_tc_body(const TcArgs& a) {
+__global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sa = smem;                                // [STAGES][KT][4 KB]
     uint8_t* sb = sa + TC_STAGES * TC_KT * TC_A;       // [STAGES][KT][3 planes]
@@ -152,17 +140,14 @@ __device__ __forceinline__ void gemm_tc_body(const TcArgs& a) {
 
     const int warp = warp_uniform_id(), lane = threadIdx.x & 31;
     const int KC = a.KC;
-    // tile schedule: unit u = cta, cta + NU, ...; PAIR units are (row-group pair, token tile)
-    const int rank = PAIR ? (int)(blockIdx.x & 1) : 0;
-    const int cta = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-    const int NU = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-    const int units = PAIR ? a.tiles / 2 : a.tiles;
-    const int mgs = PAIR ? a.MG / 2 : a.MG;
+    // tile schedule: unit u = cta, cta + NU, ...
+    const int cta = (int)blockIdx.x, NU = (int)gridDim.x;
+    const int units = a.tiles, mgs = a.MG;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < TC_STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], PAIR ? 2 : 1);  // MMA commit (both CTAs' when PAIR)
+            mbar_init(&empty[s], 1);  // MMA commit
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&accfull[b], 1);   // MMA commit after a tile's last k step
@@ -176,10 +161,7 @@ __device__ __forceinline__ void gemm_tc_body(const TcArgs& a) {
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
-    if (PAIR)
-        cluster_sync();  // the peer's barriers are initialised before any multicast reaches them
-    else
-        __syncthreads();
+    __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -190,35 +172,16 @@ __device__ __forceinline__ void gemm_tc_body(const TcArgs& a) {
             for (int u = cta; u < units; u += NU) {
                 int mgu, nt;
                 tc_unit(a, u, mgs, mgu, nt);
-                const int mg = PAIR ? 2 * mgu + rank : mgu;
+                const int mg = mgu;
                 const int8_t* asrc = a.codes + (int64_t)mg * KC * TC_A;
                 const uint8_t* bsrc = a.bcanon + (int64_t)nt * KC * TC_B;
                 for (int kc = 0; kc < KC; kc += TC_KT, ++it) {
                     const int s = it % TC_STAGES, n = min(TC_KT, KC - kc);
-                    if (a.l2pf) {
-                        // pull k tiles l2pf ahead of the ring into L2: the ring (4 stages, ~1 us of MMA) is
-                        // shorter than an HBM miss under load
-                        const int kp = kc + a.l2pf;
-                        if (kp < KC) {
-                            const int np = min(TC_KT, KC - kp);
-                            bulk_prefetch_l2(asrc + (int64_t)kp * TC_A, np * TC_A);
-                            if (PAIR)
-                                bulk_prefetch_l2(bsrc + (int64_t)kp * TC_B + rank * np * (TC_B / 2), np * (TC_B / 2));
-                            else
-                                bulk_prefetch_l2(bsrc + (int64_t)kp * TC_B, np * TC_B);
-                        }
-                    }
                     mbar_wait(&empty[s], ((it / TC_STAGES) & 1) ^ 1);
                     mbar_expect_tx(&full[s], n * (TC_A + TC_B));
                     // consecutive k tiles are contiguous in both operands: one copy each
                     bulk_g2s(sa + s * TC_KT * TC_A, asrc + (int64_t)kc * TC_A, n * TC_A, &full[s]);
-                    if (PAIR) {
-                        const uint32_t half = n * (TC_B / 2);  // n * 3840 B: 16-B multiple
-                        bulk_g2s_pair(sb + s * TC_KT * TC_B + rank * half, bsrc + (int64_t)kc * TC_B + rank * half,
-                                      half, &full[s]);
-                    } else {
-                        bulk_g2s(sb + s * TC_KT * TC_B, bsrc + (int64_t)kc * TC_B, n * TC_B, &full[s]);
-                    }
+                    bulk_g2s(sb + s * TC_KT * TC_B, bsrc + (int64_t)kc * TC_B, n * TC_B, &full[s]);
                 }
             }
         }
@@ -237,11 +200,8 @@ __device__ __forceinline__ void gemm_tc_body(const TcArgs& a) {
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sa + s * TC_KT * TC_A), b0 = smem_u32(sb + s * TC_KT * TC_B);
                     for (int k = 0; k < n; ++k)
-                        tc_mma(acc, umma_desc(a0 + k * TC_A), umma_desc(b0 + k * TC_B), (kc | k) != 0);
-                    if (PAIR)
-                        tc_commit_pair(&empty[s]);
-                    else
-                        tc_commit(&empty[s]);
+                        tc_mma<TC_IDESC>(acc, umma_desc(a0 + k * TC_A), umma_desc(b0 + k * TC_B), (kc | k) != 0);
+                    tc_commit(&empty[s]);
                 }
                 tc_commit(&accfull[b]);
             }
@@ -256,7 +216,7 @@ __device__ __forceinline__ void gemm_tc_body(const TcArgs& a) {
         for (int u = cta; u < units; u += NU, ++i) {
             int mgu, nt;
             tc_unit(a, u, mgs, mgu, nt);
-            const int mg = PAIR ? 2 * mgu + rank : mgu;
+            const int mg = mgu;
             const int b = i & 1;
             mbar_wait(&accfull[b], (i >> 1) & 1);
             tc_fence_after();
@@ -290,17 +250,12 @@ __device__ __forceinline__ void gemm_tc_body(const TcArgs& a) {
         }
     }
     tc_fence_before();
-    if (PAIR)
-        cluster_sync();  // no multicast copy or commit may still target an exited peer
-    else
-        __syncthreads();
+    __syncthreads();
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS));
     }
 }
-
-__global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) { gemm_tc_body<false>(a); }
 
 int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Epi& epi, cudaStream_t st) {
     static int ok[PB_MAX_DEVICES] = {};
@@ -311,7 +266,7 @@ int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Ep
         return launch_check("gemm_tc setup");
     const int sms = sm_count();
     if (sms < 0) return PB_ERR_GENERIC;
-    TcArgs a{m.codes, bcanon, m.Kp / 32, m.Mp / 128, (int)ceil_div(act.n_tok, TC_BN), 0, 0, 0, act, epi};
+    TcArgs a{m.codes, bcanon, m.Kp / 32, m.Mp / 128, (int)ceil_div(act.n_tok, TC_BN), 0, 0, act, epi};
     a.tiles = a.MG * a.NTL;
     // Token-tile passes chosen by an HBM-traffic model: a pass of ntg tiles reads every weight byte once
     // (its row group's token tiles run on neighbouring CTAs) and its digit planes once if they fit an L2
@@ -332,6 +287,271 @@ int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Ep
     const int grid = std::min(a.tiles, sms);  // persistent: one CTA per SM (TMEM 512 columns)
     k_gemm_tc<<<grid, TC_THREADS, TC_SMEM, st>>>(a);
     return launch_check("gemm_tc");
+}
+
+
+// ------------------------------------------------------------------ batched decode: stream-K, one token tile
+
+template <int BN>
+struct SkCfg {
+    static constexpr int N = 3 * BN;                         // digit columns (MMA N)
+    static constexpr int B_KT = N * 32;                      // digit-plane bytes per 32-wide k tile
+    static constexpr int KT = 8;                             // k tiles per stage (32 KB of weights)
+    static constexpr int STAGES = BN == 32 ? 3 : 4;
+    static constexpr int ACC = N <= 64 ? 64 : 128;           // TMEM columns per accumulator set
+    static constexpr uint32_t IDESC = tc_idesc_i8(N);
+    static constexpr size_t SMEM = (size_t)STAGES * KT * (TC_A + B_KT) + (2 * STAGES + 4) * 8 + 16;
+};
+
+struct TcSkArgs {
+    const int8_t* codes;
+    const uint8_t* bcanon;  // [KC][3][BN x 32 B] (k_canonwrite with tile width BN)
+    int KC, MG;
+    int64_t total;          // MG * KC units
+    int G;                  // CTAs
+    Act act;
+    Epi epi;
+    int* partials;          // [G][2 segments][128 rows][N] s32 (a CTA's first / last partial row group)
+    int* counters;          // [MG][4 lane quarters], zero between launches
+};
+
+__device__ __forceinline__ int64_t sk_u0(int64_t c, int64_t total, int G) { return c * total / G; }
+__device__ __forceinline__ int sk_owner_of(int64_t u, int64_t total, int G) { return (int)(((u + 1) * G - 1) / total); }
+
+template <int BN>
+__device__ __forceinline__ void sk_epilogue_row(const TcSkArgs& a, int o, int lane, const int* h, const int* m,
+                                                const int* l, int c0) {
+    const bool want_max = a.epi.tokmax != nullptr;
+#pragma unroll 4
+    for (int j = 0; j < 16; ++j) {
+        const int tok = c0 + j;
+        float mx = 0.f;
+        if (tok < a.act.n_tok && o < a.epi.M) {
+            const long long iv = (long long)h[j] * 65536 + (long long)m[j] * 256 + (long long)l[j];
+            const float y = epi_store(a.epi, tok, o, (float)iv * a.act.back[tok]);
+            if (want_max) mx = fabsf(y * a.epi.s_next[o]);
+        }
+        if (want_max) {
+            mx = warp_max(mx);
+            if (lane == 0 && tok < a.act.n_tok) atomicMax(reinterpret_cast<int*>(a.epi.tokmax) + tok, __float_as_int(mx));
+        }
+    }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
+    using C = SkCfg<BN>;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* sa = smem;                                // [STAGES][KT][4 KB]
+    uint8_t* sb = sa + C::STAGES * C::KT * TC_A;       // [STAGES][KT][N x 32 B]
+    uint64_t* full = reinterpret_cast<uint64_t*>(sb + C::STAGES * C::KT * C::B_KT);
+    uint64_t* empty = full + C::STAGES;
+    uint64_t* accfull = empty + C::STAGES;  // [2]
+    uint64_t* accempty = accfull + 2;       // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
+
+    const int warp = warp_uniform_id(), lane = threadIdx.x & 31;
+    const int KC = a.KC, c = (int)blockIdx.x;
+    const int64_t u0 = sk_u0(c, a.total, a.G), u1 = sk_u0(c + 1, a.total, a.G);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&accfull[b], 1);
+            mbar_init(&accempty[b], 4);
+        }
+        mbar_fence_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(2 * C::ACC));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- producer: weights never depend on earlier kernels, so the first
+        // STAGES stages of weights are requested before the PDL wait; their digit planes
+        // (written by the operand kernel) follow once it has completed
+        if (lane == 0) {
+            int it = 0, pend_kc[C::STAGES], pend_n[C::STAGES];
+            bool waited = false;
+            for (int64_t u = u0; u < u1;) {
+                const int mg = (int)(u / KC), ka = (int)(u % KC);
+                const int kb = u1 - u < (int64_t)(KC - ka) ? ka + (int)(u1 - u) : KC;
+                const int8_t* asrc = a.codes + (int64_t)mg * KC * TC_A;
+                for (int kc = ka; kc < kb; kc += C::KT, ++it) {
+                    const int s = it % C::STAGES, n = min(C::KT, kb - kc);
+                    mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+                    mbar_expect_tx(&full[s], n * (TC_A + C::B_KT));
+                    bulk_g2s(sa + s * C::KT * TC_A, asrc + (int64_t)kc * TC_A, n * TC_A, &full[s]);
+                    if (waited) {
+                        bulk_g2s(sb + s * C::KT * C::B_KT, a.bcanon + (int64_t)kc * C::B_KT, n * C::B_KT, &full[s]);
+                    } else {
+                        pend_kc[s] = kc;
+                        pend_n[s] = n;
+                        if (it + 1 == C::STAGES) {
+                            pdl_wait();
+                            pdl_trigger();
+                            waited = true;
+                            for (int i = 0; i <= it; ++i)
+                                bulk_g2s(sb + i * C::KT * C::B_KT, a.bcanon + (int64_t)pend_kc[i] * C::B_KT,
+                                         pend_n[i] * C::B_KT, &full[i]);
+                        }
+                    }
+                }
+                u += kb - ka;
+            }
+            if (!waited) {  // fewer stages than the ring holds
+                pdl_wait();
+                pdl_trigger();
+                for (int i = 0; i < it; ++i)
+                    bulk_g2s(sb + i * C::KT * C::B_KT, a.bcanon + (int64_t)pend_kc[i] * C::B_KT, pend_n[i] * C::B_KT,
+                             &full[i]);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer: segment i (one row group's k range) accumulates in set i & 1
+        if (lane == 0) {
+            int it = 0, i = 0;
+            for (int64_t u = u0; u < u1; ++i) {
+                const int ka = (int)(u % KC);
+                const int kb = u1 - u < (int64_t)(KC - ka) ? ka + (int)(u1 - u) : KC;
+                const int b = i & 1;
+                mbar_wait(&accempty[b], ((i >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t acc = tmem + b * C::ACC;
+                for (int kc = ka; kc < kb; kc += C::KT, ++it) {
+                    const int s = it % C::STAGES, n = min(C::KT, kb - kc);
+                    mbar_wait(&full[s], (it / C::STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sa + s * C::KT * TC_A), b0 = smem_u32(sb + s * C::KT * C::B_KT);
+                    for (int k = 0; k < n; ++k)
+                        tc_mma<C::IDESC>(acc, umma_desc(a0 + k * TC_A), umma_desc(b0 + k * C::B_KT),
+                                         (kc - ka) | k);
+                    tc_commit(&empty[s]);
+                }
+                tc_commit(&accfull[b]);
+                u += kb - ka;
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue (warps 2-5): TMEM lanes 32 (warp % 4) .. + 31 = rows of the group
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const int first_mg = (int)(u0 / KC);
+        int i = 0;
+        for (int64_t u = u0; u < u1; ++i) {
+            const int mg = (int)(u / KC), ka = (int)(u % KC);
+            const int kb = u1 - u < (int64_t)(KC - ka) ? ka + (int)(u1 - u) : KC;
+            u += kb - ka;
+            const int b = i & 1;
+            mbar_wait(&accfull[b], (i >> 1) & 1);
+            tc_fence_after();
+            const int o = mg * TC_BM + row;
+            const uint32_t tbase = tmem + b * C::ACC + ((uint32_t)(quarter * 32) << 16);
+            if (ka == 0 && kb == KC) {  // whole row group in this CTA
+                for (int c0 = 0; c0 < BN; c0 += 16) {
+                    int h[16], m[16], l[16];
+                    tmem_ld16(tbase + c0, h);
+                    tmem_ld16(tbase + BN + c0, m);
+                    tmem_ld16(tbase + 2 * BN + c0, l);
+                    sk_epilogue_row<BN>(a, o, lane, h, m, l, c0);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&accempty[b]);
+                continue;
+            }
+            // split row group: park this CTA's s32 digit sums, the last contributor merges
+            const int slot = mg == first_mg ? 0 : 1;
+            int* pw = a.partials + (((int64_t)c * 2 + slot) * TC_BM + row) * C::N;
+            for (int c0 = 0; c0 < C::N; c0 += 16) {
+                int v[16];
+                tmem_ld16(tbase + c0, v);
+#pragma unroll
+                for (int q = 0; q < 16; q += 4)
+                    __stcg(reinterpret_cast<int4*>(pw + c0 + q), make_int4(v[q], v[q + 1], v[q + 2], v[q + 3]));
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&accempty[b]);
+            __threadfence();
+            __syncwarp();
+            const int cf = sk_owner_of((int64_t)mg * KC, a.total, a.G);
+            const int cl = sk_owner_of((int64_t)mg * KC + KC - 1, a.total, a.G);
+            int last = 0;
+            if (lane == 0) last = atomicAdd(a.counters + mg * 4 + quarter, 1) == cl - cf;
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (!last) continue;
+            __threadfence();
+            if (lane == 0) a.counters[mg * 4 + quarter] = 0;  // ready for the next launch
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+                int h[16] = {}, m[16] = {}, l[16] = {};
+                for (int cc = cf; cc <= cl; ++cc) {
+                    const int sl = mg == (int)(sk_u0(cc, a.total, a.G) / KC) ? 0 : 1;
+                    const int* pr = a.partials + (((int64_t)cc * 2 + sl) * TC_BM + row) * C::N;
+#pragma unroll
+                    for (int q = 0; q < 16; q += 4) {
+                        const int4 x = __ldcg(reinterpret_cast<const int4*>(pr + c0 + q));
+                        const int4 y = __ldcg(reinterpret_cast<const int4*>(pr + BN + c0 + q));
+                        const int4 z = __ldcg(reinterpret_cast<const int4*>(pr + 2 * BN + c0 + q));
+                        h[q] += x.x, h[q + 1] += x.y, h[q + 2] += x.z, h[q + 3] += x.w;
+                        m[q] += y.x, m[q + 1] += y.y, m[q + 2] += y.z, m[q + 3] += y.w;
+                        l[q] += z.x, l[q + 1] += z.y, l[q + 2] += z.z, l[q + 3] += z.w;
+                    }
+                }
+                sk_epilogue_row<BN>(a, o, lane, h, m, l, c0);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * C::ACC));
+    }
+}
+
+template <int BN>
+static int launch_sk(const Mat& m, const uint8_t* bcanon, const Act& act, const Epi& epi, int* partials,
+                     int64_t partial_bytes, int* counters, cudaStream_t st) {
+    using C = SkCfg<BN>;
+    static int ok[PB_MAX_DEVICES] = {};
+    if (per_device(ok, [](int) {
+            return cudaFuncSetAttribute(k_gemm_tc_sk<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)C::SMEM) == cudaSuccess ? 1 : -1;
+        }) < 0)
+        return launch_check("gemm_tc_sk setup");
+    const int sms = sm_count();
+    if (sms < 0) return PB_ERR_GENERIC;
+    TcSkArgs a{m.codes, bcanon, m.Kp / 32, m.Mp / 128, 0, 0, act, epi, partials, counters};
+    a.total = (int64_t)a.KC * a.MG;
+    a.G = (int)std::min<int64_t>(sms, a.total);
+    if ((int64_t)a.G * 2 * TC_BM * C::N * 4 > partial_bytes) {
+        set_error("gemm_tc_sk: partials workspace too small");
+        return PB_ERR_CAPACITY;
+    }
+    return launch_pdl(k_gemm_tc_sk<BN>, dim3((unsigned)a.G), dim3(TC_THREADS), C::SMEM, st, a);
+}
+
+int launch_gemm_tc_sk(const Mat& m, const uint8_t* bcanon, int tile_tokens, const Act& act, const Epi& epi,
+                      int* partials, int64_t partial_bytes, int* counters, cudaStream_t st) {
+    if (act.n_tok > tile_tokens) {
+        set_error("gemm_tc_sk: more tokens than one tile");
+        return PB_ERR_GENERIC;
+    }
+    if (tile_tokens == 16) return launch_sk<16>(m, bcanon, act, epi, partials, partial_bytes, counters, st);
+    if (tile_tokens == 32) return launch_sk<32>(m, bcanon, act, epi, partials, partial_bytes, counters, st);
+    set_error("gemm_tc_sk: tile of 16 or 32 tokens");
+    return PB_ERR_GENERIC;
 }
 
 }  // namespace pb

@@ -233,12 +233,12 @@ __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
 
 // Same operand for the tcgen05 GEMM (pb_gemm_tc.cu): the three int8 digit
 // planes of a = rint(y s 2^(shift + 8)), each in the UMMA canonical K-major
-// no-swizzle layout of the weight tiles: per (TC_TOKENS-token tile nt, 32-wide
-// k tile kc, digit p) a TC_TOKENS x 32 B block at ((nt * KC + kc) * 3 + p) *
-// TC_TOKENS * 32, token c, k: byte (c >> 3) * 256 + (k >> 4) * 128 + (c & 7) * 16
+// no-swizzle layout of the weight tiles: per (tw-token tile nt, 32-wide
+// k tile kc, digit p) a tw x 32 B block at ((nt * KC + kc) * 3 + p) *
+// tw * 32, token c, k: byte (c >> 3) * 256 + (k >> 4) * 128 + (c & 7) * 16
 // + (k & 15). One thread per (token, k tile, 16-wide k half) -> three 16-byte
 // stores. Padding tokens are zeros.
-__global__ void __launch_bounds__(256) k_canonwrite(ProArgs a, uint8_t* __restrict__ bcanon, int n_tok) {
+__global__ void __launch_bounds__(256) k_canonwrite(ProArgs a, uint8_t* __restrict__ bcanon, int n_tok, int tw) {
     __shared__ float4 s_st;
     const int tok = blockIdx.y;
     const float* x = a.x + (int64_t)tok * a.K;
@@ -277,8 +277,8 @@ __global__ void __launch_bounds__(256) k_canonwrite(ProArgs a, uint8_t* __restri
             w[2][i >> 2] |= (uint32_t)(uint8_t)l << (8 * (i & 3));
         }
     }
-    constexpr int PLANE = TC_TOKENS * 32;
-    const int nt = tok / TC_TOKENS, c = tok % TC_TOKENS;
+    const int PLANE = tw * 32;  // tile width tw: 80 (prefill GEMM) or 16 / 32 (batched-decode GEMM)
+    const int nt = tok / tw, c = tok % tw;
     uint8_t* blk = bcanon + ((int64_t)nt * KC + kc) * 3 * PLANE + (c >> 3) * 256 + kh * 128 + (c & 7) * 16;
 #pragma unroll
     for (int p = 0; p < 3; ++p)
@@ -309,7 +309,7 @@ int prepare_fused_operand(int mode, const ProSrc& src, const float* x, int n_tok
 
 int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int K, int Kp, const float* gamma,
                     const float* beta, const Mat& m, int tc, uint4* frag, float* back, float4* stats, float* xo,
-                    float* y32, cudaStream_t st, uint8_t* bcanon) {
+                    float* y32, cudaStream_t st, uint8_t* bcanon, int bcanon_tile) {
     constexpr int early = 1;  // weight-side operand inputs loaded before the PDL wait
     ProArgs a{mode, x, K, Kp, gamma, beta, y32 ? nullptr : m.scales, m.n_outl, m.outl_idx, tc, frag, back, stats,
               xo, y32, src, early};
@@ -328,8 +328,8 @@ int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int 
     }
     if (bcanon) {
         const int items = (Kp / 32) * 2;
-        k_canonwrite<<<dim3((unsigned)ceil_div(items, 256), (unsigned)round_up(n_tok, TC_TOKENS)), 256, 0, st>>>(a, bcanon,
-                                                                                                      n_tok);
+        k_canonwrite<<<dim3((unsigned)ceil_div(items, 256), (unsigned)round_up(n_tok, bcanon_tile)), 256, 0, st>>>(
+            a, bcanon, n_tok, bcanon_tile);
         return launch_check("canonwrite");
     }
     const int items = (Kp / 32) * 4;

@@ -167,7 +167,7 @@ int pb_span_create(const pb_span_config* cfg, pb_span** out) {
     // tokens per step from which the matmuls run on tcgen05 instead of the IMMA GEMV:
     // at the 176B width 32 already win (1084 -> 916 us per block at batch 32), at
     // 7B1 width the GEMV still wins at 32 (profiles/r1_gemv_timeline_and_tail.txt)
-    if (s->d > 8192) s->tc_min = 32;
+    if (s->d > 8192) s->tc_min = 16;
     if (cfg->tc_min_tokens > 0) s->tc_min = cfg->tc_min_tokens;
     if (!rc && int8 && NT >= s->tc_min) rc = dalloc(s, &s->bcanon, ceil_div(NT, TC_TOKENS) * (kp_max / 32) * 3 * TC_TOKENS * 32);
     if (!rc) rc = dalloc(s, &s->back, NT);
@@ -352,6 +352,9 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
     const bool int8 = s->cfg.weights == PB_WEIGHTS_INT8;
     const int tc = choose_tc(n_tok);
     const bool use_tc = int8 && s->bcanon && n_tok >= s->tc_min;
+    // batched decode (<= 32 tokens): the stream-K tcgen05 kernel on a 16- or 32-token tile
+    const int sk_tile = n_tok <= 16 ? 16 : 32;
+    const bool use_sk = use_tc && n_tok <= 32;
     const int MGd = (int)ceil_div(d, 128);
     int launches = 0;
     for (int j = 0; j < s->cfg.n_blocks; ++j) {
@@ -393,12 +396,20 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                 }
                 int ev = prof_begin(s, st);
                 if (int rc = launch_prologue(mode, srct, x, n_tok, K, m.Kp, g, be, m, tc, nullptr, s->back, s->stats,
-                                             s->xo, nullptr, st, s->bcanon))
+                                             s->xo, nullptr, st, s->bcanon, use_sk ? sk_tile : TC_TOKENS))
                     return rc;
                 prof_end(s, ev, 2, 4.0 * n_tok * K, st);
                 launches += srct.kind == SRC_STATS ? 3 : 2;
                 Act a{nullptr, s->back, n_tok, 0};
                 ev = prof_begin(s, st);
+                if (use_sk) {
+                    // memory-bound: algorithmic bytes as for the GEMV (PROF kind 6)
+                    const double bytes = (double)m.M * m.K + 4.0 * m.K + 4.0 * m.M + 4.0 * m.n_outl * m.M;
+                    int rc = launch_gemm_tc_sk(m, s->bcanon, sk_tile, a, e, reinterpret_cast<int*>(s->partials),
+                                               4 * s->partial_cap, s->counters + (1 << 18), st);
+                    prof_end(s, ev, 6, bytes, st);
+                    return rc;
+                }
                 int rc = launch_gemm_tc(m, s->bcanon, a, e, st);
                 // tensor roofline: int8 ops issued = 2 * M * K * 3 digit columns per token
                 prof_end(s, ev, 5, 2.0 * m.M * m.K * 3.0 * n_tok, st);

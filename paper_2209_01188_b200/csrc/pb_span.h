@@ -105,15 +105,19 @@ int quantize_blockwise(const float* x, int64_t n, int block, int8_t* codes, floa
 int dequantize_blockwise(const int8_t* codes, const float* scales, int64_t n, int block, float* out,
                          cudaStream_t st);
 
+constexpr int TC_MIN_TOKENS_DEFAULT = 64;
+constexpr int TC_TOKENS = 80;  // tokens per tcgen05 tile (3 digit accumulators x 80 columns, double-buffered in TMEM)
 // prologue: y = LN(x) (PRO_LN) or x (PRO_SCALE); writes the int8-digit operand of
 // y * scales, the per-token 2^-shift, outlier activations xo, and (f32 mode) y.
 int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int K, int Kp, const float* gamma,
                     const float* beta, const Mat& m, int tc, uint4* frag, float* back, float4* stats, float* xo,
-                    float* y32, cudaStream_t st, uint8_t* bcanon = nullptr);
+                    float* y32, cudaStream_t st, uint8_t* bcanon = nullptr, int bcanon_tile = TC_TOKENS);
 // tcgen05 GEMM over a canonical-layout B operand (pb_gemm_tc.cu)
 int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Epi& epi, cudaStream_t st);
-constexpr int TC_MIN_TOKENS_DEFAULT = 64;
-constexpr int TC_TOKENS = 80;  // tokens per tcgen05 tile (3 digit accumulators x 80 columns, double-buffered in TMEM)
+// batched decode (n_tok <= tile_tokens in {16, 32}): stream-K tcgen05 GEMM over a canonical B operand
+// written with tile width tile_tokens; partials / counters are the span's split-merge workspaces
+int launch_gemm_tc_sk(const Mat& m, const uint8_t* bcanon, int tile_tokens, const Act& act, const Epi& epi,
+                      int* partials, int64_t partial_bytes, int* counters, cudaStream_t st);
 // (max_k |gamma_k| s_k, max_k |beta_k| s_k) -> host
 int bound_consts(const float* gamma, const float* beta, const float* scales, int K, float* gs, float* bs,
                  cudaStream_t st);

@@ -103,7 +103,7 @@ class BlockSpan:
     def last_launches(self) -> int:
         return int(_lib.lib().pb_span_last_launches(self._h))
 
-    PROF_GEMV, PROF_ATTN, PROF_PROLOGUE, PROF_GEMM_F32, PROF_CODEC = range(5)
+    PROF_GEMV, PROF_ATTN, PROF_PROLOGUE, PROF_GEMM_F32, PROF_CODEC, PROF_TC_GEMM, PROF_TC_DECODE = range(7)
 
     def profile(self, on: bool) -> None:
         """Bracket every launch with CUDA events (resets previous records)."""

@@ -215,3 +215,46 @@ def test_c3_bloom7b1_eight_sessions_two_spans_vs_f64():
     for s in spans:
         s.close()
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("shape_name,B", [("bloom-176b", 32), ("bloom-7b1", 16), ("bloom-7b1", 11)])
+def test_batched_decode_tcgen05_stream_k_vs_f64(shape_name, B):
+    """Batched decode through the stream-K tcgen05 kernel (k_gemm_tc_sk: one
+    16- or 32-token tile, split row groups merged as exact s32 partials): B
+    sessions with different contexts, prefill then 3 batched decode steps,
+    every session against float64 (fp16-rounded K/V as the cache stores
+    them)."""
+    import torch
+
+    from paper_2209_01188_b200.model import SHAPES
+    from paper_2209_01188_b200.span import BlockSpan
+    from torch_ref import RefBlock
+
+    cfg = SHAPES[shape_name]
+    span = BlockSpan(cfg, 0, 2, int8=True, page_tokens=64, max_tokens=64, max_seqs=32, n_pages=2 * B + 4,
+                     tc_min_tokens=8)
+    span.generate_weights(42)
+    refs = [RefBlock(span, j) for j in range(2)]
+    gen = torch.Generator(device="cuda").manual_seed(31)
+    lens = [1 + (i * 7) % 5 for i in range(B)]
+    seqs = [span.new_sequence() for _ in range(B)]
+    kvs = [[[None, None], [None, None]] for _ in range(B)]
+    pos = [0] * B
+    inputs = [torch.randn(t, cfg.hidden, device="cuda", generator=gen) * 0.05 for t in lens]
+    for step in range(4):
+        span.profile(True)
+        outs = span.step(list(zip(seqs, inputs)))
+        sk = span.profile_read(span.PROF_TC_DECODE)[1]
+        span.profile(False)
+        if step > 0:
+            assert sk == 8, sk  # 4 matmuls x 2 blocks on the stream-K kernel
+        for i in range(B):
+            want = inputs[i].double()
+            for r, kv in zip(refs, kvs[i]):
+                want = r.step(want, kv, pos[i], kv_fp16=True)
+            assert _rel(outs[i].double(), want) <= TOL, (step, i)
+            pos[i] += inputs[i].shape[0]
+        inputs = [torch.randn(1, cfg.hidden, device="cuda", generator=gen) * 0.05 for _ in range(B)]
+    del refs
+    span.close()
+    torch.cuda.empty_cache()
