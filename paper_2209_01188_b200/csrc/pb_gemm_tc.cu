@@ -292,12 +292,12 @@ int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Ep
 
 // ------------------------------------------------------------------ batched decode: stream-K, one token tile
 
-template <int BN>
+template <int BN, int KT_ = 8, int ST_ = (BN == 32 ? 4 : 4)>
 struct SkCfg {
     static constexpr int N = 3 * BN;                         // digit columns (MMA N)
     static constexpr int B_KT = N * 32;                      // digit-plane bytes per 32-wide k tile
-    static constexpr int KT = 8;                             // k tiles per stage (32 KB of weights)
-    static constexpr int STAGES = BN == 32 ? 3 : 4;
+    static constexpr int KT = KT_;                           // k tiles per stage
+    static constexpr int STAGES = ST_;
     static constexpr int ACC = N <= 64 ? 64 : 128;           // TMEM columns per accumulator set
     static constexpr uint32_t IDESC = tc_idesc_i8(N);
     static constexpr size_t SMEM = (size_t)STAGES * KT * (TC_A + B_KT) + (2 * STAGES + 4) * 8 + 16;
@@ -338,9 +338,9 @@ __device__ __forceinline__ void sk_epilogue_row(const TcSkArgs& a, int o, int la
     }
 }
 
-template <int BN>
+template <int BN, int KT_, int ST_>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
-    using C = SkCfg<BN>;
+    using C = SkCfg<BN, KT_, ST_>;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sa = smem;                                // [STAGES][KT][4 KB]
     uint8_t* sb = sa + C::STAGES * C::KT * TC_A;       // [STAGES][KT][N x 32 B]
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
         // STAGES stages of weights are requested before the PDL wait; their digit planes
         // (written by the operand kernel) follow once it has completed
         if (lane == 0) {
-            int it = 0, pend_kc[C::STAGES], pend_n[C::STAGES];
+            int it = 0, pend_kc[C::STAGES], pend_n[C::STAGES];  // stages issued before the PDL wait
             bool waited = false;
             for (int64_t u = u0; u < u1;) {
                 const int mg = (int)(u / KC), ka = (int)(u % KC);
@@ -520,13 +520,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
     }
 }
 
-template <int BN>
+template <int BN, int KT_, int ST_>
 static int launch_sk(const Mat& m, const uint8_t* bcanon, const Act& act, const Epi& epi, int* partials,
                      int64_t partial_bytes, int* counters, cudaStream_t st) {
-    using C = SkCfg<BN>;
+    using C = SkCfg<BN, KT_, ST_>;
+    static_assert(C::SMEM <= 232448, "smem");
     static int ok[PB_MAX_DEVICES] = {};
     if (per_device(ok, [](int) {
-            return cudaFuncSetAttribute(k_gemm_tc_sk<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            return cudaFuncSetAttribute(k_gemm_tc_sk<BN, KT_, ST_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)C::SMEM) == cudaSuccess ? 1 : -1;
         }) < 0)
         return launch_check("gemm_tc_sk setup");
@@ -539,7 +540,7 @@ static int launch_sk(const Mat& m, const uint8_t* bcanon, const Act& act, const 
         set_error("gemm_tc_sk: partials workspace too small");
         return PB_ERR_CAPACITY;
     }
-    return launch_pdl(k_gemm_tc_sk<BN>, dim3((unsigned)a.G), dim3(TC_THREADS), C::SMEM, st, a);
+    return launch_pdl(k_gemm_tc_sk<BN, KT_, ST_>, dim3((unsigned)a.G), dim3(TC_THREADS), C::SMEM, st, a);
 }
 
 int launch_gemm_tc_sk(const Mat& m, const uint8_t* bcanon, int tile_tokens, const Act& act, const Epi& epi,
@@ -548,8 +549,20 @@ int launch_gemm_tc_sk(const Mat& m, const uint8_t* bcanon, int tile_tokens, cons
         set_error("gemm_tc_sk: more tokens than one tile");
         return PB_ERR_GENERIC;
     }
-    if (tile_tokens == 16) return launch_sk<16>(m, bcanon, act, epi, partials, partial_bytes, counters, st);
-    if (tile_tokens == 32) return launch_sk<32>(m, bcanon, act, epi, partials, partial_bytes, counters, st);
+    static const int cfg = [] {  // TEMPORARY sweep knob
+        const char* e = getenv("PB_SK_CFG");
+        return e ? atoi(e) : 0;
+    }();
+    if (tile_tokens == 16) return launch_sk<16, 8, 4>(m, bcanon, act, epi, partials, partial_bytes, counters, st);
+    if (tile_tokens == 32) {
+        switch (cfg) {
+            case 1: return launch_sk<32, 8, 3>(m, bcanon, act, epi, partials, partial_bytes, counters, st);
+            case 2: return launch_sk<32, 4, 8>(m, bcanon, act, epi, partials, partial_bytes, counters, st);
+            case 3: return launch_sk<32, 4, 6>(m, bcanon, act, epi, partials, partial_bytes, counters, st);
+            case 4: return launch_sk<32, 2, 14>(m, bcanon, act, epi, partials, partial_bytes, counters, st);
+            default: return launch_sk<32, 8, 4>(m, bcanon, act, epi, partials, partial_bytes, counters, st);
+        }
+    }
     set_error("gemm_tc_sk: tile of 16 or 32 tokens");
     return PB_ERR_GENERIC;
 }
