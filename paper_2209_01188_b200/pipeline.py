@@ -160,6 +160,18 @@ class P2PRing:
         succ = (rank + 1) % world
         _lib.check(self.L.pb_hop_open(C.create_string_buffer(handles[succ], 64), device, C.byref(peer)))
         self.peer = peer.value
+        # Ranks sharing one physical GPU must not spin on each other's flags in
+        # kernels (separate contexts time-slice; a spinning kernel can stall the
+        # context switch): there the receiver polls its flag from the host.
+        import torch
+
+        self.device = device
+        uuids = [None] * world
+        dist.all_gather_object(uuids, str(torch.cuda.get_device_properties(device).uuid))
+        self.host_wait = len(set(uuids)) < world
+        if self.host_wait:
+            self._poll_stream = torch.cuda.Stream(device=device)
+            self._poll_host = torch.zeros(1, dtype=torch.int64).pin_memory()
 
     def _slot(self, base: int, j: int) -> int:
         return base + 8 * self.FLAGS + (j % self.slots) * self.slot_bytes
@@ -171,9 +183,31 @@ class P2PRing:
         return self._slot(self.peer, j)
 
     def wait(self, j: int, stream: int) -> None:
+        """Order `stream`'s next work after job j's payload arrived: a one-thread
+        acquire-spin kernel on that stream (GPUs of their own), or a host poll
+        when ranks share a GPU (the caller's thread blocks until the flag is set)."""
         from . import _lib
 
+        if self.host_wait:
+            return self._poll(j)
         _lib.check(self.L.pb_hop_wait(self.base + 8 * (j % self.slots), j + 1, self.timeout_ms, stream))
+
+    def _poll(self, j: int) -> None:
+        import time
+
+        import torch
+
+        flag = dev_view(self.base + 8 * (j % self.slots), 8, torch.device("cuda", self.device)).view(torch.int64)
+        deadline = time.monotonic() + self.timeout_ms / 1000.0
+        with torch.cuda.stream(self._poll_stream):
+            while True:
+                self._poll_host.copy_(flag, non_blocking=True)
+                self._poll_stream.synchronize()
+                if int(self._poll_host[0]) >= j + 1:
+                    return
+                if time.monotonic() > deadline:
+                    raise TimeoutError(f"hop: no signal for job {j} after {self.timeout_ms} ms")
+                time.sleep(20e-6)
 
     def signal(self, j: int, stream: int) -> None:
         """Publish job j (payload already stored in the successor's slot j % slots)."""
