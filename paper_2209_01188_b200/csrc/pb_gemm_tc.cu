@@ -59,7 +59,8 @@ constexpr int TC_PLANE = TC_BN * 32;       // one digit plane per k tile
 constexpr int TC_B = 3 * TC_PLANE;
 constexpr int TC_ACC = 256;                // TMEM columns per accumulator set (3 x 80 used)
 constexpr int TC_TMEM_COLS = 512;
-constexpr size_t TC_SMEM = (size_t)TC_STAGES * TC_KT * (TC_A + TC_B) + (2 * TC_STAGES + 4) * 8 + 16;
+constexpr size_t TC_SMEM =
+    (size_t)TC_STAGES * TC_KT * (TC_A + TC_B) + (2 * TC_STAGES + 4) * 8 + 16 + TC_BN * sizeof(TokInfo);
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
@@ -137,6 +138,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
     uint64_t* accfull = empty + TC_STAGES;  // [2]
     uint64_t* accempty = accfull + 2;       // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
+    TokInfo* s_tok = reinterpret_cast<TokInfo*>(tmem_slot + 4);  // [TC_BN] of the tile being finished
 
     const int warp = warp_uniform_id(), lane = threadIdx.x & 31;
     const int KC = a.KC;
@@ -211,13 +213,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
         // ---------------- epilogue (warps 2-5): TMEM lanes 32 (warp % 4) .. + 31
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
-        const bool want_max = a.epi.tokmax != nullptr;
         int i = 0;
         for (int u = cta; u < units; u += NU, ++i) {
             int mgu, nt;
             tc_unit(a, u, mgs, mgu, nt);
             const int mg = mgu;
             const int b = i & 1;
+            // this tile's per-token constants (all 4 warps done with the previous tile's)
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            stage_tokens(a.epi, a.act.back, a.act.n_tok, nt * TC_BN, TC_BN, s_tok, (int)threadIdx.x - 64, 128);
+            asm volatile("bar.sync 1, 128;" ::: "memory");
             mbar_wait(&accfull[b], (i >> 1) & 1);
             tc_fence_after();
             const int o = mg * TC_BM + row;
@@ -227,22 +232,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
                 tmem_ld16(tbase + c0, h);
                 tmem_ld16(tbase + TC_BN + c0, m);
                 tmem_ld16(tbase + 2 * TC_BN + c0, l);
-#pragma unroll 4
-                for (int j = 0; j < 16; ++j) {
-                    const int tok = nt * TC_BN + c0 + j;
-                    float mx = 0.f;
-                    if (tok < a.act.n_tok && o < a.epi.M) {
-                        // exact integer (|iv| < 2^47), one rounding to f32: same value as the f64 sum
-                        const long long iv = (long long)h[j] * 65536 + (long long)m[j] * 256 + (long long)l[j];
-                        const float y = epi_store(a.epi, tok, o, (float)iv * a.act.back[tok]);
-                        if (want_max) mx = fabsf(y * a.epi.s_next[o]);
-                    }
-                    if (want_max) {
-                        mx = warp_max(mx);
-                        if (lane == 0 && tok < a.act.n_tok)
-                            atomicMax(reinterpret_cast<int*>(a.epi.tokmax) + tok, __float_as_int(mx));
-                    }
-                }
+                tc_epi16(a.epi, o, lane, nt * TC_BN + c0, s_tok + c0, h, m, l);
             }
             tc_fence_before();
             __syncwarp();
@@ -292,6 +282,9 @@ int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Ep
 
 // ------------------------------------------------------------------ batched decode: stream-K, one token tile
 
+#ifndef SK_NSETS
+#define SK_NSETS 2
+#endif
 template <int BN, int KT_ = 8, int ST_ = (BN == 32 ? 4 : 4)>
 struct SkCfg {
     static constexpr int N = 3 * BN;                         // digit columns (MMA N)
@@ -299,8 +292,10 @@ struct SkCfg {
     static constexpr int KT = KT_;                           // k tiles per stage
     static constexpr int STAGES = ST_;
     static constexpr int ACC = N <= 64 ? 64 : 128;           // TMEM columns per accumulator set
+    static constexpr int NSETS = SK_NSETS;                   // accumulator sets (segments in flight)
     static constexpr uint32_t IDESC = tc_idesc_i8(N);
-    static constexpr size_t SMEM = (size_t)STAGES * KT * (TC_A + B_KT) + (2 * STAGES + 4) * 8 + 16;
+    static constexpr size_t SMEM =
+        (size_t)STAGES * KT * (TC_A + B_KT) + (2 * STAGES + 2 * NSETS) * 8 + 16 + BN * sizeof(TokInfo);
 };
 
 struct TcSkArgs {
@@ -318,26 +313,6 @@ struct TcSkArgs {
 __device__ __forceinline__ int64_t sk_u0(int64_t c, int64_t total, int G) { return c * total / G; }
 __device__ __forceinline__ int sk_owner_of(int64_t u, int64_t total, int G) { return (int)(((u + 1) * G - 1) / total); }
 
-template <int BN>
-__device__ __forceinline__ void sk_epilogue_row(const TcSkArgs& a, int o, int lane, const int* h, const int* m,
-                                                const int* l, int c0) {
-    const bool want_max = a.epi.tokmax != nullptr;
-#pragma unroll 4
-    for (int j = 0; j < 16; ++j) {
-        const int tok = c0 + j;
-        float mx = 0.f;
-        if (tok < a.act.n_tok && o < a.epi.M) {
-            const long long iv = (long long)h[j] * 65536 + (long long)m[j] * 256 + (long long)l[j];
-            const float y = epi_store(a.epi, tok, o, (float)iv * a.act.back[tok]);
-            if (want_max) mx = fabsf(y * a.epi.s_next[o]);
-        }
-        if (want_max) {
-            mx = warp_max(mx);
-            if (lane == 0 && tok < a.act.n_tok) atomicMax(reinterpret_cast<int*>(a.epi.tokmax) + tok, __float_as_int(mx));
-        }
-    }
-}
-
 template <int BN, int KT_, int ST_>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
     using C = SkCfg<BN, KT_, ST_>;
@@ -346,9 +321,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
     uint8_t* sb = sa + C::STAGES * C::KT * TC_A;       // [STAGES][KT][N x 32 B]
     uint64_t* full = reinterpret_cast<uint64_t*>(sb + C::STAGES * C::KT * C::B_KT);
     uint64_t* empty = full + C::STAGES;
-    uint64_t* accfull = empty + C::STAGES;  // [2]
-    uint64_t* accempty = accfull + 2;       // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
+    uint64_t* accfull = empty + C::STAGES;  // [NSETS]
+    uint64_t* accempty = accfull + C::NSETS;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + C::NSETS);
+    TokInfo* s_tok = reinterpret_cast<TokInfo*>(tmem_slot + 4);  // 16-B aligned
 
     const int warp = warp_uniform_id(), lane = threadIdx.x & 31;
     const int KC = a.KC, c = (int)blockIdx.x;
@@ -359,7 +335,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < C::NSETS; ++b) {
             mbar_init(&accfull[b], 1);
             mbar_init(&accempty[b], 4);
         }
@@ -367,7 +343,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(2 * C::ACC));
+                     "r"(C::NSETS * C::ACC));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -389,9 +365,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
                 for (int kc = ka; kc < kb; kc += C::KT, ++it) {
                     const int s = it % C::STAGES, n = min(C::KT, kb - kc);
                     mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+#if defined(SK_EXP) && (SK_EXP & 2)
+                    mbar_expect_tx(&full[s], n * TC_A);
+                    bulk_g2s(sa + s * C::KT * TC_A, asrc + (int64_t)kc * TC_A, n * TC_A, &full[s]);
+                    if (true) {
+                    } else if (waited) {
+#else
                     mbar_expect_tx(&full[s], n * (TC_A + C::B_KT));
                     bulk_g2s(sa + s * C::KT * TC_A, asrc + (int64_t)kc * TC_A, n * TC_A, &full[s]);
                     if (waited) {
+#endif
                         bulk_g2s(sb + s * C::KT * C::B_KT, a.bcanon + (int64_t)kc * C::B_KT, n * C::B_KT, &full[s]);
                     } else {
                         pend_kc[s] = kc;
@@ -417,14 +400,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer: segment i (one row group's k range) accumulates in set i & 1
+        // ---------------- MMA issuer: segment i (one row group's k range) accumulates in set i % NSETS
         if (lane == 0) {
             int it = 0, i = 0;
             for (int64_t u = u0; u < u1; ++i) {
                 const int ka = (int)(u % KC);
                 const int kb = u1 - u < (int64_t)(KC - ka) ? ka + (int)(u1 - u) : KC;
-                const int b = i & 1;
-                mbar_wait(&accempty[b], ((i >> 1) & 1) ^ 1);
+                const int b = i % C::NSETS;
+                mbar_wait(&accempty[b], ((i / C::NSETS) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t acc = tmem + b * C::ACC;
                 for (int kc = ka; kc < kb; kc += C::KT, ++it) {
@@ -432,9 +415,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
                     mbar_wait(&full[s], (it / C::STAGES) & 1);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sa + s * C::KT * TC_A), b0 = smem_u32(sb + s * C::KT * C::B_KT);
+#if !(defined(SK_EXP) && (SK_EXP & 1))
                     for (int k = 0; k < n; ++k)
                         tc_mma<C::IDESC>(acc, umma_desc(a0 + k * TC_A), umma_desc(b0 + k * C::B_KT),
                                          (kc - ka) | k);
+#endif
                     tc_commit(&empty[s]);
                 }
                 tc_commit(&accfull[b]);
@@ -447,15 +432,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const int first_mg = (int)(u0 / KC);
+        // the per-token constants (scale, KV page / slot) come from the operand kernel: after the PDL wait
+        pdl_wait();
+        stage_tokens(a.epi, a.act.back, a.act.n_tok, 0, BN, s_tok, (int)threadIdx.x - 64, 128);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
         int i = 0;
         for (int64_t u = u0; u < u1; ++i) {
             const int mg = (int)(u / KC), ka = (int)(u % KC);
             const int kb = u1 - u < (int64_t)(KC - ka) ? ka + (int)(u1 - u) : KC;
             u += kb - ka;
-            const int b = i & 1;
-            mbar_wait(&accfull[b], (i >> 1) & 1);
+            const int b = i % C::NSETS;
+            mbar_wait(&accfull[b], (i / C::NSETS) & 1);
             tc_fence_after();
             const int o = mg * TC_BM + row;
+#if defined(SK_EXP) && (SK_EXP & 4)
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&accempty[b]);
+            continue;
+#endif
             const uint32_t tbase = tmem + b * C::ACC + ((uint32_t)(quarter * 32) << 16);
             if (ka == 0 && kb == KC) {  // whole row group in this CTA
                 for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -463,7 +458,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
                     tmem_ld16(tbase + c0, h);
                     tmem_ld16(tbase + BN + c0, m);
                     tmem_ld16(tbase + 2 * BN + c0, l);
-                    sk_epilogue_row<BN>(a, o, lane, h, m, l, c0);
+                    tc_epi16(a.epi, o, lane, c0, s_tok + c0, h, m, l);
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -508,7 +503,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
                         l[q] += z.x, l[q + 1] += z.y, l[q + 2] += z.z, l[q + 3] += z.w;
                     }
                 }
-                sk_epilogue_row<BN>(a, o, lane, h, m, l, c0);
+                tc_epi16(a.epi, o, lane, c0, s_tok + c0, h, m, l);
             }
         }
     }
@@ -516,7 +511,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * C::ACC));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::NSETS * C::ACC));
     }
 }
 
