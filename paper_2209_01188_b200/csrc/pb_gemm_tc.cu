@@ -306,7 +306,7 @@ struct TcSkArgs {
     int G;                  // CTAs
     Act act;
     Epi epi;
-    int* partials;          // [G][2 segments][128 rows][N] s32 (a CTA's first / last partial row group)
+    int* skacc;             // [MG][N][128 rows] s32 sums of split row groups, zero between launches
     int* counters;          // [MG][4 lane quarters], zero between launches
 };
 
@@ -458,22 +458,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
                     tmem_ld16(tbase + c0, h);
                     tmem_ld16(tbase + BN + c0, m);
                     tmem_ld16(tbase + 2 * BN + c0, l);
+#if !(defined(SK_EXP) && (SK_EXP & 16))
                     tc_epi16(a.epi, o, lane, c0, s_tok + c0, h, m, l);
+#endif
                 }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&accempty[b]);
                 continue;
             }
-            // split row group: park this CTA's s32 digit sums, the last contributor merges
-            const int slot = mg == first_mg ? 0 : 1;
-            int* pw = a.partials + (((int64_t)c * 2 + slot) * TC_BM + row) * C::N;
+            // split row group: add this CTA's s32 digit sums into the row group's
+            // accumulator (fire-and-forget reductions at L2, [mg][column][row]: a
+            // warp's 32 rows are one 128-B line), then count in; the last
+            // contributor reads the sums once, zeroes them for the next launch
+            // and runs the epilogue. Exact integers: arrival order is irrelevant.
+            int* acc = a.skacc + (int64_t)mg * C::N * TC_BM + row;
             for (int c0 = 0; c0 < C::N; c0 += 16) {
                 int v[16];
                 tmem_ld16(tbase + c0, v);
 #pragma unroll
-                for (int q = 0; q < 16; q += 4)
-                    __stcg(reinterpret_cast<int4*>(pw + c0 + q), make_int4(v[q], v[q + 1], v[q + 2], v[q + 3]));
+                for (int q = 0; q < 16; ++q) atomicAdd(acc + (c0 + q) * TC_BM, v[q]);  // RED.ADD (result unused)
             }
             tc_fence_before();
             __syncwarp();
@@ -489,19 +493,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
             __threadfence();
             if (lane == 0) a.counters[mg * 4 + quarter] = 0;  // ready for the next launch
             for (int c0 = 0; c0 < BN; c0 += 16) {
-                int h[16] = {}, m[16] = {}, l[16] = {};
-                for (int cc = cf; cc <= cl; ++cc) {
-                    const int sl = mg == (int)(sk_u0(cc, a.total, a.G) / KC) ? 0 : 1;
-                    const int* pr = a.partials + (((int64_t)cc * 2 + sl) * TC_BM + row) * C::N;
+                int h[16], m[16], l[16];
 #pragma unroll
-                    for (int q = 0; q < 16; q += 4) {
-                        const int4 x = __ldcg(reinterpret_cast<const int4*>(pr + c0 + q));
-                        const int4 y = __ldcg(reinterpret_cast<const int4*>(pr + BN + c0 + q));
-                        const int4 z = __ldcg(reinterpret_cast<const int4*>(pr + 2 * BN + c0 + q));
-                        h[q] += x.x, h[q + 1] += x.y, h[q + 2] += x.z, h[q + 3] += x.w;
-                        m[q] += y.x, m[q + 1] += y.y, m[q + 2] += y.z, m[q + 3] += y.w;
-                        l[q] += z.x, l[q + 1] += z.y, l[q + 2] += z.z, l[q + 3] += z.w;
-                    }
+                for (int j = 0; j < 16; ++j) {
+                    h[j] = __ldcg(acc + (c0 + j) * TC_BM);
+                    m[j] = __ldcg(acc + (BN + c0 + j) * TC_BM);
+                    l[j] = __ldcg(acc + (2 * BN + c0 + j) * TC_BM);
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    __stcg(acc + (c0 + j) * TC_BM, 0);
+                    __stcg(acc + (BN + c0 + j) * TC_BM, 0);
+                    __stcg(acc + (2 * BN + c0 + j) * TC_BM, 0);
                 }
                 tc_epi16(a.epi, o, lane, c0, s_tok + c0, h, m, l);
             }
@@ -516,8 +519,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
 }
 
 template <int BN, int KT_, int ST_>
-static int launch_sk(const Mat& m, const uint8_t* bcanon, const Act& act, const Epi& epi, int* partials,
-                     int64_t partial_bytes, int* counters, cudaStream_t st) {
+static int launch_sk(const Mat& m, const uint8_t* bcanon, const Act& act, const Epi& epi, int* skacc,
+                     int64_t skacc_bytes, int* counters, cudaStream_t st) {
     using C = SkCfg<BN, KT_, ST_>;
     static_assert(C::SMEM <= 232448, "smem");
     static int ok[PB_MAX_DEVICES] = {};
@@ -528,18 +531,18 @@ static int launch_sk(const Mat& m, const uint8_t* bcanon, const Act& act, const 
         return launch_check("gemm_tc_sk setup");
     const int sms = sm_count();
     if (sms < 0) return PB_ERR_GENERIC;
-    TcSkArgs a{m.codes, bcanon, m.Kp / 32, m.Mp / 128, 0, 0, act, epi, partials, counters};
+    TcSkArgs a{m.codes, bcanon, m.Kp / 32, m.Mp / 128, 0, 0, act, epi, skacc, counters};
     a.total = (int64_t)a.KC * a.MG;
     a.G = (int)std::min<int64_t>(sms, a.total);
-    if ((int64_t)a.G * 2 * TC_BM * C::N * 4 > partial_bytes) {
-        set_error("gemm_tc_sk: partials workspace too small");
+    if ((int64_t)a.MG * TC_BM * C::N * 4 > skacc_bytes) {
+        set_error("gemm_tc_sk: split accumulator workspace too small");
         return PB_ERR_CAPACITY;
     }
     return launch_pdl(k_gemm_tc_sk<BN, KT_, ST_>, dim3((unsigned)a.G), dim3(TC_THREADS), C::SMEM, st, a);
 }
 
 int launch_gemm_tc_sk(const Mat& m, const uint8_t* bcanon, int tile_tokens, const Act& act, const Epi& epi,
-                      int* partials, int64_t partial_bytes, int* counters, cudaStream_t st) {
+                      int* skacc, int64_t skacc_bytes, int* counters, cudaStream_t st) {
     if (act.n_tok > tile_tokens) {
         set_error("gemm_tc_sk: more tokens than one tile");
         return PB_ERR_GENERIC;
@@ -548,14 +551,14 @@ int launch_gemm_tc_sk(const Mat& m, const uint8_t* bcanon, int tile_tokens, cons
         const char* e = getenv("PB_SK_CFG");
         return e ? atoi(e) : 0;
     }();
-    if (tile_tokens == 16) return launch_sk<16, 8, 4>(m, bcanon, act, epi, partials, partial_bytes, counters, st);
+    if (tile_tokens == 16) return launch_sk<16, 8, 4>(m, bcanon, act, epi, skacc, skacc_bytes, counters, st);
     if (tile_tokens == 32) {
         switch (cfg) {
-            case 1: return launch_sk<32, 8, 3>(m, bcanon, act, epi, partials, partial_bytes, counters, st);
-            case 2: return launch_sk<32, 4, 8>(m, bcanon, act, epi, partials, partial_bytes, counters, st);
-            case 3: return launch_sk<32, 4, 6>(m, bcanon, act, epi, partials, partial_bytes, counters, st);
-            case 4: return launch_sk<32, 2, 14>(m, bcanon, act, epi, partials, partial_bytes, counters, st);
-            default: return launch_sk<32, 8, 4>(m, bcanon, act, epi, partials, partial_bytes, counters, st);
+            case 1: return launch_sk<32, 8, 3>(m, bcanon, act, epi, skacc, skacc_bytes, counters, st);
+            case 2: return launch_sk<32, 4, 8>(m, bcanon, act, epi, skacc, skacc_bytes, counters, st);
+            case 3: return launch_sk<32, 4, 6>(m, bcanon, act, epi, skacc, skacc_bytes, counters, st);
+            case 4: return launch_sk<32, 2, 14>(m, bcanon, act, epi, skacc, skacc_bytes, counters, st);
+            default: return launch_sk<32, 8, 4>(m, bcanon, act, epi, skacc, skacc_bytes, counters, st);
         }
     }
     set_error("gemm_tc_sk: tile of 16 or 32 tokens");

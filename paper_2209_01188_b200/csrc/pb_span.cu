@@ -93,7 +93,7 @@ void free_span(pb_span* s) {
     }
     void* ptrs[] = {s->kv, s->slopes, s->xa, s->mid, s->q, s->ctx, s->act, s->xo, s->y32, s->frag, s->bcanon, s->back, s->stats, s->pst_x, s->pst_mid, s->tokmax_ctx, s->tokmax_act,
                     s->partials, s->counters, s->attn_part, s->d_tok_seq, s->d_tok_pos, s->d_pages, s->d_grp_first, s->d_grp_count,
-                    s->hop_codes, s->hop_scales, s->d_unit_base};
+                    s->hop_codes, s->hop_scales, s->d_unit_base, s->sk_acc};
     for (void* p : ptrs) cudaFree(p);
     for (int i = 0; i < pb_span::NSLOT; ++i) {
         if (s->h_meta[i]) cudaFreeHost(s->h_meta[i]);
@@ -178,6 +178,11 @@ int pb_span_create(const pb_span_config* cfg, pb_span** out) {
     if (!rc) rc = dalloc(s, &s->tokmax_act, NT);
     s->partial_cap = (int64_t)8 << 20;
     if (!rc) rc = dalloc(s, &s->partials, s->partial_cap);
+    if (!rc && s->bcanon) {  // batched-decode tcgen05 kernel: split-row-group sums, zero between launches
+        s->sk_acc_elems = ceil_div(std::max(3 * d, rd), 128) * 96 * 128;
+        rc = dalloc(s, &s->sk_acc, s->sk_acc_elems);
+        if (!rc && cudaMemset(s->sk_acc, 0, sizeof(int) * s->sk_acc_elems) != cudaSuccess) rc = PB_ERR_GENERIC;
+    }
     if (!rc) rc = dalloc(s, &s->counters, 1 << 20);
     s->attn_cap = attention_part_floats(NT, s->H, s->dh, cfg->max_seq);
     if (!rc) rc = dalloc(s, &s->attn_part, s->attn_cap);
@@ -405,8 +410,8 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                 if (use_sk) {
                     // memory-bound: algorithmic bytes as for the GEMV (PROF kind 6)
                     const double bytes = (double)m.M * m.K + 4.0 * m.K + 4.0 * m.M + 4.0 * m.n_outl * m.M;
-                    int rc = launch_gemm_tc_sk(m, s->bcanon, sk_tile, a, e, reinterpret_cast<int*>(s->partials),
-                                               4 * s->partial_cap, s->counters + (1 << 18), st);
+                    int rc = launch_gemm_tc_sk(m, s->bcanon, sk_tile, a, e, s->sk_acc, 4 * s->sk_acc_elems,
+                                               s->counters + (1 << 18), st);
                     prof_end(s, ev, 6, bytes, st);
                     return rc;
                 }

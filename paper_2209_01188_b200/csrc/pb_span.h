@@ -117,7 +117,7 @@ int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Ep
 // batched decode (n_tok <= tile_tokens in {16, 32}): stream-K tcgen05 GEMM over a canonical B operand
 // written with tile width tile_tokens; partials / counters are the span's split-merge workspaces
 int launch_gemm_tc_sk(const Mat& m, const uint8_t* bcanon, int tile_tokens, const Act& act, const Epi& epi,
-                      int* partials, int64_t partial_bytes, int* counters, cudaStream_t st);
+                      int* skacc, int64_t skacc_bytes, int* counters, cudaStream_t st);
 // (max_k |gamma_k| s_k, max_k |beta_k| s_k) -> host
 int bound_consts(const float* gamma, const float* beta, const float* scales, int K, float* gs, float* bs,
                  cudaStream_t st);

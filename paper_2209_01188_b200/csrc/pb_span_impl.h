@@ -29,6 +29,8 @@ struct pb_span {
     float4 *pst_x = nullptr, *pst_mid = nullptr;  // per-128-row LN summaries [NT][d/128]
     float *tokmax_ctx = nullptr, *tokmax_act = nullptr;  // operand ranges [NT]
     float* partials = nullptr;
+    int* sk_acc = nullptr;        // [MG][3 * 32][128] s32 split-row-group sums of k_gemm_tc_sk (kept zero)
+    int64_t sk_acc_elems = 0;
     int64_t partial_cap = 0;
     int* counters = nullptr;
     float* attn_part = nullptr;
