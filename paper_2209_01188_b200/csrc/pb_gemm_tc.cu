@@ -53,7 +53,8 @@ constexpr int TC_BM = 128;
 constexpr int TC_BN = TC_TOKENS;           // tokens per tile (per digit accumulator)
 constexpr int TC_KT = 4;                   // k tiles per pipeline stage (MMAs issued per wait/commit)
 constexpr int TC_STAGES = 4;
-constexpr int TC_THREADS = 192;
+constexpr int TC_EPI_WARPS = 8;            // two per TMEM lane quarter, splitting the tile's 16-token chunks
+constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
 constexpr int TC_A = 4096;                 // int8 codes per k tile (128 rows x 32)
 constexpr int TC_PLANE = TC_BN * 32;       // one digit plane per k tile
 constexpr int TC_B = 3 * TC_PLANE;
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&accfull[b], 1);   // MMA commit after a tile's last k step
-            mbar_init(&accempty[b], 4);  // the 4 epilogue warps
+            mbar_init(&accempty[b], TC_EPI_WARPS);
         }
         mbar_fence_init();
     }
@@ -210,8 +211,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
         }
         __syncwarp();
     } else {
-        // ---------------- epilogue (warps 2-5): TMEM lanes 32 (warp % 4) .. + 31
-        const int quarter = warp & 3;
+        // ---------------- epilogue (warps 2-9): TMEM lanes 32 (warp % 4) .. + 31; the two warps
+        // of a lane quarter take alternate 16-token chunks
+        const int quarter = warp & 3, half = (warp - 2) >> 2;
         const int row = quarter * 32 + lane;
         int i = 0;
         for (int u = cta; u < units; u += NU, ++i) {
@@ -219,15 +221,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
             tc_unit(a, u, mgs, mgu, nt);
             const int mg = mgu;
             const int b = i & 1;
-            // this tile's per-token constants (all 4 warps done with the previous tile's)
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            stage_tokens(a.epi, a.act.back, a.act.n_tok, nt * TC_BN, TC_BN, s_tok, (int)threadIdx.x - 64, 128);
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            // this tile's per-token constants (all epilogue warps done with the previous tile's)
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");
+            stage_tokens(a.epi, a.act.back, a.act.n_tok, nt * TC_BN, TC_BN, s_tok, (int)threadIdx.x - 64,
+                         32 * TC_EPI_WARPS);
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");
             mbar_wait(&accfull[b], (i >> 1) & 1);
             tc_fence_after();
             const int o = mg * TC_BM + row;
             const uint32_t tbase = tmem + b * TC_ACC + ((uint32_t)(quarter * 32) << 16);
-            for (int c0 = 0; c0 < TC_BN; c0 += 16) {
+            for (int c0 = half * 16; c0 < TC_BN; c0 += 32) {
                 int h[16], m[16], l[16];
                 tmem_ld16(tbase + c0, h);
                 tmem_ld16(tbase + TC_BN + c0, m);
@@ -307,7 +310,7 @@ struct TcSkArgs {
     Act act;
     Epi epi;
     int* skacc;             // [MG][N][128 rows] s32 sums of split row groups, zero between launches
-    int* counters;          // [MG][4 lane quarters], zero between launches
+    int* counters;          // [MG][4 lane quarters][2 token halves], zero between launches
 };
 
 __device__ __forceinline__ int64_t sk_u0(int64_t c, int64_t total, int G) { return c * total / G; }
@@ -337,7 +340,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
         }
         for (int b = 0; b < C::NSETS; ++b) {
             mbar_init(&accfull[b], 1);
-            mbar_init(&accempty[b], 4);
+            mbar_init(&accempty[b], TC_EPI_WARPS);
         }
         mbar_fence_init();
     }
@@ -428,14 +431,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
         }
         __syncwarp();
     } else {
-        // ---------------- epilogue (warps 2-5): TMEM lanes 32 (warp % 4) .. + 31 = rows of the group
-        const int quarter = warp & 3;
+        // ---------------- epilogue (warps 2-9): TMEM lanes 32 (warp % 4) .. + 31 = rows of the group;
+        // warp half h finishes tokens 16 h .. 16 h + 15 (BN = 16: half 1 only releases the set)
+        const int quarter = warp & 3, half = (warp - 2) >> 2;
         const int row = quarter * 32 + lane;
-        const int first_mg = (int)(u0 / KC);
+        const int c0 = half * 16;
+        const bool mine = c0 < BN;
         // the per-token constants (scale, KV page / slot) come from the operand kernel: after the PDL wait
         pdl_wait();
-        stage_tokens(a.epi, a.act.back, a.act.n_tok, 0, BN, s_tok, (int)threadIdx.x - 64, 128);
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        stage_tokens(a.epi, a.act.back, a.act.n_tok, 0, BN, s_tok, (int)threadIdx.x - 64, 32 * TC_EPI_WARPS);
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");
         int i = 0;
         for (int64_t u = u0; u < u1; ++i) {
             const int mg = (int)(u / KC), ka = (int)(u % KC);
@@ -452,16 +457,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
             continue;
 #endif
             const uint32_t tbase = tmem + b * C::ACC + ((uint32_t)(quarter * 32) << 16);
+            if (!mine) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&accempty[b]);
+                continue;
+            }
             if (ka == 0 && kb == KC) {  // whole row group in this CTA
-                for (int c0 = 0; c0 < BN; c0 += 16) {
-                    int h[16], m[16], l[16];
-                    tmem_ld16(tbase + c0, h);
-                    tmem_ld16(tbase + BN + c0, m);
-                    tmem_ld16(tbase + 2 * BN + c0, l);
+                int h[16], m[16], l[16];
+                tmem_ld16(tbase + c0, h);
+                tmem_ld16(tbase + BN + c0, m);
+                tmem_ld16(tbase + 2 * BN + c0, l);
 #if !(defined(SK_EXP) && (SK_EXP & 16))
-                    tc_epi16(a.epi, o, lane, c0, s_tok + c0, h, m, l);
+                tc_epi16(a.epi, o, lane, c0, s_tok + c0, h, m, l);
 #endif
-                }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&accempty[b]);
@@ -473,11 +482,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
             // contributor reads the sums once, zeroes them for the next launch
             // and runs the epilogue. Exact integers: arrival order is irrelevant.
             int* acc = a.skacc + (int64_t)mg * C::N * TC_BM + row;
-            for (int c0 = 0; c0 < C::N; c0 += 16) {
+            for (int p = 0; p < 3; ++p) {  // digit p of this warp's 16 tokens: columns p BN + c0 ..
                 int v[16];
-                tmem_ld16(tbase + c0, v);
+                tmem_ld16(tbase + p * BN + c0, v);
 #pragma unroll
-                for (int q = 0; q < 16; ++q) atomicAdd(acc + (c0 + q) * TC_BM, v[q]);  // RED.ADD (result unused)
+                for (int q = 0; q < 16; ++q) atomicAdd(acc + (p * BN + c0 + q) * TC_BM, v[q]);  // RED.ADD
             }
             tc_fence_before();
             __syncwarp();
@@ -487,12 +496,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
             const int cf = sk_owner_of((int64_t)mg * KC, a.total, a.G);
             const int cl = sk_owner_of((int64_t)mg * KC + KC - 1, a.total, a.G);
             int last = 0;
-            if (lane == 0) last = atomicAdd(a.counters + mg * 4 + quarter, 1) == cl - cf;
+            int* cnt = a.counters + mg * 8 + quarter * 2 + half;
+            if (lane == 0) last = atomicAdd(cnt, 1) == cl - cf;
             last = __shfl_sync(0xffffffffu, last, 0);
             if (!last) continue;
             __threadfence();
-            if (lane == 0) a.counters[mg * 4 + quarter] = 0;  // ready for the next launch
-            for (int c0 = 0; c0 < BN; c0 += 16) {
+            if (lane == 0) *cnt = 0;  // ready for the next launch
+            {
                 int h[16], m[16], l[16];
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
