@@ -1,53 +1,75 @@
 // Wire codec: blockwise absmax int8 (quant.py:33-66 via transport/wire.py:98-105,125-137).
 //
-// HBM-bound: 4 B read + 1 B + 4/64 B written per element on encode. For the
-// default block of 64, a 16-lane half-warp owns one block (4 elements per lane
-// as one float4), so a warp moves two blocks per iteration with 128-bit loads,
-// a 4-step shuffle max and one 32-bit store of codes per lane. Other block
-// sizes use one warp per block with a strided loop. Bit-exact with the
-// reference (see wire_code in pb_common.cuh).
+// HBM-bound: 4 B read + 1 B + 4/64 B written per element on encode, the
+// reverse on decode. Other block sizes than the default 64 use one warp per
+// block with a strided loop. Bit-exact with the reference (see wire_code in
+// pb_common.cuh; tests/test_gpu_codec.py).
 #include "pb_common.cuh"
 
 namespace pb {
 
+// block 64: a lane owns 16 consecutive elements (four 128-bit streaming loads
+// issued together), four lanes own a block (two-step shuffle max), a warp moves
+// 8 blocks = 2 KB of f32 per iteration and stores its codes as one 16-B word
+// per lane. The code of x is round_half_away(|x| / s) decided exactly: the
+// candidate comes from |x| * (1/s) (one reciprocal per block instead of an
+// IEEE division per element; within one unit of the exact quotient) and the two
+// fma residuals of exact_round_away_pos settle the half-integer boundary.
+__device__ __forceinline__ int wire_code_r(float x, float s, float r, float amax) {
+    if (s < 2.3509887e-38f) return wire_code(x, s, amax);  // zero / tiny scales: the reference's corner cases
+    const float a = fabsf(x);
+    float m = floorf(a * r + 0.5f);
+    if (m > 200.f) m = 200.f;
+    else if (fmaf(-(m + 0.5f), s, a) >= 0.f) m += 1.f;
+    else if (m > 0.f && fmaf(-(m - 0.5f), s, a) < 0.f) m -= 1.f;
+    const int c = m > 127.f ? 127 : (int)m;
+    return x < 0.f ? -c : c;
+}
+
 __global__ void __launch_bounds__(256) k_wire_quant64(const float* __restrict__ x, int64_t n, int8_t* __restrict__ codes,
                                                       float* __restrict__ scales) {
-    const int64_t nb = (n + 63) / 64;
     const int lane = threadIdx.x & 31;
-    const int half = lane >> 4;       // which block of the pair
-    const int sub = lane & 15;        // 4 elements each
+    const int64_t nchunks = (n + 511) / 512;  // warp iterations of 8 blocks
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t b = warp * 2 + half; b - half < nb; b += nwarps * 2) {
-        const int64_t base = b * 64 + sub * 4;
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        const bool blk_ok = b < nb;
-        if (blk_ok) {
-            if (base + 3 < n && ((reinterpret_cast<uintptr_t>(x + base) & 15) == 0)) {
-                float4 f = __ldcs(reinterpret_cast<const float4*>(x + base));
-                v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-            } else {
+    const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(codes)) & 15) == 0;
+    for (int64_t ch = warp; ch < nchunks; ch += nwarps) {
+        const int64_t base = ch * 512 + lane * 16;
+        float v[16];
+        if (vec && base + 15 < n) {
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (base + i < n) v[i] = x[base + i];
+            for (int q = 0; q < 4; ++q) {
+                const float4 f = __ldcs(reinterpret_cast<const float4*>(x + base) + q);
+                v[4 * q] = f.x, v[4 * q + 1] = f.y, v[4 * q + 2] = f.z, v[4 * q + 3] = f.w;
             }
-        }
-        float m = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3])));
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (!blk_ok) continue;
-        const float s = __fdiv_rn(m, 127.f);  // == f32(f64(absmax)/127): see pb_common.cuh
-        uint32_t packed = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) packed |= (uint32_t)(uint8_t)wire_code(v[i], s, m) << (8 * i);
-        if (base + 3 < n && ((reinterpret_cast<uintptr_t>(codes + base) & 3) == 0)) {
-            *reinterpret_cast<uint32_t*>(codes + base) = packed;
         } else {
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-                if (base + i < n) codes[base + i] = (int8_t)(packed >> (8 * i));
+            for (int i = 0; i < 16; ++i) v[i] = base + i < n ? x[base + i] : 0.f;
         }
-        if (sub == 0) scales[b] = s;
+        float m = 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) m = fmaxf(m, fabsf(v[i]));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+        const int64_t b = base >> 6;
+        if (b * 64 >= n) continue;
+        const float s = __fdiv_rn(m, 127.f);  // == f32(f64(absmax)/127): see pb_common.cuh
+        const float r = s > 0.f ? __frcp_rn(s) : 0.f;
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            w[q] = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) w[q] |= (uint32_t)(uint8_t)wire_code_r(v[4 * q + i], s, r, m) << (8 * i);
+        }
+        if (vec && base + 15 < n) {
+            *reinterpret_cast<uint4*>(codes + base) = make_uint4(w[0], w[1], w[2], w[3]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                if (base + i < n) codes[base + i] = (int8_t)(w[i >> 2] >> (8 * (i & 3)));
+        }
+        if ((lane & 3) == 0) scales[b] = s;
     }
 }
 
@@ -76,10 +98,35 @@ __global__ void __launch_bounds__(256) k_wire_dequant(const int8_t* __restrict__
         out[i] = __fmul_rn((float)codes[i], scales[i / block]);
 }
 
+// block 64 (the wire default): 16 elements per thread, one 16-B code load, one
+// scale, four 16-B stores
+__global__ void __launch_bounds__(256) k_wire_dequant64(const int8_t* __restrict__ codes,
+                                                        const float* __restrict__ scales, int64_t n,
+                                                        float* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t * 16 < n; t += stride) {
+        const int64_t base = t * 16;
+        if (base + 15 < n) {
+            const uint4 c = __ldcs(reinterpret_cast<const uint4*>(codes + base));
+            const float s = scales[base >> 6];
+            const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                float4 f;
+                f.x = __fmul_rn((float)(int8_t)(cw[q] & 0xff), s);
+                f.y = __fmul_rn((float)(int8_t)((cw[q] >> 8) & 0xff), s);
+                f.z = __fmul_rn((float)(int8_t)((cw[q] >> 16) & 0xff), s);
+                f.w = __fmul_rn((float)(int8_t)(cw[q] >> 24), s);
+                __stcs(reinterpret_cast<float4*>(out + base) + q, f);
+            }
+        } else {
+            for (int64_t i = base; i < n; ++i) out[i] = __fmul_rn((float)codes[i], scales[i >> 6]);
+        }
+    }
+}
+
 static int grid_for(int64_t work_items, int per_block) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = sm_count() > 0 ? sm_count() : 148;
     int64_t g = ceil_div(work_items, per_block);
     int64_t cap = (int64_t)sms * 8;
     return (int)(g < 1 ? 1 : (g > cap ? cap : g));
@@ -88,7 +135,7 @@ static int grid_for(int64_t work_items, int per_block) {
 int quantize_blockwise(const float* x, int64_t n, int block, int8_t* codes, float* scales, cudaStream_t st) {
     if (n == 0) return PB_OK;
     if (block == 64) {
-        k_wire_quant64<<<grid_for(ceil_div(n, 64) * 16, 256), 256, 0, st>>>(x, n, codes, scales);
+        k_wire_quant64<<<grid_for(ceil_div(n, 512) * 32, 256), 256, 0, st>>>(x, n, codes, scales);
     } else {
         k_wire_quant_any<<<grid_for(ceil_div(n, block) * 32, 256), 256, 0, st>>>(x, n, block, codes, scales);
     }
@@ -98,7 +145,11 @@ int quantize_blockwise(const float* x, int64_t n, int block, int8_t* codes, floa
 int dequantize_blockwise(const int8_t* codes, const float* scales, int64_t n, int block, float* out,
                          cudaStream_t st) {
     if (n == 0) return PB_OK;
-    k_wire_dequant<<<grid_for(n, 256), 256, 0, st>>>(codes, scales, n, block, out);
+    const bool vec = ((reinterpret_cast<uintptr_t>(codes) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    if (block == 64 && vec)
+        k_wire_dequant64<<<grid_for(ceil_div(n, 16), 256), 256, 0, st>>>(codes, scales, n, out);
+    else
+        k_wire_dequant<<<grid_for(n, 256), 256, 0, st>>>(codes, scales, n, block, out);
     return launch_check("wire_dequant");
 }
 

@@ -235,7 +235,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
                 tmem_ld16(tbase + c0, h);
                 tmem_ld16(tbase + TC_BN + c0, m);
                 tmem_ld16(tbase + 2 * TC_BN + c0, l);
+#if !(defined(SK_EXP) && (SK_EXP & 32))
                 tc_epi16(a.epi, o, lane, nt * TC_BN + c0, s_tok + c0, h, m, l);
+#endif
             }
             tc_fence_before();
             __syncwarp();
