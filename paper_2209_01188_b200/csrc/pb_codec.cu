@@ -8,10 +8,10 @@
 
 namespace pb {
 
-// block 64: a lane owns 32 consecutive elements (eight 128-bit streaming loads
-// issued together), two lanes own a block (one shuffle for the max), a warp
-// moves 16 blocks = 4 KB of f32 per iteration and stores its codes as two 16-B
-// words per lane. The code of x is round_half_away(|x| / s) decided exactly: the
+// block 64: a lane owns 16 consecutive elements (four 128-bit streaming loads
+// issued together), four lanes own a block (two-step shuffle max), a warp moves
+// 8 blocks = 2 KB of f32 per iteration and stores its codes as one 16-B word
+// per lane. The code of x is round_half_away(|x| / s) decided exactly: the
 // candidate comes from |x| * (1/s) (one reciprocal per block instead of an
 // IEEE division per element; within one unit of the exact quotient) and the two
 // fma residuals of exact_round_away_pos settle the half-integer boundary.
@@ -29,47 +29,47 @@ __device__ __forceinline__ int wire_code_r(float x, float s, float r, float amax
 __global__ void __launch_bounds__(256) k_wire_quant64(const float* __restrict__ x, int64_t n, int8_t* __restrict__ codes,
                                                       float* __restrict__ scales) {
     const int lane = threadIdx.x & 31;
-    const int64_t nchunks = (n + 1023) / 1024;  // warp iterations of 16 blocks
+    const int64_t nchunks = (n + 511) / 512;  // warp iterations of 8 blocks
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(codes)) & 15) == 0;
     for (int64_t ch = warp; ch < nchunks; ch += nwarps) {
-        const int64_t base = ch * 1024 + lane * 32;
-        float v[32];
-        if (vec && base + 31 < n) {
+        const int64_t base = ch * 512 + lane * 16;
+        float v[16];
+        if (vec && base + 15 < n) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < 4; ++q) {
                 const float4 f = __ldcs(reinterpret_cast<const float4*>(x + base) + q);
                 v[4 * q] = f.x, v[4 * q + 1] = f.y, v[4 * q + 2] = f.z, v[4 * q + 3] = f.w;
             }
         } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = base + i < n ? x[base + i] : 0.f;
+            for (int i = 0; i < 16; ++i) v[i] = base + i < n ? x[base + i] : 0.f;
         }
         float m = 0.f;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) m = fmaxf(m, fabsf(v[i]));
+        for (int i = 0; i < 16; ++i) m = fmaxf(m, fabsf(v[i]));
         m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
         const int64_t b = base >> 6;
         if (b * 64 >= n) continue;
         const float s = __fdiv_rn(m, 127.f);  // == f32(f64(absmax)/127): see pb_common.cuh
         const float r = s > 0.f ? __frcp_rn(s) : 0.f;
-        uint32_t w[8];
+        uint32_t w[4];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 4; ++q) {
             w[q] = 0;
 #pragma unroll
             for (int i = 0; i < 4; ++i) w[q] |= (uint32_t)(uint8_t)wire_code_r(v[4 * q + i], s, r, m) << (8 * i);
         }
-        if (vec && base + 31 < n) {
-            reinterpret_cast<uint4*>(codes + base)[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            reinterpret_cast<uint4*>(codes + base)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        if (vec && base + 15 < n) {
+            *reinterpret_cast<uint4*>(codes + base) = make_uint4(w[0], w[1], w[2], w[3]);
         } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
+            for (int i = 0; i < 16; ++i)
                 if (base + i < n) codes[base + i] = (int8_t)(w[i >> 2] >> (8 * (i & 3)));
         }
-        if ((lane & 1) == 0) scales[b] = s;
+        if ((lane & 3) == 0) scales[b] = s;
     }
 }
 
@@ -135,7 +135,7 @@ static int grid_for(int64_t work_items, int per_block) {
 int quantize_blockwise(const float* x, int64_t n, int block, int8_t* codes, float* scales, cudaStream_t st) {
     if (n == 0) return PB_OK;
     if (block == 64) {
-        k_wire_quant64<<<grid_for(ceil_div(n, 1024) * 32, 256), 256, 0, st>>>(x, n, codes, scales);
+        k_wire_quant64<<<grid_for(ceil_div(n, 512) * 32, 256), 256, 0, st>>>(x, n, codes, scales);
     } else {
         k_wire_quant_any<<<grid_for(ceil_div(n, block) * 32, 256), 256, 0, st>>>(x, n, block, codes, scales);
     }
