@@ -22,6 +22,9 @@ static uint64_t* g_trace = nullptr;
 static int64_t g_trace_cap = 0, g_trace_used = 0;
 static std::vector<int64_t> g_trace_meta;
 
+static bool trace_active() { return g_trace != nullptr; }
+constexpr int GRAPH_MAX_TOKENS = 64;
+
 uint64_t* trace_region(int kind, int ctas) {
     if (!g_trace || g_trace_used + TRACE_WORDS * (int64_t)ctas > g_trace_cap) return nullptr;
     uint64_t* p = g_trace + g_trace_used;
@@ -101,6 +104,11 @@ void free_span(pb_span* s) {
         if (s->meta_ev[i]) cudaEventDestroy(s->meta_ev[i]);
     }
     for (auto e : s->prof_ev) cudaEventDestroy(e);
+    for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second.exec);
+    s->graphs.clear();
+    if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
+    cudaFree(s->g_in);
+    cudaFree(s->g_out);
 }
 
 __global__ void k_fill(float* p, int64_t n, float v) {
@@ -178,6 +186,11 @@ int pb_span_create(const pb_span_config* cfg, pb_span** out) {
     if (!rc) rc = dalloc(s, &s->tokmax_act, NT);
     s->partial_cap = (int64_t)8 << 20;
     if (!rc) rc = dalloc(s, &s->partials, s->partial_cap);
+    if (!rc && cfg->graphs) {
+        rc = dalloc(s, &s->g_in, (int64_t)GRAPH_MAX_TOKENS * d);
+        if (!rc) rc = dalloc(s, &s->g_out, (int64_t)GRAPH_MAX_TOKENS * d);
+        if (!rc && cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking) != cudaSuccess) rc = PB_ERR_GENERIC;
+    }
     if (!rc && s->bcanon) {  // batched-decode tcgen05 kernel: split-row-group sums, zero between launches
         s->sk_acc_elems = ceil_div(std::max(3 * d, rd), 128) * 96 * 128;
         rc = dalloc(s, &s->sk_acc, s->sk_acc_elems);
@@ -607,6 +620,55 @@ static int stage_meta(pb_span* s, int n_tok, int n_seq, const int32_t* tok_seq, 
     return PB_OK;
 }
 
+// Decode steps as CUDA graphs (pb_span_config.graphs): at small shapes a step is
+// bound by the host issuing ~5 launches per block (560M: 121 launches, 970 us of
+// host time for 1070 us per step), not by the GPU. The launch sequence of
+// run_blocks depends only on the shape key below; the per-step metadata
+// (positions, pages, attention work units) reaches the device through the
+// usual staged copies into fixed buffers, and the hidden states through g_in /
+// g_out, so one captured graph per key replays every step of that shape (a
+// batch-1 session re-captures when its attention stage count grows, every 64
+// tokens).
+static int run_blocks_graph(pb_span* s, int n_tok, int max_pos, const float* d_in, float* d_out, cudaStream_t st) {
+    const pb_span::GraphKey key{n_tok, s->last_n_seq, s->n_groups, s->total_units, s->max_stages, s->max_group,
+                                s->last_n_seq == n_tok ? 1 : 0};
+    auto it = s->graphs.find(key);
+    if (it == s->graphs.end()) {
+        if (s->graphs.size() >= 64) {  // bounded cache
+            for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second.exec);
+            s->graphs.clear();
+        }
+        // capture on a private stream (the legacy default stream cannot be captured), after
+        // the metadata copies of this step so the capture's dependencies start clean
+        cudaEvent_t ev;
+        PB_CHECK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        PB_CHECK_CUDA(cudaEventRecord(ev, st));
+        PB_CHECK_CUDA(cudaStreamWaitEvent(s->cap_stream, ev, 0));
+        PB_CHECK_CUDA(cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal));
+        const int rc = run_blocks(s, n_tok, max_pos, s->g_in, s->g_out, s->cap_stream);
+        cudaGraph_t g = nullptr;
+        const cudaError_t ec = cudaStreamEndCapture(s->cap_stream, &g);
+        cudaEventDestroy(ev);
+        if (rc) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        PB_CHECK_CUDA(ec);
+        pb_span::GraphEntry e;
+        const cudaError_t ei = cudaGraphInstantiate(&e.exec, g, 0);
+        cudaGraphDestroy(g);
+        PB_CHECK_CUDA(ei);
+        e.launches = s->last_launches;
+        it = s->graphs.emplace(key, e).first;
+    }
+    const size_t bytes = sizeof(float) * (size_t)n_tok * s->d;
+    if (d_in != s->g_in) PB_CHECK_CUDA(cudaMemcpyAsync(s->g_in, d_in, bytes, cudaMemcpyDeviceToDevice, st));
+    PB_CHECK_CUDA(cudaGraphLaunch(it->second.exec, st));
+    if (d_out != s->g_out) PB_CHECK_CUDA(cudaMemcpyAsync(d_out, s->g_out, bytes, cudaMemcpyDeviceToDevice, st));
+    s->last_launches = it->second.launches;
+    return PB_OK;
+}
+
 extern "C" int pb_span_step(pb_span* span, int32_t n_tok, int32_t n_seq, const int32_t* h_tok_seq,
                             const int32_t* h_tok_pos, const int32_t* h_pages, const float* d_in, float* d_out,
                             void* stream) {
@@ -616,6 +678,8 @@ extern "C" int pb_span_step(pb_span* span, int32_t n_tok, int32_t n_seq, const i
     auto st = (cudaStream_t)stream;
     int max_pos = 0;
     if (int rc = stage_meta(span, n_tok, n_seq, h_tok_seq, h_tok_pos, h_pages, &max_pos, st)) return rc;
+    if (span->cfg.graphs && n_tok <= GRAPH_MAX_TOKENS && !span->prof_on && !trace_active())
+        return run_blocks_graph(span, n_tok, max_pos, d_in, d_out, st);
     return run_blocks(span, n_tok, max_pos, d_in, d_out, st);
 }
 

@@ -3,8 +3,10 @@
 // tape + BACKWARD). Not part of the C-ABI.
 #pragma once
 
+#include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "pb_common.cuh"
@@ -59,6 +61,14 @@ struct pb_span {
     int64_t bytes = 0;
     int32_t last_launches = 0;
     int last_n_seq = 0;
+    // CUDA-graph replay of decode steps: the launch sequence of run_blocks depends only on
+    // this key (n_tok, n_seq, n_groups, total_units, max_stages, max_group, decode-only); inputs
+    // and outputs go through the fixed buffers g_in / g_out, metadata through d_tok_* as usual
+    using GraphKey = std::tuple<int, int, int, int64_t, int, int, int>;
+    struct GraphEntry { cudaGraphExec_t exec = nullptr; int32_t launches = 0; };
+    std::map<GraphKey, GraphEntry> graphs;
+    cudaStream_t cap_stream = nullptr;
+    float *g_in = nullptr, *g_out = nullptr;  // [64][d]
     std::mutex mu;  // one step at a time per span (the stream is shared)
 };
 

@@ -330,3 +330,29 @@ def test_bloom176b_tcgen05_prefill_vs_f64_reference():
         err = float((got - want).abs().max() / want.abs().max())
         assert err <= TOL, (a, err)
     span.close()
+
+
+@pytest.mark.parametrize("name", ["mid"])
+def test_graph_replay_bit_identical(name):
+    """Decode steps replayed as CUDA graphs (pb_span_config.graphs) give the
+    same bits as the launch-by-launch path, across the 64-token attention
+    stage boundary (a re-capture) and for batched steps."""
+    import torch
+
+    shape = SHAPES[name]
+    outs = {}
+    for graphs in (False, True):
+        span = make_span(shape, graphs=graphs)
+        rng = np.random.default_rng(2)
+        seqs = [span.new_sequence() for _ in range(2)]
+        res = [span.step([(seqs[0], torch.from_numpy(rng.normal(size=(60, shape.hidden)).astype(np.float32)).cuda())])[0]]
+        for i in range(10):  # positions 60..69 cross the 64-key stage boundary
+            x = torch.from_numpy(rng.normal(size=(1, shape.hidden)).astype(np.float32)).cuda()
+            res.append(span.step([(seqs[0], x)])[0])
+        for i in range(3):  # a batch of two sessions
+            x = torch.from_numpy(rng.normal(size=(2, shape.hidden)).astype(np.float32)).cuda()
+            res.extend(span.step([(seqs[0], x[:1]), (seqs[1], x[1:])]))
+        outs[graphs] = [r.cpu().numpy() for r in res]
+        span.close()
+    for a, b in zip(outs[False], outs[True]):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
