@@ -5,7 +5,7 @@
 // One query per (session, head) makes this pure K/V streaming (2 flops per
 // byte): no tensor cores, no shared-memory ring. CTA c owns one chunk of CS
 // 64-key stages of one (group, head) (cta_base[g] prefix, host-built), 4 warps
-// x AD_KPW keys per iteration, the chunk's K and V rows read straight from HBM into
+// x 16 keys per stage, the chunk's K and V rows read straight from HBM into
 // registers: lane l owns DH/32 dims, so a warp's 32 lanes read one 256-B key
 // row (the rows' 16-B chunks are XOR-swizzled by slot & 7 by the QKV
 // epilogue). Scores in f32 with the f32 query (16 per warp, butterfly-reduced
@@ -23,10 +23,9 @@
 namespace pb {
 
 constexpr int AD_WARPS = 4;
-constexpr int AD_KPW = 8;  // keys per warp per iteration (loads in flight per lane: 2 x AD_KPW)
 
 template <int DH>
-__global__ void __launch_bounds__(AD_WARPS * 32, 8) k_attn_dec(AttnArgs a, const int64_t* __restrict__ cta_base, int CS) {
+__global__ void __launch_bounds__(AD_WARPS * 32) k_attn_dec(AttnArgs a, const int64_t* __restrict__ cta_base, int CS) {
     constexpr int DPL = DH / 32;  // dims per lane (4 or 2)
     __shared__ float wst[AD_WARPS][DH + 2];
     __shared__ int s_last;
@@ -67,14 +66,14 @@ __global__ void __launch_bounds__(AD_WARPS * 32, 8) k_attn_dec(AttnArgs a, const
 #pragma unroll
     for (int e = 0; e < DPL; ++e) acc[e] = 0.f;
 
-    for (int kb = kbeg + warp * AD_KPW; kb < kend; kb += AD_WARPS * AD_KPW) {
-        // AD_KPW consecutive keys share one page (AD_KPW | P)
+    for (int kb = kbeg + warp * 16; kb < kend; kb += AD_WARPS * 16) {
+        // 16 consecutive keys share one page (16 | P)
         const int page = pt[kb / a.P];
         const half* kbase = a.kv + (int64_t)page * 2 * kv_stride + head_off;
-        const int n = min(AD_KPW, kend - kb);
-        uint2 kr[AD_KPW], vr[AD_KPW];  // DPL = 4: 4 halves per row and lane (uint2); DPL = 2: 2 halves (.x)
+        const int n = min(16, kend - kb);
+        uint2 kr[16], vr[16];  // DPL = 4: 4 halves per row and lane (uint2); DPL = 2: 2 halves (.x)
 #pragma unroll
-        for (int j = 0; j < AD_KPW; ++j) {
+        for (int j = 0; j < 16; ++j) {
             if (j < n) {
                 const int slot = (kb + j) % a.P;
                 const half* row = kbase + (int64_t)slot * DH + (((lchunk ^ (slot & 7)) << 3) | loff);
@@ -87,9 +86,9 @@ __global__ void __launch_bounds__(AD_WARPS * 32, 8) k_attn_dec(AttnArgs a, const
                 }
             }
         }
-        float s[AD_KPW];
+        float s[16];
 #pragma unroll
-        for (int j = 0; j < AD_KPW; ++j) {
+        for (int j = 0; j < 16; ++j) {
             const half2 k01 = *reinterpret_cast<const half2*>(&kr[j].x);
             float d = q[0] * __low2float(k01) + q[1] * __high2float(k01);
             if (DPL == 4) {
@@ -101,10 +100,10 @@ __global__ void __launch_bounds__(AD_WARPS * 32, 8) k_attn_dec(AttnArgs a, const
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-            for (int j = 0; j < AD_KPW; ++j) s[j] += __shfl_xor_sync(0xffffffffu, s[j], o);
+            for (int j = 0; j < 16; ++j) s[j] += __shfl_xor_sync(0xffffffffu, s[j], o);
         float mx = m_run;
 #pragma unroll
-        for (int j = 0; j < AD_KPW; ++j) {
+        for (int j = 0; j < 16; ++j) {
             s[j] = j < n ? s[j] + slope * (float)(kb + j - pos) : -INFINITY;
             mx = fmaxf(mx, s[j]);
         }
@@ -113,7 +112,7 @@ __global__ void __launch_bounds__(AD_WARPS * 32, 8) k_attn_dec(AttnArgs a, const
 #pragma unroll
         for (int e = 0; e < DPL; ++e) acc[e] *= corr;
 #pragma unroll
-        for (int j = 0; j < AD_KPW; ++j) {
+        for (int j = 0; j < 16; ++j) {
             if (j < n) {
                 const float p = expf(s[j] - mx);
                 l_run += p;
