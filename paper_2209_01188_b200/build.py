@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpetals_b200.so")
-SOURCES = ["pb_codec.cu", "pb_weights.cu", "pb_gemv.cu", "pb_gemm_tc.cu", "pb_attn.cu", "pb_attn_mma.cu", "pb_attn_dec.cu", "pb_span.cu", "pb_head.cu", "pb_train.cu", "pb_hop.cu"]
+SOURCES = ["pb_codec.cu", "pb_weights.cu", "pb_gemv.cu", "pb_gemm_tc.cu", "pb_attn.cu", "pb_attn_mma.cu", "pb_span.cu", "pb_head.cu", "pb_train.cu", "pb_hop.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -10,7 +10,6 @@
 #include <string>
 #include <vector>
 
-#include "pb_attn_common.cuh"
 #include "pb_common.cuh"
 #include "pb_span.h"
 
@@ -97,7 +96,7 @@ void free_span(pb_span* s) {
     }
     void* ptrs[] = {s->kv, s->slopes, s->xa, s->mid, s->q, s->ctx, s->act, s->xo, s->y32, s->frag, s->bcanon, s->back, s->stats, s->pst_x, s->pst_mid, s->tokmax_ctx, s->tokmax_act,
                     s->partials, s->counters, s->attn_part, s->d_tok_seq, s->d_tok_pos, s->d_pages, s->d_grp_first, s->d_grp_count,
-                    s->hop_codes, s->hop_scales, s->d_unit_base, s->sk_acc, s->d_cta_base};
+                    s->hop_codes, s->hop_scales, s->d_unit_base, s->sk_acc};
     for (void* p : ptrs) cudaFree(p);
     for (int i = 0; i < pb_span::NSLOT; ++i) {
         if (s->h_meta[i]) cudaFreeHost(s->h_meta[i]);
@@ -207,12 +206,11 @@ int pb_span_create(const pb_span_config* cfg, pb_span** out) {
     if (!rc) rc = dalloc(s, &s->d_grp_first, NT);
     if (!rc) rc = dalloc(s, &s->d_grp_count, NT);
     if (!rc) rc = dalloc(s, &s->d_unit_base, NT + 1);
-    if (!rc) rc = dalloc(s, &s->d_cta_base, NT + 1);
     if (!rc) rc = dalloc(s, &s->hop_codes, (int64_t)NT * d);
     if (!rc) rc = dalloc(s, &s->hop_scales, ceil_div((int64_t)NT * d, 64));
     for (int i = 0; !rc && i < pb_span::NSLOT; ++i) {
         if (cudaMallocHost((void**)&s->h_meta[i], sizeof(int32_t) * s->meta_ints) != cudaSuccess ||
-            cudaMallocHost((void**)&s->h_ub[i], sizeof(int64_t) * 2 * (NT + 1)) != cudaSuccess ||
+            cudaMallocHost((void**)&s->h_ub[i], sizeof(int64_t) * (NT + 1)) != cudaSuccess ||
             cudaEventCreateWithFlags(&s->meta_ev[i], cudaEventDisableTiming) != cudaSuccess) {
             set_error("pinned staging allocation failed");
             rc = PB_ERR_GENERIC;
@@ -511,11 +509,7 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                     s->max_group};
         {
             const int ev = prof_begin(s, st);
-            // decode steps (one query per group) use the streaming single-query kernel
-            const bool dec = s->max_group == 1 && (s->dh == 64 || s->dh == 128) && s->attn_dec;
-            if (int rc = dec ? run_attn_dec(aa, s->d_cta_base, s->dec_ctas, s->dec_cs, s->attn_cap, st)
-                             : launch_attention(aa, s->attn_cap, st))
-                return rc;
+            if (int rc = launch_attention(aa, s->attn_cap, st)) return rc;
             // fp16 K and V rows read for every query token (2 T h 2 B per session-block)
             double kv_bytes = 0.0;
             for (int i = 0; i < n_tok; ++i) kv_bytes += 4.0 * (s->h_tok_pos_last[i] + 1) * d;
@@ -622,18 +616,6 @@ static int stage_meta(pb_span* s, int n_tok, int n_seq, const int32_t* tok_seq, 
     for (int g = 0; g < ng; ++g) mg_ = std::max(mg_, (int)gc[g]);
     s->max_group = mg_;
     PB_CHECK_CUDA(cudaMemcpyAsync(s->d_unit_base, ub, sizeof(int64_t) * (ng + 1), cudaMemcpyHostToDevice, st));
-    // single-query decode attention (k_attn_dec): one CTA per (group, head, chunk of dec_cs stages),
-    // chunks sized so a (group, head) has at most AM_MAXC of them
-    s->dec_cs = std::max(1, (int)ceil_div(mst, AM_MAXC));
-    int64_t* cb = ub + (ng + 1);
-    int64_t ct = 0;
-    for (int g = 0; g < ng; ++g) {
-        cb[g] = ct;
-        ct += (int64_t)s->H * ceil_div((int)ceil_div(tok_pos[gf[g]] + gc[g], 64), s->dec_cs);
-    }
-    cb[ng] = ct;
-    s->dec_ctas = ct;
-    PB_CHECK_CUDA(cudaMemcpyAsync(s->d_cta_base, cb, sizeof(int64_t) * (ng + 1), cudaMemcpyHostToDevice, st));
     PB_CHECK_CUDA(cudaEventRecord(s->meta_ev[slot], st));
     return PB_OK;
 }
@@ -649,7 +631,7 @@ static int stage_meta(pb_span* s, int n_tok, int n_seq, const int32_t* tok_seq, 
 // tokens).
 static int run_blocks_graph(pb_span* s, int n_tok, int max_pos, const float* d_in, float* d_out, cudaStream_t st) {
     const pb_span::GraphKey key{n_tok, s->last_n_seq, s->n_groups, s->total_units, s->max_stages, s->max_group,
-                                s->last_n_seq == n_tok ? 1 : 0, s->dec_ctas};
+                                s->last_n_seq == n_tok ? 1 : 0};
     auto it = s->graphs.find(key);
     if (it == s->graphs.end()) {
         if (s->graphs.size() >= 64) {  // bounded cache

@@ -184,8 +184,6 @@ struct AttnArgs {
     uint64_t* trace = nullptr; // diagnostics (pb_trace_set)
 };
 int launch_attention(const AttnArgs& a, int64_t part_cap, cudaStream_t st);
-// single-query decode attention (pb_attn_dec.cu): n_ctas = sum over groups of H x chunks of cs stages
-int run_attn_dec(const AttnArgs& a, const int64_t* d_cta_base, int64_t n_ctas, int cs, int64_t cap, cudaStream_t st);
 
 
 

@@ -14,10 +14,6 @@
 
 using pb::BlockW;
 
-#ifndef PB_ATTN_DEC
-#define PB_ATTN_DEC 1
-#endif
-
 struct pb_span {
     pb_span_config cfg{};
     int d = 0, H = 0, dh = 0, rd = 0, max_pages = 0;
@@ -45,10 +41,6 @@ struct pb_span {
     int32_t *d_grp_first = nullptr, *d_grp_count = nullptr;
     int n_groups = 0;
     int64_t* d_unit_base = nullptr;  // stream-K attention units per query group
-    int64_t* d_cta_base = nullptr;   // k_attn_dec CTAs per query group (single-query decode steps)
-    int64_t dec_ctas = 0;
-    int dec_cs = 1;                  // 64-key stages per k_attn_dec chunk
-    bool attn_dec = PB_ATTN_DEC;     // A/B builds (-DPB_ATTN_DEC=0): the tensor-core kernel for decode too
     int64_t total_units = 0;
     int max_stages = 0;
     int max_group = 0;
@@ -72,7 +64,7 @@ struct pb_span {
     // CUDA-graph replay of decode steps: the launch sequence of run_blocks depends only on
     // this key (n_tok, n_seq, n_groups, total_units, max_stages, max_group, decode-only); inputs
     // and outputs go through the fixed buffers g_in / g_out, metadata through d_tok_* as usual
-    using GraphKey = std::tuple<int, int, int, int64_t, int, int, int, int64_t>;
+    using GraphKey = std::tuple<int, int, int, int64_t, int, int, int>;
     struct GraphEntry { cudaGraphExec_t exec = nullptr; int32_t launches = 0; };
     std::map<GraphKey, GraphEntry> graphs;
     cudaStream_t cap_stream = nullptr;
