@@ -195,24 +195,6 @@ int bound_consts(const float* gamma, const float* beta, const float* scales, int
     return PB_OK;
 }
 
-// Warm L2 with the first bytes of every stream-K CTA range of the GEMV that
-// consumes this operand, while HBM would otherwise idle: during the attention
-// kernel (wo: issued before the dependency wait, the operand writer being
-// resident early) or during the operand writer itself (after the wait: the
-// previous GEMV has drained). The GEMV's TMA copies of those stages then hit L2.
-__device__ __forceinline__ void l2_prefetch_gemv(const ProArgs& a) {
-    if (!a.pf_codes) return;
-    const int64_t nthr = (int64_t)gridDim.x * gridDim.y * blockDim.x;
-    const int64_t gt = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
-    for (int64_t c = gt; c < a.pf_G; c += nthr) {
-        const int64_t u0 = c * a.pf_total / a.pf_G, u1 = (c + 1) * a.pf_total / a.pf_G;
-        const int64_t beg = u0 * 4096 + a.pf_skip;
-        const int64_t end = min(u1 * 4096, beg + a.pf_bytes);
-        for (int64_t b = beg; b < end; b += 32768)
-            bulk_prefetch_l2(a.pf_codes + b, (uint32_t)min((int64_t)32768, end - b));
-    }
-}
-
 // k_fragwrite: one thread per (token, 32-wide k tile, lane quad q).
 // Specialised per (operand mode, statistics source) so the code on the
 // dependency-release critical path is compact (it runs cold in the
@@ -231,9 +213,7 @@ __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
     const int it = blockIdx.x * blockDim.x + threadIdx.x;
     FragParams fp;
     if (it < KC * 4) frag_params(a, it >> 2, it & 3, fp);  // weights: before the dependency wait
-    if (a.pf_early) l2_prefetch_gemv(a);
     pdl_wait();
-    if (!a.pf_early) l2_prefetch_gemv(a);
     if (!a.early) pdl_trigger();
     if (threadIdx.x == 0) trace_stamp(a.trace, tcta, 1);
     const int tok = blockIdx.y;
@@ -329,18 +309,10 @@ int prepare_fused_operand(int mode, const ProSrc& src, const float* x, int n_tok
 
 int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int K, int Kp, const float* gamma,
                     const float* beta, const Mat& m, int tc, uint4* frag, float* back, float4* stats, float* xo,
-                    float* y32, cudaStream_t st, uint8_t* bcanon, int bcanon_tile, const ProArgs* l2pf) {
+                    float* y32, cudaStream_t st, uint8_t* bcanon, int bcanon_tile) {
     constexpr int early = 1;  // weight-side operand inputs loaded before the PDL wait
     ProArgs a{mode, x, K, Kp, gamma, beta, y32 ? nullptr : m.scales, m.n_outl, m.outl_idx, tc, frag, back, stats,
               xo, y32, src, early};
-    if (l2pf) {
-        a.pf_codes = l2pf->pf_codes;
-        a.pf_total = l2pf->pf_total;
-        a.pf_G = l2pf->pf_G;
-        a.pf_skip = l2pf->pf_skip;
-        a.pf_bytes = l2pf->pf_bytes;
-        a.pf_early = l2pf->pf_early;
-    }
     if (y32) a.src = ProSrc{};
     if (a.src.kind == SRC_STATS && (mode == PRO_LN || !y32)) {
         k_rowstats<<<n_tok, STATS_THREADS, 0, st>>>(a);

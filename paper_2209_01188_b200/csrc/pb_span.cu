@@ -23,12 +23,6 @@ static int64_t g_trace_cap = 0, g_trace_used = 0;
 static std::vector<int64_t> g_trace_meta;
 
 static bool trace_active() { return g_trace != nullptr; }
-#ifndef PB_PF_WO_KB
-#define PB_PF_WO_KB 256   // L2 prefetch per wo-GEMV CTA during attention (KB)
-#endif
-#ifndef PB_PF_GAP_KB
-#define PB_PF_GAP_KB 128  // L2 prefetch per GEMV CTA during its operand writer (KB)
-#endif
 constexpr int GRAPH_MAX_TOKENS = 64;
 
 uint64_t* trace_region(int kind, int ctas) {
@@ -468,24 +462,9 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                     prof_end(s, ev, 0, bytes, st);
                     return rc;
                 }
-                // decode GEMVs (one CTA per SM, stream-K over MG x KC units): warm L2 with the
-                // start of every CTA's range while HBM idles (attention / operand writer)
-                ProArgs pf{};
-                const ProArgs* pfp = nullptr;
-                const int sms = sm_count();
-                const int64_t units = (int64_t)(m.Mp / 128) * (m.Kp / 32);
-                if (n_tok <= 2 && tc == 2 && sms > 0 && units / 32 >= sms && (PB_PF_WO_KB > 0 || PB_PF_GAP_KB > 0)) {
-                    pf.pf_codes = m.codes;
-                    pf.pf_total = units;
-                    pf.pf_G = sms;
-                    pf.pf_early = mi == 1;  // wo: during the attention kernel
-                    pf.pf_skip = pf.pf_early ? 0 : 4 * 32768;  // else past the GEMV's own first ring fill
-                    pf.pf_bytes = (pf.pf_early ? PB_PF_WO_KB : PB_PF_GAP_KB) * 1024;
-                    if (pf.pf_bytes > 0) pfp = &pf;
-                }
                 int ev = prof_begin(s, st);
                 if (int rc = launch_prologue(mode, src, x, n_tok, K, m.Kp, g, be, m, tc, s->frag, s->back, s->stats,
-                                             s->xo, nullptr, st, nullptr, TC_TOKENS, pfp))
+                                             s->xo, nullptr, st))
                     return rc;
                 prof_end(s, ev, 2, 4.0 * n_tok * K, st);
                 launches += src.kind == SRC_STATS ? 3 : 2;  // (rowstats +) fragwrite + gemv

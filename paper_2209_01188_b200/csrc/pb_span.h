@@ -107,13 +107,11 @@ int dequantize_blockwise(const int8_t* codes, const float* scales, int64_t n, in
 
 constexpr int TC_MIN_TOKENS_DEFAULT = 64;
 constexpr int TC_TOKENS = 80;  // tokens per tcgen05 tile (3 digit accumulators x 80 columns, double-buffered in TMEM)
-struct ProArgs;
 // prologue: y = LN(x) (PRO_LN) or x (PRO_SCALE); writes the int8-digit operand of
 // y * scales, the per-token 2^-shift, outlier activations xo, and (f32 mode) y.
 int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int K, int Kp, const float* gamma,
                     const float* beta, const Mat& m, int tc, uint4* frag, float* back, float4* stats, float* xo,
-                    float* y32, cudaStream_t st, uint8_t* bcanon = nullptr, int bcanon_tile = TC_TOKENS,
-                    const ProArgs* l2pf = nullptr);
+                    float* y32, cudaStream_t st, uint8_t* bcanon = nullptr, int bcanon_tile = TC_TOKENS);
 // tcgen05 GEMM over a canonical-layout B operand (pb_gemm_tc.cu)
 int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Epi& epi, cudaStream_t st);
 // batched decode (n_tok <= tile_tokens in {16, 32}): stream-K tcgen05 GEMM over a canonical B operand
@@ -142,11 +140,6 @@ struct ProArgs {
     ProSrc src;
     int early;
     uint64_t* trace = nullptr;  // diagnostics (pb_trace_set)
-    // L2 prefetch of the consuming GEMV's weights (k_fragwrite): for each of
-    // the GEMV's pf_G stream-K CTAs, bytes [skip, skip + bytes) of its unit range
-    const int8_t* pf_codes = nullptr;
-    int64_t pf_total = 0;
-    int pf_G = 0, pf_skip = 0, pf_bytes = 0, pf_early = 0;
 };
 
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
