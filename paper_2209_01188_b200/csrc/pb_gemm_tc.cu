@@ -60,9 +60,6 @@ constexpr int TC_PLANE = TC_BN * 32;       // one digit plane per k tile
 constexpr int TC_B = 3 * TC_PLANE;
 constexpr int TC_ACC = 256;                // TMEM columns per accumulator set (3 x 80 used)
 constexpr int TC_TMEM_COLS = 512;
-#ifndef PB_TC_PAIR
-#define PB_TC_PAIR 1  // prefill on CTA pairs (k_gemm_tc2); 0: the one-CTA kernel (A/B builds)
-#endif
 constexpr size_t TC_SMEM =
     (size_t)TC_STAGES * TC_KT * (TC_A + TC_B) + (2 * TC_STAGES + 4) * 8 + 16 + TC_BN * sizeof(TokInfo);
 
@@ -255,206 +252,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
     }
 }
 
-// ------------------------------------------------------------------ prefill, CTA pair (cta_group::2)
-//
-// The one-CTA kernel holds 16 k tiles (11.5 KB each: 4 KB of weights + 7.5 KB
-// of digit planes) in its ring -- about 1 us of tensor work, less than a
-// refill's latency under load, so the tensor pipe idles ~half the time
-// (ncu: 42 % active, smem and L2 pipes far from busy). With a CTA pair on one
-// TPC issuing tcgen05.mma.cta_group::2 (M = 256: the pair's two row groups,
-// N = 240), each CTA stages its own 128 weight rows and HALF of the digit
-// planes (120 of the 240 B rows, 3.75 KB per k tile): 7.75 KB per k tile per
-// SM for the same tensor work, so the same shared memory buys 6 stages of 4 k
-// tiles (1.5x the depth). The leader (rank 0) issues the MMAs once both CTAs'
-// stages landed (the follower's idle MMA warp forwards its full barriers to
-// the leader); commits are multicast to both CTAs; both epilogues read their
-// own TMEM (their own 128 rows) and release the accumulator set to the leader.
-
-constexpr int TC2_STAGES = 6;
-constexpr int TC2_BH = TC_B / 2;  // 3840 B: 120 digit-plane rows per k tile
-constexpr size_t TC2_SMEM =
-    (size_t)TC2_STAGES * TC_KT * (TC_A + TC2_BH) + (3 * TC2_STAGES + 4) * 8 + 16 + TC_BN * sizeof(TokInfo);
-constexpr uint32_t TC2_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)((3 * TC_BN) >> 3) << 17) |
-                               ((uint32_t)(256 >> 4) << 24);
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// shared::cluster address of `p` (a local smem object) in CTA `rank` of the cluster
-__device__ __forceinline__ uint32_t mapa_rank(const void* p, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-// bounded wait: a protocol error traps (kills the context) instead of hanging the GPU
-__device__ __forceinline__ void mbar_wait_b(uint64_t* bar, uint32_t parity) {
-    uint32_t ok = 0;
-    for (uint32_t n = 0; !ok; ++n) {
-        asm volatile(
-            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-        if (n > (1u << 28)) __trap();
-    }
-}
-__device__ __forceinline__ void tc2_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(TC2_IDESC), "r"(accumulate));
-}
-__device__ __forceinline__ void tc2_commit_both(uint64_t* bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-            smem_u32(bar)),
-        "h"((uint16_t)3)
-        : "memory");
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) k_gemm_tc2(TcArgs a) {
-    extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* sa = smem;                                  // [STAGES][KT][4 KB]: this CTA's 128 weight rows
-    uint8_t* sb = sa + TC2_STAGES * TC_KT * TC_A;        // [STAGES][KT][3840 B]: this CTA's half of the planes
-    uint64_t* full = reinterpret_cast<uint64_t*>(sb + TC2_STAGES * TC_KT * TC2_BH);
-    uint64_t* full2 = full + TC2_STAGES;   // leader: the follower's stage landed (forwarded)
-    uint64_t* empty = full2 + TC2_STAGES;  // MMA commit (multicast to both CTAs)
-    uint64_t* accfull = empty + TC2_STAGES;  // [2] MMA commit (multicast)
-    uint64_t* accempty = accfull + 2;        // [2] leader: both CTAs' epilogue warps
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
-    TokInfo* s_tok = reinterpret_cast<TokInfo*>(tmem_slot + 4);
-
-    const int warp = warp_uniform_id(), lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
-    const int KC = a.KC;
-    const int pair = (int)(blockIdx.x >> 1), NP = (int)(gridDim.x >> 1);
-    const int units = (a.MG / 2) * a.NTL, mgs = a.MG / 2;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < TC2_STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&full2[s], 1);
-            mbar_init(&empty[s], 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&accfull[b], 1);
-            mbar_init(&accempty[b], 2 * TC_EPI_WARPS);
-        }
-        mbar_fence_init();
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(TC_TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-    }
-    tc_fence_before();
-    cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated in both
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp == 0) {
-        // ---------------- TMA producer (both CTAs): own weight rows + own half of the planes
-        if (lane == 0) {
-            int it = 0;
-            for (int u = pair; u < units; u += NP) {
-                int mgu, nt;
-                tc_unit(a, u, mgs, mgu, nt);
-                const int mg = 2 * mgu + (int)rank;
-                const int8_t* asrc = a.codes + (int64_t)mg * KC * TC_A;
-                const uint8_t* bsrc = a.bcanon + (int64_t)nt * KC * TC_B + rank * TC2_BH;
-                for (int kc = 0; kc < KC; kc += TC_KT, ++it) {
-                    const int s = it % TC2_STAGES, n = min(TC_KT, KC - kc);
-                    mbar_wait_b(&empty[s], ((it / TC2_STAGES) & 1) ^ 1);
-                    mbar_expect_tx(&full[s], n * (TC_A + TC2_BH));
-                    bulk_g2s(sa + s * TC_KT * TC_A, asrc + (int64_t)kc * TC_A, n * TC_A, &full[s]);
-                    for (int k = 0; k < n; ++k)  // this CTA's 120 rows of k tile kc + k (strided by TC_B)
-                        bulk_g2s(sb + (s * TC_KT + k) * TC2_BH, bsrc + (int64_t)(kc + k) * TC_B, TC2_BH, &full[s]);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (rank == 0) {
-            // ---------------- MMA issuer (leader): a stage is consumable once both halves landed
-            if (lane == 0) {
-                int it = 0, i = 0;
-                for (int u = pair; u < units; u += NP, ++i) {
-                    const int b = i & 1;
-                    mbar_wait_b(&accempty[b], ((i >> 1) & 1) ^ 1);
-                    tc_fence_after();
-                    const uint32_t acc = tmem + b * TC_ACC;
-                    for (int kc = 0; kc < KC; kc += TC_KT, ++it) {
-                        const int s = it % TC2_STAGES, n = min(TC_KT, KC - kc);
-                        mbar_wait_b(&full[s], (it / TC2_STAGES) & 1);
-                        mbar_wait_b(&full2[s], (it / TC2_STAGES) & 1);
-                        tc_fence_after();
-                        const uint32_t a0 = smem_u32(sa + s * TC_KT * TC_A), b0 = smem_u32(sb + s * TC_KT * TC2_BH);
-                        for (int k = 0; k < n; ++k)
-                            tc2_mma(acc, umma_desc(a0 + k * TC_A), umma_desc(b0 + k * TC2_BH), (kc | k) != 0);
-                        tc2_commit_both(&empty[s]);
-                    }
-                    tc2_commit_both(&accfull[b]);
-                }
-            }
-        } else if (lane == 0) {
-            // ---------------- follower: forward each landed stage to the leader's full2 barrier
-            const uint32_t leader_full2 = mapa_rank(full2, 0);
-            int it = 0;
-            for (int u = pair; u < units; u += NP)
-                for (int kc = 0; kc < KC; kc += TC_KT, ++it) {
-                    const int s = it % TC2_STAGES;
-                    mbar_wait_b(&full[s], (it / TC2_STAGES) & 1);
-                    mbar_arrive_remote(leader_full2 + 8 * s);
-                }
-        }
-        __syncwarp();
-    } else {
-        // ---------------- epilogue (warps 2-9) of this CTA's 128 rows; releases go to the leader
-        const int quarter = warp & 3, half = (warp - 2) >> 2;
-        const int row = quarter * 32 + lane;
-        const uint32_t leader_accempty = mapa_rank(accempty, 0);
-        int i = 0;
-        for (int u = pair; u < units; u += NP, ++i) {
-            int mgu, nt;
-            tc_unit(a, u, mgs, mgu, nt);
-            const int mg = 2 * mgu + (int)rank;
-            const int b = i & 1;
-            asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");
-            stage_tokens(a.epi, a.act.back, a.act.n_tok, nt * TC_BN, TC_BN, s_tok, (int)threadIdx.x - 64,
-                         32 * TC_EPI_WARPS);
-            asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");
-            mbar_wait_b(&accfull[b], (i >> 1) & 1);
-            tc_fence_after();
-            const int o = mg * TC_BM + row;
-            const uint32_t tbase = tmem + b * TC_ACC + ((uint32_t)(quarter * 32) << 16);
-            for (int c0 = half * 16; c0 < TC_BN; c0 += 32) {
-                int h[16], m[16], l[16];
-                tmem_ld16(tbase + c0, h);
-                tmem_ld16(tbase + TC_BN + c0, m);
-                tmem_ld16(tbase + 2 * TC_BN + c0, l);
-                tc_epi16(a.epi, o, lane, nt * TC_BN + c0, s_tok + c0, h, m, l);
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_remote(leader_accempty + 8 * b);
-        }
-    }
-    tc_fence_before();
-    cluster_sync_all();  // no MMA, commit or remote arrive still targets either CTA
-    if (warp == 1) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS));
-    }
-}
-
 int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Epi& epi, cudaStream_t st) {
     static int ok[PB_MAX_DEVICES] = {};
     if (per_device(ok, [](int) {
@@ -481,18 +278,6 @@ int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Ep
             const int64_t cost = passes * a_all + (bp <= budget ? (int64_t)a.NTL * plane : passes * waves * bp);
             if (cost < best) best = cost, a.ntg = n;
         }
-    }
-    if (PB_TC_PAIR && a.MG % 2 == 0 && sms >= 2) {
-        static int ok2[PB_MAX_DEVICES] = {};
-        if (per_device(ok2, [](int) {
-                return cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)TC2_SMEM) == cudaSuccess ? 1 : -1;
-            }) < 0)
-            return launch_check("gemm_tc2 setup");
-        // persistent: one CTA pair per TPC; units are (row-group pair, token tile)
-        const int pairs = std::min((a.MG / 2) * a.NTL, sms / 2);
-        k_gemm_tc2<<<2 * pairs, TC_THREADS, TC2_SMEM, st>>>(a);
-        return launch_check("gemm_tc2");
     }
     const int grid = std::min(a.tiles, sms);  // persistent: one CTA per SM (TMEM 512 columns)
     k_gemm_tc<<<grid, TC_THREADS, TC_SMEM, st>>>(a);
