@@ -39,9 +39,9 @@ PIN_MIN_BYTES = 4096  # smaller payloads (session ids, decode headers) stay in o
 class PinnedPool:
     """Page-locked host blocks in power-of-two size classes, reused across
     frames (cudaHostAlloc costs far more than a frame). Blocks are torch uint8
-    tensors. A returned block carries a CUDA event recorded on the device's
-    current stream: a DMA still reading it (a step that failed before its
-    stream was synchronized) completes before the block is refilled."""
+    tensors. A handler that DMAs from its payload must have completed the copy
+    before it returns (the server's _decode synchronizes its copy stream): the
+    block is refilled by the next frame right after."""
 
     def __init__(self, device: int, max_cached_bytes: int = 1 << 30):
         self.device = device
@@ -60,24 +60,16 @@ class PinnedPool:
         c = self._cls(n)
         with self._lock:
             lst = self._free.get(c)
-            item = lst.pop() if lst else None
-            if item is not None:
+            if lst:
                 self._cached -= c
-        if item is not None:
-            block, ev = item
-            ev.synchronize()
-            return block
+                return lst.pop()
         return torch.empty(c, dtype=torch.uint8).pin_memory()
 
     def give(self, block) -> None:
-        import torch
-
         c = block.numel()
-        ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream(self.device))
         with self._lock:
             if self._cached + c <= self.max_cached:
-                self._free.setdefault(c, []).append((block, ev))
+                self._free.setdefault(c, []).append(block)
                 self._cached += c
 
 

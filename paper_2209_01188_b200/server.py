@@ -267,6 +267,7 @@ class ServerNode:
         self.timing: list = []  # PB_SERVER_TIMING diagnostics
         self._tapes: dict[bytes, tuple[float, object]] = {}  # tape_id -> (born, device tape [B, n_blocks, t, d])
         self._tapes_lock = threading.Lock()
+        self._io = threading.local()
         self._stop = threading.Event()
         self.rpc: RpcServer | None = None
         self._ckpt = checkpoint
@@ -521,6 +522,35 @@ class ServerNode:
             raise RemoteError(ERR_UNKNOWN_SESSION, "unknown session")
         return s
 
+    # Request / reply codec work runs on a per-handler-thread CUDA stream: on the
+    # compute stream a reply's quantize + D2H (and a request's H2D) would queue
+    # behind whatever step the scheduler launched next -- milliseconds per hop
+    # at the 176B shape. The H2D is complete when _decode returns (the page-locked
+    # receive block goes back to the pool right after the handler).
+
+    def _io_stream(self):
+        import torch
+
+        st = getattr(self._io, "stream", None)
+        if st is None:
+            st = self._io.stream = torch.cuda.Stream(device=self.span.device)
+        return st
+
+    def _decode(self, data):
+        import torch
+
+        st = self._io_stream()
+        with torch.cuda.stream(st):
+            x = codec.decode_tensor(data, device=self.span.device)
+        st.synchronize()
+        return x
+
+    def _encode(self, t, encoding):
+        import torch
+
+        with torch.cuda.stream(self._io_stream()):
+            return codec.encode_tensor(t, encoding)
+
     @staticmethod
     def _internal(e: Exception) -> RemoteError:
         return RemoteError(ERR_GENERIC, f"internal error: {e}")
@@ -563,7 +593,7 @@ class ServerNode:
                 session.position += t
                 raise RemoteError(ERR_GENERIC, "internal error: non-finite tensor")
             tm = [time.perf_counter()] if _TIMING else None
-            x = codec.decode_tensor(tensor, device=self.span.device)
+            x = self._decode(tensor)
             if tm:
                 tm.append(time.perf_counter())
             try:
@@ -580,7 +610,7 @@ class ServerNode:
             session.position += t
             if tm:
                 tm.append(time.perf_counter())
-            reply = codec.encode_tensor(out, self._reply_encoding())
+            reply = self._encode(out, self._reply_encoding())
             session.last_step = (start_pos, digest, reply)
             if tm:
                 tm.append(time.perf_counter())
@@ -635,7 +665,7 @@ class ServerNode:
     def _forward(self, payload) -> bytes:
         try:
             finite = codec.payload_finite(payload)
-            batch = codec.decode_tensor(payload, device=self.span.device)
+            batch = self._decode(payload)
         except SwarmError as e:
             raise self._internal(e) from e
         if batch.ndim != 3:
@@ -651,7 +681,7 @@ class ServerNode:
         tape_id = os.urandom(16)
         with self._tapes_lock:  # server.py:426-428
             self._tapes[tape_id] = (time.monotonic(), tape)
-        return tape_id + codec.encode_tensor(out, self._reply_encoding())
+        return tape_id + self._encode(out, self._reply_encoding())
 
     def _backward(self, payload) -> bytes:
         """server.py:431-450: consume-once tape, f32 reply (gradients travel at full precision)."""
@@ -663,11 +693,11 @@ class ServerNode:
             raise RemoteError(ERR_UNKNOWN_TAPE, "unknown or expired tape")
         _, tape = item
         try:
-            grad = codec.decode_tensor(payload[16:], device=self.span.device)
+            grad = self._decode(payload[16:])
         except SwarmError as e:
             raise self._internal(e) from e
         if grad.ndim != 3 or grad.shape[0] != tape.shape[0]:
             raise RemoteError(ERR_BAD_REQUEST, "BACKWARD grad shape mismatch")
         if tuple(grad.shape[1:]) != tuple(tape.shape[2:]):
             raise self._internal(InputError("BACKWARD grad shape mismatch"))
-        return codec.encode_tensor(self.span.backward(tape, grad), codec.ENC_F32)
+        return self._encode(self.span.backward(tape, grad), codec.ENC_F32)
