@@ -652,6 +652,15 @@ def e2e_record(pl, args, cfg, T0):
     for t in ts:
         t.join()
     wall = time.perf_counter() - t_start
+    if os.environ.get("PB_SERVER_TIMING") == "1" and node.timing:  # diagnostic: per-STEP host split (ms)
+        cols = list(zip(*node.timing[-K * S:]))
+        print("[e2e] STEP decode / compute / encode ms (median):",
+              [round(1e3 * statistics.median(c), 3) for c in cols], file=sys.stderr, flush=True)
+        bt = getattr(node.sched, "timing", None)
+        if bt:
+            d = [[b - a for a, b in zip(t, t[1:])] for t in bt[-K * S:]]
+            print("[e2e] box job send / rank-0 launch / egress launch / ring+egress ms (median):",
+                  [round(1e3 * statistics.median(c), 3) for c in zip(*d)], file=sys.stderr, flush=True)
     node.stop()
     if errors:
         return {"error": errors[0]}

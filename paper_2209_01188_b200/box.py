@@ -40,6 +40,7 @@ import logging
 import os
 import queue
 import threading
+import time
 from dataclasses import dataclass
 
 from .errors import CapacityError, InputError
@@ -50,6 +51,7 @@ from .span import BlockSpan, Sequence
 log = logging.getLogger(__name__)
 
 OP_STEP, OP_RELEASE, OP_FORWARD, OP_BACKWARD, OP_DROP, OP_STOP = 1, 2, 3, 4, 5, 6
+_TIMING = os.environ.get("PB_SERVER_TIMING") == "1"
 HEAD = 12  # op, job, n_seq, fmt, key, B, t, r0, c0, c, tape, (reserved); then (slot, t) pairs
 FMT_F32, FMT_INT8 = 0, 1
 
@@ -338,6 +340,7 @@ class BoxScheduler:
         self.batches = self.batched_steps = 0
         self.egress = state.new_stream()
         self._pending_sends = []
+        self.timing = []  # PB_SERVER_TIMING: (send, rank-0 launch, egress launch, done) per job
         self._stop = False
         self._t = threading.Thread(target=self._loop, name="box-sched", daemon=True)
         self._c = threading.Thread(target=self._complete_loop, name="box-done", daemon=True)
@@ -462,10 +465,14 @@ class BoxScheduler:
     def _launch(self, desc, x, n_tok, place):
         """Send job desc, launch rank 0's part and the egress; `place(out)`
         runs on the completion thread once the ring closed."""
+        t0 = time.perf_counter()
         self._send(desc)
+        t1 = time.perf_counter()
         self.state.apply(desc, x)
+        t2 = time.perf_counter()
         waitable, out = self.state.egress(int(desc[1]), n_tok, self.egress)
-        self.done_q.put((waitable, out, place))
+        t3 = time.perf_counter()
+        self.done_q.put((waitable, out, place, (t0, t1, t2, t3)))
 
     def _submit_steps(self, batch):
         import torch
@@ -550,8 +557,10 @@ class BoxScheduler:
             item = self.done_q.get()
             if item is None:
                 return
-            ev, out, place = item
+            ev, out, place, ts = item
             ev.synchronize()
+            if _TIMING:
+                self.timing.append((*ts, time.perf_counter()))
             self.slots_free.release()
             place(out)
 

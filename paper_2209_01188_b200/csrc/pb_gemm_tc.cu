@@ -235,9 +235,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(TcArgs a) {
                 tmem_ld16(tbase + c0, h);
                 tmem_ld16(tbase + TC_BN + c0, m);
                 tmem_ld16(tbase + 2 * TC_BN + c0, l);
-#if !(defined(SK_EXP) && (SK_EXP & 32))
                 tc_epi16(a.epi, o, lane, nt * TC_BN + c0, s_tok + c0, h, m, l);
-#endif
             }
             tc_fence_before();
             __syncwarp();
@@ -287,17 +285,14 @@ int launch_gemm_tc(const Mat& m, const uint8_t* bcanon, const Act& act, const Ep
 
 // ------------------------------------------------------------------ batched decode: stream-K, one token tile
 
-#ifndef SK_NSETS
-#define SK_NSETS 2
-#endif
-template <int BN, int KT_ = 8, int ST_ = (BN == 32 ? 4 : 4)>
+template <int BN, int KT_ = 8, int ST_ = 4>
 struct SkCfg {
     static constexpr int N = 3 * BN;                         // digit columns (MMA N)
     static constexpr int B_KT = N * 32;                      // digit-plane bytes per 32-wide k tile
     static constexpr int KT = KT_;                           // k tiles per stage
     static constexpr int STAGES = ST_;
     static constexpr int ACC = N <= 64 ? 64 : 128;           // TMEM columns per accumulator set
-    static constexpr int NSETS = SK_NSETS;                   // accumulator sets (segments in flight)
+    static constexpr int NSETS = 2;  // accumulator sets (segments in flight); 4 measured equal
     static constexpr uint32_t IDESC = tc_idesc_i8(N);
     static constexpr size_t SMEM =
         (size_t)STAGES * KT * (TC_A + B_KT) + (2 * STAGES + 2 * NSETS) * 8 + 16 + BN * sizeof(TokInfo);
@@ -370,16 +365,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
                 for (int kc = ka; kc < kb; kc += C::KT, ++it) {
                     const int s = it % C::STAGES, n = min(C::KT, kb - kc);
                     mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
-#if defined(SK_EXP) && (SK_EXP & 2)
-                    mbar_expect_tx(&full[s], n * TC_A);
-                    bulk_g2s(sa + s * C::KT * TC_A, asrc + (int64_t)kc * TC_A, n * TC_A, &full[s]);
-                    if (true) {
-                    } else if (waited) {
-#else
                     mbar_expect_tx(&full[s], n * (TC_A + C::B_KT));
                     bulk_g2s(sa + s * C::KT * TC_A, asrc + (int64_t)kc * TC_A, n * TC_A, &full[s]);
                     if (waited) {
-#endif
                         bulk_g2s(sb + s * C::KT * C::B_KT, a.bcanon + (int64_t)kc * C::B_KT, n * C::B_KT, &full[s]);
                     } else {
                         pend_kc[s] = kc;
@@ -420,11 +408,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
                     mbar_wait(&full[s], (it / C::STAGES) & 1);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sa + s * C::KT * TC_A), b0 = smem_u32(sb + s * C::KT * C::B_KT);
-#if !(defined(SK_EXP) && (SK_EXP & 1))
                     for (int k = 0; k < n; ++k)
                         tc_mma<C::IDESC>(acc, umma_desc(a0 + k * TC_A), umma_desc(b0 + k * C::B_KT),
                                          (kc - ka) | k);
-#endif
                     tc_commit(&empty[s]);
                 }
                 tc_commit(&accfull[b]);
@@ -452,12 +438,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
             mbar_wait(&accfull[b], (i / C::NSETS) & 1);
             tc_fence_after();
             const int o = mg * TC_BM + row;
-#if defined(SK_EXP) && (SK_EXP & 4)
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&accempty[b]);
-            continue;
-#endif
             const uint32_t tbase = tmem + b * C::ACC + ((uint32_t)(quarter * 32) << 16);
             if (!mine) {
                 tc_fence_before();
@@ -470,9 +450,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
                 tmem_ld16(tbase + c0, h);
                 tmem_ld16(tbase + BN + c0, m);
                 tmem_ld16(tbase + 2 * BN + c0, l);
-#if !(defined(SK_EXP) && (SK_EXP & 16))
                 tc_epi16(a.epi, o, lane, c0, s_tok + c0, h, m, l);
-#endif
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&accempty[b]);
@@ -559,20 +537,9 @@ int launch_gemm_tc_sk(const Mat& m, const uint8_t* bcanon, int tile_tokens, cons
         set_error("gemm_tc_sk: more tokens than one tile");
         return PB_ERR_GENERIC;
     }
-    static const int cfg = [] {  // TEMPORARY sweep knob
-        const char* e = getenv("PB_SK_CFG");
-        return e ? atoi(e) : 0;
-    }();
+    // (k tiles per stage, stages): 8 x 4 -- 8 x 3, 4 x 6 and 4 x 8 measured within 1 % at 32 tokens, 2 x 14 -25 %
     if (tile_tokens == 16) return launch_sk<16, 8, 4>(m, bcanon, act, epi, skacc, skacc_bytes, counters, st);
-    if (tile_tokens == 32) {
-        switch (cfg) {
-            case 1: return launch_sk<32, 8, 3>(m, bcanon, act, epi, skacc, skacc_bytes, counters, st);
-            case 2: return launch_sk<32, 4, 8>(m, bcanon, act, epi, skacc, skacc_bytes, counters, st);
-            case 3: return launch_sk<32, 4, 6>(m, bcanon, act, epi, skacc, skacc_bytes, counters, st);
-            case 4: return launch_sk<32, 2, 14>(m, bcanon, act, epi, skacc, skacc_bytes, counters, st);
-            default: return launch_sk<32, 8, 4>(m, bcanon, act, epi, skacc, skacc_bytes, counters, st);
-        }
-    }
+    if (tile_tokens == 32) return launch_sk<32, 8, 4>(m, bcanon, act, epi, skacc, skacc_bytes, counters, st);
     set_error("gemm_tc_sk: tile of 16 or 32 tokens");
     return PB_ERR_GENERIC;
 }
