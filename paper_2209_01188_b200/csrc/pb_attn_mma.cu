@@ -361,13 +361,12 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_attn_mma(AttnArgs a, int G, i
     if (threadIdx.x == 32) trace_stamp(a.trace, c, 3);
 }
 
-// Prefill variant (query groups of up to AP_G = 32 consecutive positions of
+// Prefill variant (query groups of up to 32 consecutive positions of
 // one sequence): the same stream-K units and producer, but warp w owns queries
 // 8w .. 8w+7 of the group (rows g hi / g+8 lo of its MMA tiles) and runs over
 // all 64 keys of every stage, so each K/V byte feeds 32 queries instead of 8.
 // No cross-warp merge: a warp's online-softmax state is its queries' final
 // (or per-CTA partial) state.
-constexpr int AP_G = 32;
 
 template <int DH>
 constexpr size_t attn_pf_smem() {
@@ -386,7 +385,6 @@ __global__ void __launch_bounds__((AM_WARPS + 1) * 32) k_attn_pf(AttnArgs a, int
     uint64_t* empty = full + AM_ST;
     int* s_flag = reinterpret_cast<int*>(empty + AM_ST);
     int* s_pages = s_flag + 4;                                        // [AM_PT]
-    float* s_red = reinterpret_cast<float*>(s_pages + AM_PT);         // [WARPS][8]
 
     const int c = blockIdx.x;
     const int64_t u0 = (int64_t)c * U / G, u1 = (int64_t)(c + 1) * U / G;

@@ -697,7 +697,6 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
     if (threadIdx.x == 32) trace_stamp(a.trace, tcta, 1);
     bool first_stage = true;
     const int cw = warp - 1;  // consumer warp: m-tiles 2cw, 2cw+1 of the group
-    const int g = lane >> 2, q = lane & 3;
     // ldmatrix roles: matrix mi = lane / 8 (row half mi & 1, k half mi >> 1), row ri = lane % 8
     const uint32_t a_lane = (uint32_t)(((lane >> 3) & 1) * 256 + (lane >> 4) * 128 + (lane & 7) * 16);
     const uint32_t sa_u = smem_u32(sa);

@@ -207,20 +207,12 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const float* __restrict__ dy, co
     }
 }
 
-__device__ __forceinline__ float gelu_f(float x) {  // model.py:286-292
-    const float c = 0.7978845608028654f;
-    return 0.5f * x * (1.f + tanhf(c * (x + 0.044715f * x * x * x)));
-}
 __device__ __forceinline__ float gelu_g(float x) {  // model.py:295-298
     const float c = 0.7978845608028654f;
     const float t = tanhf(c * (x + 0.044715f * x * x * x));
     return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * c * (1.f + 3.f * 0.044715f * x * x);
 }
 
-__global__ void k_gelu(const float* __restrict__ pre, float* __restrict__ act, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        act[i] = gelu_f(pre[i]);
-}
 __global__ void k_gelu_bwd(const float* __restrict__ pre, float* __restrict__ g, int64_t n) {  // g *= gelu'(pre)
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         g[i] *= gelu_g(pre[i]);
