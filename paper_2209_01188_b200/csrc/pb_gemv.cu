@@ -97,9 +97,6 @@ constexpr int STATS_THREADS = 1024;
 __global__ void __launch_bounds__(STATS_THREADS) k_rowstats(ProArgs a) {
     __shared__ double redd[32];
     __shared__ float redf[32];
-    // PDL: the operand writer behind launches now and waits for this grid itself
-    pdl_wait();
-    pdl_trigger();
     const int tok = blockIdx.x;
     const float* x = a.x + (int64_t)tok * a.K;
     const bool vec = (a.K & 3) == 0 && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
@@ -243,10 +240,6 @@ __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
 // stores. Padding tokens are zeros.
 __global__ void __launch_bounds__(256) k_canonwrite(ProArgs a, uint8_t* __restrict__ bcanon, int n_tok, int tw) {
     __shared__ float4 s_st;
-    // PDL: the tcgen05 GEMM behind launches now (its producer streams weights until
-    // its own dependency wait); this grid waits for the producer of x / statistics
-    pdl_wait();
-    pdl_trigger();
     const int tok = blockIdx.y;
     const float* x = a.x + (int64_t)tok * a.K;
     const bool real = tok < n_tok;
@@ -307,7 +300,8 @@ int prepare_fused_operand(int mode, const ProSrc& src, const float* x, int n_tok
     ProArgs a{mode, x, K, Kp, gamma, beta, m.scales, m.n_outl, m.outl_idx, tc, nullptr, back, stats, xo, nullptr, src, 1};
     a.src.zero_tokmax = nullptr;  // the fused QKV launch resets both ranges (launch_gemv_fused zero_a/zero_b)
     if (a.src.kind == SRC_STATS) {
-        if (int rc = launch_pdl(k_rowstats, dim3(n_tok), dim3(STATS_THREADS), 0, st, a)) return rc;
+        k_rowstats<<<n_tok, STATS_THREADS, 0, st>>>(a);
+        if (int rc = launch_check("rowstats")) return rc;
     }
     *out = a;
     return PB_OK;
@@ -321,7 +315,8 @@ int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int 
               xo, y32, src, early};
     if (y32) a.src = ProSrc{};
     if (a.src.kind == SRC_STATS && (mode == PRO_LN || !y32)) {
-        if (int rc = launch_pdl(k_rowstats, dim3(n_tok), dim3(STATS_THREADS), 0, st, a)) return rc;
+        k_rowstats<<<n_tok, STATS_THREADS, 0, st>>>(a);
+        if (int rc = launch_check("rowstats")) return rc;
     }
     if (y32) {
         if (mode != PRO_LN) {  // plain copy semantics: stats unused, mu=0 inv=1 not needed
@@ -333,8 +328,9 @@ int launch_prologue(int mode, const ProSrc& src, const float* x, int n_tok, int 
     }
     if (bcanon) {
         const int items = (Kp / 32) * 2;
-        return launch_pdl(k_canonwrite, dim3((unsigned)ceil_div(items, 256), (unsigned)round_up(n_tok, bcanon_tile)),
-                          dim3(256), 0, st, a, bcanon, n_tok, bcanon_tile);
+        k_canonwrite<<<dim3((unsigned)ceil_div(items, 256), (unsigned)round_up(n_tok, bcanon_tile)), 256, 0, st>>>(
+            a, bcanon, n_tok, bcanon_tile);
+        return launch_check("canonwrite");
     }
     const int items = (Kp / 32) * 4;
     a.trace = trace_region(TR_FRAG, (int)ceil_div(items, 256) * n_tok);
