@@ -623,10 +623,7 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
         // G CTAs, G ranges, every range exactly once
         if (threadIdx.x == 0) {
             int r = (int)(smid() % (uint32_t)a.G);
-            for (int tries = 0; atomicCAS(a.claims + r, 0, 1) != 0; ++tries) {
-                r = r + 1 == a.G ? 0 : r + 1;
-                if (tries > 4 * a.G) __trap();  // cannot happen with G CTAs and G ranges: fail loudly, never hang
-            }
+            while (atomicCAS(a.claims + r, 0, 1) != 0) r = r + 1 == a.G ? 0 : r + 1;
             *reinterpret_cast<volatile int*>(smem + 0) = r;  // parked in the (not yet used) A ring
         }
         __syncthreads();
