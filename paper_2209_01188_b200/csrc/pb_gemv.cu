@@ -381,30 +381,10 @@ struct SkArgs {
     ProArgs pro;
     float* zero_a;  // accumulators of later producers reset by this launch (QKV: max|ctx s|, max|act s|)
     float* zero_b;
-    // SM-weighted partition (decode, one CTA per SM): range c = units [total P[c], total P[c+1])
-    // (P: 2^24 fixed-point prefix of per-SM streaming rates, frozen per span step), claimed by
-    // the CTA on SM c (or the next free range); each CTA folds its measured rate into rates[sm]
-    const uint32_t* part;  // [G + 1] or nullptr: uniform c total / G
-    int* claims;           // [G + 1]: range taken flags + finished-CTA count (zero between launches)
-    float* rates;          // [G] units per ns, exponential average
 };
 
 __device__ __forceinline__ int sk_owner(int64_t u, int G, int64_t total) {
     return (int)(((u + 1) * G - 1) / total);
-}
-__device__ __forceinline__ int64_t sk_begin(const SkArgs& a, int c) {
-    return a.part ? (int64_t)(((uint64_t)a.total * a.part[c]) >> 24) : (int64_t)c * a.total / a.G;
-}
-// range owning unit u: the largest c with sk_begin(c) <= u
-__device__ __forceinline__ int sk_owner_w(const SkArgs& a, int64_t u) {
-    if (!a.part) return sk_owner(u, a.G, a.total);
-    int lo = 0, hi = a.G - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (sk_begin(a, mid) <= u) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
 }
 
 // Fused epilogue of one 128-row group (consumer warps only): the integer
@@ -616,23 +596,9 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
 
     const int warp = warp_uniform_id(), lane = threadIdx.x & 31;
     const int chunk = blockIdx.y;
-    int c = blockIdx.x;
-    if (a.part) {
-        // weighted ranges: take the one sized for this SM; should two CTAs of the grid meet on
-        // one SM (an SM still busy elsewhere at launch), the second takes the next free range --
-        // G CTAs, G ranges, every range exactly once
-        if (threadIdx.x == 0) {
-            int r = (int)(smid() % (uint32_t)a.G);
-            while (atomicCAS(a.claims + r, 0, 1) != 0) r = r + 1 == a.G ? 0 : r + 1;
-            *reinterpret_cast<volatile int*>(smem + 0) = r;  // parked in the (not yet used) A ring
-        }
-        __syncthreads();
-        c = *reinterpret_cast<volatile int*>(smem + 0);
-        __syncthreads();
-    }
-    const int64_t u0 = sk_begin(a, c), u1 = sk_begin(a, c + 1);
+    const int c = blockIdx.x;
+    const int64_t u0 = (int64_t)c * a.total / a.G, u1 = (int64_t)(c + 1) * a.total / a.G;
     const int tcta = chunk * a.G + c;
-    uint64_t t_first = 0;  // thread 32: streaming interval of this CTA (rate calibration)
     if (threadIdx.x == 0) {
         trace_stamp(a.trace, tcta, 0);
         for (int s = 0; s < SK_STAGES; ++s) {
@@ -751,10 +717,7 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
             const int n = min(SK_KCS, kb - kc);
             mbar_wait(&full[stage], phase);
             if (first_stage) {
-                if (threadIdx.x == 32) {
-                    trace_stamp(a.trace, tcta, 2);
-                    t_first = gtime();
-                }
+                if (threadIdx.x == 32) trace_stamp(a.trace, tcta, 2);
                 first_stage = false;
             }
             const uint8_t* Bs = sb + stage * B_STAGE;
@@ -786,7 +749,7 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
 
         // ---- segment finished: complete group or a piece of a split group
         const int64_t g0 = (int64_t)mg * a.KC, g1 = g0 + a.KC;
-        const int c_first = sk_owner_w(a, g0), c_last = sk_owner_w(a, g1 - 1);
+        const int c_first = sk_owner(g0, a.G, a.total), c_last = sk_owner(g1 - 1, a.G, a.total);
         if (c_first != c_last) {
             const int slot = (u0 < g0) ? 1 : 0;  // not this CTA's first segment -> slot 1
             int* mine = reinterpret_cast<int*>(a.partials) + (((int64_t)chunk * a.G + c) * 2 + slot) * PER;
@@ -815,7 +778,7 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
 #pragma unroll
                     for (int r = 0; r < 4; ++r) acc[i][j][r] = 0;
             for (int cc = c_first; cc <= c_last; ++cc) {
-                const int64_t cu0 = sk_begin(a, cc);
+                const int64_t cu0 = (int64_t)cc * a.total / a.G;
                 const int* p = reinterpret_cast<const int*>(a.partials) +
                                (((int64_t)chunk * a.G + cc) * 2 + (cu0 < g0 ? 1 : 0)) * PER;
 #pragma unroll
@@ -835,57 +798,13 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
     }
     if (threadIdx.x == 32) trace_stamp(a.trace, tcta, 3);
     }  // consumers
-    if (a.part && threadIdx.x == 32) {
-        // fold this SM's streaming rate into the calibration (ranges of >= 64 k tiles only:
-        // shorter ones are dominated by the start-up latency), then count this CTA out; the
-        // last one clears the claims for the launch that reuses them
-        const uint64_t t_end = gtime();
-        const uint32_t sm = smid() % (uint32_t)a.G;
-        if (u1 - u0 >= 64 && t_first && t_end > t_first) {
-            const float r = (float)(u1 - u0) / (float)(t_end - t_first);
-            a.rates[sm] = a.rates[sm] > 0.f ? 0.9f * a.rates[sm] + 0.1f * r : r;
-        }
-        __threadfence();
-        if (atomicAdd(a.claims + a.G, 1) == a.G - 1) {
-            for (int i = 0; i <= a.G; ++i) a.claims[i] = 0;
-            __threadfence();
-        }
-    }
-}
-
-// Per span step: freeze the SM-weighted partition from the calibrated rates
-// (ranges proportional to each SM's measured streaming rate; SMs without a
-// measurement get the mean).
-__global__ void k_sm_balance(const float* __restrict__ rates, uint32_t* __restrict__ part, int G) {
-    __shared__ double pre[1024];
-    if (G > 1024) return;
-    double mean = 0.0;
-    int n = 0;
-    for (int i = 0; i < G; ++i)
-        if (rates[i] > 0.f) mean += rates[i], ++n;
-    mean = n ? mean / n : 1.0;
-    if (threadIdx.x == 0) {
-        double acc = 0.0;
-        for (int i = 0; i < G; ++i) {
-            pre[i] = acc;
-            acc += rates[i] > 0.f ? rates[i] : mean;
-        }
-        for (int i = 0; i < G; ++i) part[i] = (uint32_t)llround(pre[i] / acc * 16777216.0);
-        part[0] = 0;
-        part[G] = 1u << 24;
-    }
-}
-
-int sm_balance(const float* rates, uint32_t* part, int G, cudaStream_t st) {
-    k_sm_balance<<<1, 32, 0, st>>>(rates, part, G);
-    return launch_check("sm_balance");
 }
 
 
 template <int TC, int SK_KCS, int SK_STAGES, bool FUSED = false>
 static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
                      int64_t partial_cap, cudaStream_t st, const ProArgs* pro = nullptr, float* zero_a = nullptr,
-                     float* zero_b = nullptr, Balance* bal = nullptr) {
+                     float* zero_b = nullptr) {
     constexpr int THREADS = SK_THREADS + (FUSED ? 32 * SK_OPW : 0);
     constexpr int NT = digit_ntiles(TC);
     const size_t smem = (size_t)SK_STAGES * (SK_KCS * 4096 + SK_KCS * NT * 256) + 128 * (8 * NT + 1) * 4 + 16 +
@@ -926,11 +845,6 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
     a.partials = partials;
     a.counters = counters;
     a.trace = trace_region(TR_GEMV, (int)G * chunks);
-    if (bal && bal->part && chunks == 1 && G == bal->n_sm && G == (int64_t)sms * blocks_per_sm) {
-        a.part = bal->part;
-        a.rates = bal->rates;
-        a.claims = bal->claims + (int64_t)(bal->next++ % Balance::kRing) * (bal->n_sm + 1);
-    }
     if (FUSED) {
         a.pro = *pro;
         a.pro.trace = nullptr;
@@ -947,22 +861,21 @@ bool gemv_fusable(const Act& act, int K) {
 }
 
 int launch_gemv_fused(const Mat& m, const Act& act, const Epi& epi, const ProArgs& pro, float* zero_a,
-                      float* zero_b, float* partials, int* counters, int64_t partial_cap, cudaStream_t st,
-                      Balance* bal) {
+                      float* zero_b, float* partials, int* counters, int64_t partial_cap, cudaStream_t st) {
     if (!gemv_fusable(act, pro.K)) {
         set_error("fused-operand GEMV: unsupported shape");
         return PB_ERR_GENERIC;
     }
-    return sk_launch<2, 8, 4, true>(m, act, epi, partials, counters, partial_cap, st, &pro, zero_a, zero_b, bal);
+    return sk_launch<2, 8, 4, true>(m, act, epi, partials, counters, partial_cap, st, &pro, zero_a, zero_b);
 }
 
 // Stage shapes (k tiles per stage x stages) per column tile, chosen by sweeps
 // (profiles/r1_gemv_timeline_and_tail.txt, profiles/r1_small_shape_gemv_minu.txt):
 // decode 8 x 4 (32 KB stages, one CTA per SM), 3..8 tokens 8 x 2, 17..32 tokens 2 x 4.
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters, int64_t partial_cap,
-                cudaStream_t st, Balance* bal) {
+                cudaStream_t st) {
     switch (act.tc) {
-        case 2: return sk_launch<2, 8, 4>(m, act, epi, partials, counters, partial_cap, st, nullptr, nullptr, nullptr, bal);
+        case 2: return sk_launch<2, 8, 4>(m, act, epi, partials, counters, partial_cap, st);
         case 8: return sk_launch<8, 8, 2>(m, act, epi, partials, counters, partial_cap, st);
         case 16: return sk_launch<16, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
         case 32: return sk_launch<32, 2, 4>(m, act, epi, partials, counters, partial_cap, st);

@@ -96,8 +96,7 @@ void free_span(pb_span* s) {
     }
     void* ptrs[] = {s->kv, s->slopes, s->xa, s->mid, s->q, s->ctx, s->act, s->xo, s->y32, s->frag, s->bcanon, s->back, s->stats, s->pst_x, s->pst_mid, s->tokmax_ctx, s->tokmax_act,
                     s->partials, s->counters, s->attn_part, s->d_tok_seq, s->d_tok_pos, s->d_pages, s->d_grp_first, s->d_grp_count,
-                    s->hop_codes, s->hop_scales, s->d_unit_base, s->sk_acc, s->bal.rates, s->bal.part,
-                    s->bal.claims};
+                    s->hop_codes, s->hop_scales, s->d_unit_base, s->sk_acc};
     for (void* p : ptrs) cudaFree(p);
     for (int i = 0; i < pb_span::NSLOT; ++i) {
         if (s->h_meta[i]) cudaFreeHost(s->h_meta[i]);
@@ -187,17 +186,6 @@ int pb_span_create(const pb_span_config* cfg, pb_span** out) {
     if (!rc) rc = dalloc(s, &s->tokmax_act, NT);
     s->partial_cap = (int64_t)8 << 20;
     if (!rc) rc = dalloc(s, &s->partials, s->partial_cap);
-    if (!rc && int8 && PB_SM_BALANCE) {
-        const int n = sm_count();
-        s->bal.n_sm = n;
-        if (n <= 0) rc = PB_ERR_GENERIC;
-        if (!rc) rc = dalloc(s, &s->bal.rates, n);
-        if (!rc) rc = dalloc(s, &s->bal.part, n + 1);
-        if (!rc) rc = dalloc(s, &s->bal.claims, (int64_t)Balance::kRing * (n + 1));
-        if (!rc && (cudaMemset(s->bal.rates, 0, sizeof(float) * n) != cudaSuccess ||
-                    cudaMemset(s->bal.claims, 0, sizeof(int) * Balance::kRing * (n + 1)) != cudaSuccess))
-            rc = PB_ERR_GENERIC;
-    }
     if (!rc && cfg->graphs) {
         rc = dalloc(s, &s->g_in, (int64_t)GRAPH_MAX_TOKENS * d);
         if (!rc) rc = dalloc(s, &s->g_out, (int64_t)GRAPH_MAX_TOKENS * d);
@@ -387,10 +375,6 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
     const bool use_sk = use_tc && n_tok <= 32;
     const int MGd = (int)ceil_div(d, 128);
     int launches = 0;
-    if (int8 && !use_tc && tc == 2 && s->bal.part) {  // freeze this step's SM-weighted GEMV partition
-        if (int rc = sm_balance(s->bal.rates, s->bal.part, s->bal.n_sm, st)) return rc;
-        ++launches;
-    }
     for (int j = 0; j < s->cfg.n_blocks; ++j) {
         BlockW& b = s->blocks[j];
         const float* x_in = j == 0 ? in : s->xa;
@@ -474,7 +458,7 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                     const double bytes = (double)m.M * m.K + 4.0 * m.K + 4.0 * m.M + 4.0 * m.n_outl * m.M;
                     int rc = launch_gemv_fused(m, a, e, pa, mi == 0 ? s->tokmax_ctx : nullptr,
                                                mi == 0 ? s->tokmax_act : nullptr, s->partials, s->counters,
-                                               s->partial_cap, st, &s->bal);
+                                               s->partial_cap, st);
                     prof_end(s, ev, 0, bytes, st);
                     return rc;
                 }
@@ -487,7 +471,7 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                 ev = prof_begin(s, st);
                 // algorithmic bytes: codes + per-feature scales + bias (+ f32 outlier rows)
                 const double bytes = (double)m.M * m.K + 4.0 * m.K + 4.0 * m.M + 4.0 * m.n_outl * m.M;
-                int rc = launch_gemv(m, a, e, s->partials, s->counters, s->partial_cap, st, &s->bal);
+                int rc = launch_gemv(m, a, e, s->partials, s->counters, s->partial_cap, st);
                 prof_end(s, ev, 0, bytes, st);
                 return rc;
             }

@@ -142,21 +142,8 @@ struct ProArgs {
     uint64_t* trace = nullptr;  // diagnostics (pb_trace_set)
 };
 
-// SM-weighted stream-K partition of the decode GEMV (one CTA per SM): calibrated
-// per-SM streaming rates, the partition frozen from them once per span step, and a
-// ring of claim tables (one per launch in flight).
-struct Balance {
-    float* rates = nullptr;       // [n_sm]
-    uint32_t* part = nullptr;     // [n_sm + 1]
-    int* claims = nullptr;        // [kRing][n_sm + 1]
-    int n_sm = 0;
-    int next = 0;                 // host-side ring position
-    static constexpr int kRing = 8;
-};
-int sm_balance(const float* rates, uint32_t* part, int G, cudaStream_t st);
-
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
-                int64_t partial_cap, cudaStream_t st, Balance* bal = nullptr);
+                int64_t partial_cap, cudaStream_t st);
 // decode (<= 2 tokens per column chunk): the operand is built inside the GEMV
 // by an operand warp (no k_fragwrite launch); prepare_fused_operand runs the
 // block-0 row statistics if needed and returns the operand description
@@ -165,8 +152,7 @@ int prepare_fused_operand(int mode, const ProSrc& src, const float* x, int n_tok
                           const float* beta, const Mat& m, int tc, float* back, float4* stats, float* xo,
                           cudaStream_t st, ProArgs* out);
 int launch_gemv_fused(const Mat& m, const Act& act, const Epi& epi, const ProArgs& pro, float* zero_a,
-                      float* zero_b, float* partials, int* counters, int64_t partial_cap, cudaStream_t st,
-                      Balance* bal = nullptr);
+                      float* zero_b, float* partials, int* counters, int64_t partial_cap, cudaStream_t st);
 int launch_gemm_f32(const Mat& m, const float* y, int n_tok, const Epi& epi, float* part, int64_t part_cap,
                     cudaStream_t st);
 int choose_tc(int n_tok);

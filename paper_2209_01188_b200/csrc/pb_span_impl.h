@@ -14,10 +14,6 @@
 
 using pb::BlockW;
 
-#ifndef PB_SM_BALANCE
-#define PB_SM_BALANCE 1  // A/B builds: 0 = uniform stream-K ranges for the decode GEMV
-#endif
-
 struct pb_span {
     pb_span_config cfg{};
     int d = 0, H = 0, dh = 0, rd = 0, max_pages = 0;
@@ -62,7 +58,6 @@ struct pb_span {
     std::vector<int32_t> h_tok_pos_last;
     int8_t* hop_codes = nullptr;
     float* hop_scales = nullptr;
-    pb::Balance bal;  // SM-weighted decode-GEMV partition (PB_SM_BALANCE)
     int64_t bytes = 0;
     int32_t last_launches = 0;
     int last_n_seq = 0;
