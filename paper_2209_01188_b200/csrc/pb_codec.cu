@@ -4,6 +4,8 @@
 // reverse on decode. Other block sizes than the default 64 use one warp per
 // block with a strided loop. Bit-exact with the reference (see wire_code in
 // pb_common.cuh; tests/test_gpu_codec.py).
+#include <algorithm>
+
 #include "pb_common.cuh"
 
 namespace pb {
@@ -135,7 +137,16 @@ static int grid_for(int64_t work_items, int per_block) {
 int quantize_blockwise(const float* x, int64_t n, int block, int8_t* codes, float* scales, cudaStream_t st) {
     if (n == 0) return PB_OK;
     if (block == 64) {
-        k_wire_quant64<<<grid_for(ceil_div(n, 512) * 32, 256), 256, 0, st>>>(x, n, codes, scales);
+        // one wave: as many CTAs as are resident at once (a second partial wave doubled the latency)
+        static int occ[PB_MAX_DEVICES] = {};
+        const int per_sm = per_device(occ, [](int) {
+            int b = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_wire_quant64, 256, 0);
+            return b > 0 ? b : 1;
+        });
+        const int64_t cap = (int64_t)std::max(per_sm, 1) * std::max(sm_count(), 1);
+        const int64_t want = ceil_div(ceil_div(n, 512) * 32, 256);
+        k_wire_quant64<<<(unsigned)std::max<int64_t>(1, std::min(cap, want)), 256, 0, st>>>(x, n, codes, scales);
     } else {
         k_wire_quant_any<<<grid_for(ceil_div(n, block) * 32, 256), 256, 0, st>>>(x, n, block, codes, scales);
     }

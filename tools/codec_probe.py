@@ -1,7 +1,8 @@
-"""Wire codec at the C5 row shape [512, 14336]: blockwise int8
-quantize and dequantize on the device, timed with CUDA events; algorithmic
-bytes per element: quantize 4 (read f32) + 1 (codes) + 4/64 (scales), dequant
-the same in reverse.
+"""Wire codec kernels at the C5 row shape [512, 14336], timed
+through the C-ABI with preallocated device buffers (the Python codec API adds
+a finiteness check with a host sync, which is not the kernel): blockwise int8
+quantize and dequantize, CUDA events, L2 flushed between iterations.
+Algorithmic bytes per element: 4 (f32) + 1 (code) + 4/64 (scale).
 
   python tools/codec_probe.py [--rows 512] [--hidden 14336] [--iters 50]
 """
@@ -22,12 +23,19 @@ def main():
     a = p.parse_args()
     import torch
 
-    from paper_2209_01188_b200 import codec
+    from paper_2209_01188_b200 import _lib
 
+    L = _lib.lib()
     x = torch.randn(a.rows, a.hidden, device="cuda") * 0.05
     n = x.numel()
-    q = codec.quantize_blockwise(x)
-    y = codec.dequantize_blockwise(q)
+    codes = torch.empty(n, dtype=torch.int8, device="cuda")
+    scales = torch.empty(-(-n // 64), device="cuda")
+    y = torch.empty_like(x)
+    st = _lib.stream_ptr()
+    quant = lambda: _lib.check(L.pb_quantize_blockwise(_lib.ptr(x), n, 64, _lib.ptr(codes), _lib.ptr(scales), st))  # noqa: E731
+    dequant = lambda: _lib.check(L.pb_dequantize_blockwise(_lib.ptr(codes), _lib.ptr(scales), n, 64, _lib.ptr(y), st))  # noqa: E731
+    quant()
+    dequant()
     torch.cuda.synchronize()
     peak = 6459.0
     pk = os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")
@@ -35,7 +43,7 @@ def main():
         peak = json.load(open(pk))["hbm_gbs"]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > L2 (126 MB) between iterations
     out = {}
-    for name, fn in (("quantize", lambda: codec.quantize_blockwise(x)), ("dequantize", lambda: codec.dequantize_blockwise(q))):
+    for name, fn in (("quantize", quant), ("dequantize", dequant)):
         ms = 0.0
         for _ in range(a.iters):
             flush.zero_()
