@@ -19,6 +19,7 @@ def main():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--batches", default="1,2,4,8,16,32")
     p.add_argument("--paths", default="gemv,tc", help="gemv (tc_min_tokens huge) and/or tc (default threshold)")
+    p.add_argument("--tc-min", type=int, default=0, help="tc path: tokens from which tcgen05 runs (0: default)")
     args = p.parse_args()
     import json
 
@@ -35,7 +36,7 @@ def main():
     Bmax = max(batches)
     for path in args.paths.split(","):
         span = BlockSpan(cfg, 0, L, int8=True, page_tokens=64, n_pages=Bmax * (args.ctx // 64 + 2) + 2,
-                         max_tokens=64, max_seqs=64, tc_min_tokens=100000 if path == "gemv" else 0)
+                         max_tokens=64, max_seqs=64, tc_min_tokens=100000 if path == "gemv" else args.tc_min)
         span.generate_weights(42)
         for B in batches:
             seqs = [span.new_sequence() for _ in range(B)]
