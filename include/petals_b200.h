@@ -77,7 +77,7 @@ typedef struct {
     float outlier_threshold; /* quant.py:14 (6.0) */
     int32_t device;
     int32_t tc_min_tokens; /* tokens per step from which the matmuls run on the tcgen05 kernels instead of
-                              the IMMA GEMV; 0 = the measured default (64, or 16 above hidden 8192) */
+                              the IMMA GEMV; 0 = the measured default (9) */
     int32_t graphs;        /* 1: pb_span_step replays decode steps (<= 64 tokens) as CUDA graphs, one per
                               launch shape (tokens, sequences, attention work units), captured on first use */
 } pb_span_config;

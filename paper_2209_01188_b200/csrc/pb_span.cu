@@ -172,11 +172,7 @@ int pb_span_create(const pb_span_config* cfg, pb_span** out) {
     if (!rc && !int8) rc = dalloc(s, &s->y32, (int64_t)NT * rd);
     const int64_t kp_max = round_up(rd, 32);
     if (!rc && int8) rc = dalloc(s, &s->frag, (int64_t)(NT + 31) * kp_max * 4 / 16 + 64);
-    // tokens per step from which the matmuls run on tcgen05 instead of the IMMA GEMV:
-    // at the 176B width 32 already win (1084 -> 916 us per block at batch 32), at
-    // 7B1 width the GEMV still wins at 32 (profiles/r1_gemv_timeline_and_tail.txt)
-    if (s->d > 8192) s->tc_min = 16;
-    if (cfg->tc_min_tokens > 0) s->tc_min = cfg->tc_min_tokens;
+    if (cfg->tc_min_tokens > 0) s->tc_min = cfg->tc_min_tokens;  // else TC_MIN_TOKENS_DEFAULT
     if (!rc && int8 && NT >= s->tc_min) rc = dalloc(s, &s->bcanon, ceil_div(NT, TC_TOKENS) * (kp_max / 32) * 3 * TC_TOKENS * 32);
     if (!rc) rc = dalloc(s, &s->back, NT);
     if (!rc) rc = dalloc(s, &s->stats, NT);

@@ -105,7 +105,11 @@ int quantize_blockwise(const float* x, int64_t n, int block, int8_t* codes, floa
 int dequantize_blockwise(const int8_t* codes, const float* scales, int64_t n, int block, float* out,
                          cudaStream_t st);
 
-constexpr int TC_MIN_TOKENS_DEFAULT = 64;
+// tokens per step from which the matmuls run on tcgen05 (9..32: the stream-K kernel, more: the
+// prefill GEMM). Measured (tools/batch_probe.py): 176B 12 sessions 644 -> 500 us per block, 7B1 16
+// sessions 188 -> 165, 32 sessions 295 -> 200; at 8 tokens the IMMA GEMV still wins (459 vs 487, 113
+// vs 140)
+constexpr int TC_MIN_TOKENS_DEFAULT = 9;
 constexpr int TC_TOKENS = 80;  // tokens per tcgen05 tile (3 digit accumulators x 80 columns, double-buffered in TMEM)
 // prologue: y = LN(x) (PRO_LN) or x (PRO_SCALE); writes the int8-digit operand of
 // y * scales, the per-token 2^-shift, outlier activations xo, and (f32 mode) y.
