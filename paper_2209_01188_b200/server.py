@@ -545,10 +545,16 @@ class ServerNode:
         st.synchronize()
         return x
 
-    def _encode(self, t, encoding):
+    def _encode(self, t, encoding, producer=None):
+        """producer: the stream that computed `t` when that work may still be
+        queued (FORWARD / BACKWARD run on the handler's default stream); STEP
+        outputs are complete when the scheduler hands them over."""
         import torch
 
-        with torch.cuda.stream(self._io_stream()):
+        st = self._io_stream()
+        if producer is not None:
+            st.wait_stream(producer)
+        with torch.cuda.stream(st):
             return codec.encode_tensor(t, encoding)
 
     @staticmethod
@@ -681,7 +687,9 @@ class ServerNode:
         tape_id = os.urandom(16)
         with self._tapes_lock:  # server.py:426-428
             self._tapes[tape_id] = (time.monotonic(), tape)
-        return tape_id + self._encode(out, self._reply_encoding())
+        import torch
+
+        return tape_id + self._encode(out, self._reply_encoding(), torch.cuda.current_stream(self.span.device))
 
     def _backward(self, payload) -> bytes:
         """server.py:431-450: consume-once tape, f32 reply (gradients travel at full precision)."""
@@ -700,4 +708,7 @@ class ServerNode:
             raise RemoteError(ERR_BAD_REQUEST, "BACKWARD grad shape mismatch")
         if tuple(grad.shape[1:]) != tuple(tape.shape[2:]):
             raise self._internal(InputError("BACKWARD grad shape mismatch"))
-        return self._encode(self.span.backward(tape, grad), codec.ENC_F32)
+        import torch
+
+        gin = self.span.backward(tape, grad)
+        return self._encode(gin, codec.ENC_F32, torch.cuda.current_stream(self.span.device))
