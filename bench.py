@@ -577,7 +577,9 @@ def e2e_record(pl, args, cfg, T0):
     from paper_2209_01188_b200.server import ServerConfig, ServerNode
     from paper_2209_01188_b200 import codec
 
-    N, S, K, W = pl.world, pl.S, args.steps, args.warmup
+    N, K, W = pl.world, args.steps, args.warmup
+    S = pl.S * args.batch  # client sessions: the headline's micro-batches x batch-1 sessions each
+    unit = UNIT if args.batch == 1 else "tokens/s"
     pl.set_batch(1)
     for grp in pl.seqs:
         for s in grp:
@@ -665,7 +667,7 @@ def e2e_record(pl, args, cfg, T0):
     if errors:
         return {"error": errors[0]}
     step_bytes = len(step_msgs[0])
-    return {"value": K * S / wall, "unit": UNIT, "h2d_bytes_per_step": step_bytes, "d2h_bytes_per_step": step_bytes,
+    return {"value": K * S / wall, "unit": unit, "h2d_bytes_per_step": step_bytes, "d2h_bytes_per_step": step_bytes,
             "wall_s": wall, "sessions": S, "ctx_end": T0 + W + K,
             "path": ("TCP STEP frames (int8 TensorMsg) -> " + ("ServerNode" if N == 1 else
                      f"box front end over {N} GPUs (one ServerEntry [0, 70), peer-memory hops)") +
