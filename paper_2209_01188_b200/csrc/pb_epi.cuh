@@ -86,6 +86,16 @@ __device__ __forceinline__ void stage_tokens(const Epi& e, const float* back, in
 __device__ __forceinline__ void tc_epi16(const Epi& e, int o, int lane, int tok0, const TokInfo* ti, const int* h,
                                          const int* m, const int* l) {
     const bool row_ok = o < e.M;
+    if (e.kind == EPI_BWD) {  // dx_k = s_k * sum_o g_o codes[o][k] (pb_train.cu)
+        if (!row_ok) return;
+        const float rs = e.rowscale[o];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const long long iv = (long long)h[j] * 65536 + (long long)m[j] * 256 + (long long)l[j];
+            if (ti[j].valid) e.out[(int64_t)(tok0 + j) * e.M + o] = (float)iv * ti[j].back * rs;
+        }
+        return;
+    }
     const float bias = row_ok ? e.bias[o] : 0.f;
     float v[16];
 #pragma unroll

@@ -48,7 +48,8 @@ struct BlockW {
     float gs1 = 0.f, bs1 = 0.f, gs2 = 0.f, bs2 = 0.f;
 };
 
-enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_GELU = 2, EPI_PLAIN = 3 };
+// EPI_BWD (tcgen05 only): BACKWARD through an int8 matrix (pb_train.cu), out = acc * rowscale[o], no bias
+enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_GELU = 2, EPI_PLAIN = 3, EPI_BWD = 4 };
 
 // Epilogue parameters shared by every GEMV/GEMM flavour.
 struct Epi {
@@ -71,6 +72,7 @@ struct Epi {
     float4* pstats;          // EPI_RESID -> LN consumer: [n_tok][M/128] {mean, M2, min, max} per 128-row group
     float* tokmax;           // EPI_GELU -> scale consumer: atomicMax of |out * s_next| per token
     const float* s_next;     // [M] scales of the consuming matrix
+    const float* rowscale;   // EPI_BWD: [M] per-row factor (the forward matrix's input-feature scales)
 };
 
 // B-operand (activation) layout parameters for one GEMV launch.

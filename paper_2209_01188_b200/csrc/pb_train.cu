@@ -4,18 +4,19 @@
 //
 // Tape-less recompute: the FORWARD step records only each block's input rows
 // (pb_span_step_tape); BACKWARD recomputes the block's intermediates from them
-// in f32 (LN1, qkv, softmax probabilities, ctx, mid, LN2, pre-activation) and
-// then runs the reference backward formulas. The weights are the span's own:
-// f32 matrices as stored, int8 matrices dequantized (codes x feature scales,
-// f32 outlier rows) into a scratch f32 copy per matrix, so the gradient is
-// that of the function the span's FORWARD computes.
+// (LN1, qkv, softmax probabilities, ctx, mid, LN2, pre-activation) and then
+// runs the reference backward formulas, so the gradient is that of the
+// function the span's FORWARD computes.
 //
-// Every matmul is one tiled SIMT kernel (64 x 64 tiles, 4 x 4 per thread,
-// f32 accumulation) in either orientation: C = A W (forward) or C = A W^T
-// (backward through a weight). Attention works on [H][t][t] probability and
-// score-gradient planes.
+// int8 matrices run on the tcgen05 GEMM (pb_gemm_tc.cu) in both directions:
+// the recompute exactly as FORWARD's prefill does it, the backward product
+// g W^T over a per-call transposed copy of the codes (see mm_bwd_tc). f32
+// matrices (test spans) use one tiled SIMT kernel (64 x 64 tiles, f32
+// accumulation) in either orientation. Attention works on [H][t][t]
+// probability and score-gradient planes.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 
 #include "pb_common.cuh"
 #include "pb_span_impl.h"
@@ -23,83 +24,203 @@
 namespace pb {
 namespace {
 
-// ---------------------------------------------------------------- weights
+// ---------------------------------------------------------------- int8 matrices on tcgen05
+//
+// Recompute (y = op(x) W + b) runs the span's own prefill path: k_rowstats +
+// k_canonwrite digit planes, k_gemm_tc with the plain epilogue, so the
+// recomputed intermediates are the ones FORWARD produced. BACKWARD through a
+// matrix (dx_k = s_k sum_o g_o codes[o][k], outlier features exact in f32)
+// needs the codes with the contraction over the outputs o: k_transpose_codes
+// rewrites one matrix into canonical tiles of W^T (rows k, 32-wide o tiles)
+// in a scratch buffer (one read + one write of the codes), the upstream
+// gradient becomes the digit-plane operand (scales 1), and k_gemm_tc's
+// EPI_BWD epilogue applies s_k. Outlier features (s_k = 0, codes 0) are then
+// overwritten with their f32 dot products (k_outl_bwd).
 
-// W[k][o] (reference [in, out] layout, f32) from the canonical int8 tiles
-__global__ void k_dequant(const int8_t* __restrict__ codes, const float* __restrict__ scales, int K, int M, int KC,
-                          float* __restrict__ w) {
-    const int64_t total = (int64_t)K * M;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int k = (int)(t / M), o = (int)(t % M);
-        const int r = o & 127, kk = k & 31;
-        const int8_t c = codes[((int64_t)(o >> 7) * KC + (k >> 5)) * 4096 + (r >> 3) * 256 + (kk >> 4) * 128 +
-                               (r & 7) * 16 + (kk & 15)];
-        w[t] = (float)c * scales[k];
+// 128 o x 128 k of the source (4 tiles of one row group) -> 4 tiles of W^T (row group k0/128, o tiles
+// 4 og .. 4 og + 3); tile bytes: row r, col c at (r >> 3) * 256 + (c >> 4) * 128 + (r & 7) * 16 + (c & 15)
+constexpr int TP = 132;  // smem row pitch [o][k] (4-byte stores, conflict-free byte-column reads)
+__global__ void __launch_bounds__(256) k_transpose_codes(const int8_t* __restrict__ src, int KC, int8_t* __restrict__ dst,
+                                                         int KCt) {
+    __shared__ uint32_t s[128 * TP / 4];
+    const int og = blockIdx.x, kg = blockIdx.y;
+    uint8_t* sb = reinterpret_cast<uint8_t*>(s);
+    for (int c = threadIdx.x; c < 4 * 256; c += 256) {
+        const int i = c >> 8, cc = c & 255;
+        const int r = ((cc >> 4) << 3) | (cc & 7), kh = (cc >> 3) & 1;
+        const int kt = kg * 4 + i;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (kt < KC) v = reinterpret_cast<const uint4*>(src + ((int64_t)og * KC + kt) * 4096)[cc];
+        uint32_t* row = reinterpret_cast<uint32_t*>(sb + r * TP + i * 32 + kh * 16);
+        row[0] = v.x, row[1] = v.y, row[2] = v.z, row[3] = v.w;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < 4 * 256; c += 256) {
+        const int i = c >> 8, cc = c & 255;
+        const int ot = og * 4 + i;
+        if (ot >= KCt) break;  // i is uniform per 256-chunk pass
+        const int kr = ((cc >> 4) << 3) | (cc & 7), oh = (cc >> 3) & 1;
+        const uint8_t* col = sb + (i * 32 + oh * 16) * TP + kr;
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            w[q] = (uint32_t)col[(4 * q) * TP] | ((uint32_t)col[(4 * q + 1) * TP] << 8) |
+                   ((uint32_t)col[(4 * q + 2) * TP] << 16) | ((uint32_t)col[(4 * q + 3) * TP] << 24);
+        reinterpret_cast<uint4*>(dst + ((int64_t)kg * KCt + ot) * 4096)[cc] = make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
-__global__ void k_outlier_rows(const int32_t* __restrict__ idx, const float* __restrict__ rows, int n_outl, int M,
-                               float* __restrict__ w) {
-    const int64_t total = (int64_t)n_outl * M;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int j = (int)(t / M), o = (int)(t % M);
-        w[(int64_t)idx[j] * M + o] = rows[t];  // quant.py:105: outlier features exact in f32
+// dx[t][idx_j] = sum_o g[t][o] rows[j][o] (quant.py:105 outlier features: W[idx_j, :] in f32); one CTA per (j, t)
+__global__ void __launch_bounds__(256) k_outl_bwd(const float* __restrict__ g, const int32_t* __restrict__ idx,
+                                                  const float* __restrict__ rows, int M, int K,
+                                                  float* __restrict__ dx) {
+    __shared__ float red[8];
+    const int j = blockIdx.x, t = blockIdx.y;
+    const float* gr = g + (int64_t)t * M;
+    const float* wr = rows + (int64_t)j * M;
+    float s = 0.f;
+    for (int o = threadIdx.x; o < M; o += 256) s = fmaf(gr[o], wr[o], s);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float v = 0.f;
+        for (int w = 0; w < 8; ++w) v += red[w];
+        dx[(int64_t)t * K + idx[j]] = v;
     }
+}
+
+__global__ void k_fill(float* __restrict__ p, int64_t n, float v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
 }
 
 int grid_for(int64_t n) { return (int)std::min<int64_t>(std::max<int64_t>(ceil_div(n, 256), 1), 148 * 32); }
 
-// f32 [K][M] view of matrix m (the stored f32 matrix, or a dequantized copy in scratch)
-int weight_f32(const Mat& m, float* scratch, const float** out, cudaStream_t st) {
-    if (!m.int8) {
-        *out = m.w32;
-        return PB_OK;
-    }
-    k_dequant<<<grid_for((int64_t)m.K * m.M), 256, 0, st>>>(m.codes, m.scales, m.K, m.M, m.Kp / 32, scratch);
-    if (int rc = launch_check("dequant")) return rc;
+// scratch of one BACKWARD call (sizes: bwd_ws_sizes)
+struct TcWs {
+    uint8_t* bcanon = nullptr;  // digit planes [round_up(t, TC_TOKENS) / TC_TOKENS][KC][3][TC_TOKENS x 32 B]
+    float* back = nullptr;      // [t]
+    float4* stats = nullptr;    // [t]
+    float* xo = nullptr;        // [t][max n_outl]
+    float* ones = nullptr;      // [max Kp of W^T] operand scales of the gradient
+    int8_t* tcodes = nullptr;   // W^T tiles of the matrix being back-propagated
+};
+
+// transposed view of m: rows k (padded to 128), contraction over o (padded to 32)
+Mat transposed(const Mat& m, const TcWs& w) {
+    Mat t;
+    t.M = m.K;
+    t.K = m.M;
+    t.Mp = (int)round_up(m.K, 128);
+    t.Kp = (int)round_up(m.M, 32);
+    t.codes = w.tcodes;
+    t.scales = w.ones;
+    return t;
+}
+
+// y [t][M] = op(x) W + b; op = LN(gamma, beta) (mode PRO_LN) or identity (PRO_SCALE)
+int mm_fwd_tc(const Mat& m, const float* bias, int mode, const float* x, const float* gamma, const float* beta,
+              int t, float* y, const TcWs& w, cudaStream_t st) {
+    if (int rc = launch_prologue(mode, ProSrc{}, x, t, m.K, m.Kp, gamma, beta, m, 0, nullptr, w.back, w.stats, w.xo,
+                                 nullptr, st, w.bcanon, TC_TOKENS))
+        return rc;
+#ifdef PB_BWD_TRACE
+    { cudaError_t e0 = cudaStreamSynchronize(st); fprintf(stderr, "fwd prologue %s M %d K %d Mp %d Kp %d outl %d t %d\n", cudaGetErrorString(e0), m.M, m.K, m.Mp, m.Kp, m.n_outl, t); }
+#endif
+    Epi e{};
+    e.kind = EPI_PLAIN;
+    e.M = m.M;
+    e.bias = bias;
+    e.n_outl = m.n_outl;
+    e.outl_idx = m.outl_idx;
+    e.outl_rows = m.outl_rows;
+    e.xo = w.xo;
+    e.out = y;
+    return launch_gemm_tc(m, w.bcanon, Act{nullptr, w.back, t, 0}, e, st);
+}
+
+// dx [t][K] = g [t][M] W^T
+int mm_bwd_tc(const Mat& m, const float* g, int t, float* dx, const TcWs& w, cudaStream_t st) {
+    const Mat mt = transposed(m, w);
+    k_transpose_codes<<<dim3((unsigned)(m.Mp / 128), (unsigned)(mt.Mp / 128)), 256, 0, st>>>(m.codes, m.Kp / 32,
+                                                                                             w.tcodes, mt.Kp / 32);
+    if (int rc = launch_check("transpose_codes")) return rc;
+#ifdef PB_BWD_TRACE
+    { cudaError_t e0 = cudaStreamSynchronize(st); fprintf(stderr, "transpose %s\n", cudaGetErrorString(e0)); }
+#endif
+    if (int rc = launch_prologue(PRO_SCALE, ProSrc{}, g, t, mt.K, mt.Kp, nullptr, nullptr, mt, 0, nullptr, w.back,
+                                 w.stats, nullptr, nullptr, st, w.bcanon, TC_TOKENS))
+        return rc;
+#ifdef PB_BWD_TRACE
+    { cudaError_t e0 = cudaStreamSynchronize(st); fprintf(stderr, "prologue %s M %d K %d Mp %d Kp %d\n", cudaGetErrorString(e0), mt.M, mt.K, mt.Mp, mt.Kp); }
+#endif
+    Epi e{};
+    e.kind = EPI_BWD;
+    e.M = mt.M;
+    e.rowscale = m.scales;
+    e.out = dx;
+    if (int rc = launch_gemm_tc(mt, w.bcanon, Act{nullptr, w.back, t, 0}, e, st)) return rc;
     if (m.n_outl) {
-        k_outlier_rows<<<grid_for((int64_t)m.n_outl * m.M), 256, 0, st>>>(m.outl_idx, m.outl_rows, m.n_outl, m.M,
-                                                                        scratch);
-        if (int rc = launch_check("outlier_rows")) return rc;
+        k_outl_bwd<<<dim3((unsigned)m.n_outl, (unsigned)t), 256, 0, st>>>(g, m.outl_idx, m.outl_rows, m.M, m.K, dx);
+        return launch_check("outl_bwd");
     }
-    *out = scratch;
     return PB_OK;
 }
 
-// ---------------------------------------------------------------- GEMM
+// ---------------------------------------------------------------- batched strided SIMT GEMM (f32)
+//
+// C(b, i, j) = alpha sum_p A(b, i, p) B(b, p, j) (+ bias[j]) with arbitrary element strides, so one
+// kernel serves the f32 weight matrices (either orientation) and every per-head attention product on
+// the [t][3d] q|k|v rows and the [H][t][t] probability planes. 64 x 64 output tiles, 16-deep k slices
+// staged in shared memory (loads coalesced along whichever operand index has stride 1), 4 x 4 outputs
+// per thread, f32 accumulation. Causal modes bound the work: CM_OUT skips output tiles strictly above
+// the diagonal (j > i everywhere: masked scores), CM_P_LE_I contracts p <= i only, CM_P_GE_I p >= i.
+enum { CM_NONE = 0, CM_OUT = 1, CM_P_LE_I = 2, CM_P_GE_I = 3 };
+
+struct BG {
+    const float* A;
+    int64_t a_b, a_i, a_p;
+    const float* B;
+    int64_t b_b, b_p, b_j;
+    float* C;
+    int64_t c_b, c_i, c_j;
+    const float* bias;
+    int I, J, P;
+    float alpha;
+    int causal;
+};
 
 constexpr int GB = 64, GK = 16;
 
-// C[i][j] (+= or =) sum_p A[i][p] B(p, j) (+ bias[j]); B(p, j) = W[p][j] (TRANS = false,
-// W is [P][N]) or W[j][p] (TRANS = true, W is [N][P]).
-template <bool TRANS>
-__global__ void __launch_bounds__(256) k_sgemm(const float* __restrict__ A, const float* __restrict__ W,
-                                               const float* __restrict__ bias, float* __restrict__ C, int I, int J,
-                                               int P) {
+__global__ void __launch_bounds__(256) k_bgemm(BG g) {
     __shared__ float As[GK][GB + 4];
     __shared__ float Bs[GK][GB + 4];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int i0 = blockIdx.y * GB, j0 = blockIdx.x * GB;
+    const int64_t bz = blockIdx.z;
+    if (g.causal == CM_OUT && j0 > i0 + GB - 1) return;
+    int p_lo = 0, p_hi = g.P;
+    if (g.causal == CM_P_LE_I) p_hi = min(g.P, i0 + GB);
+    if (g.causal == CM_P_GE_I) p_lo = i0 & ~(GK - 1);
+    const float* A = g.A + bz * g.a_b;
+    const float* B = g.B + bz * g.b_b;
+    const bool a_pc = g.a_p == 1, b_jc = g.b_j == 1;
     float acc[4][4] = {};
-    for (int p0 = 0; p0 < P; p0 += GK) {
+    for (int p0 = p_lo; p0 < p_hi; p0 += GK) {
         for (int e = threadIdx.x; e < GB * GK; e += 256) {
-            const int ii = e / GK, pp = e % GK;  // A tile: rows i, cols p (coalesced along p)
+            int ii, pp;
+            if (a_pc) ii = e / GK, pp = e % GK;
+            else pp = e / GB, ii = e % GB;
             const int i = i0 + ii, p = p0 + pp;
-            As[pp][ii] = (i < I && p < P) ? A[(int64_t)i * P + p] : 0.f;
+            As[pp][ii] = (i < g.I && p < p_hi) ? A[i * g.a_i + p * g.a_p] : 0.f;
         }
         for (int e = threadIdx.x; e < GB * GK; e += 256) {
             int jj, pp;
-            if (TRANS) {
-                jj = e / GK;
-                pp = e % GK;  // W[j][p]: coalesced along p
-            } else {
-                pp = e / GB;
-                jj = e % GB;  // W[p][j]: coalesced along j
-            }
+            if (b_jc) pp = e / GB, jj = e % GB;
+            else jj = e / GK, pp = e % GK;
             const int j = j0 + jj, p = p0 + pp;
-            float v = 0.f;
-            if (j < J && p < P) v = TRANS ? W[(int64_t)j * P + p] : W[(int64_t)p * J + j];
-            Bs[pp][jj] = v;
+            Bs[pp][jj] = (j < g.J && p < p_hi) ? B[p * g.b_p + j * g.b_j] : 0.f;
         }
         __syncthreads();
 #pragma unroll
@@ -116,24 +237,29 @@ __global__ void __launch_bounds__(256) k_sgemm(const float* __restrict__ A, cons
         }
         __syncthreads();
     }
+    float* C = g.C + bz * g.c_b;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         const int i = i0 + ty * 4 + r;
-        if (i >= I) continue;
+        if (i >= g.I) continue;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const int j = j0 + tx * 4 + c;
-            if (j < J) C[(int64_t)i * J + j] = acc[r][c] + (bias ? bias[j] : 0.f);
+            if (j < g.J) C[i * g.c_i + j * g.c_j] = acc[r][c] * g.alpha + (g.bias ? g.bias[j] : 0.f);
         }
     }
 }
 
+int bgemm(const BG& g, int batch, cudaStream_t st) {
+    k_bgemm<<<dim3((unsigned)ceil_div(g.J, GB), (unsigned)ceil_div(g.I, GB), (unsigned)batch), 256, 0, st>>>(g);
+    return launch_check("bgemm");
+}
+
+// f32 weights: C [I][J] = A [I][P] W (+ bias), W [P][J] (trans = false) or C = A W^T, W [J][P] (trans = true)
 int gemm(bool trans, const float* A, const float* W, const float* bias, float* C, int I, int J, int P,
          cudaStream_t st) {
-    dim3 grid((unsigned)ceil_div(J, GB), (unsigned)ceil_div(I, GB));
-    if (trans) k_sgemm<true><<<grid, 256, 0, st>>>(A, W, bias, C, I, J, P);
-    else k_sgemm<false><<<grid, 256, 0, st>>>(A, W, bias, C, I, J, P);
-    return launch_check("sgemm");
+    BG g{A, 0, P, 1, W, 0, trans ? 1 : J, trans ? P : 1, C, 0, J, 1, bias, I, J, P, 1.f, CM_NONE};
+    return bgemm(g, 1, st);
 }
 
 // ---------------------------------------------------------------- LayerNorm / GELU
@@ -225,22 +351,18 @@ __global__ void k_add(const float* __restrict__ a, float* __restrict__ b, int64_
 // ---------------------------------------------------------------- attention (one row, positions 0 .. t-1)
 // qkv [t][3d]: q | k | v column thirds (model.py:342-344), head h at columns h dh ..
 
-// P[h][i][j] (j <= i) = softmax_j(q_i . k_j / sqrt(dh) + slope_h (j - i)); one CTA per (h, i)
-__global__ void __launch_bounds__(256) k_attn_probs(const float* __restrict__ qkv, int t, int d, int dh,
-                                                    const float* __restrict__ slopes, float* __restrict__ P) {
+// in place on the [H][t][t] plane holding q_i . k_j / sqrt(dh) (j <= i): P[h][i][j] = softmax_j(s_ij +
+// slope_h (j - i)), zero for j > i (model.py:347-357); one CTA per (h, i)
+__global__ void __launch_bounds__(256) k_softmax_rows(float* __restrict__ P, int t, const float* __restrict__ slopes) {
     __shared__ float red[8];
     const int h = blockIdx.x, i = blockIdx.y;
-    const float* q = qkv + (int64_t)i * 3 * d + h * dh;
     float* prow = P + ((int64_t)h * t + i) * t;
-    const float sq = sqrtf((float)dh);
+    const float sl = slopes[h];
     float mx = -INFINITY;
     for (int j = threadIdx.x; j <= i; j += 256) {
-        const float* k = qkv + (int64_t)j * 3 * d + d + h * dh;
-        float s = 0.f;
-        for (int e = 0; e < dh; ++e) s = fmaf(q[e], k[e], s);
-        s = s / sq + slopes[h] * (float)(j - i);
-        prow[j] = s;
-        mx = fmaxf(mx, s);
+        const float v = prow[j] + sl * (float)(j - i);
+        prow[j] = v;
+        mx = fmaxf(mx, v);
     }
     mx = warp_max(mx);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
@@ -262,35 +384,15 @@ __global__ void __launch_bounds__(256) k_attn_probs(const float* __restrict__ qk
     for (int j = threadIdx.x; j < t; j += 256) prow[j] = j <= i ? prow[j] / sum : 0.f;
 }
 
-// ctx[i][h dh + e] = sum_j P[h][i][j] v[j][h dh + e]; one CTA per (h, i), threads over e
-__global__ void k_attn_ctx(const float* __restrict__ qkv, const float* __restrict__ P, int t, int d, int dh,
-                           float* __restrict__ ctx) {
-    const int h = blockIdx.x, i = blockIdx.y;
-    const float* prow = P + ((int64_t)h * t + i) * t;
-    for (int e = threadIdx.x; e < dh; e += blockDim.x) {
-        float s = 0.f;
-        for (int j = 0; j <= i; ++j) s = fmaf(prow[j], qkv[(int64_t)j * 3 * d + 2 * d + h * dh + e], s);
-        ctx[(int64_t)i * d + h * dh + e] = s;
-    }
-}
-
-// dS[h][i][j] = P (dP - sum_j dP P), dP[h][i][j] = dctx_i . v_j (model.py:400-403); one CTA per (h, i)
-__global__ void __launch_bounds__(256) k_attn_dscores(const float* __restrict__ qkv, const float* __restrict__ P,
-                                                      const float* __restrict__ dctx, int t, int d, int dh,
-                                                      float* __restrict__ dS) {
+// in place on the plane holding dP = dctx_i . v_j: dS = P (dP - sum_j dP P), zero for j > i
+// (model.py:400-403); one CTA per (h, i)
+__global__ void __launch_bounds__(256) k_dscores_rows(const float* __restrict__ P, float* __restrict__ dS, int t) {
     __shared__ float red[8];
     const int h = blockIdx.x, i = blockIdx.y;
     const float* prow = P + ((int64_t)h * t + i) * t;
     float* drow = dS + ((int64_t)h * t + i) * t;
-    const float* dc = dctx + (int64_t)i * d + h * dh;
     float rs = 0.f;
-    for (int j = threadIdx.x; j <= i; j += 256) {
-        const float* v = qkv + (int64_t)j * 3 * d + 2 * d + h * dh;
-        float s = 0.f;
-        for (int e = 0; e < dh; ++e) s = fmaf(dc[e], v[e], s);
-        drow[j] = s;
-        rs = fmaf(s, prow[j], rs);
-    }
+    for (int j = threadIdx.x; j <= i; j += 256) rs = fmaf(drow[j], prow[j], rs);
     rs = warp_sum(rs);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = rs;
     __syncthreads();
@@ -299,34 +401,37 @@ __global__ void __launch_bounds__(256) k_attn_dscores(const float* __restrict__ 
     for (int j = threadIdx.x; j < t; j += 256) drow[j] = j <= i ? prow[j] * (drow[j] - rs) : 0.f;
 }
 
-// dq_i = sum_j dS[h][i][j] k_j / sqrt(dh) -> dqkv[i][h dh + e]; one CTA per (h, i)
-__global__ void k_attn_dq(const float* __restrict__ qkv, const float* __restrict__ dS, int t, int d, int dh,
-                          float* __restrict__ dqkv) {
-    const int h = blockIdx.x, i = blockIdx.y;
-    const float* drow = dS + ((int64_t)h * t + i) * t;
-    const float inv_sq = 1.0f / sqrtf((float)dh);
-    for (int e = threadIdx.x; e < dh; e += blockDim.x) {
-        float s = 0.f;
-        for (int j = 0; j <= i; ++j) s = fmaf(drow[j], qkv[(int64_t)j * 3 * d + d + h * dh + e], s);
-        dqkv[(int64_t)i * 3 * d + h * dh + e] = s * inv_sq;
-    }
+// attention of one row over its own positions (empty cache) on the batched GEMM, heads as the batch;
+// qkv [t][3d] (q | k | v thirds, head h at columns h dh ..), planes [H][t][t]
+int attn_fwd(const float* qkv, float* P, float* ctx, int t, int d, int H, int dh, const float* slopes,
+             cudaStream_t st) {
+    const int64_t tt = (int64_t)t * t, r3 = 3 * (int64_t)d;
+    // S = q k^T / sqrt(dh) (upper tiles skipped)
+    BG s{qkv, dh, r3, 1, qkv + d, dh, 1, r3, P, tt, t, 1, nullptr, t, t, dh, 1.0f / sqrtf((float)dh), CM_OUT};
+    if (int rc = bgemm(s, H, st)) return rc;
+    k_softmax_rows<<<dim3(H, t), 256, 0, st>>>(P, t, slopes);
+    // ctx = P v
+    BG c{P, tt, t, 1, qkv + 2 * d, dh, r3, 1, ctx, dh, d, 1, nullptr, t, dh, t, 1.f, CM_P_LE_I};
+    return bgemm(c, H, st);
 }
 
-// dk_j = sum_i dS[h][i][j] q_i / sqrt(dh), dv_j = sum_i P[h][i][j] dctx_i (i >= j); one CTA per (h, j)
-__global__ void k_attn_dkdv(const float* __restrict__ qkv, const float* __restrict__ P, const float* __restrict__ dS,
-                            const float* __restrict__ dctx, int t, int d, int dh, float* __restrict__ dqkv) {
-    const int h = blockIdx.x, j = blockIdx.y;
-    const float inv_sq = 1.0f / sqrtf((float)dh);
-    for (int e = threadIdx.x; e < dh; e += blockDim.x) {
-        float sk = 0.f, sv = 0.f;
-        for (int i = j; i < t; ++i) {
-            const int64_t pi = ((int64_t)h * t + i) * t + j;
-            sk = fmaf(dS[pi], qkv[(int64_t)i * 3 * d + h * dh + e], sk);
-            sv = fmaf(P[pi], dctx[(int64_t)i * d + h * dh + e], sv);
-        }
-        dqkv[(int64_t)j * 3 * d + d + h * dh + e] = sk * inv_sq;
-        dqkv[(int64_t)j * 3 * d + 2 * d + h * dh + e] = sv;
-    }
+// dctx [t][d] -> dqkv [t][3d] (model.py:399-409)
+int attn_bwd(const float* qkv, const float* P, float* dS, const float* dctx, float* dqkv, int t, int d, int H,
+             int dh, cudaStream_t st) {
+    const int64_t tt = (int64_t)t * t, r3 = 3 * (int64_t)d;
+    const float isq = 1.0f / sqrtf((float)dh);
+    // dP = dctx v^T, then dS = P (dP - rowsum(dP P))
+    BG dp{dctx, dh, d, 1, qkv + 2 * d, dh, 1, r3, dS, tt, t, 1, nullptr, t, t, dh, 1.f, CM_OUT};
+    if (int rc = bgemm(dp, H, st)) return rc;
+    k_dscores_rows<<<dim3(H, t), 256, 0, st>>>(P, dS, t);
+    // dq = dS k / sqrt(dh)
+    BG dq{dS, tt, t, 1, qkv + d, dh, r3, 1, dqkv, dh, r3, 1, nullptr, t, dh, t, isq, CM_P_LE_I};
+    if (int rc = bgemm(dq, H, st)) return rc;
+    // dk = dS^T q / sqrt(dh), dv = P^T dctx (contraction over i >= j)
+    BG dk{dS, tt, 1, t, qkv, dh, r3, 1, dqkv + d, dh, r3, 1, nullptr, t, dh, t, isq, CM_P_GE_I};
+    if (int rc = bgemm(dk, H, st)) return rc;
+    BG dv{P, tt, 1, t, dctx, dh, d, 1, dqkv + 2 * d, dh, r3, 1, nullptr, t, dh, t, 1.f, CM_P_GE_I};
+    return bgemm(dv, H, st);
 }
 
 int ew_grid(int64_t n) { return grid_for(n); }
@@ -335,7 +440,7 @@ int ew_grid(int64_t n) { return grid_for(n); }
 
 // One block's BACKWARD for one row: g [t][d] in, dx [t][d] out (model.py:383-418).
 static int block_backward(pb_span* s, int j, const float* x, const float* g, float* dx, int t, float* ws,
-                          float* wscratch, cudaStream_t st) {
+                          const TcWs& tw, cudaStream_t st) {
     const int d = s->d, rd = s->rd, H = s->H, dh = s->dh;
     BlockW& b = s->blocks[j];
     const int64_t td = (int64_t)t * d;
@@ -355,34 +460,42 @@ static int block_backward(pb_span* s, int j, const float* x, const float* g, flo
     float* dmid = act + (int64_t)t * rd;
     float* tmp = dmid + td;              // [t][max(d, rd)]
     float* dqkv = tmp + (int64_t)t * rd;
-    const float* w;
+    // y = op(x) W_i + b_i: int8 on tcgen05 (op applied by the operand writer), f32 on the SIMT GEMM (op(x) = h)
+    auto fwd = [&](int i, int mode, const float* xin, const float* h, const float* gam, const float* bet,
+                   float* y) -> int {
+        const Mat& m = b.mat[i];
+#ifdef PB_BWD_TRACE
+        { cudaError_t e0 = cudaStreamSynchronize(st); fprintf(stderr, "fwd %d pre %s\n", i, cudaGetErrorString(e0)); }
+#endif
+        if (m.int8) return mm_fwd_tc(m, b.bias[i], mode, xin, gam, bet, t, y, tw, st);
+        return gemm(false, h, m.w32, b.bias[i], y, t, m.M, m.K, st);
+    };
+    // dx = g W_i^T
+    auto bwd = [&](int i, const float* gin, float* out) -> int {
+        const Mat& m = b.mat[i];
+#ifdef PB_BWD_TRACE
+        { cudaError_t e0 = cudaStreamSynchronize(st); fprintf(stderr, "bwd %d pre %s\n", i, cudaGetErrorString(e0)); }
+#endif
+        if (m.int8) return mm_bwd_tc(m, gin, t, out, tw, st);
+        return gemm(true, gin, m.w32, nullptr, out, t, m.K, m.M, st);
+    };
     // ---- recompute the forward intermediates (model.py:340-368)
     k_ln_fwd<<<t, 256, 0, st>>>(x, b.ln1_g, b.ln1_b, d, h1, xh1, inv1);
-    if (int rc = weight_f32(b.mat[0], wscratch, &w, st)) return rc;
-    if (int rc = gemm(false, h1, w, b.bias[0], qkv, t, 3 * d, d, st)) return rc;
-    k_attn_probs<<<dim3(H, t), 256, 0, st>>>(qkv, t, d, dh, s->slopes, P);
-    k_attn_ctx<<<dim3(H, t), 128, 0, st>>>(qkv, P, t, d, dh, ctx);
-    if (int rc = weight_f32(b.mat[1], wscratch, &w, st)) return rc;
-    if (int rc = gemm(false, ctx, w, b.bias[1], mid, t, d, d, st)) return rc;
+    if (int rc = fwd(0, PRO_LN, x, h1, b.ln1_g, b.ln1_b, qkv)) return rc;
+    if (int rc = attn_fwd(qkv, P, ctx, t, d, H, dh, s->slopes, st)) return rc;
+    if (int rc = fwd(1, PRO_SCALE, ctx, ctx, nullptr, nullptr, mid)) return rc;
     k_add<<<ew_grid(td), 256, 0, st>>>(x, mid, td);  // mid = x + attn_out
     k_ln_fwd<<<t, 256, 0, st>>>(mid, b.ln2_g, b.ln2_b, d, h2, xh2, inv2);
-    if (int rc = weight_f32(b.mat[2], wscratch, &w, st)) return rc;
-    if (int rc = gemm(false, h2, w, b.bias[2], pre, t, rd, d, st)) return rc;
+    if (int rc = fwd(2, PRO_LN, mid, h2, b.ln2_g, b.ln2_b, pre)) return rc;
     // ---- backward (model.py:397-417)
-    if (int rc = weight_f32(b.mat[3], wscratch, &w, st)) return rc;
-    if (int rc = gemm(true, g, w, nullptr, act, t, rd, d, st)) return rc;  // dact = g Wout^T
+    if (int rc = bwd(3, g, act)) return rc;                                             // dact = g Wout^T
     k_gelu_bwd<<<ew_grid((int64_t)t * rd), 256, 0, st>>>(pre, act, (int64_t)t * rd);  // dpre
-    if (int rc = weight_f32(b.mat[2], wscratch, &w, st)) return rc;
-    if (int rc = gemm(true, act, w, nullptr, tmp, t, d, rd, st)) return rc;  // dh2 = dpre Win^T
-    k_ln_bwd<<<t, 256, 0, st>>>(tmp, xh2, inv2, b.ln2_g, d, g, dmid);       // dmid = g + LN2'(dh2)
-    if (int rc = weight_f32(b.mat[1], wscratch, &w, st)) return rc;
-    if (int rc = gemm(true, dmid, w, nullptr, tmp, t, d, d, st)) return rc;  // dctx = dmid Wo^T
-    k_attn_dscores<<<dim3(H, t), 256, 0, st>>>(qkv, P, tmp, t, d, dh, dS);
-    k_attn_dq<<<dim3(H, t), 128, 0, st>>>(qkv, dS, t, d, dh, dqkv);
-    k_attn_dkdv<<<dim3(H, t), 128, 0, st>>>(qkv, P, dS, tmp, t, d, dh, dqkv);
-    if (int rc = weight_f32(b.mat[0], wscratch, &w, st)) return rc;
-    if (int rc = gemm(true, dqkv, w, nullptr, tmp, t, d, 3 * d, st)) return rc;  // dh1 = dqkv Wqkv^T
-    k_ln_bwd<<<t, 256, 0, st>>>(tmp, xh1, inv1, b.ln1_g, d, dmid, dx);         // dx = dmid + LN1'(dh1)
+    if (int rc = bwd(2, act, tmp)) return rc;                                           // dh2 = dpre Win^T
+    k_ln_bwd<<<t, 256, 0, st>>>(tmp, xh2, inv2, b.ln2_g, d, g, dmid);                   // dmid = g + LN2'(dh2)
+    if (int rc = bwd(1, dmid, tmp)) return rc;                                          // dctx = dmid Wo^T
+    if (int rc = attn_bwd(qkv, P, dS, tmp, dqkv, t, d, H, dh, st)) return rc;
+    if (int rc = bwd(0, dqkv, tmp)) return rc;                                  // dh1 = dqkv Wqkv^T
+    k_ln_bwd<<<t, 256, 0, st>>>(tmp, xh1, inv1, b.ln1_g, d, dmid, dx);          // dx = dmid + LN1'(dh1)
     return launch_check("block_backward");
 }
 
@@ -402,25 +515,41 @@ extern "C" int pb_span_backward(pb_span* span, const float* d_tape, int32_t t, c
     // workspace: see block_backward's carve-up
     const int64_t ws_floats = 9 * td + 2 * (int64_t)t + 2 * (int64_t)H * t * t + 3 * td + 3 * (int64_t)t * rd +
                               3 * td + 64;
-    int64_t wmax = 0;
+    // tcgen05 scratch: digit planes for the widest contraction, W^T tiles of the largest matrix
+    int64_t kp_max = 0, tcode_max = 0, n_outl = 0;
     for (const auto& b : span->blocks)
         for (const auto& m : b.mat)
-            if (m.int8) wmax = std::max<int64_t>(wmax, (int64_t)m.K * m.M);
-    float *ws = nullptr, *wscratch = nullptr, *g = nullptr;
+            if (m.int8) {
+                kp_max = std::max<int64_t>(kp_max, std::max<int64_t>(m.Kp, round_up(m.M, 32)));
+                tcode_max = std::max<int64_t>(tcode_max, round_up(m.K, 128) * round_up(m.M, 32));
+                n_outl = std::max<int64_t>(n_outl, m.n_outl);
+            }
+    float *ws = nullptr, *g = nullptr;
     PB_CHECK_CUDA(cudaMallocAsync(&ws, sizeof(float) * ws_floats, st));
     PB_CHECK_CUDA(cudaMallocAsync(&g, sizeof(float) * 2 * td, st));
-    if (wmax) PB_CHECK_CUDA(cudaMallocAsync(&wscratch, sizeof(float) * wmax, st));
+    TcWs tw;
+    if (kp_max) {
+        PB_CHECK_CUDA(cudaMallocAsync(&tw.bcanon, (size_t)round_up(t, TC_TOKENS) * kp_max * 3, st));
+        PB_CHECK_CUDA(cudaMallocAsync(&tw.back, sizeof(float) * t, st));
+        PB_CHECK_CUDA(cudaMallocAsync(&tw.stats, sizeof(float4) * t, st));
+        PB_CHECK_CUDA(cudaMallocAsync(&tw.xo, sizeof(float) * std::max<int64_t>(1, t * n_outl), st));
+        PB_CHECK_CUDA(cudaMallocAsync(&tw.ones, sizeof(float) * kp_max, st));
+        PB_CHECK_CUDA(cudaMallocAsync(&tw.tcodes, (size_t)tcode_max, st));
+        k_fill<<<grid_for(kp_max), 256, 0, st>>>(tw.ones, kp_max, 1.f);
+    }
     PB_CHECK_CUDA(cudaMemcpyAsync(g, d_grad_out, sizeof(float) * td, cudaMemcpyDeviceToDevice, st));
     int rc = PB_OK;
     float* cur = g;
     float* nxt = g + td;
     for (int j = span->cfg.n_blocks - 1; j >= 0 && !rc; --j) {
         float* out = j == 0 ? d_grad_in : nxt;
-        rc = block_backward(span, j, d_tape + (int64_t)j * td, cur, out, t, ws, wscratch, st);
+        rc = block_backward(span, j, d_tape + (int64_t)j * td, cur, out, t, ws, tw, st);
         std::swap(cur, nxt);
     }
     cudaFreeAsync(ws, st);
     cudaFreeAsync(g, st);
-    if (wscratch) cudaFreeAsync(wscratch, st);
+    for (void* p : {(void*)tw.bcanon, (void*)tw.back, (void*)tw.stats, (void*)tw.xo, (void*)tw.ones,
+                    (void*)tw.tcodes})
+        if (p) cudaFreeAsync(p, st);
     return rc;
 }

@@ -100,8 +100,10 @@ def test_backward_zero_grad_is_zero():
     span.close()
 
 
-def test_bloom7b1_block_backward_vs_f64_autograd():
-    """One 7B1-shape block (h=4096, H=32), a 48-token row: the span's
+@pytest.mark.parametrize("t", [48, 161])
+def test_bloom7b1_block_backward_vs_f64_autograd(t):
+    """One 7B1-shape block (h=4096, H=32), a 48-token row (one tcgen05
+    token tile) and a 161-token row (three, the last one padded): the span's
     BACKWARD vs float64 torch autograd of the same dequantized block."""
     import torch
 
@@ -114,7 +116,6 @@ def test_bloom7b1_block_backward_vs_f64_autograd():
     span.generate_weights(42)
     ref = RefBlock(span, 0)
     g = torch.Generator(device="cuda").manual_seed(3)
-    t = 48
     x = torch.randn(1, t, cfg.hidden, device="cuda", generator=g) * 0.05
     gr = torch.rand(1, t, cfg.hidden, device="cuda", generator=g) * 2 - 1
     _, tape = span.forward(x, tape=True)
