@@ -69,6 +69,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-b32", action="store_true")
     p.add_argument("--no-c2", action="store_true")
+    p.add_argument("--no-f2", action="store_true", help="skip the BACKWARD (f2) sub-record")
     p.add_argument("--b32-ctx", type=int, default=64,
                    help="context of the b=32 sessions (N=1: 172.7 GB of weights leave ~8 GB of HBM for KV)")
     p.add_argument("--synthetic-kv", action="store_true", help="skip the real prefill (KV content is synthetic)")
@@ -498,6 +499,46 @@ def c2_record(args):
             "note": "24 blocks h=1024 on one GPU, 128-token prefix, batch-1 decode timed with CUDA events"}
 
 
+def f2_record(args):
+    """SURVEY §8 f2 (BACKWARD, server.py:431-450): one 512-position row back
+    through two 176B-shape blocks (tape-less recompute + backward, int8
+    matrices on tcgen05, attention on 3xTF32 mma). Per block and row: 2 t 20 h^2
+    useful matmul flops (recompute qkv/wo/mlp_in 8 h^2 weights, backward all
+    four matrices 12 h^2)."""
+    import torch
+
+    from paper_2209_01188_b200.model import SHAPES
+    from paper_2209_01188_b200.span import BlockSpan
+
+    cfg, L, t = SHAPES["bloom-176b"], 2, 512
+    span = BlockSpan(cfg, 0, L, int8=True, page_tokens=64, n_pages=t // 64 + 4, max_tokens=256, max_seqs=8)
+    span.generate_weights(args.seed)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(1, t, cfg.hidden, device="cuda", generator=g) * 0.05
+    gr = torch.rand(1, t, cfg.hidden, device="cuda", generator=g) * 2 - 1
+    _, tape = span.forward(x, tape=True)
+    span.backward(tape, gr)  # warm-up: workspace arena, kernel setup
+    torch.cuda.synchronize()
+    reps = 4
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        out = span.backward(tape, gr)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps / L
+    finite = bool(torch.isfinite(out).all())
+    span.close()
+    del tape, out
+    useful = 2.0 * t * 20 * cfg.hidden ** 2 / (ms / 1e3) / 1e12
+    bf16 = measured_tflops()
+    return {"metric": "BLOOM-176B BACKWARD positions/s per block (one 512-position row)", "value": t / (ms / 1e3),
+            "unit": "positions/s", "ms_per_block": ms, "rows": 1, "t": t, "blocks": L, "finite": finite,
+            "useful_matmul_tflops": useful, "tensor_frac_vs_bf16_dense": useful / bf16 if bf16 else None,
+            "note": "tape-less recompute + backward per block; int8 matrices on the tcgen05 GEMM (3 int8 digit "
+                    "columns per position: issued int8 ops = 3x useful), attention products on 3xTF32 mma.sync"}
+
+
 def b32_record(pl, args, cfg):
     """BASELINE's tokens/s (b=32): each micro-batch is 32 batch-1 sessions
     stepped together (one launch sequence per block for all 32 tokens)."""
@@ -692,6 +733,10 @@ def run_ours(args):
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         c2 = c2_record(args)  # before the 176B span: HBM is nearly full with it
         torch.cuda.empty_cache()
+    f2 = None
+    if not args.no_f2 and rank0 and args.shape == "bloom-176b":
+        f2 = f2_record(args)
+        torch.cuda.empty_cache()
     pl = Pipeline(args, cfg)
     S, N, rank, B = pl.S, pl.world, pl.rank, pl.B
     K, W = args.steps, args.warmup
@@ -771,6 +816,7 @@ def run_ours(args):
         "e2e": e2e,
         "b32": b32,
         "c2": c2,
+        "f2": f2,
         "setup_s": {"weights_gen_quant": pl.gen_s, "prefill": pf_s},
         "prefill": {"tokens": T0 * S * B, "wall_s": pf_s, "tokens_per_s_wall": T0 * S * B / max(pf_s, 1e-9),
                     "tcgen05_gemm": {"launches": tc_n, "ms": tc_ms,

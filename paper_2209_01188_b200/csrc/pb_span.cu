@@ -96,7 +96,7 @@ void free_span(pb_span* s) {
     }
     void* ptrs[] = {s->kv, s->slopes, s->xa, s->mid, s->q, s->ctx, s->act, s->xo, s->y32, s->frag, s->bcanon, s->back, s->stats, s->pst_x, s->pst_mid, s->tokmax_ctx, s->tokmax_act,
                     s->partials, s->counters, s->attn_part, s->d_tok_seq, s->d_tok_pos, s->d_pages, s->d_grp_first, s->d_grp_count,
-                    s->hop_codes, s->hop_scales, s->d_unit_base, s->sk_acc};
+                    s->hop_codes, s->hop_scales, s->d_unit_base, s->sk_acc, s->train_ws};
     for (void* p : ptrs) cudaFree(p);
     for (int i = 0; i < pb_span::NSLOT; ++i) {
         if (s->h_meta[i]) cudaFreeHost(s->h_meta[i]);

@@ -69,6 +69,9 @@ struct pb_span {
     std::map<GraphKey, GraphEntry> graphs;
     cudaStream_t cap_stream = nullptr;
     float *g_in = nullptr, *g_out = nullptr;  // [64][d]
+    // BACKWARD workspace (pb_train.cu): one grow-only arena, kept across calls
+    uint8_t* train_ws = nullptr;
+    int64_t train_ws_bytes = 0;
     std::mutex mu;  // one step at a time per span (the stream is shared)
 };
 

@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdio>
 
+#include "pb_async.cuh"
 #include "pb_common.cuh"
 #include "pb_span_impl.h"
 
@@ -168,14 +169,13 @@ int mm_bwd_tc(const Mat& m, const float* g, int t, float* dx, const TcWs& w, cud
     return PB_OK;
 }
 
-// ---------------------------------------------------------------- batched strided SIMT GEMM (f32)
+// ---------------------------------------------------------------- batched strided GEMM (f32 accuracy)
 //
 // C(b, i, j) = alpha sum_p A(b, i, p) B(b, p, j) (+ bias[j]) with arbitrary element strides, so one
 // kernel serves the f32 weight matrices (either orientation) and every per-head attention product on
-// the [t][3d] q|k|v rows and the [H][t][t] probability planes. 64 x 64 output tiles, 16-deep k slices
-// staged in shared memory (loads coalesced along whichever operand index has stride 1), 4 x 4 outputs
-// per thread, f32 accumulation. Causal modes bound the work: CM_OUT skips output tiles strictly above
-// the diagonal (j > i everywhere: masked scores), CM_P_LE_I contracts p <= i only, CM_P_GE_I p >= i.
+// the [t][3d] q|k|v rows and the [H][t][t] probability planes. Causal modes bound the work: CM_OUT
+// skips output tiles strictly above the diagonal (j > i everywhere: masked scores), CM_P_LE_I
+// contracts p <= i only, CM_P_GE_I p >= i (the skipped terms are zeros of the probability planes).
 enum { CM_NONE = 0, CM_OUT = 1, CM_P_LE_I = 2, CM_P_GE_I = 3 };
 
 struct BG {
@@ -191,67 +191,144 @@ struct BG {
     int causal;
 };
 
-constexpr int GB = 64, GK = 16;
+// Tensor cores at f32 accuracy ("3xTF32"): every operand splits into hi = tf32(x) and
+// lo = tf32(x - hi), and each product accumulates a_lo b_hi + a_hi b_lo + a_hi b_hi
+// (mma.sync.m16n8k8 tf32, f32 accumulators): ~22 mantissa bits per product. 128 x 128 output tiles,
+// 32-deep k slices double-buffered in shared memory by 4-byte cp.async (any stride, zero fill;
+// [p][i] / [p][j] with pitch 136: conflict-free fragment loads), 8 warps as 2 x 4 of 64 x 32,
+// two CTAs per SM. Measured (176B, t = 2048, ncu): the single-buffered version was latency-bound
+// (long-scoreboard stalls, 8 warps per SM), no faster than a 64 x 64 SIMT kernel.
+constexpr int XB = 128, XK = 32, XP = XB + 8;
 
-__global__ void __launch_bounds__(256) k_bgemm(BG g) {
-    __shared__ float As[GK][GB + 4];
-    __shared__ float Bs[GK][GB + 4];
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int i0 = blockIdx.y * GB, j0 = blockIdx.x * GB;
+__device__ __forceinline__ uint32_t tf32_bits(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ void mma_tf32(float* c, const uint32_t* a, const uint32_t* b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool ok) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 4 : 0)
+                 : "memory");
+}
+
+// one 32-deep k slice of both operands into a stage (zero-filled outside the matrix / p range)
+__device__ __forceinline__ void x3_load(const BG& g, const float* A, const float* B, float* As, float* Bs, int i0,
+                                        int j0, int p0, int p_hi, bool a_pc, bool b_jc) {
+#pragma unroll 4
+    for (int e = threadIdx.x; e < XB * XK; e += 256) {
+        int ii, pp;
+        if (a_pc) ii = e / XK, pp = e % XK;
+        else pp = e / XB, ii = e % XB;
+        const int i = i0 + ii, p = p0 + pp;
+        const bool ok = i < g.I && p < p_hi;
+        cp_async4(As + pp * XP + ii, ok ? A + i * g.a_i + p * g.a_p : A, ok);
+    }
+#pragma unroll 4
+    for (int e = threadIdx.x; e < XB * XK; e += 256) {
+        int jj, pp;
+        if (b_jc) pp = e / XB, jj = e % XB;
+        else jj = e / XK, pp = e % XK;
+        const int j = j0 + jj, p = p0 + pp;
+        const bool ok = j < g.J && p < p_hi;
+        cp_async4(Bs + pp * XP + jj, ok ? B + p * g.b_p + j * g.b_j : B, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+constexpr int X_STAGE = 2 * XK * XP;  // floats per stage (A then B)
+constexpr int X_SMEM = 2 * X_STAGE * (int)sizeof(float);
+
+__global__ void __launch_bounds__(256, 2) k_bgemm_x3(BG g) {
+    extern __shared__ float xs[];  // [2 stages][A: XK x XP | B: XK x XP]
+    const int i0 = blockIdx.y * XB, j0 = blockIdx.x * XB;
     const int64_t bz = blockIdx.z;
-    if (g.causal == CM_OUT && j0 > i0 + GB - 1) return;
+    if (g.causal == CM_OUT && j0 > i0 + XB - 1) return;
     int p_lo = 0, p_hi = g.P;
-    if (g.causal == CM_P_LE_I) p_hi = min(g.P, i0 + GB);
-    if (g.causal == CM_P_GE_I) p_lo = i0 & ~(GK - 1);
+    if (g.causal == CM_P_LE_I) p_hi = min(g.P, i0 + XB);
+    if (g.causal == CM_P_GE_I) p_lo = i0 & ~(XK - 1);
     const float* A = g.A + bz * g.a_b;
     const float* B = g.B + bz * g.b_b;
     const bool a_pc = g.a_p == 1, b_jc = g.b_j == 1;
-    float acc[4][4] = {};
-    for (int p0 = p_lo; p0 < p_hi; p0 += GK) {
-        for (int e = threadIdx.x; e < GB * GK; e += 256) {
-            int ii, pp;
-            if (a_pc) ii = e / GK, pp = e % GK;
-            else pp = e / GB, ii = e % GB;
-            const int i = i0 + ii, p = p0 + pp;
-            As[pp][ii] = (i < g.I && p < p_hi) ? A[i * g.a_i + p * g.a_p] : 0.f;
-        }
-        for (int e = threadIdx.x; e < GB * GK; e += 256) {
-            int jj, pp;
-            if (b_jc) pp = e / GB, jj = e % GB;
-            else jj = e / GK, pp = e % GK;
-            const int j = j0 + jj, p = p0 + pp;
-            Bs[pp][jj] = (j < g.J && p < p_hi) ? B[p * g.b_p + j * g.b_j] : 0.f;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;
+    const int gq = lane >> 2, tq = lane & 3;
+    float acc[4][4][4] = {};
+    const int n_sl = p_hi > p_lo ? (p_hi - p_lo + XK - 1) / XK : 0;
+    if (n_sl > 0) x3_load(g, A, B, xs, xs + XK * XP, i0, j0, p_lo, p_hi, a_pc, b_jc);
+    for (int sl = 0; sl < n_sl; ++sl) {
+        if (sl + 1 < n_sl) {
+            float* nx = xs + ((sl + 1) & 1) * X_STAGE;
+            x3_load(g, A, B, nx, nx + XK * XP, i0, j0, p_lo + (sl + 1) * XK, p_hi, a_pc, b_jc);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         __syncthreads();
+        const float* As = xs + (sl & 1) * X_STAGE;
+        const float* Bs = As + XK * XP;
 #pragma unroll
-        for (int pp = 0; pp < GK; ++pp) {
-            float a[4], b[4];
+        for (int k8 = 0; k8 < XK; k8 += 8) {
+            uint32_t ah[4][4], al[4][4], bh[4][2], bl[4][2];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) a[r] = As[pp][ty * 4 + r];
+            for (int mt = 0; mt < 4; ++mt) {
+                const int r = wm + mt * 16 + gq;
+                const float v[4] = {As[(k8 + tq) * XP + r], As[(k8 + tq) * XP + r + 8], As[(k8 + tq + 4) * XP + r],
+                                    As[(k8 + tq + 4) * XP + r + 8]};
 #pragma unroll
-            for (int c = 0; c < 4; ++c) b[c] = Bs[pp][tx * 4 + c];
+                for (int q = 0; q < 4; ++q) {
+                    ah[mt][q] = tf32_bits(v[q]);
+                    al[mt][q] = tf32_bits(v[q] - __uint_as_float(ah[mt][q]));
+                }
+            }
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
+            for (int nt = 0; nt < 4; ++nt) {
+                const int c = wn + nt * 8 + gq;
+                const float v[2] = {Bs[(k8 + tq) * XP + c], Bs[(k8 + tq + 4) * XP + c]};
 #pragma unroll
-                for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
+                for (int q = 0; q < 2; ++q) {
+                    bh[nt][q] = tf32_bits(v[q]);
+                    bl[nt][q] = tf32_bits(v[q] - __uint_as_float(bh[nt][q]));
+                }
+            }
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                    mma_tf32(acc[mt][nt], al[mt], bh[nt]);
+                    mma_tf32(acc[mt][nt], ah[mt], bl[nt]);
+                    mma_tf32(acc[mt][nt], ah[mt], bh[nt]);
+                }
         }
-        __syncthreads();
+        __syncthreads();  // the stage is refilled by the next iteration's load
     }
     float* C = g.C + bz * g.c_b;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int i = i0 + ty * 4 + r;
-        if (i >= g.I) continue;
+    for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const int j = j0 + tx * 4 + c;
-            if (j < g.J) C[i * g.c_i + j * g.c_j] = acc[r][c] * g.alpha + (g.bias ? g.bias[j] : 0.f);
-        }
-    }
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int i = i0 + wm + mt * 16 + gq + (q >> 1) * 8, j = j0 + wn + nt * 8 + tq * 2 + (q & 1);
+                if (i < g.I && j < g.J) C[i * g.c_i + j * g.c_j] = acc[mt][nt][q] * g.alpha + (g.bias ? g.bias[j] : 0.f);
+            }
 }
 
 int bgemm(const BG& g, int batch, cudaStream_t st) {
-    k_bgemm<<<dim3((unsigned)ceil_div(g.J, GB), (unsigned)ceil_div(g.I, GB), (unsigned)batch), 256, 0, st>>>(g);
+    static int ok[PB_MAX_DEVICES] = {};
+    if (per_device(ok, [](int) {
+            return cudaFuncSetAttribute(k_bgemm_x3, cudaFuncAttributeMaxDynamicSharedMemorySize, X_SMEM) ==
+                           cudaSuccess ? 1 : -1;
+        }) < 0)
+        return launch_check("bgemm setup");
+    k_bgemm_x3<<<dim3((unsigned)ceil_div(g.J, XB), (unsigned)ceil_div(g.I, XB), (unsigned)batch), 256, X_SMEM, st>>>(g);
     return launch_check("bgemm");
 }
 
@@ -524,17 +601,43 @@ extern "C" int pb_span_backward(pb_span* span, const float* d_tape, int32_t t, c
                 tcode_max = std::max<int64_t>(tcode_max, round_up(m.K, 128) * round_up(m.M, 32));
                 n_outl = std::max<int64_t>(n_outl, m.n_outl);
             }
-    float *ws = nullptr, *g = nullptr;
-    PB_CHECK_CUDA(cudaMallocAsync(&ws, sizeof(float) * ws_floats, st));
-    PB_CHECK_CUDA(cudaMallocAsync(&g, sizeof(float) * 2 * td, st));
+    // carve-up of the span's grow-only arena (256-byte aligned pieces)
+    int64_t off = 0;
+    auto piece = [&](int64_t bytes) {
+        const int64_t at = off;
+        off += round_up(std::max<int64_t>(bytes, 1), 256);
+        return at;
+    };
+    const int64_t o_ws = piece(sizeof(float) * ws_floats), o_g = piece(sizeof(float) * 2 * td);
+    int64_t o_bc = 0, o_back = 0, o_stats = 0, o_xo = 0, o_ones = 0, o_tc = 0;
+    if (kp_max) {
+        o_bc = piece(round_up(t, TC_TOKENS) * kp_max * 3);
+        o_back = piece(sizeof(float) * t);
+        o_stats = piece(sizeof(float4) * t);
+        o_xo = piece(sizeof(float) * t * n_outl);
+        o_ones = piece(sizeof(float) * kp_max);
+        o_tc = piece(tcode_max);
+    }
+    if (off > span->train_ws_bytes) {
+        // grow (rare): plain cudaMalloc after the stream drains, so any later stream may use it
+        PB_CHECK_CUDA(cudaStreamSynchronize(st));
+        if (span->train_ws) PB_CHECK_CUDA(cudaFree(span->train_ws));
+        span->train_ws = nullptr;
+        span->train_ws_bytes = 0;
+        PB_CHECK_CUDA(cudaMalloc(&span->train_ws, off));
+        span->train_ws_bytes = off;
+    }
+    uint8_t* base = span->train_ws;
+    float* ws = reinterpret_cast<float*>(base + o_ws);
+    float* g = reinterpret_cast<float*>(base + o_g);
     TcWs tw;
     if (kp_max) {
-        PB_CHECK_CUDA(cudaMallocAsync(&tw.bcanon, (size_t)round_up(t, TC_TOKENS) * kp_max * 3, st));
-        PB_CHECK_CUDA(cudaMallocAsync(&tw.back, sizeof(float) * t, st));
-        PB_CHECK_CUDA(cudaMallocAsync(&tw.stats, sizeof(float4) * t, st));
-        PB_CHECK_CUDA(cudaMallocAsync(&tw.xo, sizeof(float) * std::max<int64_t>(1, t * n_outl), st));
-        PB_CHECK_CUDA(cudaMallocAsync(&tw.ones, sizeof(float) * kp_max, st));
-        PB_CHECK_CUDA(cudaMallocAsync(&tw.tcodes, (size_t)tcode_max, st));
+        tw.bcanon = base + o_bc;
+        tw.back = reinterpret_cast<float*>(base + o_back);
+        tw.stats = reinterpret_cast<float4*>(base + o_stats);
+        tw.xo = reinterpret_cast<float*>(base + o_xo);
+        tw.ones = reinterpret_cast<float*>(base + o_ones);
+        tw.tcodes = reinterpret_cast<int8_t*>(base + o_tc);
         k_fill<<<grid_for(kp_max), 256, 0, st>>>(tw.ones, kp_max, 1.f);
     }
     PB_CHECK_CUDA(cudaMemcpyAsync(g, d_grad_out, sizeof(float) * td, cudaMemcpyDeviceToDevice, st));
@@ -546,10 +649,5 @@ extern "C" int pb_span_backward(pb_span* span, const float* d_tape, int32_t t, c
         rc = block_backward(span, j, d_tape + (int64_t)j * td, cur, out, t, ws, tw, st);
         std::swap(cur, nxt);
     }
-    cudaFreeAsync(ws, st);
-    cudaFreeAsync(g, st);
-    for (void* p : {(void*)tw.bcanon, (void*)tw.back, (void*)tw.stats, (void*)tw.xo, (void*)tw.ones,
-                    (void*)tw.tcodes})
-        if (p) cudaFreeAsync(p, st);
     return rc;
 }
