@@ -83,8 +83,10 @@ __device__ __forceinline__ void stage_tokens(const Epi& e, const float* back, in
 
 // 16 consecutive tokens (tile columns c0 .. c0 + 15, global tokens tok0 ..) of output row o;
 // h / m / l are the three digit accumulators (exact s32), recombined exactly in int64
+// s_tmax: per-CTA shared-memory max |y s_next| indexed by token (the caller flushes it), or null for
+// global atomics
 __device__ __forceinline__ void tc_epi16(const Epi& e, int o, int lane, int tok0, const TokInfo* ti, const int* h,
-                                         const int* m, const int* l) {
+                                         const int* m, const int* l, float* s_tmax = nullptr) {
     const bool row_ok = o < e.M;
     if (e.kind == EPI_BWD) {  // dx_k = s_k * sum_o g_o codes[o][k] (pb_train.cu)
         if (!row_ok) return;
@@ -149,7 +151,8 @@ __device__ __forceinline__ void tc_epi16(const Epi& e, int o, int lane, int tok0
         for (int j = 0; j < 16; ++j) {
             float mx = (row_ok && ti[j].valid) ? fabsf(v[j] * sn) : 0.f;
             mx = warp_max(mx);
-            if (lane == 0 && ti[j].valid) atomicMax(reinterpret_cast<int*>(e.tokmax) + tok0 + j, __float_as_int(mx));
+            if (lane == 0 && ti[j].valid)
+                atomicMax(reinterpret_cast<int*>(s_tmax ? s_tmax : e.tokmax) + tok0 + j, __float_as_int(mx));
         }
     }
 }

@@ -295,7 +295,8 @@ struct SkCfg {
     static constexpr int NSETS = 2;  // accumulator sets (segments in flight); 4 measured equal
     static constexpr uint32_t IDESC = tc_idesc_i8(N);
     static constexpr size_t SMEM =
-        (size_t)STAGES * KT * (TC_A + B_KT) + (2 * STAGES + 2 * NSETS) * 8 + 16 + BN * sizeof(TokInfo);
+        (size_t)STAGES * KT * (TC_A + B_KT) + (2 * STAGES + 2 * NSETS) * 8 + 16 + BN * sizeof(TokInfo) +
+        BN * sizeof(float);
 };
 
 struct TcSkArgs {
@@ -325,6 +326,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
     uint64_t* accempty = accfull + C::NSETS;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + C::NSETS);
     TokInfo* s_tok = reinterpret_cast<TokInfo*>(tmem_slot + 4);  // 16-B aligned
+    float* s_tmax = reinterpret_cast<float*>(s_tok + BN);          // EPI_GELU operand range, per CTA
 
     const int warp = warp_uniform_id(), lane = threadIdx.x & 31;
     const int KC = a.KC, c = (int)blockIdx.x;
@@ -428,6 +430,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
         // the per-token constants (scale, KV page / slot) come from the operand kernel: after the PDL wait
         pdl_wait();
         stage_tokens(a.epi, a.act.back, a.act.n_tok, 0, BN, s_tok, (int)threadIdx.x - 64, 32 * TC_EPI_WARPS);
+        // the per-token max |y s_next| (EPI_GELU) is reduced in shared memory and leaves the CTA as
+        // BN global atomics at the end: every row group's warps hitting the same BN addresses in L2
+        // serialised the mlp_in launch (448 row groups x 4 quarters x BN atomics on one 128-B line)
+        float* tmax = a.epi.tokmax ? s_tmax : nullptr;
+        if ((int)threadIdx.x - 64 < BN) s_tmax[threadIdx.x - 64] = 0.f;
         asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");
         int i = 0;
         for (int64_t u = u0; u < u1; ++i) {
@@ -450,7 +457,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
                 tmem_ld16(tbase + c0, h);
                 tmem_ld16(tbase + BN + c0, m);
                 tmem_ld16(tbase + 2 * BN + c0, l);
-                tc_epi16(a.epi, o, lane, c0, s_tok + c0, h, m, l);
+                tc_epi16(a.epi, o, lane, c0, s_tok + c0, h, m, l, tmax);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&accempty[b]);
@@ -496,8 +503,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
                     __stcg(acc + (BN + c0 + j) * TC_BM, 0);
                     __stcg(acc + (2 * BN + c0 + j) * TC_BM, 0);
                 }
-                tc_epi16(a.epi, o, lane, c0, s_tok + c0, h, m, l);
+                tc_epi16(a.epi, o, lane, c0, s_tok + c0, h, m, l, tmax);
             }
+        }
+        if (tmax) {
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");
+            const int t = (int)threadIdx.x - 64;
+            if (t < BN && t < a.act.n_tok)
+                atomicMax(reinterpret_cast<int*>(a.epi.tokmax) + t, __float_as_int(s_tmax[t]));
         }
     }
     tc_fence_before();
