@@ -716,7 +716,11 @@ extern "C" int pb_span_step_int8(pb_span* span, int32_t n_tok, int32_t n_seq, co
         ++extra;
     }
     float* out = d_out_f32 ? d_out_f32 : span->xa;
-    if (int rc = run_blocks(span, n_tok, max_pos, in, out, st, d_tape)) return rc;
+    // the span-to-span hop path (box front end, pipelined bench) replays decode steps as graphs too
+    const bool graph = !d_tape && span->cfg.graphs && n_tok <= GRAPH_MAX_TOKENS && !span->prof_on && !trace_active();
+    if (int rc = graph ? run_blocks_graph(span, n_tok, max_pos, in, out, st)
+                       : run_blocks(span, n_tok, max_pos, in, out, st, d_tape))
+        return rc;
     if (d_out_codes) {
         const int ev = prof_begin(span, st);
         if (int rc = quantize_blockwise(out, n, 64, d_out_codes, d_out_scales, st)) return rc;
