@@ -167,11 +167,11 @@ class _Session:
 
 
 class _Job:
-    __slots__ = ("seq", "x", "out", "err", "done")
+    __slots__ = ("seq", "x", "out", "err", "done", "ev")
 
     def __init__(self, seq, x):
         self.seq, self.x = seq, x
-        self.out = self.err = None
+        self.out = self.err = self.ev = None
         self.done = threading.Event()
 
 
@@ -189,11 +189,16 @@ class StepScheduler:
         self._t.start()
 
     def run(self, seq, x):
+        """Queue one STEP and return its output once the GPU has produced it.
+        The scheduler thread only enqueues the batch and moves on to the next
+        one; the wait for the batch's completion event happens here, in the
+        handler's thread (x stays referenced until the step has read it)."""
         job = _Job(seq, x)
         self.q.put(job)
         job.done.wait()
         if job.err is not None:
             raise job.err
+        job.ev.synchronize()
         return job.out
 
     def stop(self):
@@ -237,9 +242,11 @@ class StepScheduler:
             try:
                 if ready:
                     outs = self.span.step([(j.seq, j.x) for j in ready])
-                    torch.cuda.current_stream(self.span.device).synchronize()
+                    # no host sync: the next batch is enqueued behind this one on the same stream
+                    ev = torch.cuda.Event()
+                    ev.record(torch.cuda.current_stream(self.span.device))
                     for j, o in zip(ready, outs):
-                        j.out = o
+                        j.out, j.ev = o, ev
             except Exception as e:  # noqa: BLE001
                 for j in ready:
                     j.err = e
