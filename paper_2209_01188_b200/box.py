@@ -45,7 +45,7 @@ from dataclasses import dataclass
 
 from .errors import CapacityError, InputError
 from .pipeline import DevPtr, P2PRing, dev_view, split_blocks
-from .server import ServerConfig, ServerNode, _Job
+from .server import ServerConfig, ServerNode, _NonFinite
 from .span import BlockSpan, Sequence
 
 log = logging.getLogger(__name__)
@@ -318,6 +318,15 @@ class _Fwd:
         self.err = None
 
 
+class _BoxJob:
+    __slots__ = ("seq", "x", "out", "err", "done")
+
+    def __init__(self, seq, x):
+        self.seq, self.x = seq, x
+        self.out = self.err = None
+        self.done = threading.Event()
+
+
 class BoxScheduler:
     """Rank 0's single control thread: coalesces concurrent STEPs of distinct
     sessions into ring jobs (StepScheduler's batching), reserves rank 0's
@@ -360,7 +369,7 @@ class BoxScheduler:
         if t > self.max_tokens:
             self.call("reserve", seq, seq.length + t)
             return torch.cat([self.run(seq, x[c0:c0 + self.max_tokens]) for c0 in range(0, t, self.max_tokens)])
-        job = _Job(seq, x)
+        job = _BoxJob(seq, x)
         self.q.put(("step", job))
         job.done.wait()
         if job.err is not None:
@@ -666,6 +675,19 @@ class BoxFrontEnd(ServerNode):
 
     def _make_scheduler(self):
         return self.span.sched
+
+    def _run_step(self, seq, msg, encoding: int) -> bytes:
+        import torch
+
+        st = self._io_stream()
+        with torch.cuda.stream(st):
+            x = msg.decode()
+        st.synchronize()
+        out = self.sched.run(seq, x)
+        try:
+            return self._encode(out, encoding)
+        except InputError as e:
+            raise _NonFinite(str(e)) from e  # computed, then failed encoding (position advances)
 
     def _shutdown(self):
         super()._shutdown()

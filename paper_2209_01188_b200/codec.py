@@ -230,6 +230,42 @@ def _h2d(arr, pinned, off, nbytes, dtype, dev):
     return torch.from_numpy(arr.copy()).to(dev)
 
 
+class DeviceTensorMsg:
+    """A TensorMsg's sections on the device, not decoded: f32 values, or int8
+    codes + block scales (upload_tensor)."""
+
+    __slots__ = ("encoding", "dims", "block_size", "values", "codes", "scales")
+
+    def __init__(self, encoding, dims, block_size=0, values=None, codes=None, scales=None):
+        self.encoding, self.dims, self.block_size = encoding, tuple(dims), block_size
+        self.values, self.codes, self.scales = values, codes, scales
+
+    @property
+    def rows(self) -> int:
+        return int(self.dims[0]) if self.dims else 1
+
+    def decode(self):
+        """-> CUDA f32 tensor of dims (int8: one dequantize kernel on the current stream)."""
+        if self.encoding == ENC_F32:
+            return self.values
+        return dequantize_blockwise(QuantizedBlockwise(self.block_size, self.scales, self.codes, self.dims))
+
+
+def upload_tensor(data, device=None) -> DeviceTensorMsg:
+    """TensorMsg -> its sections on the device (DMA only, no kernel: the
+    STEP scheduler decodes a whole batch on its own stream)."""
+    import torch
+
+    dev = device or _dev()
+    view, pinned = _buf(data)
+    enc, dims, bs, scales, payload, (poff, soff) = _parse(view)
+    if enc == ENC_F32:
+        return DeviceTensorMsg(enc, dims, values=_h2d(payload, pinned, poff, 4 * payload.size, torch.float32,
+                                                      dev).reshape(dims))
+    return DeviceTensorMsg(enc, dims, bs, codes=_h2d(payload, pinned, poff, payload.size, torch.int8, dev),
+                           scales=_h2d(scales, pinned, soff, 4 * scales.size, torch.float32, dev))
+
+
 def decode_tensor(data, device=None):
     """TensorMsg -> CUDA f32 tensor (int8 decoded on the GPU)."""
     import torch

@@ -166,18 +166,28 @@ class _Session:
         self.poisoned = False  # a non-finite hidden state entered the caches (reference: NaN KV)
 
 
-class _Job:
-    __slots__ = ("seq", "x", "out", "err", "done", "ev")
+class _NonFinite(InputError):
+    """The computed hidden state is not finite: encoding the reply fails."""
 
-    def __init__(self, seq, x):
-        self.seq, self.x = seq, x
-        self.out = self.err = self.ev = None
+
+class _Job:
+    __slots__ = ("seq", "msg", "t", "enc", "res", "err", "done", "ev")
+
+    def __init__(self, seq, msg, enc):
+        self.seq, self.msg, self.enc = seq, msg, enc
+        self.t = msg.rows
+        self.res = self.err = self.ev = None
         self.done = threading.Event()
 
 
 class StepScheduler:
     """Coalesces concurrent STEPs of distinct sessions into one batched span
-    step (one launch sequence per block for the whole batch)."""
+    step (one launch sequence per block for the whole batch), with the wire
+    codec of the whole batch on the scheduler's stream: the handlers only DMA
+    their TensorMsg sections to the device (codec.upload_tensor) and slice
+    their reply out of one pinned copy of the batch's encoded output. (Codec
+    kernels on the handlers' own streams queued behind the next batch's
+    persistent kernels, which hold every SM: 1-2 ms per STEP at 8 sessions.)"""
 
     # batches queued on the GPU at once. Measured (7B1, one GPU, 8 / 16 sessions over TCP, bench e2e):
     # 1 -> 847 / 1031 tokens/s, 2 -> 835 / 966, 3 -> 763 / 874, unbounded -> 501 / 651
@@ -192,22 +202,90 @@ class StepScheduler:
         self._t = threading.Thread(target=self._loop, daemon=True)
         self._t.start()
 
-    def run(self, seq, x):
-        """Queue one STEP and return its output once the GPU has produced it.
-        The scheduler thread only enqueues the batch and moves on to the next
-        one; the wait for the batch's completion event happens here, in the
-        handler's thread (x stays referenced until the step has read it)."""
-        job = _Job(seq, x)
+    def run(self, seq, msg, encoding: int) -> bytes:
+        """Queue one STEP (msg: codec.DeviceTensorMsg [t, d]) and return the
+        reply TensorMsg bytes in `encoding`. The scheduler thread only enqueues
+        the batch and moves on; the wait for the batch's completion event
+        happens here, in the handler's thread (msg stays referenced until the
+        step has read it). Non-finite output raises InputError, as encoding
+        it does (transport/wire.py:89-90)."""
+        job = _Job(seq, msg, encoding)
         self.q.put(job)
         job.done.wait()
         if job.err is not None:
             raise job.err
         job.ev.synchronize()
-        return job.out
+        return self._reply(job)
 
     def stop(self):
         self._stop = True
         self.q.put(None)
+
+    # ---------------------------------------------------------------- batch execution
+
+    def _execute(self, ready) -> None:
+        """One batch on the current stream: decode, step, encode, one D2H copy."""
+        import torch
+
+        span, d = self.span, self.span.config.hidden
+        dev = span.device
+        seqs, lens = [j.seq for j in ready], [j.t for j in ready]
+        ntok, enc = sum(lens), ready[0].enc
+        codes = scales = y = None
+        whole = d % 64 == 0  # 64-value blocks never straddle rows: one batch-wide quantization
+        if (enc == codec.ENC_INT8 and whole and ntok <= span.max_tokens and len(ready) <= span.max_seqs
+                and all(j.msg.encoding == codec.ENC_INT8 and j.msg.block_size == 64 for j in ready)):
+            # int8 in, int8 out: dequantize, blocks, quantize inside one C-ABI call (pb_span_step_int8)
+            cat = (lambda xs: xs[0]) if len(ready) == 1 else torch.cat
+            y = torch.empty(ntok, d, dtype=torch.float32, device=dev)
+            codes = torch.empty(ntok * d, dtype=torch.int8, device=dev)
+            scales = torch.empty(ntok * d // 64, dtype=torch.float32, device=dev)
+            span.step_codes(seqs, lens, in_codes=cat([j.msg.codes for j in ready]),
+                            in_scales=cat([j.msg.scales for j in ready]), out_codes=codes, out_scales=scales, out_f32=y)
+        else:
+            outs = span.step([(j.seq, j.msg.decode().reshape(j.t, d)) for j in ready])
+            y = outs[0] if len(outs) == 1 else torch.cat(outs)
+            if enc == codec.ENC_INT8:
+                if whole:
+                    q = codec.quantize_blockwise(y.reshape(-1), 64)
+                    codes, scales = q.codes, q.scales
+                else:
+                    qs = [codec.quantize_blockwise(y[r0:r0 + t].reshape(-1), 64)
+                          for r0, t in zip(np.cumsum([0] + lens[:-1]), lens)]
+                    codes, scales = torch.cat([q.codes for q in qs]), torch.cat([q.scales for q in qs])
+        flags = torch.isfinite(y).all(dim=1).to(torch.uint8)
+        # one pinned buffer: [scales f32 | codes int8] (int8 reply) or [values f32], then the row flags
+        nsc = 0 if scales is None else scales.numel()
+        body = 4 * nsc + codes.numel() if codes is not None else 4 * ntok * d
+        buf = torch.empty(body + ntok, dtype=torch.uint8, pin_memory=True)
+        if codes is not None:
+            buf[:4 * nsc].view(torch.float32).copy_(scales, non_blocking=True)
+            buf[4 * nsc:body].view(torch.int8).copy_(codes, non_blocking=True)
+        else:
+            buf[:body].view(torch.float32).copy_(y.reshape(-1), non_blocking=True)
+        buf[body:].copy_(flags, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(dev))
+        host = buf.numpy()
+        r0 = c0 = s0 = 0
+        for j, t in zip(ready, lens):
+            nb = -(-t * d // 64)
+            j.res = (buf, host, body, nsc, r0, c0, s0)
+            j.ev = ev
+            r0, c0, s0 = r0 + t, c0 + t * d, s0 + nb
+        return ev
+
+    def _reply(self, job) -> bytes:
+        buf, host, body, nsc, r0, c0, s0 = job.res
+        t, d = job.t, self.span.config.hidden
+        if not host[body + r0:body + r0 + t].all():
+            raise _NonFinite("non-finite tensor")
+        head = codec.encode_header(job.enc, (t, d))
+        if job.enc == codec.ENC_F32:
+            return head + host[4 * c0:4 * (c0 + t * d)].tobytes()
+        nb = -(-t * d // 64)
+        return (head + struct.pack(">I", 64) + host[4 * s0:4 * (s0 + nb)].tobytes()
+                + host[4 * nsc + c0:4 * nsc + c0 + t * d].tobytes())
 
     def _loop(self):
         import torch
@@ -225,7 +303,7 @@ class StepScheduler:
             # batching) instead of each becoming a small launch of its own
             while len(inflight) >= self.MAX_INFLIGHT:
                 inflight.pop(0).synchronize()
-            batch, ntok = [job], job.x.shape[0]
+            batch, ntok = [job], job.t
             while len(batch) < self.max_seqs:
                 try:
                     nxt = self.q.get_nowait()
@@ -234,30 +312,24 @@ class StepScheduler:
                 if nxt is None:
                     self._stop = True
                     break
-                if ntok + nxt.x.shape[0] > self.max_tokens:
+                if ntok + nxt.t > self.max_tokens or nxt.enc != job.enc:
                     pending = nxt
                     break
                 batch.append(nxt)
-                ntok += nxt.x.shape[0]
+                ntok += nxt.t
             # pages are reserved per job: a session the pool cannot extend fails
             # alone (CapacityError -> the handler makes room or answers BUSY)
             # instead of failing every co-batched session
             ready = []
             for j in batch:
                 try:
-                    self.span.reserve(j.seq, j.seq.length + j.x.shape[0])
+                    self.span.reserve(j.seq, j.seq.length + j.t)
                     ready.append(j)
                 except CapacityError as e:
                     j.err = e
             try:
                 if ready:
-                    outs = self.span.step([(j.seq, j.x) for j in ready])
-                    # no host sync: the next batch is enqueued behind this one on the same stream
-                    ev = torch.cuda.Event()
-                    ev.record(torch.cuda.current_stream(self.span.device))
-                    inflight.append(ev)
-                    for j, o in zip(ready, outs):
-                        j.out, j.ev = o, ev
+                    inflight.append(self._execute(ready))
             except Exception as e:  # noqa: BLE001
                 for j in ready:
                     j.err = e
@@ -563,6 +635,20 @@ class ServerNode:
         st.synchronize()
         return x
 
+    def _run_step(self, seq, msg, encoding: int) -> bytes:
+        """One STEP through the span (hook: the box front end runs it through its ring)."""
+        return self.sched.run(seq, msg, encoding)
+
+    def _upload(self, data):
+        """STEP ingress: the TensorMsg sections to the device (DMA only)."""
+        import torch
+
+        st = self._io_stream()
+        with torch.cuda.stream(st):
+            msg = codec.upload_tensor(data, device=self.span.device)
+        st.synchronize()
+        return msg
+
     def _encode(self, t, encoding, producer=None):
         """producer: the stream that computed `t` when that work may still be
         queued (FORWARD / BACKWARD run on the handler's default stream); STEP
@@ -617,24 +703,27 @@ class ServerNode:
                 session.position += t
                 raise RemoteError(ERR_GENERIC, "internal error: non-finite tensor")
             tm = [time.perf_counter()] if _TIMING else None
-            x = self._decode(tensor)
+            msg = self._upload(tensor)
             if tm:
                 tm.append(time.perf_counter())
+            enc = self._reply_encoding()
             try:
-                out = self.sched.run(session.seq, x)
+                reply = self._run_step(session.seq, msg, enc)
             except CapacityError:
                 # the pool is short of pages for this step: the reference never
                 # refuses a step for memory (it evicts after computing,
                 # server.py:389), so evict idle LRU sessions now and retry once
                 self._make_room(session, t)
                 try:
-                    out = self.sched.run(session.seq, x)
+                    reply = self._run_step(session.seq, msg, enc)
                 except CapacityError as e:
                     raise RemoteError(ERR_BUSY, f"KV pool exhausted: {e}") from e
+            except _NonFinite:
+                session.position += t  # computed, then failed encoding the reply (as the reference)
+                raise
             session.position += t
             if tm:
                 tm.append(time.perf_counter())
-            reply = self._encode(out, self._reply_encoding())
             session.last_step = (start_pos, digest, reply)
             if tm:
                 tm.append(time.perf_counter())
