@@ -225,12 +225,13 @@ def make_train():
 
 def make_c2():
     """Config 2 (BLOOM-560M shape, 24 blocks, h=1024, H=16): int8-weights
-    greedy generation with a 128-token prefix (then 39 decode steps), reference qw semantics.
-    Expensive on CPU (~1-2 min); stores tokens and last-position hiddens."""
+    greedy generation with a 128-token prefix then 128 decode steps (SURVEY
+    §8: C2 T0=128, then 128 decode steps), reference qw semantics. Expensive on
+    CPU (several minutes); stores tokens and last-position hiddens."""
     cfg = M.ModelConfig(n_layers=24, hidden=1024, n_heads=16, vocab=250880, max_seq=2048)
     ckpt = M.gen_checkpoint(42, cfg)
     prompt = np.random.default_rng(7).integers(0, cfg.vocab, 128).tolist()
-    toks, hid = qw_generate(ckpt, prompt, 40)
+    toks, hid = qw_generate(ckpt, prompt, 129)
     np.savez_compressed(os.path.join(OUT, "c2.npz"), prompt=np.array(prompt), tokens=np.array(toks), hidden=hid)
 
 

@@ -204,8 +204,11 @@ def test_capacity_errors():
 
 def test_c2_bloom560m_tokens_bit_exact(golden):
     """Config 2: BLOOM-560M shape, int8 weights generated on device, 128-token
-    prefix then 39 decode steps (40 greedy tokens), equal to the reference's
-    qw-mode generation (tests/golden/c2.npz)."""
+    prefix then 128 decode steps, equal to the reference's qw-mode generation
+    (tests/golden/c2.npz). Teacher-forced as SURVEY §8 asks (the golden token
+    is fed back whatever was predicted, so one near-tie cannot derail the rest
+    of the comparison); every predicted token must equal the reference's, and
+    the smallest top-1/top-2 logit margin is reported."""
     import torch
 
     from paper_2209_01188_b200 import codec
@@ -214,22 +217,26 @@ def test_c2_bloom560m_tokens_bit_exact(golden):
 
     torch.backends.cuda.matmul.allow_tf32 = False
     g = golden("c2")
+    want = g["tokens"].tolist()
+    assert len(want) == 129
     cfg = S["bloom-560m"]
     span = BlockSpan(cfg, 0, cfg.n_layers, int8=True, page_tokens=64, max_tokens=256, n_pages=16)
     span.generate_weights(42)
     emb = codec.gen_tensor(42, "embed", cfg.vocab * cfg.hidden).reshape(cfg.vocab, cfg.hidden)
     seq = span.new_sequence()
     pending = torch.as_tensor(g["prompt"], device="cuda")
-    toks, hid = [], []
-    for _ in range(len(g["tokens"])):
+    toks, hid, margins = [], [], []
+    for i in range(len(want)):
         h = span.step([(seq, emb[pending])])[0]
         hid.append(h[-1].cpu().numpy())
         hn = torch.nn.functional.layer_norm(h[-1:].double(), (cfg.hidden,), eps=1e-5)
         logits = (hn @ emb.double().T)[0]
-        nxt = int(torch.argmax(logits))
-        toks.append(nxt)
-        pending = torch.tensor([nxt], device="cuda")
-    assert toks == g["tokens"].tolist()
+        top = torch.topk(logits, 2).values
+        margins.append(float((top[0] - top[1]) / logits.abs().max()))
+        toks.append(int(torch.argmax(logits)))
+        pending = torch.tensor([want[i]], device="cuda")  # teacher forcing
+    print(f"C2: {len(want)} tokens, min top-1/top-2 logit margin {min(margins):.3e} of max|logit|")
+    assert toks == want
     assert rel_err(np.stack(hid), g["hidden"]) <= TOL
     span.close()
 
