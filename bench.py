@@ -699,6 +699,10 @@ def e2e_record(pl, args, cfg, T0):
         cols = list(zip(*node.timing[-K * S:]))
         print("[e2e] STEP decode / compute / encode ms (median):",
               [round(1e3 * statistics.median(c), 3) for c in cols], file=sys.stderr, flush=True)
+        stt = getattr(node, "step_timing", None)
+        if stt:
+            print("[e2e] box STEP decode / ring / encode ms (median):",
+                  [round(1e3 * statistics.median(c), 3) for c in zip(*stt[-K * S:])], file=sys.stderr, flush=True)
         bt = getattr(node.sched, "timing", None)
         if bt:
             d = [[b - a for a, b in zip(t, t[1:])] for t in bt[-K * S:]]

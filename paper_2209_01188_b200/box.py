@@ -345,6 +345,8 @@ class BoxScheduler:
         self.q: queue.Queue = queue.Queue()
         self.done_q: queue.Queue = queue.Queue()
         self.slots_free = threading.Semaphore(plan.in_flight)
+        self.busy = 0  # jobs launched and not yet completed
+        self._busy_lock = threading.Lock()
         self.job_ids = itertools.count()
         self.batches = self.batched_steps = 0
         self.egress = state.new_stream()
@@ -441,7 +443,13 @@ class BoxScheduler:
                         break
                     batch.append(nxt[1])
                     ntok += nxt[1].x.shape[0]
-                self._submit_steps(batch)
+                # spread concurrent sessions over the idle pipeline stages instead of coalescing
+                # them into one job that would leave the other stages idle (measured: 2 sessions on
+                # a 2-GPU box arrive together and ran as one 2-token job per period)
+                parts = min(len(batch), max(1, self.plan.world - self.busy))
+                per = -(-len(batch) // parts)
+                for i in range(0, len(batch), per):
+                    self._submit_steps(batch[i:i + per])
                 continue
             ev, args = item[1], item[2]
             try:
@@ -481,6 +489,8 @@ class BoxScheduler:
         t2 = time.perf_counter()
         waitable, out = self.state.egress(int(desc[1]), n_tok, self.egress)
         t3 = time.perf_counter()
+        with self._busy_lock:
+            self.busy += 1
         self.done_q.put((waitable, out, place, (t0, t1, t2, t3)))
 
     def _submit_steps(self, batch):
@@ -570,6 +580,8 @@ class BoxScheduler:
             ev.synchronize()
             if _TIMING:
                 self.timing.append((*ts, time.perf_counter()))
+            with self._busy_lock:
+                self.busy -= 1
             self.slots_free.release()
             place(out)
 
@@ -658,6 +670,7 @@ class BoxFrontEnd(ServerNode):
             raise InputError("the box front end loads weights per GPU: give a seed or a checkpoint path")
         super().__init__(config)
         self.world, self.dist, self._state = world, dist, state
+        self.step_timing: list = []  # PB_SERVER_TIMING: (decode, ring, encode) seconds per STEP
 
     def _pick_range(self):
         r = super()._pick_range()
@@ -679,15 +692,21 @@ class BoxFrontEnd(ServerNode):
     def _run_step(self, seq, msg, encoding: int) -> bytes:
         import torch
 
+        t0 = time.perf_counter()
         st = self._io_stream()
         with torch.cuda.stream(st):
             x = msg.decode()
         st.synchronize()
+        t1 = time.perf_counter()
         out = self.sched.run(seq, x)
+        t2 = time.perf_counter()
         try:
-            return self._encode(out, encoding)
+            reply = self._encode(out, encoding)
         except InputError as e:
             raise _NonFinite(str(e)) from e  # computed, then failed encoding (position advances)
+        if _TIMING:
+            self.step_timing.append((t1 - t0, t2 - t1, time.perf_counter() - t2))
+        return reply
 
     def _shutdown(self):
         super()._shutdown()
