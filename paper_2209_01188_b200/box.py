@@ -39,9 +39,14 @@ import itertools
 import logging
 import os
 import queue
+import struct
 import threading
 import time
 from dataclasses import dataclass
+
+import numpy as np
+
+from . import codec
 
 from .errors import CapacityError, InputError
 from .pipeline import DevPtr, P2PRing, dev_view, split_blocks
@@ -198,6 +203,28 @@ class RankState:
             ev.record(stream)
         return ev, out
 
+    def egress_codes(self, j: int, n_tok: int, stream):
+        """Rank 0, int8 ring: on `stream`, wait for job j's result in our mailbox
+        and copy its wire codes + block scales (the last sub-span's own
+        quantization of its f32 output, i.e. exactly the int8 reply) to one
+        pinned buffer [scales f32 | codes]. Returns (event, buffer)."""
+        import torch
+
+        from . import _lib
+
+        d, n = self.d, n_tok * self.d
+        nb = -(-n // 64)
+        with torch.cuda.stream(stream):
+            self.ring.wait(j, _lib.stream_ptr(stream))
+            slot = dev_view(self.ring.local_slot(j), payload_bytes(n_tok, d, self.plan.fmt), self.span.device)
+            off = -(-n // 16) * 16
+            buf = torch.empty(4 * nb + n, dtype=torch.uint8, pin_memory=True)
+            buf[:4 * nb].copy_(slot[off:off + 4 * nb], non_blocking=True)
+            buf[4 * nb:].copy_(slot[:n], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        return ev, buf
+
     def apply(self, desc, x=None):
         op = int(desc[0])
         if op == OP_STEP:
@@ -319,10 +346,11 @@ class _Fwd:
 
 
 class _BoxJob:
-    __slots__ = ("seq", "x", "out", "err", "done")
+    __slots__ = ("seq", "x", "msg", "enc", "t", "out", "err", "done")
 
-    def __init__(self, seq, x):
-        self.seq, self.x = seq, x
+    def __init__(self, seq, x=None, msg=None, enc=None):
+        self.seq, self.x, self.msg, self.enc = seq, x, msg, enc
+        self.t = int(x.shape[0]) if x is not None else msg.rows
         self.out = self.err = None
         self.done = threading.Event()
 
@@ -378,6 +406,27 @@ class BoxScheduler:
             raise job.err
         return job.out
 
+    def run_msg(self, seq, msg, encoding: int) -> bytes:
+        """One session's STEP as wire bytes in and out (t <= max_tokens): the
+        scheduler decodes the batch on rank 0's stream, and with an int8 ring
+        and an int8 reply the reply is the last sub-span's own codes, copied
+        once per job from the mailbox (no decode / re-encode on the handler)."""
+        job = _BoxJob(seq, msg=msg, enc=encoding)
+        self.q.put(("step", job))
+        job.done.wait()
+        if job.err is not None:
+            raise job.err
+        if job.enc is None:  # f32 result (the ring or the reply is not int8): encoded by the caller
+            return job.out
+        buf, host, sbytes, r0, t = job.out
+        d = self.span.config.hidden
+        s0, nb = r0 * d // 64, -(-t * d // 64)
+        sc = host[4 * s0:4 * (s0 + nb)]
+        if not np.isfinite(sc.view(np.float32)).all():
+            raise _NonFinite("non-finite tensor")
+        codes = host[sbytes + r0 * d:sbytes + (r0 + t) * d]
+        return codec.encode_header(codec.ENC_INT8, (t, d)) + struct.pack(">I", 64) + sc.tobytes() + codes.tobytes()
+
     def call(self, kind, *args):
         """Run a control operation (release / forward / backward / drop) in order."""
         ev = _Fwd(None, None, 0)
@@ -432,17 +481,19 @@ class BoxScheduler:
                 self.done_q.put(None)
                 return
             if kind == "step":
-                batch, ntok = [item[1]], item[1].x.shape[0]
+                batch, ntok = [item[1]], item[1].t
+                key = (item[1].msg is None, item[1].enc)
                 while len(batch) < self.max_seqs and ntok < self.max_tokens:
                     try:
                         nxt = self.q.get_nowait()
                     except queue.Empty:
                         break
-                    if nxt[0] != "step" or ntok + nxt[1].x.shape[0] > self.max_tokens:
+                    if (nxt[0] != "step" or ntok + nxt[1].t > self.max_tokens
+                            or (nxt[1].msg is None, nxt[1].enc) != key):
                         pending = nxt
                         break
                     batch.append(nxt[1])
-                    ntok += nxt[1].x.shape[0]
+                    ntok += nxt[1].t
                 # spread concurrent sessions over the idle pipeline stages instead of coalescing
                 # them into one job that would leave the other stages idle (measured: 2 sessions on
                 # a 2-GPU box arrive together and ran as one 2-token job per period)
@@ -479,15 +530,17 @@ class BoxScheduler:
                 ev.err = e
             ev.done.set()
 
-    def _launch(self, desc, x, n_tok, place):
+    def _launch(self, desc, x, n_tok, place, codes=False):
         """Send job desc, launch rank 0's part and the egress; `place(out)`
-        runs on the completion thread once the ring closed."""
+        runs on the completion thread once the ring closed (codes: the int8
+        result copied out as wire codes + scales, RankState.egress_codes)."""
         t0 = time.perf_counter()
         self._send(desc)
         t1 = time.perf_counter()
         self.state.apply(desc, x)
         t2 = time.perf_counter()
-        waitable, out = self.state.egress(int(desc[1]), n_tok, self.egress)
+        egress = self.state.egress_codes if codes else self.state.egress
+        waitable, out = egress(int(desc[1]), n_tok, self.egress)
         t3 = time.perf_counter()
         with self._busy_lock:
             self.busy += 1
@@ -499,9 +552,9 @@ class BoxScheduler:
         ready = []
         for job in batch:
             try:
-                if job.x.shape[0] > self.max_tokens:
+                if job.t > self.max_tokens:
                     raise InputError("internal: oversized job reached the box scheduler")
-                self.span.reserve(job.seq, job.seq.length + job.x.shape[0])
+                self.span.reserve(job.seq, job.seq.length + job.t)
                 ready.append(job)
             except (CapacityError, InputError) as e:
                 job.err = e
@@ -514,18 +567,33 @@ class BoxScheduler:
             desc = self._desc(OP_STEP, job=j, n=len(ready), fmt=self.plan.fmt)
             for i, job in enumerate(ready):
                 desc[HEAD + 2 * i] = job.seq.slot
-                desc[HEAD + 2 * i + 1] = job.x.shape[0]
+                desc[HEAD + 2 * i + 1] = job.t
                 self.state.seqs[job.seq.slot] = job.seq
-            x = ready[0].x if len(ready) == 1 else torch.cat([jb.x for jb in ready])
+            d = self.span.config.hidden
+            # wire inputs are decoded here, on rank 0's stream, in order with the hop
+            xs = [jb.x if jb.x is not None else jb.msg.decode().reshape(jb.t, d) for jb in ready]
+            x = xs[0] if len(xs) == 1 else torch.cat(xs)
             x = x.to(device=self.span.device, dtype=torch.float32).contiguous()
-            lens = [jb.x.shape[0] for jb in ready]
+            lens = [jb.t for jb in ready]
+            codes = (self.plan.fmt == FMT_INT8 and d % 64 == 0
+                     and all(jb.msg is not None and jb.enc == codec.ENC_INT8 for jb in ready))
 
-            def place(out, ready=ready, lens=lens):
+            def place(out, ready=ready, lens=lens, codes=codes, d=d):
+                if codes:
+                    host = out.numpy()
+                    sbytes = 4 * -(-sum(lens) * d // 64)
+                    r0 = 0
+                    for jb, t in zip(ready, lens):
+                        jb.out = (out, host, sbytes, r0, t)
+                        r0 += t
+                        jb.done.set()
+                    return
                 for jb, o in zip(ready, torch.split(out, lens)):
                     jb.out = o
+                    jb.enc = None  # an f32 result: the handler encodes it
                     jb.done.set()
 
-            self._launch(desc, x, x.shape[0], place)
+            self._launch(desc, x, x.shape[0], place, codes=codes)
             self.batches += 1
             self.batched_steps += len(ready)
         except Exception as e:  # noqa: BLE001
@@ -693,12 +761,22 @@ class BoxFrontEnd(ServerNode):
         import torch
 
         t0 = time.perf_counter()
-        st = self._io_stream()
-        with torch.cuda.stream(st):
-            x = msg.decode()
-        st.synchronize()
-        t1 = time.perf_counter()
-        out = self.sched.run(seq, x)
+        t1 = t0
+        out = None
+        if msg.rows <= self.sched.max_tokens:
+            res = self.sched.run_msg(seq, msg, encoding)
+            if isinstance(res, bytes):
+                if _TIMING:
+                    self.step_timing.append((0.0, time.perf_counter() - t0, 0.0))
+                return res
+            out = res
+        else:
+            st = self._io_stream()
+            with torch.cuda.stream(st):
+                x = msg.decode()
+            st.synchronize()
+            t1 = time.perf_counter()
+            out = self.sched.run(seq, x)
         t2 = time.perf_counter()
         try:
             reply = self._encode(out, encoding)
