@@ -143,7 +143,9 @@ int pb_span_step_tape(pb_span* span, int32_t n_tok, int32_t n_seq, const int32_t
 /* BACKWARD of one FORWARD row (server.py:431-450 -> model.py:383-418 block_backward over the hosted
  * blocks in reverse): d_grad_in[t][hidden] = dL/d(span input) given d_grad_out[t][hidden], the row's
  * tape d_tape[n_blocks][t][hidden] (positions 0 .. t-1, empty cache). Intermediates are recomputed
- * from the tape in f32 with the span's own weights (int8 spans: dequantized codes + f32 outliers). */
+ * from the tape with the span's own weights (int8 spans: the tcgen05 GEMM on the codes in both
+ * directions, f32 outlier features; f32 spans: f32 matmuls). The first call of a row length grows a
+ * span-owned workspace arena (kept until pb_span_destroy). */
 int pb_span_backward(pb_span* span, const float* d_tape, int32_t t, const float* d_grad_out, float* d_grad_in,
                      void* stream);
 
