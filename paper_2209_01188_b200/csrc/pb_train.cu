@@ -16,7 +16,6 @@
 // probability and score-gradient planes.
 #include <algorithm>
 #include <cmath>
-#include <cstdio>
 
 #include "pb_async.cuh"
 #include "pb_common.cuh"
@@ -126,9 +125,6 @@ int mm_fwd_tc(const Mat& m, const float* bias, int mode, const float* x, const f
     if (int rc = launch_prologue(mode, ProSrc{}, x, t, m.K, m.Kp, gamma, beta, m, 0, nullptr, w.back, w.stats, w.xo,
                                  nullptr, st, w.bcanon, TC_TOKENS))
         return rc;
-#ifdef PB_BWD_TRACE
-    { cudaError_t e0 = cudaStreamSynchronize(st); fprintf(stderr, "fwd prologue %s M %d K %d Mp %d Kp %d outl %d t %d\n", cudaGetErrorString(e0), m.M, m.K, m.Mp, m.Kp, m.n_outl, t); }
-#endif
     Epi e{};
     e.kind = EPI_PLAIN;
     e.M = m.M;
@@ -147,15 +143,9 @@ int mm_bwd_tc(const Mat& m, const float* g, int t, float* dx, const TcWs& w, cud
     k_transpose_codes<<<dim3((unsigned)(m.Mp / 128), (unsigned)(mt.Mp / 128)), 256, 0, st>>>(m.codes, m.Kp / 32,
                                                                                              w.tcodes, mt.Kp / 32);
     if (int rc = launch_check("transpose_codes")) return rc;
-#ifdef PB_BWD_TRACE
-    { cudaError_t e0 = cudaStreamSynchronize(st); fprintf(stderr, "transpose %s\n", cudaGetErrorString(e0)); }
-#endif
     if (int rc = launch_prologue(PRO_SCALE, ProSrc{}, g, t, mt.K, mt.Kp, nullptr, nullptr, mt, 0, nullptr, w.back,
                                  w.stats, nullptr, nullptr, st, w.bcanon, TC_TOKENS))
         return rc;
-#ifdef PB_BWD_TRACE
-    { cudaError_t e0 = cudaStreamSynchronize(st); fprintf(stderr, "prologue %s M %d K %d Mp %d Kp %d\n", cudaGetErrorString(e0), mt.M, mt.K, mt.Mp, mt.Kp); }
-#endif
     Epi e{};
     e.kind = EPI_BWD;
     e.M = mt.M;
@@ -541,18 +531,12 @@ static int block_backward(pb_span* s, int j, const float* x, const float* g, flo
     auto fwd = [&](int i, int mode, const float* xin, const float* h, const float* gam, const float* bet,
                    float* y) -> int {
         const Mat& m = b.mat[i];
-#ifdef PB_BWD_TRACE
-        { cudaError_t e0 = cudaStreamSynchronize(st); fprintf(stderr, "fwd %d pre %s\n", i, cudaGetErrorString(e0)); }
-#endif
         if (m.int8) return mm_fwd_tc(m, b.bias[i], mode, xin, gam, bet, t, y, tw, st);
         return gemm(false, h, m.w32, b.bias[i], y, t, m.M, m.K, st);
     };
     // dx = g W_i^T
     auto bwd = [&](int i, const float* gin, float* out) -> int {
         const Mat& m = b.mat[i];
-#ifdef PB_BWD_TRACE
-        { cudaError_t e0 = cudaStreamSynchronize(st); fprintf(stderr, "bwd %d pre %s\n", i, cudaGetErrorString(e0)); }
-#endif
         if (m.int8) return mm_bwd_tc(m, gin, t, out, tw, st);
         return gemm(true, gin, m.w32, nullptr, out, t, m.K, m.M, st);
     };
