@@ -223,8 +223,9 @@ class StepScheduler:
 
     # ---------------------------------------------------------------- batch execution
 
-    def _execute(self, ready) -> None:
-        """One batch on the current stream: decode, step, encode, one D2H copy."""
+    def _execute(self, ready):
+        """One batch on the current stream: decode, step, encode, one D2H copy.
+        Returns the batch's completion event (its jobs get their reply slices)."""
         import torch
 
         span, d = self.span, self.span.config.hidden
