@@ -100,18 +100,20 @@ def test_backward_zero_grad_is_zero():
     span.close()
 
 
-@pytest.mark.parametrize("t", [48, 161])
-def test_bloom7b1_block_backward_vs_f64_autograd(t):
-    """One 7B1-shape block (h=4096, H=32), a 48-token row (one tcgen05
-    token tile) and a 161-token row (three, the last one padded): the span's
-    BACKWARD vs float64 torch autograd of the same dequantized block."""
+@pytest.mark.parametrize("shape_name,t", [("bloom-7b1", 48), ("bloom-7b1", 161), ("bloom-176b", 100)])
+def test_block_backward_vs_f64_autograd(shape_name, t):
+    """One block of the 7B1 shape (h=4096, H=32) at a 48-token row (one
+    tcgen05 token tile) and a 161-token row (three, the last one padded), and
+    of the 176B shape (h=14336, H=112) at 100 tokens: the span's BACKWARD
+    (int8 matmuls on tcgen05 in both directions, attention on 3xTF32) vs
+    float64 torch autograd of the same dequantized block."""
     import torch
 
     from paper_2209_01188_b200.model import SHAPES as S
     from paper_2209_01188_b200.span import BlockSpan
     from torch_ref import RefBlock
 
-    cfg = S["bloom-7b1"]
+    cfg = S[shape_name]
     span = BlockSpan(cfg, 0, 1, int8=True, page_tokens=64, max_tokens=64, n_pages=4)
     span.generate_weights(42)
     ref = RefBlock(span, 0)
@@ -126,4 +128,43 @@ def test_bloom7b1_block_backward_vs_f64_autograd(t):
     want = xd.grad
     err = float((got - want).abs().max() / want.abs().max())
     assert err <= TOL, err
+    del ref, y, xd
+    span.close()
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("t", [9, 100])
+def test_int8_backward_with_outlier_features_matches_oracle(t):
+    """BACKWARD through int8 matrices with f32 outlier features (3 input rows
+    of every matrix scaled x200, kept exact: their gradient rows come from
+    k_outl_bwd, the rest from the transposed-code tcgen05 GEMM) vs the
+    oracle's block_backward on the dequantized blocks (codes x scales + the
+    exact outlier rows), from the span's own FORWARD tape (the blocks'
+    inputs: with x200 outliers the fp16 KV cache of FORWARD moves them ~2 %
+    from an f32 forward, which is not what is tested here). 9-token rows
+    (one token tile) and 100-token rows (two)."""
+    import torch
+
+    from paper_2209_01188_b200.model import ModelConfig
+    from paper_2209_01188_b200.span import BlockSpan
+
+    shape = O.Shape(2, 256, 4, 512, 256)
+    rng = np.random.default_rng(9)
+    blocks = [O.make_block(42, shape, i) for i in range(2)]
+    for b in blocks:
+        for w in (b.wqkv, b.wo, b.wmlp_in, b.wmlp_out):
+            w[rng.choice(w.shape[0], 3, replace=False), :] *= np.float32(200.0)
+    span = BlockSpan(ModelConfig(2, 256, 4, 512, 256), 0, 2, int8=True, page_tokens=16, max_tokens=256)
+    span.load_weights(blocks)
+    assert all(len(span.outliers(j, m)) == 3 for j in range(2) for m in range(4))
+    deq = [O.dequantized_block(b) for b in blocks]
+    x = (rng.normal(size=(1, t, 256)) * 0.5).astype(np.float32)
+    gr = rng.uniform(-1, 1, (1, t, 256)).astype(np.float32)
+    _, tape = span.forward(torch.from_numpy(x).cuda(), tape=True)
+    gin = span.backward(tape, torch.from_numpy(gr).cuda())[0].cpu().numpy()
+    xs = tape[0].cpu().numpy()
+    want = gr[0]
+    for j in reversed(range(2)):
+        want = O.block_backward(deq[j], xs[j], want, shape)
+    assert rel_err(gin, want) <= TOL, rel_err(gin, want)
     span.close()
