@@ -84,6 +84,7 @@ void free_span(pb_span* s) {
     for (auto& b : s->blocks) {
         for (auto& m : b.mat) {
             cudaFree(m.codes);
+            cudaFree(m.tcodes);
             cudaFree(m.scales);
             cudaFree(m.w32);
             m.free_outliers();

@@ -14,6 +14,7 @@ struct Mat {
     int M = 0, K = 0, Mp = 0, Kp = 0;  // padded: Mp % 128 == 0, Kp % 32 == 0
     bool int8 = true;
     int8_t* codes = nullptr;   // [Mp/128][Kp/32] 4 KB canonical K-major tiles (pb_weights.cu; int8 mode)
+    int8_t* tcodes = nullptr;  // BACKWARD: the same codes as tiles of W^T, cached when HBM allows (pb_train.cu)
     float* scales = nullptr;   // [Kp] per input feature, 0 on outliers / padding
     float* w32 = nullptr;      // [K][M] reference layout (f32 mode)
     int n_outl = 0;

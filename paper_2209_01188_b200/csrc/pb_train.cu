@@ -104,7 +104,8 @@ struct TcWs {
     float4* stats = nullptr;    // [t]
     float* xo = nullptr;        // [t][max n_outl]
     float* ones = nullptr;      // [max Kp of W^T] operand scales of the gradient
-    int8_t* tcodes = nullptr;   // W^T tiles of the matrix being back-propagated
+    int8_t* tcodes = nullptr;   // W^T tiles of the matrix being back-propagated (when not cached)
+    bool cache = false;         // keep W^T tiles per matrix (Mat::tcodes): HBM has room for all of them
 };
 
 // transposed view of m: rows k (padded to 128), contraction over o (padded to 32)
@@ -138,11 +139,19 @@ int mm_fwd_tc(const Mat& m, const float* bias, int mode, const float* x, const f
 }
 
 // dx [t][K] = g [t][M] W^T
-int mm_bwd_tc(const Mat& m, const float* g, int t, float* dx, const TcWs& w, cudaStream_t st) {
-    const Mat mt = transposed(m, w);
-    k_transpose_codes<<<dim3((unsigned)(m.Mp / 128), (unsigned)(mt.Mp / 128)), 256, 0, st>>>(m.codes, m.Kp / 32,
-                                                                                             w.tcodes, mt.Kp / 32);
-    if (int rc = launch_check("transpose_codes")) return rc;
+int mm_bwd_tc(Mat& m, const float* g, int t, float* dx, const TcWs& w, cudaStream_t st) {
+    Mat mt = transposed(m, w);
+    if (!m.tcodes) {
+        int8_t* dst = w.tcodes;
+        if (w.cache) {  // weights never change after loading: transpose once, keep it
+            PB_CHECK_CUDA(cudaMalloc(&m.tcodes, (size_t)mt.Mp * mt.Kp));
+            dst = m.tcodes;
+        }
+        k_transpose_codes<<<dim3((unsigned)(m.Mp / 128), (unsigned)(mt.Mp / 128)), 256, 0, st>>>(
+            m.codes, m.Kp / 32, dst, mt.Kp / 32);
+        if (int rc = launch_check("transpose_codes")) return rc;
+    }
+    if (m.tcodes) mt.codes = m.tcodes;
     if (int rc = launch_prologue(PRO_SCALE, ProSrc{}, g, t, mt.K, mt.Kp, nullptr, nullptr, mt, 0, nullptr, w.back,
                                  w.stats, nullptr, nullptr, st, w.bcanon, TC_TOKENS))
         return rc;
@@ -536,7 +545,7 @@ static int block_backward(pb_span* s, int j, const float* x, const float* g, flo
     };
     // dx = g W_i^T
     auto bwd = [&](int i, const float* gin, float* out) -> int {
-        const Mat& m = b.mat[i];
+        Mat& m = b.mat[i];
         if (m.int8) return mm_bwd_tc(m, gin, t, out, tw, st);
         return gemm(true, gin, m.w32, nullptr, out, t, m.K, m.M, st);
     };
@@ -585,6 +594,18 @@ extern "C" int pb_span_backward(pb_span* span, const float* d_tape, int32_t t, c
                 tcode_max = std::max<int64_t>(tcode_max, round_up(m.K, 128) * round_up(m.M, 32));
                 n_outl = std::max<int64_t>(n_outl, m.n_outl);
             }
+    // W^T tiles: cached per matrix when HBM holds all of them with room to spare (multi-GPU spans),
+    // else transposed per call into the arena (0.27 ms per 176B mlp matrix)
+    int64_t tcache = 0;
+    for (const auto& b : span->blocks)
+        for (const auto& m : b.mat)
+            if (m.int8 && !m.tcodes) tcache += round_up(m.K, 128) * round_up(m.M, 32);
+    bool cache = false;
+    if (tcache) {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
+            cache = (int64_t)free_b > tcache + ((int64_t)16 << 30);
+    }
     // carve-up of the span's grow-only arena (256-byte aligned pieces)
     int64_t off = 0;
     auto piece = [&](int64_t bytes) {
@@ -622,6 +643,7 @@ extern "C" int pb_span_backward(pb_span* span, const float* d_tape, int32_t t, c
         tw.xo = reinterpret_cast<float*>(base + o_xo);
         tw.ones = reinterpret_cast<float*>(base + o_ones);
         tw.tcodes = reinterpret_cast<int8_t*>(base + o_tc);
+        tw.cache = cache;
         k_fill<<<grid_for(kp_max), 256, 0, st>>>(tw.ones, kp_max, 1.f);
     }
     PB_CHECK_CUDA(cudaMemcpyAsync(g, d_grad_out, sizeof(float) * td, cudaMemcpyDeviceToDevice, st));

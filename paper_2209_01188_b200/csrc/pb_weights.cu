@@ -164,6 +164,11 @@ static int grid_n(int64_t n, int threads = 256) {
 
 template <class Src>
 static int quantize_matrix(Mat& m, Src src, float threshold, cudaStream_t st, const float* wt = nullptr) {
+    if (m.tcodes) {  // new codes: the BACKWARD cache of their transpose is stale
+        PB_CHECK_CUDA(cudaStreamSynchronize(st));
+        cudaFree(m.tcodes);
+        m.tcodes = nullptr;
+    }
     const int64_t K = m.K, M = m.M, KC = m.Kp / 32, MG = m.Mp / 128;
     uint8_t* d_flags = nullptr;
     PB_CHECK_CUDA(cudaMallocAsync(&d_flags, K, st));
