@@ -479,19 +479,25 @@ __device__ __forceinline__ void sk_operand_warp(const SkArgs& a, int64_t u0, int
     const ProArgs& p = a.pro;
     const int lane = threadIdx.x & 31;
     float4 st[TC];
+    bool have_st = false;
+    // the token statistics are resolved after this warp's first stage inputs are requested, so the
+    // two chains of dependent loads (summaries -> statistics; activations) overlap
+    auto resolve = [&]() {
 #pragma unroll
-    for (int t = 0; t < TC; ++t) {
-        const int tok = chunk * TC + t;
-        st[t] = tok < a.act.n_tok ? resolve_stats(p, tok) : make_float4(0.f, 1.f, 0.f, 0.f);  // warp-uniform
-        if (tok < a.act.n_tok && ow == 0) {
-            if (lane == 0) p.back[tok] = st[t].w * (1.f / 256.f);
-            if (p.xo) {
-                const float* x = p.x + (int64_t)tok * p.K;
-                for (int j = lane; j < p.n_outl; j += 32)
-                    p.xo[(int64_t)tok * p.n_outl + j] = pro_y(p, x, p.outl_idx[j], st[t].x, st[t].y);
+        for (int t = 0; t < TC; ++t) {
+            const int tok = chunk * TC + t;
+            st[t] = tok < a.act.n_tok ? resolve_stats(p, tok) : make_float4(0.f, 1.f, 0.f, 0.f);  // warp-uniform
+            if (tok < a.act.n_tok && ow == 0) {
+                if (lane == 0) p.back[tok] = st[t].w * (1.f / 256.f);
+                if (p.xo) {
+                    const float* x = p.x + (int64_t)tok * p.K;
+                    for (int j = lane; j < p.n_outl; j += 32)
+                        p.xo[(int64_t)tok * p.n_outl + j] = pro_y(p, x, p.outl_idx[j], st[t].x, st[t].y);
+                }
             }
         }
-    }
+        have_st = true;
+    };
     if (a.zero_a && blockIdx.x == 0 && ow == 0 && lane < TC && chunk * TC + lane < a.act.n_tok) {
         a.zero_a[chunk * TC + lane] = 0.f;
         a.zero_b[chunk * TC + lane] = 0.f;
@@ -530,6 +536,7 @@ __device__ __forceinline__ void sk_operand_warp(const SkArgs& a, int64_t u0, int
                                                        : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
+            if (!have_st) resolve();
             mbar_wait(&empty[stage], phase ^ 1);
             uint32_t* B = reinterpret_cast<uint32_t*>(sb + stage * B_STAGE);
 #pragma unroll
@@ -572,6 +579,7 @@ __device__ __forceinline__ void sk_operand_warp(const SkArgs& a, int64_t u0, int
         }
         u += kb - ka;
     }
+    if (!have_st) resolve();  // a warp without stages still writes the side outputs (ow == 0)
 }
 
 template <int TC, int SK_KCS, int SK_STAGES, bool FUSED = false>
