@@ -217,13 +217,15 @@ __global__ void __launch_bounds__(256) k_fragwrite(ProArgs a) {
     if (!a.early) pdl_trigger();
     if (threadIdx.x == 0) trace_stamp(a.trace, tcta, 1);
     const int tok = blockIdx.y;
+    float xv[8];  // activations first: their loads overlap the statistics' loads
+    if (it < KC * 4) frag_x(a, tok, it >> 2, it & 3, xv);
     // every warp resolves the statistics itself (warp-uniform code, no CTA
     // barrier; a lane-divergent region made the shuffles take the compiler's
     // non-converged path: ncu showed WARPSYNC.COLLECTIVE, ~5 us per resolve)
     const float4 st = resolve_stats(a, tok);
     if (threadIdx.x == 0) trace_stamp(a.trace, tcta, 5);
     if (blockIdx.x == 0) operand_token_outputs(a, tok, st, threadIdx.x, blockDim.x);
-    if (it < KC * 4) frag_item(a, tok, it >> 2, it & 3, st, fp);
+    if (it < KC * 4) frag_item(a, tok, it >> 2, it & 3, st, fp, xv);
     if (threadIdx.x == 0) trace_stamp(a.trace, tcta, 6);
     if (a.trace) {
         __syncthreads();
@@ -243,6 +245,18 @@ __global__ void __launch_bounds__(256) k_canonwrite(ProArgs a, uint8_t* __restri
     const int tok = blockIdx.y;
     const float* x = a.x + (int64_t)tok * a.K;
     const bool real = tok < n_tok;
+    const int KC = a.Kp / 32;
+    const int it = blockIdx.x * blockDim.x + threadIdx.x;
+    // this thread's 16 activations and scales first: their loads overlap the statistics' resolve
+    float xv[16], sv[16];
+    const bool mine = real && it < KC * 2;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int k = (it >> 1) * 32 + (it & 1) * 16 + i;
+        const bool in = mine && k < a.K;
+        xv[i] = in ? x[k] : 0.f;
+        sv[i] = in ? a.scales[k] : 0.f;
+    }
     if (real && threadIdx.x < 32) {
         const float4 r = resolve_stats(a, tok);
         if (threadIdx.x == 0) {
@@ -254,8 +268,6 @@ __global__ void __launch_bounds__(256) k_canonwrite(ProArgs a, uint8_t* __restri
         }
     }
     __syncthreads();
-    const int KC = a.Kp / 32;
-    const int it = blockIdx.x * blockDim.x + threadIdx.x;
     if (real && blockIdx.x == 0 && a.xo) {
         for (int j = threadIdx.x; j < a.n_outl; j += blockDim.x)
             a.xo[(int64_t)tok * a.n_outl + j] = pro_y(a, x, a.outl_idx[j], s_st.x, s_st.y);
@@ -266,10 +278,12 @@ __global__ void __launch_bounds__(256) k_canonwrite(ProArgs a, uint8_t* __restri
     if (real) {
         const float4 st = s_st;
         const float z = st.z * 256.f;
+        const bool ln = a.mode == PRO_LN;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
             const int k = kc * 32 + kh * 16 + i;
-            const float v = k < a.K ? (pro_y(a, x, k, st.x, st.y) * a.scales[k]) * z : 0.f;
+            const float y = ln ? fmaf(a.gamma[k < a.K ? k : 0], (xv[i] - st.x) * st.y, a.beta[k < a.K ? k : 0]) : xv[i];
+            const float v = k < a.K ? (y * sv[i]) * z : 0.f;  // pro_y (model.py:271-276) on the preloaded x
             int h, m, l;
             digits3(__float2int_rn(v), h, m, l);
             w[0][i >> 2] |= (uint32_t)(uint8_t)h << (8 * (i & 3));

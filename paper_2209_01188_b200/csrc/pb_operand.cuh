@@ -151,9 +151,17 @@ __device__ __forceinline__ void frag_params(const ProArgs& a, int kc, int q, Fra
 // (layout in the header comment): token tok, 32-wide k tile kc, lane quad q.
 // The statistics' shift maps max |y s| into [2^13, 2^14) (the fp16 split of the
 // tcgen05 path); 2^8 more gives the 22-bit integer range here.
-__device__ __forceinline__ void frag_item(const ProArgs& a, int tok, int kc, int q, const float4 st,
-                                          const FragParams& p) {
+// the item's 8 activations (requested before the statistics are resolved: independent loads)
+__device__ __forceinline__ void frag_x(const ProArgs& a, int tok, int kc, int q, float (&xv)[8]) {
     const float* x = a.x + (int64_t)tok * a.K;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int k = kc * 32 + 16 * (e >> 2) + 4 * q + (e & 3);
+        xv[e] = k < a.K ? x[k] : 0.f;
+    }
+}
+__device__ __forceinline__ void frag_item(const ProArgs& a, int tok, int kc, int q, const float4 st,
+                                          const FragParams& p, const float (&xv)[8]) {
     const float z = st.z * 256.f;
     const int KC = a.Kp / 32;
     const int NT = digit_ntiles(a.tc);
@@ -163,7 +171,7 @@ __device__ __forceinline__ void frag_item(const ProArgs& a, int tok, int kc, int
     for (int e = 0; e < 8; ++e) {
         const int k = kc * 32 + 16 * (e >> 2) + 4 * q + (e & 3);
         float y = 0.f;
-        if (k < a.K) y = a.mode == PRO_LN ? fmaf(p.g[e], (x[k] - st.x) * st.y, p.b[e]) : x[k];  // model.py:271-276
+        if (k < a.K) y = a.mode == PRO_LN ? fmaf(p.g[e], (xv[e] - st.x) * st.y, p.b[e]) : xv[e];  // model.py:271-276
         int h, m, l;
         digits3(__float2int_rn((y * p.s[e]) * z), h, m, l);
         w[0][e >> 2] |= (uint32_t)(uint8_t)h << (8 * (e & 3));
