@@ -389,6 +389,7 @@ struct SkArgs {
     Epi epi;
     float* partials;  // [chunk][G][2][128 * 2tc]
     int* counters;    // [chunk][MG]
+    int* sums;        // [chunk][MG][128 * COLS] s32 split-row-group sums, kept zero (null: partial slots)
     uint64_t* trace;  // diagnostics (pb_trace_set), usually null
     // fused operand (k_gemv_i8<.., FUSED>): an operand warp builds the B fragments of
     // every stage in shared memory from the activations (no k_fragwrite launch)
@@ -772,7 +773,44 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
         // ---- segment finished: complete group or a piece of a split group
         const int64_t g0 = (int64_t)mg * a.KC, g1 = g0 + a.KC;
         const int c_first = sk_owner(g0, a.G, a.total), c_last = sk_owner(g1 - 1, a.G, a.total);
-        if (c_first != c_last) {
+        if (c_first != c_last && a.sums) {
+            // split row group: this CTA's s32 sums are added into the row group's accumulator
+            // (reductions at L2, exact integers: arrival order is irrelevant); the contributor that
+            // completes the count reads the total once -- instead of every contributor's partial --
+            // and zeroes it for the next launch
+            int* sums = a.sums + ((int64_t)chunk * a.MG + mg) * PER;
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        atomicAdd(sums + (((cw * 2 + i) * NT + j) * 32 + lane) * 4 + r, acc[i][j][r]);
+            __threadfence();
+            cons_sync();
+            if (threadIdx.x == 32) {
+                int* ctr = a.counters + (int64_t)chunk * a.MG + mg;
+                const int prev = atomicAdd(ctr, 1);
+                const int last = prev == c_last - c_first;
+                if (last) *ctr = 0;
+                *s_flag = last;
+            }
+            cons_sync();
+            if (!*s_flag) continue;
+            __threadfence();
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    int4* q = reinterpret_cast<int4*>(sums + (((cw * 2 + i) * NT + j) * 32 + lane) * 4);
+                    const int4 v = __ldcg(q);
+                    acc[i][j][0] = v.x;
+                    acc[i][j][1] = v.y;
+                    acc[i][j][2] = v.z;
+                    acc[i][j][3] = v.w;
+                    __stcg(q, make_int4(0, 0, 0, 0));
+                }
+        } else if (c_first != c_last) {
             const int slot = (u0 < g0) ? 1 : 0;  // not this CTA's first segment -> slot 1
             int* mine = reinterpret_cast<int*>(a.partials) + (((int64_t)chunk * a.G + c) * 2 + slot) * PER;
 #pragma unroll
@@ -826,7 +864,7 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
 template <int TC, int SK_KCS, int SK_STAGES, bool FUSED = false>
 static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
                      int64_t partial_cap, cudaStream_t st, const ProArgs* pro = nullptr, float* zero_a = nullptr,
-                     float* zero_b = nullptr) {
+                     float* zero_b = nullptr, int* sums = nullptr, int64_t sums_elems = 0) {
     constexpr int THREADS = SK_THREADS + (FUSED ? 32 * SK_OPW : 0);
     constexpr int NT = digit_ntiles(TC);
     const size_t smem = (size_t)SK_STAGES * (SK_KCS * 4096 + SK_KCS * NT * 256) + 128 * (8 * NT + 1) * 4 + 16 +
@@ -866,6 +904,7 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
     a.epi = epi;
     a.partials = partials;
     a.counters = counters;
+    if (sums && (int64_t)chunks * a.MG * per_tile <= sums_elems) a.sums = sums;
     a.trace = trace_region(TR_GEMV, (int)G * chunks);
     if (FUSED) {
         a.pro = *pro;
@@ -895,12 +934,16 @@ int launch_gemv_fused(const Mat& m, const Act& act, const Epi& epi, const ProArg
 // (profiles/r1_gemv_timeline_and_tail.txt, profiles/r1_small_shape_gemv_minu.txt):
 // decode 8 x 4 (32 KB stages, one CTA per SM), 3..8 tokens 8 x 2, 17..32 tokens 2 x 4.
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters, int64_t partial_cap,
-                cudaStream_t st) {
+                cudaStream_t st, int* sums, int64_t sums_elems) {
     switch (act.tc) {
-        case 2: return sk_launch<2, 8, 4>(m, act, epi, partials, counters, partial_cap, st);
-        case 8: return sk_launch<8, 8, 2>(m, act, epi, partials, counters, partial_cap, st);
-        case 16: return sk_launch<16, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
-        case 32: return sk_launch<32, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
+        case 2: return sk_launch<2, 8, 4>(m, act, epi, partials, counters, partial_cap, st, nullptr, nullptr, nullptr,
+                                          sums, sums_elems);
+        case 8: return sk_launch<8, 8, 2>(m, act, epi, partials, counters, partial_cap, st, nullptr, nullptr, nullptr,
+                                          sums, sums_elems);
+        case 16: return sk_launch<16, 2, 4>(m, act, epi, partials, counters, partial_cap, st, nullptr, nullptr,
+                                            nullptr, sums, sums_elems);
+        case 32: return sk_launch<32, 2, 4>(m, act, epi, partials, counters, partial_cap, st, nullptr, nullptr,
+                                            nullptr, sums, sums_elems);
         default: set_error("bad column tile"); return PB_ERR_GENERIC;
     }
 }

@@ -468,7 +468,7 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                 ev = prof_begin(s, st);
                 // algorithmic bytes: codes + per-feature scales + bias (+ f32 outlier rows)
                 const double bytes = (double)m.M * m.K + 4.0 * m.K + 4.0 * m.M + 4.0 * m.n_outl * m.M;
-                int rc = launch_gemv(m, a, e, s->partials, s->counters, s->partial_cap, st);
+                int rc = launch_gemv(m, a, e, s->partials, s->counters, s->partial_cap, st, s->sk_acc, s->sk_acc_elems);
                 prof_end(s, ev, 0, bytes, st);
                 return rc;
             }

@@ -149,8 +149,9 @@ struct ProArgs {
     uint64_t* trace = nullptr;  // diagnostics (pb_trace_set)
 };
 
+// sums (optional): a zeroed s32 workspace [chunks][MG][128 x 8 NT] for the split-row-group merge
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
-                int64_t partial_cap, cudaStream_t st);
+                int64_t partial_cap, cudaStream_t st, int* sums = nullptr, int64_t sums_elems = 0);
 // decode (<= 2 tokens per column chunk): the operand is built inside the GEMV
 // by an operand warp (no k_fragwrite launch); prepare_fused_operand runs the
 // block-0 row statistics if needed and returns the operand description
