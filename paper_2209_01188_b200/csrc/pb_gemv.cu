@@ -597,7 +597,7 @@ __device__ __forceinline__ void sk_operand_warp(const SkArgs& a, int64_t u0, int
     if (!have_st) resolve();  // a warp without stages still writes the side outputs (ow == 0)
 }
 
-template <int TC, int SK_KCS, int SK_STAGES, bool FUSED = false>
+template <int TC, int SK_KCS, int SK_STAGES, bool FUSED = false, bool RED = false>
 __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv_i8(SkArgs a) {
     // an operand warp reuses only its own ring slots, so it can never run two rounds
     // ahead of the consumers (mbarrier parity waits cannot tell those rounds apart)
@@ -773,7 +773,7 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
         // ---- segment finished: complete group or a piece of a split group
         const int64_t g0 = (int64_t)mg * a.KC, g1 = g0 + a.KC;
         const int c_first = sk_owner(g0, a.G, a.total), c_last = sk_owner(g1 - 1, a.G, a.total);
-        if (c_first != c_last && a.sums) {
+        if (RED && c_first != c_last) {
             // split row group: this CTA's s32 sums are added into the row group's accumulator
             // (reductions at L2, exact integers: arrival order is irrelevant); the contributor that
             // completes the count reads the total once -- instead of every contributor's partial --
@@ -861,7 +861,7 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
 }
 
 
-template <int TC, int SK_KCS, int SK_STAGES, bool FUSED = false>
+template <int TC, int SK_KCS, int SK_STAGES, bool FUSED = false, bool RED = false>
 static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters,
                      int64_t partial_cap, cudaStream_t st, const ProArgs* pro = nullptr, float* zero_a = nullptr,
                      float* zero_b = nullptr, int* sums = nullptr, int64_t sums_elems = 0) {
@@ -877,9 +877,9 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
     if (!bps_dev[dev]) {
         int sms = 0, bps = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        PB_CHECK_CUDA(cudaFuncSetAttribute(k_gemv_i8<TC, SK_KCS, SK_STAGES, FUSED>,
+        PB_CHECK_CUDA(cudaFuncSetAttribute(k_gemv_i8<TC, SK_KCS, SK_STAGES, FUSED, RED>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_gemv_i8<TC, SK_KCS, SK_STAGES, FUSED>, THREADS, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_gemv_i8<TC, SK_KCS, SK_STAGES, FUSED, RED>, THREADS, smem);
         sms_dev[dev] = sms;
         bps_dev[dev] = std::max(bps, 1);
     }
@@ -904,7 +904,13 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
     a.epi = epi;
     a.partials = partials;
     a.counters = counters;
-    if (sums && (int64_t)chunks * a.MG * per_tile <= sums_elems) a.sums = sums;
+    if (RED) {
+        if (!sums || (int64_t)chunks * a.MG * per_tile > sums_elems) {
+            set_error("gemv: split-row-group sum workspace too small");
+            return PB_ERR_CAPACITY;
+        }
+        a.sums = sums;
+    }
     a.trace = trace_region(TR_GEMV, (int)G * chunks);
     if (FUSED) {
         a.pro = *pro;
@@ -912,7 +918,7 @@ static int sk_launch(const Mat& m, const Act& act, const Epi& epi, float* partia
         a.zero_a = zero_a;
         a.zero_b = zero_b;
     }
-    return launch_pdl(k_gemv_i8<TC, SK_KCS, SK_STAGES, FUSED>, dim3((unsigned)G, chunks), dim3(THREADS), smem, st, a);
+    return launch_pdl(k_gemv_i8<TC, SK_KCS, SK_STAGES, FUSED, RED>, dim3((unsigned)G, chunks), dim3(THREADS), smem, st, a);
 }
 
 bool gemv_fusable(const Act& act, int K) {
@@ -936,14 +942,17 @@ int launch_gemv_fused(const Mat& m, const Act& act, const Epi& epi, const ProArg
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters, int64_t partial_cap,
                 cudaStream_t st, int* sums, int64_t sums_elems) {
     switch (act.tc) {
-        case 2: return sk_launch<2, 8, 4>(m, act, epi, partials, counters, partial_cap, st, nullptr, nullptr, nullptr,
-                                          sums, sums_elems);
-        case 8: return sk_launch<8, 8, 2>(m, act, epi, partials, counters, partial_cap, st, nullptr, nullptr, nullptr,
-                                          sums, sums_elems);
-        case 16: return sk_launch<16, 2, 4>(m, act, epi, partials, counters, partial_cap, st, nullptr, nullptr,
-                                            nullptr, sums, sums_elems);
-        case 32: return sk_launch<32, 2, 4>(m, act, epi, partials, counters, partial_cap, st, nullptr, nullptr,
-                                            nullptr, sums, sums_elems);
+        case 2:
+            // batch-1 decode of the large shapes: reduction merge (176B: 426.0 -> 418.4 us per block); the
+            // small-shape fused kernel keeps the partial slots (a shared runtime branch cost it more than the
+            // merge saved: 560M 34.7 -> 40.3 us per block)
+            if (sums && ceil_div(act.n_tok, act.tc) * (int64_t)(m.Mp / 128) * 128 * 8 * digit_ntiles(2) <= sums_elems)
+                return sk_launch<2, 8, 4, false, true>(m, act, epi, partials, counters, partial_cap, st, nullptr,
+                                                        nullptr, nullptr, sums, sums_elems);
+            return sk_launch<2, 8, 4>(m, act, epi, partials, counters, partial_cap, st);
+        case 8: return sk_launch<8, 8, 2>(m, act, epi, partials, counters, partial_cap, st);
+        case 16: return sk_launch<16, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
+        case 32: return sk_launch<32, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
         default: set_error("bad column tile"); return PB_ERR_GENERIC;
     }
 }
