@@ -436,12 +436,12 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                 e.outl_rows = m.outl_rows;
                 e.xo = s->xo;
                 Act a{s->frag, s->back, n_tok, tc};
-                // measured (profiles/r1_gemv_timeline_and_tail.txt): fused wins where the
-                // kernel boundaries dominate (560M -12 %, 7B1 -8 % per block) but costs ~1 %
-                // at the 176B shape in a sustained run (its operand warps' extra power lowers
-                // the capped SM clock), so the switch is by hidden size
-                constexpr int fuse_max_d = 8192;
-                if (d <= fuse_max_d && gemv_fusable(a, K)) {
+                // fused operand warps for every batch-1 decode GEMV: round 1 measured them
+                // ~1 % slower at the 176B shape (their power lowered the capped SM clock);
+                // since the operand warps overlap their statistics with the first inputs
+                // they win there too (bench: 33.4 -> 35.0 steps/s, 0.98 of the sequential
+                // roofline, at a lower 1670 MHz capped clock), besides 560M and 7B1
+                if (gemv_fusable(a, K)) {
                     // decode: the GEMV's operand warp builds the int8-digit operand itself;
                     // the QKV launch resets the two range accumulators of this block
                     // (attention -> wo, wmlp_in epilogue -> wmlp_out), whose previous
