@@ -80,6 +80,9 @@ typedef struct {
                               the IMMA GEMV; 0 = the measured default (9) */
     int32_t graphs;        /* 1: pb_span_step replays decode steps (<= 64 tokens) as CUDA graphs, one per
                               launch shape (tokens, sequences, attention work units), captured on first use */
+    int32_t operand_kernel; /* 1: batch-1 decode builds its int8-digit operands in a separate kernel
+                               (k_fragwrite) instead of the GEMV's own operand warps (the default, 0);
+                               the results are bit-identical (tests/test_gpu_fused.py) */
 } pb_span_config;
 
 int pb_span_create(const pb_span_config* cfg, pb_span** out);

@@ -33,7 +33,7 @@ class SpanConfig(C.Structure):
         ("n_blocks", C.c_int32), ("first_block", C.c_int32), ("weights", C.c_int32), ("page_tokens", C.c_int32),
         ("n_pages", C.c_int32), ("max_tokens", C.c_int32), ("max_seqs", C.c_int32),
         ("outlier_threshold", C.c_float), ("device", C.c_int32), ("tc_min_tokens", C.c_int32),
-        ("graphs", C.c_int32),
+        ("graphs", C.c_int32), ("operand_kernel", C.c_int32),
     ]
 
 

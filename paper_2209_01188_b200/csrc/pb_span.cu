@@ -441,7 +441,7 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                 // since the operand warps overlap their statistics with the first inputs
                 // they win there too (bench: 33.4 -> 35.0 steps/s, 0.98 of the sequential
                 // roofline, at a lower 1670 MHz capped clock), besides 560M and 7B1
-                if (gemv_fusable(a, K)) {
+                if (!s->cfg.operand_kernel && gemv_fusable(a, K)) {
                     // decode: the GEMV's operand warp builds the int8-digit operand itself;
                     // the QKV launch resets the two range accumulators of this block
                     // (attention -> wo, wmlp_in epilogue -> wmlp_out), whose previous

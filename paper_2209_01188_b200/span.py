@@ -55,7 +55,10 @@ class Sequence:
 class BlockSpan:
     def __init__(self, config: ModelConfig, start: int, end: int, *, int8: bool = True, page_tokens: int = 64,
                  n_pages: int | None = None, max_tokens: int = 256, max_seqs: int = 64, device: int = 0,
-                 outlier_threshold: float = 6.0, tc_min_tokens: int = 0, graphs: bool = True):
+                 outlier_threshold: float = 6.0, tc_min_tokens: int = 0, graphs: bool = True,
+                 operand_kernel: bool = False):
+        """operand_kernel: batch-1 decode builds its operands in k_fragwrite instead of the
+        GEMV's operand warps (bit-identical; the A/B of tests/test_gpu_fused.py)."""
         import torch
 
         if not (0 <= start < end <= config.n_layers):
@@ -74,6 +77,7 @@ class BlockSpan:
             n_blocks=self.n_blocks, first_block=start, weights=1 if int8 else 0, page_tokens=page_tokens,
             n_pages=n_pages, max_tokens=max_tokens, max_seqs=max_seqs, outlier_threshold=outlier_threshold,
             device=device, tc_min_tokens=tc_min_tokens, graphs=1 if graphs else 0,
+            operand_kernel=1 if operand_kernel else 0,
         )
         handle = C.c_void_p()
         torch.cuda.init()

@@ -1,7 +1,7 @@
 """The fused-operand decode GEMV (operand warps build the int8-digit B
 fragments in shared memory) must produce bit-identical hidden states to the
-k_fragwrite path, with outlier features present (tools/fused_check.py run
-with and without PB_NO_FUSED_OPERAND; the switch is read once per process)."""
+k_fragwrite path, with outlier features present, at the 560M and the 176B
+shapes (tools/fused_check.py with and without BlockSpan(operand_kernel=True))."""
 
 import os
 import subprocess
@@ -18,12 +18,8 @@ def test_fused_operand_bit_identical_to_fragwrite(tmp_path):
     outs = []
     for fused in (True, False):
         f = tmp_path / f"out_{int(fused)}.npy"
-        env = dict(os.environ)
-        env.pop("PB_NO_FUSED_OPERAND", None)
-        if not fused:
-            env["PB_NO_FUSED_OPERAND"] = "1"
-        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fused_check.py"), str(f)], cwd=ROOT, env=env,
-                           capture_output=True, text=True, timeout=300)
+        args = [sys.executable, os.path.join(ROOT, "tools", "fused_check.py"), str(f)] + ([] if fused else ["kernel"])
+        r = subprocess.run(args, cwd=ROOT, capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
         outs.append(np.load(f))
         assert "outliers per matrix" in r.stdout
