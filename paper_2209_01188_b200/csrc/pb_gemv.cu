@@ -250,12 +250,23 @@ __global__ void __launch_bounds__(256) k_canonwrite(ProArgs a, uint8_t* __restri
     // this thread's 16 activations and scales first: their loads overlap the statistics' resolve
     float xv[16], sv[16];
     const bool mine = real && it < KC * 2;
+    const int k0 = (it >> 1) * 32 + (it & 1) * 16;
+    if (mine && k0 + 16 <= a.K && (a.K & 3) == 0) {  // whole 16-feature run: 128-bit loads
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        const int k = (it >> 1) * 32 + (it & 1) * 16 + i;
-        const bool in = mine && k < a.K;
-        xv[i] = in ? x[k] : 0.f;
-        sv[i] = in ? a.scales[k] : 0.f;
+        for (int i = 0; i < 4; ++i) {
+            const float4 xq = *reinterpret_cast<const float4*>(x + k0 + 4 * i);
+            const float4 sq = *reinterpret_cast<const float4*>(a.scales + k0 + 4 * i);
+            xv[4 * i] = xq.x, xv[4 * i + 1] = xq.y, xv[4 * i + 2] = xq.z, xv[4 * i + 3] = xq.w;
+            sv[4 * i] = sq.x, sv[4 * i + 1] = sq.y, sv[4 * i + 2] = sq.z, sv[4 * i + 3] = sq.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int k = k0 + i;
+            const bool in = mine && k < a.K;
+            xv[i] = in ? x[k] : 0.f;
+            sv[i] = in ? a.scales[k] : 0.f;
+        }
     }
     if (real && threadIdx.x < 32) {
         const float4 r = resolve_stats(a, tok);
