@@ -248,16 +248,21 @@ __global__ void __launch_bounds__(256) k_canonwrite(ProArgs a, uint8_t* __restri
     const int KC = a.Kp / 32;
     const int it = blockIdx.x * blockDim.x + threadIdx.x;
     // this thread's 16 activations and scales first: their loads overlap the statistics' resolve
-    float xv[16], sv[16];
+    float xv[16], sv[16], gv[16], bv[16];
     const bool mine = real && it < KC * 2;
+    const bool ln = a.mode == PRO_LN;
     const int k0 = (it >> 1) * 32 + (it & 1) * 16;
     if (mine && k0 + 16 <= a.K && (a.K & 3) == 0) {  // whole 16-feature run: 128-bit loads
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const float4 xq = *reinterpret_cast<const float4*>(x + k0 + 4 * i);
             const float4 sq = *reinterpret_cast<const float4*>(a.scales + k0 + 4 * i);
+            const float4 gq = ln ? *reinterpret_cast<const float4*>(a.gamma + k0 + 4 * i) : make_float4(1.f, 1.f, 1.f, 1.f);
+            const float4 bq = ln ? *reinterpret_cast<const float4*>(a.beta + k0 + 4 * i) : make_float4(0.f, 0.f, 0.f, 0.f);
             xv[4 * i] = xq.x, xv[4 * i + 1] = xq.y, xv[4 * i + 2] = xq.z, xv[4 * i + 3] = xq.w;
             sv[4 * i] = sq.x, sv[4 * i + 1] = sq.y, sv[4 * i + 2] = sq.z, sv[4 * i + 3] = sq.w;
+            gv[4 * i] = gq.x, gv[4 * i + 1] = gq.y, gv[4 * i + 2] = gq.z, gv[4 * i + 3] = gq.w;
+            bv[4 * i] = bq.x, bv[4 * i + 1] = bq.y, bv[4 * i + 2] = bq.z, bv[4 * i + 3] = bq.w;
         }
     } else {
 #pragma unroll
@@ -266,6 +271,8 @@ __global__ void __launch_bounds__(256) k_canonwrite(ProArgs a, uint8_t* __restri
             const bool in = mine && k < a.K;
             xv[i] = in ? x[k] : 0.f;
             sv[i] = in ? a.scales[k] : 0.f;
+            gv[i] = in && ln ? a.gamma[k] : 1.f;
+            bv[i] = in && ln ? a.beta[k] : 0.f;
         }
     }
     if (real && threadIdx.x < 32) {
@@ -289,11 +296,10 @@ __global__ void __launch_bounds__(256) k_canonwrite(ProArgs a, uint8_t* __restri
     if (real) {
         const float4 st = s_st;
         const float z = st.z * 256.f;
-        const bool ln = a.mode == PRO_LN;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
             const int k = kc * 32 + kh * 16 + i;
-            const float y = ln ? fmaf(a.gamma[k < a.K ? k : 0], (xv[i] - st.x) * st.y, a.beta[k < a.K ? k : 0]) : xv[i];
+            const float y = ln ? fmaf(gv[i], (xv[i] - st.x) * st.y, bv[i]) : xv[i];
             const float v = k < a.K ? (y * sv[i]) * z : 0.f;  // pro_y (model.py:271-276) on the preloaded x
             int h, m, l;
             digits3(__float2int_rn(v), h, m, l);
