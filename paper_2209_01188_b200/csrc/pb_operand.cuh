@@ -154,6 +154,14 @@ __device__ __forceinline__ void frag_params(const ProArgs& a, int kc, int q, Fra
 // the item's 8 activations (requested before the statistics are resolved: independent loads)
 __device__ __forceinline__ void frag_x(const ProArgs& a, int tok, int kc, int q, float (&xv)[8]) {
     const float* x = a.x + (int64_t)tok * a.K;
+    const int k0 = kc * 32 + 4 * q;
+    if ((a.K & 3) == 0 && k0 + 20 <= a.K) {  // both 4-feature runs inside the row: two 128-bit loads
+        const float4 lo = *reinterpret_cast<const float4*>(x + k0);
+        const float4 hi = *reinterpret_cast<const float4*>(x + k0 + 16);
+        xv[0] = lo.x, xv[1] = lo.y, xv[2] = lo.z, xv[3] = lo.w;
+        xv[4] = hi.x, xv[5] = hi.y, xv[6] = hi.z, xv[7] = hi.w;
+        return;
+    }
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
         const int k = kc * 32 + 16 * (e >> 2) + 4 * q + (e & 3);
