@@ -252,7 +252,8 @@ __global__ void __launch_bounds__(256) k_canonwrite(ProArgs a, uint8_t* __restri
     const bool mine = real && it < KC * 2;
     const bool ln = a.mode == PRO_LN;
     const int k0 = (it >> 1) * 32 + (it & 1) * 16;
-    if (mine && k0 + 16 <= a.K && (a.K & 3) == 0) {  // whole 16-feature run: 128-bit loads
+    // whole 16-feature run of a 16-byte aligned row (callers pass rows at any float offset): 128-bit loads
+    if (mine && k0 + 16 <= a.K && (a.K & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const float4 xq = *reinterpret_cast<const float4*>(x + k0 + 4 * i);

@@ -155,7 +155,8 @@ __device__ __forceinline__ void frag_params(const ProArgs& a, int kc, int q, Fra
 __device__ __forceinline__ void frag_x(const ProArgs& a, int tok, int kc, int q, float (&xv)[8]) {
     const float* x = a.x + (int64_t)tok * a.K;
     const int k0 = kc * 32 + 4 * q;
-    if ((a.K & 3) == 0 && k0 + 20 <= a.K) {  // both 4-feature runs inside the row: two 128-bit loads
+    // both 4-feature runs inside a 16-byte aligned row: two 128-bit loads
+    if ((a.K & 3) == 0 && k0 + 20 <= a.K && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
         const float4 lo = *reinterpret_cast<const float4*>(x + k0);
         const float4 hi = *reinterpret_cast<const float4*>(x + k0 + 16);
         xv[0] = lo.x, xv[1] = lo.y, xv[2] = lo.z, xv[3] = lo.w;
