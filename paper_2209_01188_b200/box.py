@@ -398,7 +398,14 @@ class BoxScheduler:
         t = x.shape[0]
         if t > self.max_tokens:
             self.call("reserve", seq, seq.length + t)
-            return torch.cat([self.run(seq, x[c0:c0 + self.max_tokens]) for c0 in range(0, t, self.max_tokens)])
+            parts = [self.run(seq, x[c0:c0 + self.max_tokens]) for c0 in range(0, t, self.max_tokens)]
+            out = torch.cat(parts)
+            # the parts were allocated on the egress stream: keep their memory from being reused there
+            # (the next job's egress) before this stream's concatenation has read them
+            for p in parts:
+                if p.is_cuda:
+                    p.record_stream(torch.cuda.current_stream(p.device))
+            return out
         job = _BoxJob(seq, x)
         self.q.put(("step", job))
         job.done.wait()
@@ -622,6 +629,8 @@ class BoxScheduler:
 
             def place(o, r0=r0, n=n, c0=c0, c=c):
                 out[r0:r0 + n, c0:c0 + c] = o.view(n, c, d)
+                if o.is_cuda:  # o lives in the egress stream's pool: not reused before this copy ran
+                    o.record_stream(torch.cuda.current_stream(o.device))
                 with lock:
                     remaining[0] -= 1
                     last = remaining[0] == 0
@@ -776,10 +785,10 @@ class BoxFrontEnd(ServerNode):
                 x = msg.decode()
             st.synchronize()
             t1 = time.perf_counter()
-            out = self.sched.run(seq, x)
+            out = self.sched.run(seq, x)  # (a long step: concatenated on this thread's current stream)
         t2 = time.perf_counter()
         try:
-            reply = self._encode(out, encoding)
+            reply = self._encode(out, encoding, producer=torch.cuda.current_stream(self.span.device))
         except InputError as e:
             raise _NonFinite(str(e)) from e  # computed, then failed encoding (position advances)
         if _TIMING:
