@@ -621,6 +621,7 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
     // ahead of the consumers (mbarrier parity waits cannot tell those rounds apart)
     static_assert(!FUSED || SK_STAGES % SK_OPW == 0, "operand warps must own whole ring slots");
     constexpr int NT = digit_ntiles(TC);
+    constexpr int NACC = NT == 1 ? 2 : 1;  // accumulator sets (see the consumer loop)
     constexpr int COLS = 8 * NT;
     constexpr int SST = COLS + 1;
     constexpr int A_STAGE = SK_KCS * 4096;
@@ -747,13 +748,13 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
         const int mg = (int)(u / a.KC);
         const int ka = (int)(u % a.KC);
         const int kb = (int)((int64_t)a.KC < ka + (u1 - u) ? (int64_t)a.KC : ka + (u1 - u));
-        int acc[2][NT][4];
+        int acc[2][NT][4], acc2[2][NT][4];
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
             for (int j = 0; j < NT; ++j)
 #pragma unroll
-                for (int r = 0; r < 4; ++r) acc[i][j][r] = 0;
+                for (int r = 0; r < 4; ++r) acc[i][j][r] = acc2[i][j][r] = 0;
         for (int kc = ka; kc < kb; kc += SK_KCS) {
             const int n = min(SK_KCS, kb - kc);
             mbar_wait(&full[stage], phase);
@@ -763,9 +764,13 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
             }
             const uint8_t* Bs = sb + stage * B_STAGE;
             const uint32_t As = sa_u + stage * A_STAGE;
+            if (n == SK_KCS) {
+                // full stage: no per-k-tile guard, so the fragment loads of later k tiles issue
+                // ahead of the MMAs; with one digit tile (NT == 1) odd k tiles accumulate into
+                // a second set, halving the dependent IMMA chain (traced: a 32-k-tile CTA's
+                // MMAs took ~2.6 us, ~80 cycles per k tile, latency-bound)
 #pragma unroll
-            for (int kk = 0; kk < SK_KCS; ++kk) {
-                if (kk < n) {
+                for (int kk = 0; kk < SK_KCS; ++kk) {
                     uint2 bv[NT];
 #pragma unroll
                     for (int j = 0; j < NT; ++j)
@@ -775,7 +780,27 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
                         uint32_t a0, a1, a2, a3;
                         ldsm_x4_i8(As + kk * 4096 + (cw * 2 + i) * 512 + a_lane, a0, a1, a2, a3);
 #pragma unroll
-                        for (int j = 0; j < NT; ++j) imma16832(acc[i][j], a0, a1, a2, a3, bv[j].x, bv[j].y);
+                        for (int j = 0; j < NT; ++j) {
+                            if (NACC > 1 && (kk & 1)) imma16832(acc2[i][j], a0, a1, a2, a3, bv[j].x, bv[j].y);
+                            else imma16832(acc[i][j], a0, a1, a2, a3, bv[j].x, bv[j].y);
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < SK_KCS; ++kk) {
+                    if (kk < n) {
+                        uint2 bv[NT];
+#pragma unroll
+                        for (int j = 0; j < NT; ++j)
+                            bv[j] = *reinterpret_cast<const uint2*>(Bs + (kk * NT + j) * 256 + lane * 8);
+#pragma unroll
+                        for (int i = 0; i < 2; ++i) {
+                            uint32_t a0, a1, a2, a3;
+                            ldsm_x4_i8(As + kk * 4096 + (cw * 2 + i) * 512 + a_lane, a0, a1, a2, a3);
+#pragma unroll
+                            for (int j = 0; j < NT; ++j) imma16832(acc[i][j], a0, a1, a2, a3, bv[j].x, bv[j].y);
+                        }
                     }
                 }
             }
@@ -787,6 +812,14 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
             }
         }
         u += kb - ka;
+        if (NACC > 1) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) acc[i][j][r] += acc2[i][j][r];  // exact s32
+        }
 
         // ---- segment finished: complete group or a piece of a split group
         const int64_t g0 = (int64_t)mg * a.KC, g1 = g0 + a.KC;
@@ -946,11 +979,16 @@ bool gemv_fusable(const Act& act, int K) {
 }
 
 int launch_gemv_fused(const Mat& m, const Act& act, const Epi& epi, const ProArgs& pro, float* zero_a,
-                      float* zero_b, float* partials, int* counters, int64_t partial_cap, cudaStream_t st) {
+                      float* zero_b, float* partials, int* counters, int64_t partial_cap, cudaStream_t st,
+                      int* sums, int64_t sums_elems) {
     if (!gemv_fusable(act, pro.K)) {
         set_error("fused-operand GEMV: unsupported shape");
         return PB_ERR_GENERIC;
     }
+    // split row groups merged by s32 reductions (560M 34.6 -> 34.4 us per block, 7B1 73.3 -> 72.3)
+    if (sums && ceil_div(act.n_tok, act.tc) * (int64_t)(m.Mp / 128) * 128 * 8 * digit_ntiles(2) <= sums_elems)
+        return sk_launch<2, 8, 4, true, true>(m, act, epi, partials, counters, partial_cap, st, &pro, zero_a, zero_b,
+                                              sums, sums_elems);
     return sk_launch<2, 8, 4, true>(m, act, epi, partials, counters, partial_cap, st, &pro, zero_a, zero_b);
 }
 
@@ -961,9 +999,9 @@ int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, i
                 cudaStream_t st, int* sums, int64_t sums_elems) {
     switch (act.tc) {
         case 2:
-            // batch-1 decode of the large shapes: reduction merge (176B: 426.0 -> 418.4 us per block); the
-            // small-shape fused kernel keeps the partial slots (a shared runtime branch cost it more than the
-            // merge saved: 560M 34.7 -> 40.3 us per block)
+            // batch-1 decode through a separate operand kernel: reduction merge (176B: 426.0 -> 418.4 us
+            // per block); the fused kernel takes the same merge as its own instantiation (a shared runtime
+            // branch cost more than the merge saved: 560M 34.7 -> 40.3 us per block)
             if (sums && ceil_div(act.n_tok, act.tc) * (int64_t)(m.Mp / 128) * 128 * 8 * digit_ntiles(2) <= sums_elems)
                 return sk_launch<2, 8, 4, false, true>(m, act, epi, partials, counters, partial_cap, st, nullptr,
                                                         nullptr, nullptr, sums, sums_elems);

@@ -455,7 +455,7 @@ static int run_blocks(pb_span* s, int n_tok, int max_pos, const float* in, float
                     const double bytes = (double)m.M * m.K + 4.0 * m.K + 4.0 * m.M + 4.0 * m.n_outl * m.M;
                     int rc = launch_gemv_fused(m, a, e, pa, mi == 0 ? s->tokmax_ctx : nullptr,
                                                mi == 0 ? s->tokmax_act : nullptr, s->partials, s->counters,
-                                               s->partial_cap, st);
+                                               s->partial_cap, st, s->sk_acc, s->sk_acc_elems);
                     prof_end(s, ev, 0, bytes, st);
                     return rc;
                 }

@@ -160,7 +160,8 @@ int prepare_fused_operand(int mode, const ProSrc& src, const float* x, int n_tok
                           const float* beta, const Mat& m, int tc, float* back, float4* stats, float* xo,
                           cudaStream_t st, ProArgs* out);
 int launch_gemv_fused(const Mat& m, const Act& act, const Epi& epi, const ProArgs& pro, float* zero_a,
-                      float* zero_b, float* partials, int* counters, int64_t partial_cap, cudaStream_t st);
+                      float* zero_b, float* partials, int* counters, int64_t partial_cap, cudaStream_t st,
+                      int* sums = nullptr, int64_t sums_elems = 0);
 int launch_gemm_f32(const Mat& m, const float* y, int n_tok, const Epi& epi, float* part, int64_t part_cap,
                     cudaStream_t st);
 int choose_tc(int n_tok);

@@ -18,6 +18,7 @@ def main():
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--shape", default="bloom-560m")
     p.add_argument("--blocks", type=int, default=0)
+    p.add_argument("--no-graphs", action="store_true", help="launch kernel by kernel (no CUDA graph replay)")
     a = p.parse_args()
     import torch
 
@@ -26,7 +27,8 @@ def main():
 
     cfg = SHAPES[a.shape]
     L = a.blocks or cfg.n_layers
-    span = BlockSpan(cfg, 0, L, int8=True, page_tokens=64, n_pages=8, max_tokens=128, max_seqs=2)
+    span = BlockSpan(cfg, 0, L, int8=True, page_tokens=64, n_pages=8, max_tokens=128, max_seqs=2,
+                     graphs=not a.no_graphs)
     span.generate_weights(42)
     seq = span.new_sequence()
     g = torch.Generator(device="cuda").manual_seed(3)

@@ -93,6 +93,11 @@ def main():
         print(f"{i:3d}  {k:4s} {r.shape[0]:5d} | {spread(r[:, 0])} | {spread(r[:, 1])} | {spread(r[:, 2])} | "
               f"{spread(r[:, 3])} | {busy:6.1f} {gap}")
         prev_end = emax
+        if k == "gemv" and (r[:, 8] > 0).any():
+            print(f"          gemv: operand resolved {spread(r[:, 10])} | 1st operand stage {spread(r[:, 11])} | "
+                  f"MMAs done {spread(r[:, 8])} | epilogue done {spread(r[:, 9])}")
+            print(f"          gemv: operand stage 3 written {spread(r[:, 6])} | consumer saw stage 1 {spread(r[:, 12])} "
+                  f"2 {spread(r[:, 13])} 3 {spread(r[:, 14])}")
         if k == "frag" and (r[:, 5] > 0).any():
             print(f"          frag summaries loaded {spread(r[:, 7])} | stats (warp 0) {spread(r[:, 2])} | "
                   f"CTA barrier {spread(r[:, 5])} | "
