@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
         // STAGES stages of weights are requested before the PDL wait; their digit planes
         // (written by the operand kernel) follow once it has completed
         if (lane == 0) {
+            const uint64_t pol = l2_evict_first();  // weights: read once per step
             int it = 0, pend_kc[C::STAGES], pend_n[C::STAGES];  // stages issued before the PDL wait
             bool waited = false;
             for (int64_t u = u0; u < u1;) {
@@ -368,7 +369,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc_sk(TcSkArgs a) {
                     const int s = it % C::STAGES, n = min(C::KT, kb - kc);
                     mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
                     mbar_expect_tx(&full[s], n * (TC_A + C::B_KT));
-                    bulk_g2s(sa + s * C::KT * TC_A, asrc + (int64_t)kc * TC_A, n * TC_A, &full[s]);
+                    bulk_g2s_hint(sa + s * C::KT * TC_A, asrc + (int64_t)kc * TC_A, n * TC_A, &full[s], pol);
                     if (waited) {
                         bulk_g2s(sb + s * C::KT * C::B_KT, a.bcanon + (int64_t)kc * C::B_KT, n * C::B_KT, &full[s]);
                     } else {

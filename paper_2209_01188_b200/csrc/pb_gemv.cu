@@ -661,6 +661,7 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
     } else if (FUSED && warp == 0) {
         // ---------------- producer: weights only (they never depend on earlier kernels)
         if (lane == 0) {
+            const uint64_t pol = l2_evict_first();
             int stage = 0;
             uint32_t phase = 0;
             for (int64_t u = u0; u < u1;) {
@@ -671,7 +672,7 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
                     const int n = min(SK_KCS, kb - kc);
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], n * 4096);
-                    bulk_g2s(sa + stage * A_STAGE, a.codes + ((int64_t)mg * a.KC + kc) * 4096, n * 4096, &full[stage]);
+                    bulk_g2s_hint(sa + stage * A_STAGE, a.codes + ((int64_t)mg * a.KC + kc) * 4096, n * 4096, &full[stage], pol);
                     if (++stage == SK_STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -683,6 +684,7 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
     } else if (warp == 0) {
         // ---------------- producer
         if (lane == 0) {
+            const uint64_t pol = l2_evict_first();
             int stage = 0, issued = 0;
             uint32_t phase = 0;
             int pk[SK_STAGES];  // k tiles of the stages prefetched before the dependency wait
@@ -699,7 +701,7 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
                     mbar_expect_tx(&full[stage], n * (4096 + NT * 256));
                     // weights never depend on the previous kernels: start streaming them
                     // while the operand producer (PDL predecessor) is still running
-                    bulk_g2s(sa + stage * A_STAGE, a.codes + ((int64_t)mg * a.KC + kc) * 4096, n * 4096, &full[stage]);
+                    bulk_g2s_hint(sa + stage * A_STAGE, a.codes + ((int64_t)mg * a.KC + kc) * 4096, n * 4096, &full[stage], pol);
                     if (!waited && issued < SK_STAGES) {
                         pk[issued] = kc;
                         pn[issued] = n;
