@@ -177,6 +177,7 @@ enum TraceKind { TR_GEMV = 0, TR_ATTN = 1, TR_FRAG = 2 };
 // previous kernel drains, and must execute pdl_wait() before touching anything
 // the previous kernels wrote (every such kernel calls it, so the chain stays
 // transitively ordered). pdl_trigger() lets the next kernel launch early.
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 

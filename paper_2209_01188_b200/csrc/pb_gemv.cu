@@ -531,11 +531,17 @@ __device__ __forceinline__ void sk_operand_warp(const SkArgs& a, int64_t u0, int
         }
         have_st = true;
     };
-    if (a.zero_a && blockIdx.x == 0 && ow == 0 && lane < TC && chunk * TC + lane < a.act.n_tok) {
-        a.zero_a[chunk * TC + lane] = 0.f;
-        a.zero_b[chunk * TC + lane] = 0.f;
-    }
     const bool ln = p.mode == PRO_LN;
+    bool waited = false;
+    auto wait_once = [&]() {  // dependency wait; then the range accumulators' reset (their readers are done)
+        pdl_wait();
+        pdl_trigger();
+        waited = true;
+        if (a.zero_a && blockIdx.x == 0 && ow == 0 && lane < TC && chunk * TC + lane < a.act.n_tok) {
+            a.zero_a[chunk * TC + lane] = 0.f;
+            a.zero_b[chunk * TC + lane] = 0.f;
+        }
+    };
     int stage = 0, seq = 0;
     uint32_t phase = 0;
     for (int64_t u = u0; u < u1;) {
@@ -562,6 +568,15 @@ __device__ __forceinline__ void sk_operand_warp(const SkArgs& a, int64_t u0, int
                 sc[i] = in ? *reinterpret_cast<const float4*>(p.scales + k) : make_float4(0.f, 0.f, 0.f, 0.f);
                 g4[i] = in && ln ? *reinterpret_cast<const float4*>(p.gamma + k) : make_float4(1.f, 1.f, 1.f, 1.f);
                 b4[i] = in && ln ? *reinterpret_cast<const float4*>(p.beta + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            // the scales / gamma / beta never change during a step: the first stage's are
+            // requested before the dependency wait, the activations after it
+            if (!waited) wait_once();
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const int krel = 128 * i + 4 * lane;
+                const int k = kc * 32 + krel;
+                const bool in = krel < n * 32 && k < p.K;
 #pragma unroll
                 for (int t = 0; t < TC; ++t) {
                     const int tok = chunk * TC + t;
@@ -612,6 +627,7 @@ __device__ __forceinline__ void sk_operand_warp(const SkArgs& a, int64_t u0, int
         }
         u += kb - ka;
     }
+    if (!waited) wait_once();
     if (!have_st) resolve();  // a warp without stages still writes the side outputs (ow == 0)
 }
 
@@ -654,9 +670,7 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
         pdl_wait();
         pdl_trigger();
     } else if (FUSED && warp > SK_CONS) {
-        // ---------------- operand warps
-        pdl_wait();
-        pdl_trigger();
+        // ---------------- operand warps (they wait for the predecessor themselves)
         sk_operand_warp<TC, SK_KCS, SK_STAGES>(a, u0, u1, chunk, sb, full, empty, warp - SK_CONS - 1);
     } else if (FUSED && warp == 0) {
         // ---------------- producer: weights only (they never depend on earlier kernels)
@@ -735,7 +749,15 @@ __global__ void __launch_bounds__(SK_THREADS + (FUSED ? 32 * SK_OPW : 0)) k_gemv
             pdl_trigger();
         }
     } else {
-    // ---------------- consumers
+    // ---------------- consumers: the first row group's static epilogue inputs into L1
+    // while the predecessor drains
+    {
+        const int o = (int)(u0 / a.KC) * 128 + (int)threadIdx.x - 32;
+        if (o < a.epi.M) {
+            prefetch_l1(a.epi.bias + o);
+            if (a.epi.s_next) prefetch_l1(a.epi.s_next + o);
+        }
+    }
     pdl_wait();
     pdl_trigger();
     if (threadIdx.x == 32) trace_stamp(a.trace, tcta, 1);
