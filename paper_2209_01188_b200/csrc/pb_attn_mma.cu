@@ -123,7 +123,13 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_attn_mma(AttnArgs a, int G, i
         return;
     }
 
-    // ---------------- compute warps
+    // ---------------- compute warps: the step constants of the first head (the next matmul's
+    // scales read by the finish, the ALiBi slope) into L1 while the predecessor drains
+    if (u0 < u1) {
+        const AmSeg s0 = am_seg(a, u0, u1);
+        if (a.tokmax && threadIdx.x < DH) prefetch_l1(a.s_next + s0.h * DH + threadIdx.x);
+        if (threadIdx.x == 0) prefetch_l1(a.slopes + s0.h);
+    }
     pdl_wait();
     pdl_trigger();
     if (threadIdx.x == 32) trace_stamp(a.trace, c, 1);
@@ -258,6 +264,7 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_attn_mma(AttnArgs a, int G, i
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[b]);
         }
+        if (threadIdx.x == 32 && nseg == 0) trace_stamp(a.trace, c, 11);  // diagnostics: stages done
         // ---- per-warp state for query g: m, l, O[dims] = hi rows + lo rows
         if (qv) {
             float* w = wst + (warp * AM_G + g) * (DH + 2);
@@ -341,6 +348,7 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_attn_mma(AttnArgs a, int G, i
             }
         }
         cons_bar_n<CW>();  // wst free; every warp past the merge
+        if (threadIdx.x == 32 && nseg == 0) trace_stamp(a.trace, c, 12);  // diagnostics: merged
         if (finalize && a.tokmax) {
             // operand range of the wo GEMV: exact, order-independent max per token
             for (int q = 0; q < nq; ++q) {

@@ -126,6 +126,9 @@ def main():
                       f"{n1(5):.1f} data {n1(6):.1f} done {n1(7):.1f} | seg1 start {n1(8):.1f} data {n1(9):.1f} "
                       f"done {n1(10):.1f} | end {n1(3):.1f}; single-segment CTAs end "
                       f"{np.median((r[idx[r[idx, 8] == 0], 3] - r[idx[r[idx, 8] == 0], 1]) / 1e3):.1f}")
+            rel0 = lambda col: np.median((r[idx, col] - r[idx, 1]) / 1e3)  # noqa: E731
+            print(f"attn: median us after release: first segment start {rel0(5):.2f} first K/V data {rel0(6):.2f} "
+                  f"stages done {rel0(11):.2f} merged {rel0(12):.2f} segment done {rel0(7):.2f} end {rel0(3):.2f}")
             print(f"attn: release->end p50 {np.median(dur[idx]):.1f} p90 {np.percentile(dur[idx], 90):.1f} "
                   f"max {dur[idx].max():.1f} us; same-SM pair gap median {np.median(gaps) if gaps else 0:.1f} us; "
                   f"slowest CTAs (index, SM, us): " + ", ".join(f"{c}/{sm[c]}/{dur[c]:.1f}" for c in order[:10]))
