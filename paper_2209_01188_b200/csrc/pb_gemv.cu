@@ -1018,7 +1018,7 @@ int launch_gemv_fused(const Mat& m, const Act& act, const Epi& epi, const ProArg
 
 // Stage shapes (k tiles per stage x stages) per column tile, chosen by sweeps
 // (profiles/r1_gemv_timeline_and_tail.txt, profiles/r1_small_shape_gemv_minu.txt):
-// decode 8 x 4 (32 KB stages, one CTA per SM), 3..8 tokens 8 x 2, 17..32 tokens 2 x 4.
+// decode 8 x 4 (32 KB stages, one CTA per SM), 3..8 tokens 8 x 3, 17..32 tokens 2 x 4.
 int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, int* counters, int64_t partial_cap,
                 cudaStream_t st, int* sums, int64_t sums_elems) {
     switch (act.tc) {
@@ -1030,7 +1030,9 @@ int launch_gemv(const Mat& m, const Act& act, const Epi& epi, float* partials, i
                 return sk_launch<2, 8, 4, false, true>(m, act, epi, partials, counters, partial_cap, st, nullptr,
                                                         nullptr, nullptr, sums, sums_elems);
             return sk_launch<2, 8, 4>(m, act, epi, partials, counters, partial_cap, st);
-        case 8: return sk_launch<8, 8, 2>(m, act, epi, partials, counters, partial_cap, st);
+        // 3..8 tokens: 8 x 3 (re-swept after the hoisted fragment loads: 7B1 batch 8 104.3 -> 102.1 us per
+        // block; 176B equal; 4 x 4 / 4 x 6 slower)
+        case 8: return sk_launch<8, 8, 3>(m, act, epi, partials, counters, partial_cap, st);
         case 16: return sk_launch<16, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
         case 32: return sk_launch<32, 2, 4>(m, act, epi, partials, counters, partial_cap, st);
         default: set_error("bad column tile"); return PB_ERR_GENERIC;
