@@ -119,3 +119,42 @@ def test_box_long_prompt_forward_backward():
     finally:
         c.close()
         assert box.stop() == [0, 0]
+
+
+def test_box_concurrent_long_prompts():
+    """Eight sessions send prompts longer than the token workspace at once:
+    every prompt runs as causal chunk jobs whose outputs come off the egress
+    stream while other sessions' jobs are in flight (the cross-stream buffer
+    lifetimes of BoxScheduler.run / BoxFrontEnd._run_step), and each reply
+    equals the span forward of its own prompt. (At this size it did not
+    reproduce the 7B1-scale race those lifetimes fixed; it guards the path.)"""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2209_01188_b200.client import SpanClient
+
+    shape = O.Shape(*SMALL)
+    blocks = [O.make_block(42, shape, i) for i in range(4)]
+    emb = O.make_embed(42, shape)
+    prompts = [emb[np.random.default_rng(100 + i).integers(0, 32, 40)].astype(np.float32) for i in range(8)]
+    box = _box(SMALL, "none", max_batch_tokens=16, capacity=8)
+
+    def one(i):
+        c = SpanClient(box.address)
+        try:
+            sid = c.open_session(64)
+            got = c.step(sid, 0, prompts[i])
+            c.close_session(sid)
+            return got
+        finally:
+            c.close()
+
+    try:
+        for _ in range(3):
+            with ThreadPoolExecutor(8) as ex:
+                outs = list(ex.map(one, range(8)))
+            for x, got in zip(prompts, outs):
+                want = O.forward_span(blocks, x, shape, quantized=False)
+                assert np.isfinite(got).all()
+                assert float(np.abs(got - want).max()) <= 1e-3 * float(np.abs(want).max())
+    finally:
+        assert box.stop() == [0, 0]
