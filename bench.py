@@ -61,7 +61,9 @@ def parse():
     p.add_argument("--ctx", type=int, default=2048)
     p.add_argument("--seed", type=int, default=42)
     # a multiple of the tcgen05 GEMM's 80-token tile (256 padded 4 tiles to 320 tokens)
-    p.add_argument("--prefill-chunk", type=int, default=240)
+    # tokens per prefill job, a multiple of the 80-token tcgen05 tile (480: prefill 1636 -> 1789 tokens/s and
+    # 704 -> 763 useful TFLOP/s against 240; 960 no better)
+    p.add_argument("--prefill-chunk", type=int, default=480)
     p.add_argument("--batch", type=int, default=1, help="batch-1 sessions per pipeline micro-batch (headline)")
     p.add_argument("--hop", default="p2p", choices=["p2p", "nccl"],
                    help="span-to-span hop: NVLink peer-memory mailboxes (pb_hop.cu) or NCCL send/recv")
