@@ -605,9 +605,47 @@ def forward_record(pl, args, cfg):
                     "pass that gives the tcgen05/attention shares is the timed one"}
 
 
+def _e2e_out_of_process(address, S, prefill_msgs, step_msgs, per_frame, T0, W, K, ctx):
+    """Run the e2e client sessions in a separate process (`bench.py
+    --e2e-client`); returns (wall seconds, errors, description) or (None, ...)
+    when that process cannot be used."""
+    import pickle
+    import tempfile
+
+    proc, spec = None, None
+    try:
+        with tempfile.NamedTemporaryFile("wb", suffix=".pkl", delete=False) as f:
+            pickle.dump({"address": address, "S": S, "prefill": prefill_msgs, "steps_msgs": step_msgs,
+                         "per_frame": per_frame, "T0": T0, "W": W, "K": K, "ctx": ctx}, f)
+            spec = f.name
+        proc = subprocess.Popen([sys.executable, os.path.abspath(__file__), "--e2e-client", spec],
+                                stdin=subprocess.PIPE, stdout=subprocess.PIPE, text=True)
+        line = proc.stdout.readline()
+        if line.strip() != "READY":
+            raise RuntimeError(f"client process: {line!r}")
+        proc.stdin.write("GO\n")
+        proc.stdin.flush()
+        res = json.loads(proc.stdout.readline())
+        proc.wait(timeout=60)
+        return res["wall"], res["errors"], "a separate client process, one thread per session"
+    except Exception as e:  # noqa: BLE001
+        print(f"[e2e] client process unavailable ({e!r}); clients on threads of this process", file=sys.stderr)
+        if proc is not None and proc.poll() is None:
+            proc.kill()
+        return None, [], None
+    finally:
+        if spec:
+            try:
+                os.unlink(spec)
+            except OSError:
+                pass
+
+
 def e2e_record(pl, args, cfg, T0):
-    """The headline metric through the server's public API: S client threads
-    each open a session, prefill T0 tokens with one int8 STEP frame, then send
+    """The headline metric through the server's public API: S client sessions
+    (threads of a separate client process, as the reference's clients are
+    separate programs; threads of this process if that process fails) each
+    open a session, prefill T0 tokens with int8 STEP frames, then send
     W + K one-token STEP frames (int8 TensorMsg built on the host) and read the
     replies. N=1: ServerNode on the resident span; N>1: the box front end (one
     ServerEntry [0, 70), rank 0 accepts TCP, the hops stay on the GPUs)."""
@@ -616,7 +654,6 @@ def e2e_record(pl, args, cfg, T0):
     import torch.distributed as dist
 
     from paper_2209_01188_b200.box import BoxFrontEnd, BoxPlan, RankState, payload_bytes, serve_rank, FMT_F32
-    from paper_2209_01188_b200.client import SpanClient
     from paper_2209_01188_b200.server import ServerConfig, ServerNode
     from paper_2209_01188_b200 import codec
 
@@ -653,50 +690,22 @@ def e2e_record(pl, args, cfg, T0):
                                         codec.ENC_INT8) for p in range(0, T0, per_frame)]
     step_msgs = [codec.encode_tensor(rng.standard_normal((1, d)).astype(np.float32) * 0.05, codec.ENC_INT8)
                  for _ in range(8)]
-    ready, go = threading.Barrier(S + 1), threading.Event()
-    times, errors = [0.0] * S, []
-
-    def client(i):
-        c = SpanClient(node.address, codec.ENC_INT8, timeout_ms=600_000)
+    wall, errors, clients = _e2e_out_of_process(node.address, S, prefill_msgs, step_msgs, per_frame, T0, W, K,
+                                                args.ctx)
+    if wall is None:  # the client process failed to start or report: the same sessions on threads here
+        clients = "threads of the bench process"
+        ready, go = threading.Barrier(S + 1), threading.Event()
+        ts, times, errors = _client_sessions(node.address, S, prefill_msgs, step_msgs, per_frame, T0, W, K,
+                                             args.ctx, ready, go)
         try:
-            sid = c.open_session(args.ctx)
-            pos = 0
-            for msg in prefill_msgs:
-                c.step_raw(sid, pos, msg)
-                pos += min(per_frame, T0 - pos)
-            for k in range(W):
-                c.step_raw(sid, pos, step_msgs[k % 8])
-                pos += 1
-            ready.wait()
-            go.wait()
-            t0 = time.perf_counter()
-            for k in range(K):
-                reply = c.step_raw(sid, pos, step_msgs[k % 8])
-                codec.parse_tensor(reply)  # the host reads the int8 reply (codes + scales)
-                pos += 1
-            times[i] = time.perf_counter() - t0
-            c.close_session(sid)
-        except Exception as e:  # noqa: BLE001
-            errors.append(repr(e))
-            try:
-                ready.abort()
-            except Exception:  # noqa: BLE001
-                pass
-        finally:
-            c.close()
-
-    ts = [threading.Thread(target=client, args=(i,)) for i in range(S)]
-    for t in ts:
-        t.start()
-    try:
-        ready.wait(timeout=900)
-    except threading.BrokenBarrierError:
-        pass
-    t_start = time.perf_counter()
-    go.set()
-    for t in ts:
-        t.join()
-    wall = time.perf_counter() - t_start
+            ready.wait(timeout=900)
+        except threading.BrokenBarrierError:
+            pass
+        t_start = time.perf_counter()
+        go.set()
+        for t in ts:
+            t.join()
+        wall = time.perf_counter() - t_start
     if os.environ.get("PB_SERVER_TIMING") == "1" and node.timing:  # diagnostic: per-STEP host split (ms)
         cols = list(zip(*node.timing[-K * S:]))
         print("[e2e] STEP decode / compute / encode ms (median):",
@@ -718,7 +727,8 @@ def e2e_record(pl, args, cfg, T0):
             "wall_s": wall, "sessions": S, "ctx_end": T0 + W + K,
             "path": ("TCP STEP frames (int8 TensorMsg) -> " + ("ServerNode" if N == 1 else
                      f"box front end over {N} GPUs (one ServerEntry [0, 70), peer-memory hops)") +
-                     " -> reply frames read by the client threads; prefill via int8 STEPs of <= 1169 tokens per session, untimed")}
+                     f" -> reply frames read by the clients ({clients}); prefill via int8 STEPs of <= 1169 tokens "
+                     "per session, untimed")}
 
 
 # ------------------------------------------------------------------ main
@@ -852,7 +862,80 @@ def run_ours(args):
         pl.dist.destroy_process_group()
 
 
+def _client_sessions(address, S, prefill_msgs, step_msgs, per_frame, T0, W, K, ctx, ready, go):
+    """S client sessions on threads: open, prefill T0 tokens (int8 STEP frames of
+    <= per_frame rows), W warm-up steps, then (after ready/go) K timed one-token
+    STEP frames each. Returns (per-session seconds, errors)."""
+    from paper_2209_01188_b200 import codec
+    from paper_2209_01188_b200.client import SpanClient
+
+    times, errors = [0.0] * S, []
+
+    def client(i):
+        c = SpanClient(address, codec.ENC_INT8, timeout_ms=600_000)
+        try:
+            sid = c.open_session(ctx)
+            pos = 0
+            for msg in prefill_msgs:
+                c.step_raw(sid, pos, msg)
+                pos += min(per_frame, T0 - pos)
+            for k in range(W):
+                c.step_raw(sid, pos, step_msgs[k % len(step_msgs)])
+                pos += 1
+            ready.wait()
+            go.wait()
+            t0 = time.perf_counter()
+            for k in range(K):
+                reply = c.step_raw(sid, pos, step_msgs[k % len(step_msgs)])
+                codec.parse_tensor(reply)  # the host reads the int8 reply (codes + scales)
+                pos += 1
+            times[i] = time.perf_counter() - t0
+            c.close_session(sid)
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+            try:
+                ready.abort()
+            except Exception:  # noqa: BLE001
+                pass
+        finally:
+            c.close()
+
+    ts = [threading.Thread(target=client, args=(i,)) for i in range(S)]
+    for t in ts:
+        t.start()
+    return ts, times, errors
+
+
+def e2e_client_process():
+    """`bench.py --e2e-client SPEC`: the e2e clients in their own process (as the
+    reference's clients are), so the server's threads do not share an
+    interpreter lock with them. Prints READY after every session's prefill and
+    warm-up, starts the timed steps on a line from stdin, prints the result."""
+    import pickle
+
+    with open(sys.argv[2], "rb") as f:
+        spec = pickle.load(f)
+    ready, go = threading.Barrier(spec["S"] + 1), threading.Event()
+    ts, times, errors = _client_sessions(spec["address"], spec["S"], spec["prefill"], spec["steps_msgs"],
+                                         spec["per_frame"], spec["T0"], spec["W"], spec["K"], spec["ctx"], ready, go)
+    try:
+        ready.wait(timeout=900)
+    except threading.BrokenBarrierError:
+        pass
+    print("READY", flush=True)
+    sys.stdin.readline()
+    t_start = time.perf_counter()
+    go.set()
+    for t in ts:
+        t.join()
+    wall = time.perf_counter() - t_start
+    print(json.dumps({"wall": wall, "errors": errors}), flush=True)
+
+
 def main():
+    if len(sys.argv) > 2 and sys.argv[1] == "--e2e-client":
+        e2e_client_process()
+        return
     args = parse()
     if args.impl == "reference":
         run_reference(args)
