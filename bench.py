@@ -14,13 +14,16 @@ result back to span 0, closing the ring for the session's next token.
 
 value = session-steps/s over all GPUs, CUDA events between barriers, max over
 ranks (inputs resident in HBM). Sub-records on the same line:
-  e2e    the same metric through the server's public API: client threads send
+  e2e    the same metric through the server's public API: client sessions (threads
+         of a separate client process) send
          STEP frames (int8 TensorMsg, host bytes) over TCP to the span server
          (N=1: ServerNode; N>1: the box front end, ONE server for [0, 70)
          whose hops stay on the GPUs) and read the replies;
   b32    tokens/s with 32 batch-1 sessions per micro-batch (BASELINE's b=32);
   c2     BLOOM-560M shape on one GPU, 128-token prefix, batch 1 (config 2);
   forward  C5-style FORWARD rows of 512 tokens through the pipeline;
+  prefill  the sessions' prompt prefill (480-token tcgen05 jobs);
+  f2     BACKWARD of one 512-position row through two 176B blocks;
   cpu_baseline  the reference's arithmetic (oracle port) on the host cores at
          the same context, one block, extrapolated.
 
